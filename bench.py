@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 stencil hot path (contract: README/DESIGN.md §8).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {cuda,reference}]
+
+N=1 workload = BASELINE.json configs[1]: Jacobi-2D 5-point, 16384x16384
+interior fp64, 1000 sweeps per step (one st_jacobi2d_run call). The PW
+advection (configs[2], 512^3) is measured in the same run and reported under
+"pw_advect3d" with its own roofline. N>1 (torchrun, one rank per GPU):
+configs[3], Jacobi-2D 32768^2 strong scaling over row slabs with NCCL halo
+exchange, plus configs[4] PW 1024x1024x512 z-slabs.
+
+Metric: Gpts/s = 1e9 grid-point updates per second (the paper's MCells/s /
+1000), whole job over all ranks. Inputs are synthetic, from
+stencil_inputs (seed 42, SURVEY.md §8(d) recipe). Every buffer is larger than
+the 126 MB L2, so no L2 flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Gpts/s per GPU and % of B200 HBM BW; 1/2/4/8-GPU scaling eff."
+UNIT = "Gpts/s"
+JACOBI_BYTES_PER_PT = 16  # one 8-byte read + one 8-byte write per point per sweep
+PW_BYTES_PER_PT = 48      # u,v,w read + su,sv,sw written
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel_key: str):
+    """DRAM bytes per launch from the committed ncu --set full summary, or None."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    v = d.get(kernel_key)
+    return None if v is None else v.get("dram_bytes_per_launch")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def host_info():
+    model = ""
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if ln.startswith("Model name"):
+                model = ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The CPU oracle, as it stands, on the host cores (bench.py --impl reference)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np  # noqa: F401
+    import oracle
+    import stencil_inputs as si
+    model, cores = host_info()
+    n, sweeps = 16384, args.ref_sweeps
+    a = si.jacobi2d_grid(n, n)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.jacobi2d(a, sweeps, threads=cores)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    mean = sum(times) / len(times)
+    value = n * n * sweeps / mean / 1e9
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "jacobi2d_16384x16384_fp64 (configs[1]); step = bounded sample of "
+                               f"{sweeps} sweeps of the full grid", "sweeps_per_step": sweeps},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{sweeps} Jacobi sweeps of the 16384^2 grid per step, C oracle "
+                                   f"(-O2 -ffp-contract=off, OpenMP {cores} threads) on {model}"},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def cpu_baseline_jacobi(sweeps: int):
+    import oracle
+    import stencil_inputs as si
+    model, cores = host_info()
+    n = 16384
+    a = si.jacobi2d_grid(n, n)
+    oracle.jacobi2d(a, 1, threads=cores)  # warm (page-in)
+    t0 = time.perf_counter()
+    oracle.jacobi2d(a, sweeps, threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": round(n * n * sweeps / dt / 1e9, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{sweeps} sweeps of the configs[1] 16384^2 grid (of 1000 per step), C oracle "
+                      f"-O2 -ffp-contract=off, OpenMP {cores} threads, {model}; {dt:.2f} s"}
+
+
+def cpu_baseline_pw():
+    import oracle
+    import stencil_inputs as si
+    _, cores = host_info()
+    n = 512
+    d = si.pw_inputs(n, n, n)
+    t0 = time.perf_counter()
+    oracle.pw_advect3d(d["u"], d["v"], d["w"], d, threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": round(n ** 3 / dt / 1e9, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"1 application on the configs[2] 512^3 grid; {dt:.2f} s"}
+
+
+# --------------------------------------------------------------------------- CUDA arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
+    ap.add_argument("--sweeps", type=int, default=1000, help="Jacobi sweeps per step (configs[1]: 1000)")
+    ap.add_argument("--tblock", type=int, default=0)
+    ap.add_argument("--pw-apps", type=int, default=20, help="PW applications timed")
+    ap.add_argument("--no-pw", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-sweeps", type=int, default=20)
+    ap.add_argument("--cpu-sweeps", type=int, default=40)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_2310_01882_b200 as st
+    import stencil_inputs as si
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        comm = st.Comm.from_process_group(local)
+    assert world == args.gpus or world == 1, "--gpus must match the torchrun world size"
+
+    stream = torch.cuda.current_stream()
+    hbm_peak, peak_src = peaks()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ------------------------------------------------------------------ Jacobi
+    n_glob = 16384 if world == 1 else 32768
+    ny0, ny_loc = st.st_block_split(n_glob, world, rank)
+    ld = n_glob + 2
+    rows = ny_loc + 2
+    a_host = torch.from_numpy(si.jacobi2d_grid(n_glob, n_glob, ld=ld, row0=ny0, rows=rows))
+    a0 = a_host.to(dev)
+    A = torch.empty_like(a0)
+    B = torch.empty_like(a0)
+    sweeps = args.sweeps
+
+    A.copy_(a0)
+
+    def jacobi_step():
+        # `sweeps` more sweeps of the resident grid; with an even count the state stays in A
+        r = st.st_jacobi2d_run(A, B, sweeps, tblock=args.tblock, comm=comm)
+        if r is not A:
+            A.copy_(r)
+
+    for _ in range(args.warmup):
+        jacobi_step()
+    barrier()
+    l0 = st.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        times = []
+        for _ in range(args.steps):
+            barrier()
+            ev0.record(stream)
+            jacobi_step()
+            ev1.record(stream)
+            ev1.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+        barrier()
+    launches = st.launch_count() - l0
+    step_ms = max_over_ranks(sum(times) / len(times))
+    sweep_ms = step_ms / sweeps  # every launch in the step is the sweep kernel
+    pts_total = n_glob * n_glob * sweeps
+    value = pts_total / (step_ms / 1e3) / 1e9
+    pts_rank = ny_loc * n_glob
+    achieved_gbs = JACOBI_BYTES_PER_PT * pts_rank / (sweep_ms / 1e3) / 1e9
+    clocks = clk.summary()
+
+    # ------------------------------------------------------------------ e2e (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        h_in = a_host.pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        Ae, Be = A, B
+
+        def e2e_step():
+            Ae.copy_(h_in, non_blocking=True)
+            r = st.st_jacobi2d_run(Ae, Be, sweeps, tblock=args.tblock, comm=comm)
+            h_out.copy_(r, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        e_times = []
+        for _ in range(max(1, min(args.steps, 3))):
+            barrier()
+            ev0.record(stream)
+            e2e_step()
+            ev1.record(stream)
+            ev1.synchronize()
+            e_times.append(ev0.elapsed_time(ev1))
+        e_ms = max_over_ranks(sum(e_times) / len(e_times))
+        e2e = {"value": round(pts_total / (e_ms / 1e3) / 1e9, 3), "unit": UNIT,
+               "h2d_bytes_per_step": h_in.numel() * 8, "d2h_bytes_per_step": h_out.numel() * 8,
+               "ms_per_step": round(e_ms, 3)}
+        del h_in, h_out
+    del A, B, a0
+
+    # ------------------------------------------------------------------ PW advection
+    pw = None
+    if not args.no_pw:
+        nxy = 512 if world == 1 else 1024
+        nz_glob = 512
+        z0, nz_loc = st.st_block_split(nz_glob, world, rank)
+        d = si.pw_inputs(nxy, nxy, nz_glob, plane0=z0, planes=nz_loc + 2)
+        g = {k: (torch.from_numpy(v).to(dev) if hasattr(v, "shape") else v) for k, v in d.items()}
+        outs = [torch.empty_like(g["u"]) for _ in range(3)]
+
+        def pw_app():
+            st.st_pw_advect3d(g["u"], g["v"], g["w"], *outs, g["tcx"], g["tcy"], g["tzc1"], g["tzc2"],
+                              g["tzd1"], g["tzd2"], comm=comm)
+
+        for _ in range(args.warmup):
+            pw_app()
+        barrier()
+        pl0 = st.launch_count()
+        ev0.record(stream)
+        for _ in range(args.pw_apps):
+            pw_app()
+        ev1.record(stream)
+        ev1.synchronize()
+        pw_launches = st.launch_count() - pl0
+        app_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.pw_apps)
+        pts = nxy * nxy * nz_glob
+        pw_gbs = PW_BYTES_PER_PT * nxy * nxy * nz_loc / (app_ms / 1e3) / 1e9
+        pw = {"workload": f"pw_advect3d_{nxy}x{nxy}x{nz_glob}_fp64" + ("" if world == 1 else f"_zslabs{world}"),
+              "value": round(pts / (app_ms / 1e3) / 1e9, 3), "unit": UNIT, "ms_per_app": round(app_ms, 4),
+              "apps": args.pw_apps, "gpu_launches": pw_launches,
+              "roofline": {"bound": "hbm", "achieved": round(pw_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                           "frac": round(pw_gbs / hbm_peak, 4), "traffic": ncu_traffic("pw_advect3d_kernel"),
+                           "bytes_per_pt": PW_BYTES_PER_PT, "peak_source": peak_src}}
+        if world == 1 and not args.no_cpu:
+            pw["cpu_baseline"] = cpu_baseline_pw()
+        del g, outs
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_jacobi(args.cpu_sweeps)
+
+    if comm is not None:
+        comm.close()
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True,
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SplitMix64 seed 42, SURVEY.md §8(d) recipe)",
+            "config": {"workload": f"jacobi2d_{n_glob}x{n_glob}_fp64_{sweeps}sweeps"
+                                   + ("" if world == 1 else f"_rowslabs{world}"),
+                       "sweeps_per_step": sweeps, "tblock": args.tblock, "ld": ld,
+                       "l2": "no flush needed: each buffer is %.2f GB > 126 MB L2" % (rows * ld * 8 / 1e9),
+                       "step": "st_jacobi2d_run(iters=%d) continuing from the resident state" % sweeps},
+            "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(achieved_gbs / hbm_peak, 4), "traffic": ncu_traffic("jacobi2d_stream_kernel"),
+                         "bytes_per_pt": JACOBI_BYTES_PER_PT, "kernel_ms_per_sweep": round(sweep_ms, 5),
+                         "peak_source": peak_src},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "pw_advect3d": pw,
+        }
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

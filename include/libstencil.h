@@ -1,0 +1,185 @@
+/* libstencil.h — C ABI of the B200-native stencil hot path (ABI version 1).
+ *
+ * The library implements the data-parallel hot path that the paper's
+ * Flang -> stencil-dialect flow accelerates (arXiv 2310.01882): repeated
+ * application of the stencils extracted from Fortran loop nests, on fields
+ * that stay resident in device memory ("optimised" data
+ * approach: allocation and copies hoisted out of the iteration loop, device
+ * references held by the host as pointers), with a halo swap between
+ * iterations when the grid is decomposed.
+ *
+ * Conventions (all entry points)
+ *   - Field and coefficient pointers are CUDA DEVICE pointers to IEEE binary64.
+ *     The caller allocates and owns every buffer and keeps it alive until the
+ *     stream work completes; the library never allocates per call. `st_comm`
+ *     is the only library-owned object.
+ *   - Layout (the first Fortran index is contiguous):
+ *       2-D: row-major a[y*ld + x]; rows 0..ny+1, columns 0..nx+1; ld >= nx+2,
+ *            ld EVEN (16-byte rows); base 16-byte aligned.
+ *       3-D: f[(z*(ny+2) + y)*ldx + x]; x fastest, z slowest; ldx >= nx+2, even.
+ *     The outermost cell layer is the 1-cell halo ("ring"): Listing 2's input
+ *     temp is one cell wider than its output, [-1,255]^2 -> [0,254]^2
+ *     (PAPER.md:122).
+ *   - Work is enqueued on `cuda_stream` (a cudaStream_t; NULL = legacy default
+ *     stream) after all prior work on it; calls return without a host sync.
+ *   - Errors: argument validation is synchronous, returns ST_EINVAL and
+ *     enqueues nothing. CUDA launch/API failures return ST_ECUDA, NCCL failures
+ *     ST_ENCCL (the st_comm is unusable afterwards). Asynchronous device faults
+ *     surface at the caller's next synchronisation (CUDA semantics). No
+ *     exceptions cross the ABI, nothing aborts or prints. st_last_error()
+ *     describes the most recent failure on the calling thread.
+ *   - Threads: calls without a comm are reentrant. An st_comm is used by one
+ *     thread, and all ranks issue the same sequence of comm calls (NCCL rule).
+ *   - Arithmetic: every kernel evaluates the association trees of DESIGN.md
+ *     R2/R6 with one rounding per operation (no FMA contraction), so results
+ *     are bitwise identical to the CPU oracle, for every tiling, temporal
+ *     blocking depth and decomposition.
+ */
+#ifndef LIBSTENCIL_H
+#define LIBSTENCIL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ST_OK = 0,
+  ST_EINVAL = 1,    /* bad argument; nothing was enqueued */
+  ST_ECUDA = 2,     /* CUDA runtime/driver error */
+  ST_ENCCL = 3,     /* NCCL error; the communicator is unusable */
+  ST_ENOTSUP = 4,   /* valid request this build does not support */
+  ST_EINTERNAL = 5  /* library bug */
+} st_status;
+
+#define ST_ABI_VERSION 1
+
+/* Returns ST_ABI_VERSION of the loaded library. */
+int32_t st_abi_version(void);
+
+/* Thread-local description of the last failing call on this thread ("" if none).
+ * Valid until the next st_* call on the same thread. */
+const char* st_last_error(void);
+
+/* Number of kernel launches this library has issued in this process (all
+ * devices, all threads). Diagnostic counter used by the benchmark's
+ * `gpu_launches` report; never reset. */
+uint64_t st_launch_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* Communicator (slab decomposition across ranks; one process per GPU)       */
+/* ------------------------------------------------------------------------ */
+
+typedef struct st_comm st_comm; /* opaque, library-owned */
+
+#define ST_UNIQUE_ID_BYTES 128 /* == sizeof(ncclUniqueId) */
+
+/* Rank 0 creates the id; the caller broadcasts it (e.g. over torch.distributed). */
+st_status st_comm_unique_id(uint8_t id[ST_UNIQUE_ID_BYTES]);
+
+/* Collective over `nranks` processes: creates the NCCL communicator, an
+ * internal comm stream and events on `cuda_device`. Rank r owns slab r of the
+ * slowest axis (block split, remainder to the high ranks: st_block_split). */
+st_status st_comm_init(st_comm** out, int32_t nranks, int32_t rank,
+                       const uint8_t id[ST_UNIQUE_ID_BYTES], int32_t cuda_device);
+
+/* Frees the NCCL communicator, stream and events (waits for pending comm work). */
+st_status st_comm_destroy(st_comm* comm);
+
+st_status st_comm_query(const st_comm* comm, int32_t* rank, int32_t* nranks, int32_t* cuda_device);
+
+/* Block split of n items over nranks (remainder to the high
+ * ranks). Host-only; no device needed. */
+st_status st_block_split(int64_t n, int32_t nranks, int32_t rank, int64_t* start, int64_t* count);
+
+/* One transfer of a halo swap: `count` doubles starting at element `offset`
+ * of a field, to/from rank `peer`. */
+typedef struct {
+  int32_t peer;
+  int64_t offset;
+  int64_t count;
+} st_xfer;
+
+/* The halo-swap plan of st_halo_exchange for one rank (host-only; no device
+ * needed, so the decomposition logic is testable on CPU): a field holds
+ * n_slow_local + 2*width slabs of slab_pitch doubles, slabs 0..width-1 and
+ * width+n_slow_local.. are ghosts. Sends the first/last `width` owned slabs to
+ * rank-1/rank+1 and receives into the ghost slabs; the edge ranks skip the
+ * missing side (non-periodic). Fills up to two sends and two
+ * receives, ordered by direction (low neighbour first). */
+st_status st_halo_plan(int32_t rank, int32_t nranks, int64_t n_slow_local, int64_t slab_pitch,
+                       int32_t width, st_xfer sends[2], int32_t* nsend, st_xfer recvs[2],
+                       int32_t* nrecv);
+
+/* Slowest-axis halo swap of `nfields` fields (device pointers), all in one
+ * NCCL group, ordered on `cuda_stream` (the comm stream joins back with an
+ * event). Requires n_slow_local >= width >= 1. nranks == 1: no-op. */
+st_status st_halo_exchange(st_comm* comm, double* const* fields, int32_t nfields,
+                           int64_t n_slow_local, int64_t slab_pitch, int32_t width,
+                           void* cuda_stream);
+
+/* ------------------------------------------------------------------------ */
+/* 2-D Jacobi 5-point sweep (Listing 1)                      */
+/* ------------------------------------------------------------------------ */
+
+/* `iters` sweeps of
+ *     B[y][x] = (((A[y-1][x] + A[y+1][x]) + A[y][x-1]) + A[y][x+1]) * 0.25
+ * over the interior 1 <= y <= ny_local, 1 <= x <= nx, with value semantics
+ * (stencil.apply evaluates over every cell of a snapshot), i.e.
+ * Jacobi double buffering: roles of a and b swap after every sweep.
+ *
+ *   a, b      (ny_local + 2*halo) rows x ld doubles each, non-overlapping.
+ *             `a` holds the initial state including the halo; the library
+ *             copies the halo rows a -> b. Columns 0 and nx+1 are the
+ *             Dirichlet ring and are never changed.
+ *   comm NULL halo must be 1; rows 0 and ny_local+1 are the Dirichlet ring.
+ *   comm set  rank-local row slab of a global grid; halo = ghost depth
+ *             (>= max(1, tblock)); ghost rows are refreshed from the
+ *             neighbouring ranks every `halo` sweeps, overlapped with interior
+ *             rows. On the first/last rank the ghost row adjacent to the owned
+ *             rows holds the global Dirichlet row. Requires ny_local >= halo.
+ *   iters     >= 0; 0 is a no-op.
+ *   tblock    0 = auto; 1 = one sweep per pass over HBM; T >= 2 = temporal
+ *             blocking (T sweeps per pass). Any choice gives bitwise the same
+ *             result.
+ *   *result_in_b (may be NULL) set to 1 if the result is in b (iters odd),
+ *             else 0. The other buffer's interior is unspecified afterwards.
+ */
+st_status st_jacobi2d_run(double* a, double* b, int64_t nx, int64_t ny_local, int64_t ld,
+                          int32_t halo, int64_t iters, int32_t tblock, st_comm* comm,
+                          void* cuda_stream, int32_t* result_in_b);
+
+/* ------------------------------------------------------------------------ */
+/* 3-D Piacsek-Williams advection                              */
+/* ------------------------------------------------------------------------ */
+
+/* One fused application of the three PW advection stencils (su from u, v, w;
+ * sv; sw — "three separate stencil computations across three fields ... fused
+ * into a single stencil region", 63 flops per cell), formula =
+ * DESIGN.md reading R6 (MONC pwadvection form). Overwrites the interior
+ * (1..nz_local, 1..ny, 1..nx) of su, sv, sw; never touches their halos.
+ *
+ *   u,v,w,su,sv,sw  (nz_local+2) planes x (ny+2) rows x ldx doubles each.
+ *                   su, sv, sw must not overlap each other or the inputs.
+ *                   Without comm u, v, w are read only and may alias each
+ *                   other; with comm their z-ghost planes are written and they
+ *                   must be distinct.
+ *   tcx, tcy        x/y coefficients (scalars).
+ *   tzc1..tzd2      nz_local+2 doubles each (device), indexed by local plane.
+ *   comm NULL       the halos of u, v, w are inputs.
+ *   comm set        rank-local z-slab; the z-ghost planes of u, v, w are first
+ *                   swapped with rank -/+ 1 (the PW halo swap "before the next
+ *                   timestep"), overlapped with interior planes.
+ */
+st_status st_pw_advect3d(double* u, double* v, double* w, double* su,
+                         double* sv, double* sw, int64_t nx, int64_t ny, int64_t nz_local,
+                         int64_t ldx, double tcx, double tcy, const double* tzc1,
+                         const double* tzc2, const double* tzd1, const double* tzd2,
+                         st_comm* comm, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LIBSTENCIL_H */

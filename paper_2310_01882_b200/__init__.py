@@ -1,0 +1,224 @@
+"""paper_2310_01882_b200 — B200-native stencil hot path (arXiv 2310.01882).
+
+Thin Python binding over the C ABI of ``libstencil.so`` (include/libstencil.h).
+It only marshals arguments: every step of the hot path runs in the library's
+sm_100a kernels. PyTorch supplies device memory, streams and process groups.
+
+The binding has no fallback: if ``libstencil.so`` is missing or fails to load,
+every entry point raises. It never imports the CPU oracle.
+
+Entry points (same names as the C ABI, tensors instead of raw pointers):
+    st_jacobi2d_run(a, b, iters, tblock=0, halo=1, comm=None, nx=None) -> result tensor
+    st_pw_advect3d(u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, tzd1, tzd2, comm=None, nx=None)
+    st_halo_exchange(comm, fields, n_slow_local, slab_pitch, width)
+    st_halo_plan(rank, nranks, n_slow_local, slab_pitch, width) -> (sends, recvs)   [host only]
+    st_block_split(n, nranks, rank) -> (start, count)                                [host only]
+    Comm.create(rank, nranks, unique_id, device) / Comm.from_process_group(pg, device)
+"""
+from __future__ import annotations
+
+import ctypes
+import pathlib
+
+_HERE = pathlib.Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libstencil.so"
+UNIQUE_ID_BYTES = 128
+
+ST_OK, ST_EINVAL, ST_ECUDA, ST_ENCCL, ST_ENOTSUP, ST_EINTERNAL = range(6)
+_STATUS = {1: "EINVAL", 2: "ECUDA", 3: "ENCCL", 4: "ENOTSUP", 5: "EINTERNAL"}
+
+_lib = None
+
+
+class StencilError(RuntimeError):
+    def __init__(self, code: int, fn: str, msg: str):
+        super().__init__(f"{fn}: ST_{_STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Xfer(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int32), ("offset", ctypes.c_int64), ("count", ctypes.c_int64)]
+
+
+_vp, _i64, _i32, _dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+
+_SIGS = {
+    "st_abi_version": (ctypes.c_int32, []),
+    "st_last_error": (ctypes.c_char_p, []),
+    "st_launch_count": (ctypes.c_uint64, []),
+    "st_comm_unique_id": (ctypes.c_int, [_vp]),
+    "st_comm_init": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, _i32, _vp, _i32]),
+    "st_comm_destroy": (ctypes.c_int, [_vp]),
+    "st_comm_query": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
+    "st_block_split": (ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "st_halo_plan": (ctypes.c_int, [_i32, _i32, _i64, _i64, _i32, ctypes.POINTER(Xfer),
+                                    ctypes.POINTER(_i32), ctypes.POINTER(Xfer), ctypes.POINTER(_i32)]),
+    "st_halo_exchange": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), _i32, _i64, _i64, _i32, _vp]),
+    "st_jacobi2d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i32, _i64, _i32, _vp, _vp,
+                                       ctypes.POINTER(_i32)]),
+    "st_pw_advect3d": (ctypes.c_int, [_vp] * 6 + [_i64] * 4 + [_dbl, _dbl] + [_vp] * 4 + [_vp, _vp]),
+}
+EXPORTS = tuple(_SIGS)
+
+
+def lib() -> ctypes.CDLL:
+    """Load libstencil.so (raises if it is not built — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"{LIB_PATH} is not built: run `make` (or __graft_entry__.build())")
+        handle = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        if handle.st_abi_version() != 1:
+            raise RuntimeError("libstencil ABI version mismatch")
+        _lib = handle
+    return _lib
+
+
+def _check(code: int, fn: str) -> None:
+    if code != ST_OK:
+        raise StencilError(code, fn, (lib().st_last_error() or b"").decode())
+
+
+def last_error() -> str:
+    return (lib().st_last_error() or b"").decode()
+
+
+def launch_count() -> int:
+    return int(lib().st_launch_count())
+
+
+def _stream_ptr(stream=None) -> int:
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def _f64_cuda(t, name: str):
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name}: expected a torch.Tensor")
+    if t.dtype != torch.float64 or not t.is_cuda:
+        raise TypeError(f"{name}: expected a float64 CUDA tensor, got {t.dtype} on {t.device}")
+
+
+# ----------------------------------------------------------------- comm ---
+class Comm:
+    """Owns an ``st_comm`` (NCCL communicator + comm stream) for one rank."""
+
+    def __init__(self, handle: int, rank: int, nranks: int, device: int):
+        self.handle = ctypes.c_void_p(handle)
+        self.rank, self.nranks, self.device = rank, nranks, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * UNIQUE_ID_BYTES)()
+        _check(lib().st_comm_unique_id(ctypes.cast(buf, _vp)), "st_comm_unique_id")
+        return bytes(buf)
+
+    @classmethod
+    def create(cls, rank: int, nranks: int, uid: bytes, device: int) -> "Comm":
+        assert len(uid) == UNIQUE_ID_BYTES
+        h = _vp()
+        buf = (ctypes.c_uint8 * UNIQUE_ID_BYTES).from_buffer_copy(uid)
+        _check(lib().st_comm_init(ctypes.byref(h), nranks, rank, ctypes.cast(buf, _vp), device), "st_comm_init")
+        return cls(h.value, rank, nranks, device)
+
+    @classmethod
+    def from_process_group(cls, device: int, group=None) -> "Comm":
+        """Collective: rank 0 creates the NCCL id and broadcasts it over torch.distributed."""
+        import torch.distributed as dist
+        rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls.create(rank, nranks, obj[0], device)
+
+    def close(self) -> None:
+        if self.handle:
+            _check(lib().st_comm_destroy(self.handle), "st_comm_destroy")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _comm_ptr(comm) -> _vp:
+    return None if comm is None else comm.handle
+
+
+# ------------------------------------------------------------- host-only ---
+def st_block_split(n: int, nranks: int, rank: int) -> tuple[int, int]:
+    s, c = _i64(), _i64()
+    _check(lib().st_block_split(n, nranks, rank, ctypes.byref(s), ctypes.byref(c)), "st_block_split")
+    return s.value, c.value
+
+
+def st_halo_plan(rank: int, nranks: int, n_slow_local: int, slab_pitch: int, width: int):
+    sends, recvs = (Xfer * 2)(), (Xfer * 2)()
+    ns, nr = _i32(), _i32()
+    _check(lib().st_halo_plan(rank, nranks, n_slow_local, slab_pitch, width, sends, ctypes.byref(ns),
+                              recvs, ctypes.byref(nr)), "st_halo_plan")
+    conv = lambda x: (x.peer, x.offset, x.count)
+    return [conv(sends[i]) for i in range(ns.value)], [conv(recvs[i]) for i in range(nr.value)]
+
+
+# ------------------------------------------------------------- compute ---
+def st_jacobi2d_run(a, b, iters: int, tblock: int = 0, halo: int = 1, comm: Comm | None = None,
+                    nx: int | None = None, stream=None):
+    """`iters` Jacobi sweeps on (rows, ld) float64 CUDA tensors a, b.
+
+    a, b: (ny_local + 2*halo, ld) row-major; nx defaults to ld - 2. Returns the
+    tensor holding the result (b iff iters is odd)."""
+    _f64_cuda(a, "a")
+    _f64_cuda(b, "b")
+    if a.dim() != 2 or a.shape != b.shape or a.stride(1) != 1 or b.stride(1) != 1 or a.stride(0) != b.stride(0):
+        raise ValueError("a, b: 2-D row-major tensors of equal shape and row pitch")
+    ld = a.stride(0)
+    nx = a.shape[1] - 2 if nx is None else nx
+    ny = a.shape[0] - 2 * halo
+    rib = _i32()
+    _check(lib().st_jacobi2d_run(a.data_ptr(), b.data_ptr(), nx, ny, ld, halo, iters, tblock,
+                                 _comm_ptr(comm), _stream_ptr(stream), ctypes.byref(rib)), "st_jacobi2d_run")
+    return b if rib.value else a
+
+
+def st_pw_advect3d(u, v, w, su, sv, sw, tcx: float, tcy: float, tzc1, tzc2, tzd1, tzd2,
+                   comm: Comm | None = None, nx: int | None = None, stream=None) -> None:
+    """Fused PW advection on (nz+2, ny+2, ldx) float64 CUDA tensors."""
+    fields = (u, v, w, su, sv, sw)
+    for t, name in zip(fields, ("u", "v", "w", "su", "sv", "sw")):
+        _f64_cuda(t, name)
+        if t.dim() != 3 or t.shape != u.shape or t.stride() != u.stride() or t.stride(2) != 1:
+            raise ValueError(f"{name}: 3-D (planes, rows, ldx) tensor like u")
+        if t.stride(1) != t.shape[2] or t.stride(0) != t.shape[1] * t.shape[2]:
+            raise ValueError(f"{name}: must be contiguous (pitch = shape[2])")
+    coefs = (tzc1, tzc2, tzd1, tzd2)
+    for t, name in zip(coefs, ("tzc1", "tzc2", "tzd1", "tzd2")):
+        _f64_cuda(t, name)
+        if t.dim() != 1 or t.shape[0] != u.shape[0] or not t.is_contiguous():
+            raise ValueError(f"{name}: contiguous vector of nz+2 doubles")
+    nz, ny, ldx = u.shape[0] - 2, u.shape[1] - 2, u.shape[2]
+    nx = ldx - 2 if nx is None else nx
+    _check(lib().st_pw_advect3d(*[t.data_ptr() for t in fields], nx, ny, nz, ldx, float(tcx), float(tcy),
+                                *[t.data_ptr() for t in coefs], _comm_ptr(comm), _stream_ptr(stream)),
+           "st_pw_advect3d")
+
+
+def st_halo_exchange(comm: Comm, fields, n_slow_local: int, slab_pitch: int, width: int, stream=None) -> None:
+    for i, t in enumerate(fields):
+        _f64_cuda(t, f"fields[{i}]")
+    arr = (_vp * len(fields))(*[t.data_ptr() for t in fields])
+    _check(lib().st_halo_exchange(comm.handle, arr, len(fields), n_slow_local, slab_pitch, width,
+                                  _stream_ptr(stream)), "st_halo_exchange")
+
+
+# Friendlier aliases
+jacobi2d = st_jacobi2d_run
+pw_advect3d = st_pw_advect3d
+halo_exchange = st_halo_exchange

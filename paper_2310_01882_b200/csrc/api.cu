@@ -1,0 +1,290 @@
+// api.cu — the C ABI of libstencil (include/libstencil.h): argument validation,
+// launch orchestration and error state. Every compute step runs in this
+// library's own kernels (jacobi2d.cu, pw_advect3d.cu); there is no CPU path.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "comm.h"
+#include "common.cuh"
+#include "internal.h"
+#include "tma.cuh"
+
+namespace st {
+
+namespace {
+thread_local char g_err[512] = {0};
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+void clear_error() { g_err[0] = 0; }
+const char* g_err_ptr() { return g_err; }
+std::atomic<uint64_t>& launch_counter() { return g_launches; }
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::atoi(v);
+}
+
+// ------------------------------------------------------------- TMA host ---
+st_status get_encode_tiled(PFN_encodeTiled* fn) {
+  static PFN_encodeTiled cached = nullptr;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  static cudaDriverEntryPointQueryResult qres = cudaDriverEntryPointSuccess;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qres);
+    cached = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  ST_RETURN_IF(err != cudaSuccess || qres != cudaDriverEntryPointSuccess || !cached, ST_ECUDA,
+               "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(err));
+  *fn = cached;
+  return ST_OK;
+}
+
+st_status make_tmap_3d_f64(CUtensorMap* map, const double* base, const uint64_t dims[3],
+                           uint64_t pitch_y_bytes, uint64_t pitch_z_bytes, const uint32_t box[3]) {
+  PFN_encodeTiled enc;
+  ST_TRY(get_encode_tiled(&enc));
+  const cuuint64_t gdim[3] = {dims[0], dims[1], dims[2]};
+  const cuuint64_t gstride[2] = {pitch_y_bytes, pitch_z_bytes};
+  const cuuint32_t bx[3] = {box[0], box[1], box[2]};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), gdim, gstride,
+                   bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  ST_RETURN_IF(r != CUDA_SUCCESS, ST_ECUDA, "cuTensorMapEncodeTiled(3d) failed: %d", (int)r);
+  return ST_OK;
+}
+
+st_status make_tmap_2d_f64(CUtensorMap* map, const double* base, const uint64_t dims[2],
+                           uint64_t pitch_bytes, const uint32_t box[2]) {
+  PFN_encodeTiled enc;
+  ST_TRY(get_encode_tiled(&enc));
+  const cuuint64_t gdim[2] = {dims[0], dims[1]};
+  const cuuint64_t gstride[1] = {pitch_bytes};
+  const cuuint32_t bx[2] = {box[0], box[1]};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride,
+                   bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  ST_RETURN_IF(r != CUDA_SUCCESS, ST_ECUDA, "cuTensorMapEncodeTiled(2d) failed: %d", (int)r);
+  return ST_OK;
+}
+
+// ------------------------------------------------------- Jacobi driver ---
+namespace {
+
+st_status check_device_ptr(const void* p, const char* what) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("%s: cudaPointerGetAttributes -> %s", what, cudaGetErrorString(e));
+    return ST_EINVAL;
+  }
+  ST_RETURN_IF(at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged, ST_EINVAL,
+               "%s is not a device pointer", what);
+  return ST_OK;
+}
+
+// Split `iters` sweeps into passes of at most T sweeps such that the number of
+// passes has the parity of `iters`: every pass reads one buffer and writes the
+// other, so the result lands where plain Jacobi ping-pong puts it (b iff iters odd).
+int plan_passes(int64_t iters, int t, int64_t* out, int cap) {
+  int n = 0;
+  if (t <= 1) return -1;
+  int64_t left = iters;
+  while (left >= t && n < cap) { out[n++] = t; left -= t; }
+  while (left > 0 && n < cap) {
+    const int64_t k = left >= 2 ? left : 1;  // a remainder r < T is one pass of r sweeps
+    out[n++] = k;
+    left -= k;
+  }
+  if ((n & 1) != (int)(iters & 1)) {
+    // flip the parity: split one pass of k >= 2 sweeps into (k-1) + 1
+    for (int i = 0; i < n; ++i) {
+      if (out[i] >= 2) {
+        for (int j = n; j > i + 1; --j) out[j] = out[j - 1];
+        out[i + 1] = 1;
+        out[i] -= 1;
+        ++n;
+        break;
+      }
+    }
+  }
+  return n;
+}
+
+st_status one_pass(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
+                   int64_t sweeps, int64_t ring_lo, int64_t ring_hi, cudaStream_t s) {
+  if (sweeps == 1) return jacobi2d_sweep_rows(src, dst, nx, ld, y_lo, y_hi, s);
+  return jacobi2d_tb_rows(src, dst, nx, ld, y_lo, y_hi, (int)sweeps, ring_lo, ring_hi, s);
+}
+
+// Single-domain run (no comm): halo == 1, rows 0 and ny+1 Dirichlet.
+st_status jacobi2d_single(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t iters,
+                          int32_t tblock, cudaStream_t s) {
+  if (tblock == 0 && jacobi2d_resident_fits(nx, ny)) return jacobi2d_resident(a, b, nx, ny, ld, iters, s);
+  // halo rows a -> b (ring columns are passed through by every sweep)
+  ST_CHECK_CUDA(cudaMemcpyAsync(b, a, (size_t)ld * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  ST_CHECK_CUDA(cudaMemcpyAsync(b + (ny + 1) * ld, a + (ny + 1) * ld, (size_t)ld * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+  int t = tblock;
+  if (t == 0) t = env_int("ST_JACOBI_T", 1);
+  if (t > 1 && !jacobi2d_tb_supported(t)) {
+    ST_RETURN_IF(tblock != 0, ST_ENOTSUP, "jacobi2d: tblock=%d not supported by this build", tblock);
+    t = 1;
+  }
+  double* src = a;
+  double* dst = b;
+  if (t <= 1) {
+    for (int64_t it = 0; it < iters; ++it) {
+      ST_TRY(jacobi2d_sweep_rows(src, dst, nx, ld, 1, ny, s));
+      double* tmp = src; src = dst; dst = tmp;
+    }
+    return ST_OK;
+  }
+  int64_t pass[64];
+  int64_t done = 0;
+  while (done < iters) {
+    // plan in blocks so the pass list stays bounded; each block keeps parity
+    const int64_t blk = std::min<int64_t>(iters - done, (int64_t)t * 48);
+    const int n = plan_passes(blk, t, pass, 64);
+    ST_RETURN_IF(n < 0, ST_EINTERNAL, "jacobi2d: pass planning failed");
+    for (int i = 0; i < n; ++i) {
+      ST_TRY(one_pass(src, dst, nx, ld, 1, ny, pass[i], 0, ny + 1, s));
+      double* tmp = src; src = dst; dst = tmp;
+    }
+    done += blk;
+  }
+  return ST_OK;
+}
+
+// Rank-local slab run: ghost depth h, ghosts swapped every h sweeps.
+st_status jacobi2d_slab(st_comm* comm, double* a, double* b, int64_t nx, int64_t n, int64_t ld,
+                        int32_t h, int64_t iters, cudaStream_t s) {
+  const bool lo_edge = comm->rank == 0, hi_edge = comm->rank == comm->nranks - 1;
+  const size_t hbytes = (size_t)h * (size_t)ld * sizeof(double);
+  // all ghost rows (incl. the edge ranks' Dirichlet row) a -> b
+  ST_CHECK_CUDA(cudaMemcpyAsync(b, a, hbytes, cudaMemcpyDeviceToDevice, s));
+  ST_CHECK_CUDA(cudaMemcpyAsync(b + (h + n) * ld, a + (h + n) * ld, hbytes, cudaMemcpyDeviceToDevice, s));
+  double* src = a;
+  double* dst = b;
+  // the initial state's ghosts come from the neighbours
+  ST_TRY(halo_exchange_async(comm, &src, 1, n, ld, h, s, true));
+  if (h == 1) {
+    // boundary rows first, their swap overlaps the interior rows
+    for (int64_t it = 0; it < iters; ++it) {
+      ST_TRY(jacobi2d_sweep_rows(src, dst, nx, ld, 1, 1, s));
+      if (n >= 2) ST_TRY(jacobi2d_sweep_rows(src, dst, nx, ld, n, n, s));
+      ST_TRY(halo_exchange_async(comm, &dst, 1, n, ld, 1, s, false));
+      ST_TRY(jacobi2d_sweep_rows(src, dst, nx, ld, 2, n - 1, s));
+      if (comm->nranks > 1) ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
+      double* tmp = src; src = dst; dst = tmp;
+    }
+    return ST_OK;
+  }
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t k = it % h;
+    if (k == 0 && it > 0) ST_TRY(halo_exchange_async(comm, &src, 1, n, ld, h, s, true));
+    const int64_t lo = lo_edge ? h : k + 1;
+    const int64_t hi = hi_edge ? h + n - 1 : 2 * h + n - 2 - k;
+    ST_TRY(jacobi2d_sweep_rows(src, dst, nx, ld, lo, hi, s));
+    double* tmp = src; src = dst; dst = tmp;
+  }
+  return ST_OK;
+}
+
+}  // namespace
+}  // namespace st
+
+using namespace st;
+
+extern "C" {
+
+int32_t st_abi_version(void) { return ST_ABI_VERSION; }
+
+const char* st_last_error(void) { return g_err_ptr(); }
+
+uint64_t st_launch_count(void) { return launch_counter().load(); }
+
+st_status st_jacobi2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int32_t halo,
+                          int64_t iters, int32_t tblock, st_comm* comm, void* cuda_stream,
+                          int32_t* result_in_b) {
+  clear_error();
+  ST_RETURN_IF(!a || !b, ST_EINVAL, "st_jacobi2d_run: null field pointer");
+  ST_RETURN_IF(nx < 1 || ny < 1, ST_EINVAL, "st_jacobi2d_run: empty interior (nx=%lld, ny=%lld)",
+               (long long)nx, (long long)ny);
+  ST_RETURN_IF(ld < nx + 2 || (ld & 1), ST_EINVAL, "st_jacobi2d_run: ld=%lld must be even and >= nx+2",
+               (long long)ld);
+  ST_RETURN_IF(!aligned16(a) || !aligned16(b), ST_EINVAL, "st_jacobi2d_run: fields must be 16-byte aligned");
+  ST_RETURN_IF(iters < 0 || tblock < 0 || halo < 1, ST_EINVAL,
+               "st_jacobi2d_run: iters=%lld tblock=%d halo=%d", (long long)iters, tblock, halo);
+  ST_RETURN_IF(!comm && halo != 1, ST_EINVAL, "st_jacobi2d_run: halo must be 1 without a comm");
+  ST_RETURN_IF(comm && ny < halo, ST_EINVAL, "st_jacobi2d_run: slab of %lld rows < halo %d",
+               (long long)ny, halo);
+  ST_RETURN_IF(comm && tblock > 1, ST_ENOTSUP, "st_jacobi2d_run: temporal blocking across ranks not built");
+  const size_t bytes = (size_t)(ny + 2 * halo) * (size_t)ld * sizeof(double);
+  ST_RETURN_IF(overlaps(a, bytes, b, bytes), ST_EINVAL, "st_jacobi2d_run: a and b overlap");
+  ST_TRY(check_device_ptr(a, "a"));
+  ST_TRY(check_device_ptr(b, "b"));
+  if (result_in_b) *result_in_b = (int32_t)(iters & 1);
+  if (iters == 0) return ST_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  if (!comm) return jacobi2d_single(a, b, nx, ny, ld, iters, tblock, s);
+  ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier NCCL error");
+  return jacobi2d_slab(comm, a, b, nx, ny, ld, halo, iters, s);
+}
+
+st_status st_pw_advect3d(double* u, double* v, double* w, double* su, double* sv, double* sw,
+                         int64_t nx, int64_t ny, int64_t nz, int64_t ldx, double tcx, double tcy,
+                         const double* tzc1, const double* tzc2, const double* tzd1,
+                         const double* tzd2, st_comm* comm, void* cuda_stream) {
+  clear_error();
+  const double* f[6] = {u, v, w, su, sv, sw};
+  for (int i = 0; i < 6; ++i) {
+    ST_RETURN_IF(!f[i], ST_EINVAL, "st_pw_advect3d: null field %d", i);
+    ST_RETURN_IF(!aligned16(f[i]), ST_EINVAL, "st_pw_advect3d: field %d not 16-byte aligned", i);
+  }
+  ST_RETURN_IF(!tzc1 || !tzc2 || !tzd1 || !tzd2, ST_EINVAL, "st_pw_advect3d: null coefficient array");
+  ST_RETURN_IF(nx < 1 || ny < 1 || nz < 1, ST_EINVAL, "st_pw_advect3d: empty interior");
+  ST_RETURN_IF(ldx < nx + 2 || (ldx & 1), ST_EINVAL, "st_pw_advect3d: ldx=%lld must be even and >= nx+2",
+               (long long)ldx);
+  ST_RETURN_IF(nx + 2 > (int64_t)INT32_MAX || ny + 2 > (int64_t)INT32_MAX || nz + 2 > (int64_t)INT32_MAX,
+               ST_EINVAL, "st_pw_advect3d: extents exceed TMA coordinate range");
+  const size_t bytes = (size_t)(nz + 2) * (size_t)(ny + 2) * (size_t)ldx * sizeof(double);
+  for (int o = 3; o < 6; ++o)
+    for (int i = 0; i < 6; ++i)
+      if (i != o)
+        ST_RETURN_IF(overlaps(f[o], bytes, f[i], bytes), ST_EINVAL,
+                     "st_pw_advect3d: output %d overlaps field %d", o, i);
+  if (comm)
+    ST_RETURN_IF(overlaps(u, bytes, v, bytes) || overlaps(u, bytes, w, bytes) || overlaps(v, bytes, w, bytes),
+                 ST_EINVAL, "st_pw_advect3d: u, v, w must be distinct with a comm");
+  for (int i = 0; i < 6; ++i) ST_TRY(check_device_ptr(f[i], "st_pw_advect3d field"));
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  PwArgs args{u, v, w, su, sv, sw, nx, ny, nz, ldx, tcx, tcy, tzc1, tzc2, tzd1, tzd2};
+  if (!comm || comm->nranks == 1) return pw_advect3d_planes(args, 1, nz, s);
+  ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier NCCL error");
+  // ghost planes of u, v, w in flight while the planes that do not read them are computed
+  double* fields[3] = {u, v, w};
+  const int64_t plane = (ny + 2) * ldx;
+  ST_TRY(halo_exchange_async(comm, fields, 3, nz, plane, 1, s, false));
+  ST_TRY(pw_advect3d_planes(args, 2, nz - 1, s));
+  ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
+  ST_TRY(pw_advect3d_planes(args, 1, 1, s));
+  if (nz >= 2) ST_TRY(pw_advect3d_planes(args, nz, nz, s));
+  return ST_OK;
+}
+
+}  // extern "C"

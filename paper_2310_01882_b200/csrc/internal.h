@@ -1,0 +1,50 @@
+// internal.h — launchers shared between the C-ABI layer (api.cu, comm.cu) and
+// the kernel translation units. Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "libstencil.h"
+
+namespace st {
+
+// ----------------------------------------------------------- Jacobi 2-D ---
+// One sweep dst = J(src) over buffer rows [y_lo, y_hi] (buffer row indices,
+// inclusive) and interior columns 1..nx; columns 0 and nx+1 are passed through
+// (dst = src) so the Dirichlet ring is preserved bit for bit. Rows outside the
+// range are neither read (except y_lo-1 and y_hi+1) nor written.
+st_status jacobi2d_sweep_rows(const double* src, double* dst, int64_t nx, int64_t ld,
+                              int64_t y_lo, int64_t y_hi, cudaStream_t s);
+
+// `iters` sweeps entirely inside one CTA's shared memory (small grids: both
+// buffers fit in SMEM). Writes the final state (whole (ny+2) x (nx+2) window)
+// into a (iters even) or b (iters odd).
+bool jacobi2d_resident_fits(int64_t nx, int64_t ny);
+st_status jacobi2d_resident(double* a, double* b, int64_t nx, int64_t ny, int64_t ld,
+                            int64_t iters, cudaStream_t s);
+
+// Temporal blocking: T sweeps per pass over HBM, rows [y_lo, y_hi] of dst
+// (src rows y_lo-T .. y_hi+T must be valid; intermediate levels are computed
+// redundantly on a shrinking halo and never stored). `ring_lo`/`ring_hi`
+// are buffer rows that are Dirichlet (never updated at any level), or -1.
+bool jacobi2d_tb_supported(int t);
+st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t ld,
+                           int64_t y_lo, int64_t y_hi, int t, int64_t ring_lo,
+                           int64_t ring_hi, cudaStream_t s);
+
+// ------------------------------------------------------------ PW 3-D ---
+struct PwArgs {
+  const double *u, *v, *w;
+  double *su, *sv, *sw;
+  int64_t nx, ny, nz, ldx;
+  double tcx, tcy;
+  const double *tzc1, *tzc2, *tzd1, *tzd2;
+};
+// Computes output planes [z_lo, z_hi] (local plane indices, 1-based interior).
+st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s);
+
+// --------------------------------------------------------------- misc ---
+int env_int(const char* name, int dflt);
+
+}  // namespace st

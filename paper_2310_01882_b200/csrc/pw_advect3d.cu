@@ -1,0 +1,267 @@
+// pw_advect3d.cu — fused Piacsek-Williams advection, 2.5-D z-streaming, sm_100a.
+//
+// Operation: PAPER.md:216 ("three separate stencil computations across three
+// fields which are then fused ... into a single stencil region", 63 flops per
+// cell), formula and association trees = DESIGN.md reading R6 (MONC
+// pwadvection form); every binary op rounds once.
+//
+// Design (HBM-bound: 48 algorithmic bytes per point, 63 fp64 flops):
+//  * A CTA owns a 64(x) x BY(y) column of the domain and streams a chunk of
+//    z planes. Each input plane (u, v, w with a 1-row / 2-column apron) is
+//    brought into a shared-memory ring of S plane slots by three TMA tile loads
+//    (cp.async.bulk.tensor.3d) issued by one thread and completed on an
+//    mbarrier; S-3 planes are in flight while the CTA computes.
+//  * A thread owns a 16-byte column pair at one row; its own column of u, v, w
+//    at planes z-1, z, z+1 rides in a register queue, in-plane and cross-plane
+//    neighbours are read from the ring. Outputs go straight to HBM as 16-byte
+//    stores (halo cells of su, sv, sw are never written).
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+#include "tma.cuh"
+
+namespace st {
+
+namespace {
+
+constexpr int kBX = 64;       // interior columns per tile (32 lanes x 2)
+constexpr int kSX = kBX + 4;  // smem row: 2-column apron each side (keeps pairs 16-byte aligned)
+
+template <int BY>
+struct PwTile {
+  static constexpr int SY = BY + 2;
+  static constexpr int kPlaneElems = kSX * SY;
+  static constexpr int kPlaneBytes = kPlaneElems * 8;
+  static constexpr int kPlaneStride = ((kPlaneBytes + 127) / 128) * 128 / 8;  // doubles
+  static constexpr int kSlotStride = 3 * kPlaneStride;                        // u, v, w
+  static constexpr uint32_t kTxBytes = 3u * kPlaneBytes;
+};
+
+// The 27 input values one output point reads (names: field_offset; c = centre,
+// w/e = x-1/x+1, n/s = y-1/y+1, m/p = z-1/z+1, combined offsets spelled out).
+struct PwPoint {
+  double uc, uw, ue, un, us, um, up, u_sw, u_pw;   // u_sw = U(0,+1,-1), u_pw = U(+1,0,-1)
+  double vc, vw, ve, vn, vs, vm, vp, v_ne, v_pn;   // v_ne = V(0,-1,+1), v_pn = V(+1,-1,0)
+  double wc, ww, we, wn, ws, wm, wp, w_me, w_ms;   // w_me = W(-1,0,+1), w_ms = W(-1,+1,0)
+};
+
+struct PwCoef {
+  double tcx, tcy, c1, c2, d1, d2;
+};
+
+// DESIGN.md R6; operand order mirrors the paper reading, grouping is what matters.
+__device__ __forceinline__ void pw_point(const PwPoint& p, const PwCoef& k, double& su, double& sv,
+                                         double& sw) {
+  double t1, t2, xs, ys, zs;
+  t1 = dmul(p.uw, dadd(p.uc, p.uw));
+  t2 = dmul(p.ue, dadd(p.uc, p.ue));
+  xs = dmul(k.tcx, dsub(t1, t2));
+  t1 = dmul(p.un, dadd(p.vn, p.v_ne));
+  t2 = dmul(p.us, dadd(p.vc, p.ve));
+  ys = dmul(k.tcy, dsub(t1, t2));
+  t1 = dmul(dmul(k.c1, p.um), dadd(p.wm, p.w_me));
+  t2 = dmul(dmul(k.c2, p.up), dadd(p.wc, p.we));
+  zs = dsub(t1, t2);
+  su = dadd(dadd(xs, ys), zs);
+
+  t1 = dmul(p.vw, dadd(p.uw, p.u_sw));
+  t2 = dmul(p.ve, dadd(p.uc, p.us));
+  xs = dmul(k.tcx, dsub(t1, t2));
+  t1 = dmul(p.vn, dadd(p.vc, p.vn));
+  t2 = dmul(p.vs, dadd(p.vc, p.vs));
+  ys = dmul(k.tcy, dsub(t1, t2));
+  t1 = dmul(dmul(k.c1, p.vm), dadd(p.wm, p.w_ms));
+  t2 = dmul(dmul(k.c2, p.vp), dadd(p.wc, p.ws));
+  zs = dsub(t1, t2);
+  sv = dadd(dadd(xs, ys), zs);
+
+  t1 = dmul(p.ww, dadd(p.uw, p.u_pw));
+  t2 = dmul(p.we, dadd(p.uc, p.up));
+  xs = dmul(k.tcx, dsub(t1, t2));
+  t1 = dmul(p.wn, dadd(p.vn, p.v_pn));
+  t2 = dmul(p.ws, dadd(p.vc, p.vp));
+  ys = dmul(k.tcy, dsub(t1, t2));
+  t1 = dmul(dmul(k.d1, p.wm), dadd(p.wc, p.wm));
+  t2 = dmul(dmul(k.d2, p.wp), dadd(p.wc, p.wp));
+  zs = dsub(t1, t2);
+  sw = dadd(dadd(xs, ys), zs);
+}
+
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
+template <int BY, int S>
+__global__ void __launch_bounds__(32 * BY)
+    pw_advect3d_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_v,
+                       const __grid_constant__ CUtensorMap tm_w, double* __restrict__ su,
+                       double* __restrict__ sv, double* __restrict__ sw, int64_t nx, int64_t ny,
+                       int64_t ldx, double tcx, double tcy, const double* __restrict__ tzc1,
+                       const double* __restrict__ tzc2, const double* __restrict__ tzd1,
+                       const double* __restrict__ tzd2, int64_t z_lo, int64_t z_hi,
+                       int64_t planes_per_chunk) {
+  using T = PwTile<BY>;
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[S];
+
+  const int lane = threadIdx.x & 31;
+  const int wy = threadIdx.x >> 5;
+  const int64_t x0 = (int64_t)blockIdx.x * kBX;  // padded x of the tile's first pair
+  const int64_t y0 = 1 + (int64_t)blockIdx.y * BY;
+  const int64_t za = z_lo + (int64_t)blockIdx.z * planes_per_chunk;
+  const int64_t zb = min(z_hi, za + planes_per_chunk - 1);
+  const int np = (int)(zb - za + 3);  // input planes za-1 .. zb+1
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm_u);
+    tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_w);
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int p) {  // input plane za-1+p -> slot p % S
+    double* slot = ring + (p % S) * T::kSlotStride;
+    uint64_t* bar = &full[p % S];
+    mbar_arrive_expect_tx(bar, T::kTxBytes);
+    const int32_t cx = (int32_t)(x0 - 2), cy = (int32_t)(y0 - 1), cz = (int32_t)(za - 1 + p);
+    tma_load_3d(slot, &tm_u, cx, cy, cz, bar);
+    tma_load_3d(slot + T::kPlaneStride, &tm_v, cx, cy, cz, bar);
+    tma_load_3d(slot + 2 * T::kPlaneStride, &tm_w, cx, cy, cz, bar);
+  };
+  if (threadIdx.x == 0)
+    for (int p = 0; p < S && p < np; ++p) issue(p);
+
+  // Thread geometry inside a plane slot: smem row r = wy+1, column c = 2*lane+2.
+  const int r = wy + 1;
+  const int c = 2 * lane + 2;
+  const int oc = r * kSX + c;  // own pair offset inside a field plane
+  const int64_t y = y0 + wy;
+  const int64_t x = x0 + 2 * lane;
+  const bool row_ok = y <= ny;
+  const bool ok0 = x >= 1 && x <= nx;
+  const bool ok1 = x + 1 >= 1 && x + 1 <= nx;
+
+  auto field = [&](int p, int f) -> const double* {
+    return ring + (p % S) * T::kSlotStride + f * T::kPlaneStride;
+  };
+  auto wait = [&](int p) { mbar_wait_parity(&full[p % S], (uint32_t)((p / S) & 1)); };
+
+  // register queue: own pairs at planes z-1 (m) and z (c)
+  wait(0);
+  wait(1);
+  double2 um = lds2(field(0, 0) + oc), vm = lds2(field(0, 1) + oc), wm = lds2(field(0, 2) + oc);
+  double2 uc = lds2(field(1, 0) + oc), vc = lds2(field(1, 1) + oc), wc = lds2(field(1, 2) + oc);
+
+  for (int j = 0; j + 2 < np; ++j) {  // output plane z = za + j, input planes j, j+1, j+2
+    const int64_t z = za + j;
+    wait(j + 2);
+    const double* U0 = field(j + 1, 0);
+    const double* V0 = field(j + 1, 1);
+    const double* W0 = field(j + 1, 2);
+    const double* Up = field(j + 2, 0);
+    const double* Vp = field(j + 2, 1);
+    const double* Wp = field(j + 2, 2);
+    const double* Wm = field(j, 2);
+
+    const double2 up = lds2(Up + oc), vp = lds2(Vp + oc), wp = lds2(Wp + oc);
+    const double2 un = lds2(U0 + oc - kSX), us = lds2(U0 + oc + kSX);
+    const double2 vn = lds2(V0 + oc - kSX), vs = lds2(V0 + oc + kSX);
+    const double2 wn = lds2(W0 + oc - kSX), ws = lds2(W0 + oc + kSX);
+    const double u_xw = U0[oc - 1], u_xe = U0[oc + 2];
+    const double v_xw = V0[oc - 1], v_xe = V0[oc + 2];
+    const double w_xw = W0[oc - 1], w_xe = W0[oc + 2];
+    const double u_sw0 = U0[oc + kSX - 1];   // U(0,+1,-1) for point 0
+    const double v_ne1 = V0[oc - kSX + 2];   // V(0,-1,+1) for point 1
+    const double u_pw0 = Up[oc - 1];         // U(+1,0,-1) for point 0
+    const double2 vpn = lds2(Vp + oc - kSX); // V(+1,-1,0)
+    const double w_me1 = Wm[oc + 2];         // W(-1,0,+1) for point 1
+    const double2 wms = lds2(Wm + oc + kSX); // W(-1,+1,0)
+
+    const PwCoef k = {tcx, tcy, __ldg(tzc1 + z), __ldg(tzc2 + z), __ldg(tzd1 + z), __ldg(tzd2 + z)};
+    PwPoint p0, p1;
+    p0.uc = uc.x; p0.uw = u_xw; p0.ue = uc.y; p0.un = un.x; p0.us = us.x; p0.um = um.x; p0.up = up.x;
+    p0.u_sw = u_sw0; p0.u_pw = u_pw0;
+    p0.vc = vc.x; p0.vw = v_xw; p0.ve = vc.y; p0.vn = vn.x; p0.vs = vs.x; p0.vm = vm.x; p0.vp = vp.x;
+    p0.v_ne = vn.y; p0.v_pn = vpn.x;
+    p0.wc = wc.x; p0.ww = w_xw; p0.we = wc.y; p0.wn = wn.x; p0.ws = ws.x; p0.wm = wm.x; p0.wp = wp.x;
+    p0.w_me = wm.y; p0.w_ms = wms.x;
+
+    p1.uc = uc.y; p1.uw = uc.x; p1.ue = u_xe; p1.un = un.y; p1.us = us.y; p1.um = um.y; p1.up = up.y;
+    p1.u_sw = us.x; p1.u_pw = up.x;
+    p1.vc = vc.y; p1.vw = vc.x; p1.ve = v_xe; p1.vn = vn.y; p1.vs = vs.y; p1.vm = vm.y; p1.vp = vp.y;
+    p1.v_ne = v_ne1; p1.v_pn = vpn.y;
+    p1.wc = wc.y; p1.ww = wc.x; p1.we = w_xe; p1.wn = wn.y; p1.ws = ws.y; p1.wm = wm.y; p1.wp = wp.y;
+    p1.w_me = w_me1; p1.w_ms = wms.y;
+
+    double2 ou, ov, ow;
+    pw_point(p0, k, ou.x, ov.x, ow.x);
+    pw_point(p1, k, ou.y, ov.y, ow.y);
+
+    if (row_ok) {
+      const int64_t g = (z * (ny + 2) + y) * ldx + x;
+      if (ok0 && ok1) {
+        stg2(su + g, ou);
+        stg2(sv + g, ov);
+        stg2(sw + g, ow);
+      } else if (ok0) {
+        su[g] = ou.x; sv[g] = ov.x; sw[g] = ow.x;
+      } else if (ok1) {
+        su[g + 1] = ou.y; sv[g + 1] = ov.y; sw[g + 1] = ow.y;
+      }
+    }
+
+    um = uc; vm = vc; wm = wc;
+    uc = up; vc = vp; wc = wp;
+
+    // all reads of input plane j are done -> refill its slot with plane j+S
+    __syncthreads();
+    if (threadIdx.x == 0 && j + S < np) {
+      fence_proxy_async_smem();
+      issue(j + S);
+    }
+  }
+}
+
+template <int BY, int S>
+st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s) {
+  using T = PwTile<BY>;
+  CUtensorMap tm[3];
+  const double* f[3] = {a.u, a.v, a.w};
+  const uint64_t dims[3] = {(uint64_t)(a.nx + 2), (uint64_t)(a.ny + 2), (uint64_t)(a.nz + 2)};
+  const uint32_t box[3] = {(uint32_t)kSX, (uint32_t)T::SY, 1u};
+  for (int i = 0; i < 3; ++i)
+    ST_TRY(make_tmap_3d_f64(&tm[i], f[i], dims, (uint64_t)a.ldx * 8,
+                            (uint64_t)a.ldx * 8 * (uint64_t)(a.ny + 2), box));
+  const size_t smem = (size_t)S * T::kSlotStride * sizeof(double);
+  ST_CHECK_CUDA(cudaFuncSetAttribute(pw_advect3d_kernel<BY, S>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t ntx = (a.nx + 2 + kBX - 1) / kBX;
+  const int64_t nty = (a.ny + BY - 1) / BY;
+  const int64_t nz = z_hi - z_lo + 1;
+  static const int kPpc = env_int("ST_PW_PLANES", 64);
+  const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(kPpc, nz));
+  const int64_t nzc = (nz + ppc - 1) / ppc;
+  ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "pw_advect3d: grid too large");
+  dim3 grid((unsigned)ntx, (unsigned)nty, (unsigned)nzc);
+  pw_advect3d_kernel<BY, S><<<grid, 32 * BY, smem, s>>>(tm[0], tm[1], tm[2], a.su, a.sv, a.sw, a.nx,
+                                                        a.ny, a.ldx, a.tcx, a.tcy, a.tzc1, a.tzc2,
+                                                        a.tzd1, a.tzd2, z_lo, z_hi, ppc);
+  ST_LAUNCHED();
+  return ST_OK;
+}
+
+}  // namespace
+
+st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s) {
+  if (z_hi < z_lo) return ST_OK;
+  static const int kVariant = env_int("ST_PW_VARIANT", 0);
+  switch (kVariant) {
+    case 1: return launch_pw<8, 5>(a, z_lo, z_hi, s);
+    case 2: return launch_pw<16, 4>(a, z_lo, z_hi, s);
+    case 3: return launch_pw<4, 5>(a, z_lo, z_hi, s);
+    default: return launch_pw<8, 4>(a, z_lo, z_hi, s);
+  }
+}
+
+}  // namespace st

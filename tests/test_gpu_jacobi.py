@@ -1,0 +1,119 @@
+"""GPU parity of st_jacobi2d_run against the CPU oracle (bitwise).
+
+The CUDA path evaluates ((N+S)+W)+E then *0.25 with one rounding per op and
+no contraction, exactly like the oracle, so the bar is bit-exact equality
+(stricter than north_star's 1e-12 relative tolerance)."""
+import numpy as np
+import pytest
+
+import oracle
+import stencil_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+
+def run_gpu(st, a_np, iters, tblock=0, nx=None):
+    import torch
+    a = torch.from_numpy(a_np).cuda()
+    b = torch.empty_like(a)
+    b.fill_(float("nan"))  # the library must copy the ring itself
+    r = st.st_jacobi2d_run(a, b, iters, tblock=tblock, nx=nx)
+    torch.cuda.synchronize()
+    return r.cpu().numpy()
+
+
+def assert_bitwise(got, want):
+    assert got.shape == want.shape
+    bad = np.argwhere(got.view(np.uint64) != want.view(np.uint64))
+    assert bad.size == 0, f"{len(bad)} mismatches, first at {bad[:5].tolist()}: {got[tuple(bad[0])]} vs {want[tuple(bad[0])]}"
+
+
+@pytest.mark.parametrize("tblock", [0, 1])
+def test_C1_64x64_100_sweeps(cuda_lib, tblock):
+    # configs[0]: 64x64 interior + 1-cell Dirichlet ring, 100 iterations
+    a = si.jacobi2d_grid(64, 64)
+    assert_bitwise(run_gpu(cuda_lib, a, 100, tblock), oracle.jacobi2d(a, 100))
+
+
+SHAPES = [  # (nx, ny, ld, iters): odd/even nx, nx not a multiple of the 64-col strip, 1-wide, 1-tall, padded pitch
+    (1, 1, 4, 3), (1, 37, 4, 5), (37, 1, 40, 4), (2, 2, 4, 7), (62, 9, 64, 2), (63, 9, 66, 3),
+    (64, 17, 66, 1), (65, 130, 68, 6), (127, 129, 130, 9), (190, 33, 200, 10), (1000, 300, 1002, 11),
+    (4093, 257, 4096, 4),
+]
+
+
+@pytest.mark.parametrize("nx,ny,ld,iters", SHAPES)
+@pytest.mark.parametrize("tblock", [0, 1])
+def test_ragged_shapes(cuda_lib, nx, ny, ld, iters, tblock):
+    a = si.jacobi2d_grid(nx, ny, ld=ld)
+    want = oracle.jacobi2d(a, iters, nx=nx)
+    got = run_gpu(cuda_lib, a, iters, tblock, nx=nx)
+    assert_bitwise(got[:, : nx + 2], want[:, : nx + 2])
+    # pitch padding is never written
+    assert np.array_equal(got[:, nx + 2:], a[:, nx + 2:])
+
+
+def test_iters_zero_is_identity(cuda_lib):
+    a = si.jacobi2d_grid(70, 20)
+    assert_bitwise(run_gpu(cuda_lib, a, 0, 1), a)
+
+
+def test_chunked_calls_equal_one_call(cuda_lib):
+    import torch
+    a_np = si.jacobi2d_grid(300, 200, ld=304)
+    a = torch.from_numpy(a_np).cuda()
+    b = torch.empty_like(a)
+    r1 = cuda_lib.st_jacobi2d_run(a, b, 40, tblock=1, nx=300)
+    o1 = b if r1 is a else a
+    r2 = cuda_lib.st_jacobi2d_run(r1, o1, 60, tblock=1, nx=300)
+    assert_bitwise(r2.cpu().numpy()[:, :302], oracle.jacobi2d(a_np, 100, nx=300)[:, :302])
+
+
+def test_linear_field_fixed_point_1000_sweeps(cuda_lib):
+    # J3 at a size that spans many strips and row chunks: exact fixed point
+    nx, ny = 2050, 1030
+    y, x = np.mgrid[0: ny + 2, 0: nx + 2]
+    a = (3 * x + 2 * y + 7).astype(np.float64)
+    a = np.ascontiguousarray(np.pad(a, ((0, 0), (0, 2))))
+    got = run_gpu(cuda_lib, a, 1000, 1, nx=nx)
+    assert_bitwise(got, a)
+
+
+@pytest.mark.slow
+def test_C2_full_size_10_sweeps(cuda_lib):
+    # configs[1] grid (16384^2 interior), 10 sweeps, every element vs the oracle
+    a = si.jacobi2d_grid(16384, 16384)
+    assert_bitwise(run_gpu(cuda_lib, a, 10, 1), oracle.jacobi2d(a, 10))
+
+
+def test_stream_and_sync_semantics(cuda_lib):
+    # work is ordered on the caller's (non-default) stream
+    import torch
+    a_np = si.jacobi2d_grid(500, 400)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        a = torch.from_numpy(a_np).cuda()
+        b = torch.empty_like(a)
+        r = cuda_lib.st_jacobi2d_run(a, b, 13, tblock=1)
+        out = r.cpu()
+    assert_bitwise(out.numpy(), oracle.jacobi2d(a_np, 13))
+
+
+def test_rejects_host_tensor_and_wrong_dtype(cuda_lib):
+    import torch
+    a = torch.zeros(10, 10, dtype=torch.float64)
+    with pytest.raises(TypeError):
+        cuda_lib.st_jacobi2d_run(a, a.clone(), 1)
+    g = torch.zeros(10, 10, dtype=torch.float32, device="cuda")
+    with pytest.raises(TypeError):
+        cuda_lib.st_jacobi2d_run(g, g.clone(), 1)
+
+
+def test_launches_counted(cuda_lib):
+    import torch
+    a = torch.from_numpy(si.jacobi2d_grid(200, 100)).cuda()
+    b = torch.empty_like(a)
+    n0 = cuda_lib.launch_count()
+    cuda_lib.st_jacobi2d_run(a, b, 7, tblock=1)
+    torch.cuda.synchronize()
+    assert cuda_lib.launch_count() - n0 == 7

@@ -1,0 +1,21 @@
+#!/bin/bash
+# One GPU measurement round (run under gpurun from the repo root).
+# usage: tools/gpu_round.sh TAG [what...]   what in: build tests smoke bench launches ncu sanitize
+set -u
+TAG=${1:-r}; shift || true
+WHAT=${*:-"build tests smoke bench launches ncu"}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+NCU=/usr/local/cuda/bin/ncu
+for w in $WHAT; do
+  case $w in
+    build) make -j8 all > $OUT/build.log 2>&1 || { echo BUILD FAILED; tail -30 $OUT/build.log; exit 1; } ;;
+    tests) timeout 1200 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -5 $OUT/pytest_gpu.log ;;
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?"; tail -3 $OUT/smoke.log ;;
+    bench) timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; cat $OUT/bench.json; tail -3 $OUT/bench.err ;;
+    launches) timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
+        python bench.py --steps 2 --warmup 1 --sweeps 100 --pw-apps 4 --no-e2e --no-cpu > $OUT/launches_bench.log 2>&1; echo "launches rc=$?" ;;
+    ncu) timeout 900 $NCU --set full --clock-control none --import-source on -k regex:'jacobi2d_stream|pw_advect3d_kernel' -s 2 -c 2 \
+        -o $OUT/prof python tools/prof_kernels.py --sweeps 4 --apps 3 > $OUT/ncu.log 2>&1; echo "ncu rc=$?"; tail -3 $OUT/ncu.log ;;
+  esac
+done

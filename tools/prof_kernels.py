@@ -1,0 +1,33 @@
+"""Small driver for ncu captures: a few C2 Jacobi sweeps and C3 PW applications
+(the same kernels and launch configurations bench.py times)."""
+import argparse
+import sys
+import pathlib
+
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+
+import torch
+
+import paper_2310_01882_b200 as st
+import stencil_inputs as si
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--sweeps", type=int, default=4)
+ap.add_argument("--apps", type=int, default=2)
+ap.add_argument("--tblock", type=int, default=1)
+args = ap.parse_args()
+
+n = 16384
+a = torch.from_numpy(si.jacobi2d_grid(n, n)).cuda()
+b = torch.empty_like(a)
+st.st_jacobi2d_run(a, b, args.sweeps, tblock=args.tblock)
+torch.cuda.synchronize()
+del a, b
+m = 512
+d = si.pw_inputs(m, m, m)
+g = {k: (torch.from_numpy(v).cuda() if hasattr(v, "shape") else v) for k, v in d.items()}
+outs = [torch.empty_like(g["u"]) for _ in range(3)]
+for _ in range(args.apps):
+    st.st_pw_advect3d(g["u"], g["v"], g["w"], *outs, g["tcx"], g["tcy"], g["tzc1"], g["tzc2"], g["tzd1"], g["tzd2"])
+torch.cuda.synchronize()
+print("done")
