@@ -84,6 +84,8 @@ st_status make_tmap_2d_f64(CUtensorMap* map, const double* base, const uint64_t 
 // ------------------------------------------------------- Jacobi driver ---
 namespace {
 
+constexpr int kAutoTblock = 1;  // tblock=0 on large grids (tuned on B200)
+
 st_status check_device_ptr(const void* p, const char* what) {
   cudaPointerAttributes at;
   cudaError_t e = cudaPointerGetAttributes(&at, p);
@@ -97,26 +99,25 @@ st_status check_device_ptr(const void* p, const char* what) {
   return ST_OK;
 }
 
-// Split `iters` sweeps into passes of at most T sweeps such that the number of
-// passes has the parity of `iters`: every pass reads one buffer and writes the
-// other, so the result lands where plain Jacobi ping-pong puts it (b iff iters odd).
+// Split `iters` sweeps into passes of at most T (even) sweeps such that the
+// number of passes has the parity of `iters`: every pass reads one buffer and
+// writes the other, so the result lands where plain Jacobi ping-pong puts it
+// (b iff iters odd). Passes are even-sized (temporal-blocking kernel) or 1
+// (single-sweep kernel).
 int plan_passes(int64_t iters, int t, int64_t* out, int cap) {
+  if (t < 2 || (t & 1)) return -1;
   int n = 0;
-  if (t <= 1) return -1;
   int64_t left = iters;
   while (left >= t && n < cap) { out[n++] = t; left -= t; }
-  while (left > 0 && n < cap) {
-    const int64_t k = left >= 2 ? left : 1;  // a remainder r < T is one pass of r sweeps
-    out[n++] = k;
-    left -= k;
-  }
+  if (left >= 2 && n < cap) { out[n++] = left & ~int64_t(1); left &= 1; }
+  if (left == 1 && n < cap) { out[n++] = 1; left = 0; }
+  if (left != 0) return -1;
   if ((n & 1) != (int)(iters & 1)) {
-    // flip the parity: split one pass of k >= 2 sweeps into (k-1) + 1
     for (int i = 0; i < n; ++i) {
-      if (out[i] >= 2) {
+      if (out[i] >= 2 && n < cap) {
         for (int j = n; j > i + 1; --j) out[j] = out[j - 1];
-        out[i + 1] = 1;
-        out[i] -= 1;
+        if (out[i] >= 4) { out[i + 1] = 2; out[i] -= 2; }
+        else { out[i + 1] = 1; out[i] = 1; }
         ++n;
         break;
       }
@@ -126,9 +127,9 @@ int plan_passes(int64_t iters, int t, int64_t* out, int cap) {
 }
 
 st_status one_pass(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
-                   int64_t sweeps, int64_t ring_lo, int64_t ring_hi, cudaStream_t s) {
+                   int64_t sweeps, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s) {
   if (sweeps == 1) return jacobi2d_sweep_rows(src, dst, nx, ld, y_lo, y_hi, s);
-  return jacobi2d_tb_rows(src, dst, nx, ld, y_lo, y_hi, (int)sweeps, ring_lo, ring_hi, s);
+  return jacobi2d_tb_rows(src, dst, nx, ld, y_lo, y_hi, (int)sweeps, ring_lo, ring_hi, nrows_buf, s);
 }
 
 // Single-domain run (no comm): halo == 1, rows 0 and ny+1 Dirichlet.
@@ -140,9 +141,9 @@ st_status jacobi2d_single(double* a, double* b, int64_t nx, int64_t ny, int64_t 
   ST_CHECK_CUDA(cudaMemcpyAsync(b + (ny + 1) * ld, a + (ny + 1) * ld, (size_t)ld * sizeof(double),
                                 cudaMemcpyDeviceToDevice, s));
   int t = tblock;
-  if (t == 0) t = env_int("ST_JACOBI_T", 1);
+  if (t == 0) t = env_int("ST_JACOBI_T", kAutoTblock);
   if (t > 1 && !jacobi2d_tb_supported(t)) {
-    ST_RETURN_IF(tblock != 0, ST_ENOTSUP, "jacobi2d: tblock=%d not supported by this build", tblock);
+    ST_RETURN_IF(tblock != 0, ST_ENOTSUP, "jacobi2d: tblock=%d not supported (1, 2, 4, 6, 8)", tblock);
     t = 1;
   }
   double* src = a;
@@ -162,7 +163,7 @@ st_status jacobi2d_single(double* a, double* b, int64_t nx, int64_t ny, int64_t 
     const int n = plan_passes(blk, t, pass, 64);
     ST_RETURN_IF(n < 0, ST_EINTERNAL, "jacobi2d: pass planning failed");
     for (int i = 0; i < n; ++i) {
-      ST_TRY(one_pass(src, dst, nx, ld, 1, ny, pass[i], 0, ny + 1, s));
+      ST_TRY(one_pass(src, dst, nx, ld, 1, ny, pass[i], 0, ny + 1, ny + 2, s));
       double* tmp = src; src = dst; dst = tmp;
     }
     done += blk;

@@ -24,14 +24,16 @@ bool jacobi2d_resident_fits(int64_t nx, int64_t ny);
 st_status jacobi2d_resident(double* a, double* b, int64_t nx, int64_t ny, int64_t ld,
                             int64_t iters, cudaStream_t s);
 
-// Temporal blocking: T sweeps per pass over HBM, rows [y_lo, y_hi] of dst
-// (src rows y_lo-T .. y_hi+T must be valid; intermediate levels are computed
-// redundantly on a shrinking halo and never stored). `ring_lo`/`ring_hi`
-// are buffer rows that are Dirichlet (never updated at any level), or -1.
+// Temporal blocking: T sweeps in one pass over HBM; writes rows [y_lo, y_hi]
+// of dst with the state after T sweeps (src rows y_lo-T .. y_hi+T are read
+// where they exist; intermediate levels are recomputed redundantly on a
+// shrinking halo and never stored). Buffer rows <= ring_lo and >= ring_hi are
+// Dirichlet (identical at every level); pass ring_lo = -1 / ring_hi = nrows_buf
+// for none. T must be even (2, 4, 6, 8).
 bool jacobi2d_tb_supported(int t);
 st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t ld,
                            int64_t y_lo, int64_t y_hi, int t, int64_t ring_lo,
-                           int64_t ring_hi, cudaStream_t s);
+                           int64_t ring_hi, int64_t nrows_buf, cudaStream_t s);
 
 // ------------------------------------------------------------ PW 3-D ---
 struct PwArgs {

@@ -170,12 +170,130 @@ st_status jacobi2d_resident(double* a, double* b, int64_t nx, int64_t ny, int64_
   return ST_OK;
 }
 
-bool jacobi2d_tb_supported(int) { return false; }
+namespace {
 
-st_status jacobi2d_tb_rows(const double*, double*, int64_t, int64_t, int64_t, int64_t, int, int64_t,
-                           int64_t, cudaStream_t) {
-  set_error("jacobi2d: temporal blocking not built");
-  return ST_ENOTSUP;
+// Temporal blocking in registers (T sweeps per pass over HBM).
+//
+// A warp owns a strip of 64 columns (lane = column pair) that overlaps its
+// neighbours by 2T columns: after T levels only the centre 64-2T columns are
+// exact, so strips advance by 64-2T. Rows stream through a T-level software
+// pipeline held entirely in registers: level j keeps its two most recent rows
+// (N, C); when level j produces a new row S, level j+1 produces row C. W/E
+// neighbours at every level come from warp shuffles. Dirichlet rows/columns are
+// passed through unchanged at every level, so every level is exactly one Jacobi
+// sweep and the result is bitwise the same as T single sweeps.
+template <int T>
+__global__ void __launch_bounds__(kStreamThreads)
+    jacobi2d_tb_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
+                       int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk, int64_t nstrips, int64_t ring_lo,
+                       int64_t ring_hi, int64_t nrows_buf) {
+  static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
+  constexpr int kStride = kStripCols - 2 * T;
+  const int lane = threadIdx.x & 31;
+  const int64_t strip = (int64_t)blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
+  if (strip >= nstrips) return;
+  const int64_t yc0 = y_lo + (int64_t)blockIdx.y * rows_per_chunk;
+  if (yc0 > y_hi) return;
+  const int64_t yc1 = min(y_hi, yc0 + rows_per_chunk - 1);
+
+  const int64_t x = strip * kStride - T + 2 * lane;
+  const bool has_pair = x >= 0 && x < nxp2;
+  const bool st_lane = lane >= T / 2 && lane <= 31 - T / 2;
+  const bool st0 = st_lane && x >= 0 && x < nxp2;
+  const bool st1 = st_lane && x + 1 >= 0 && x + 1 < nxp2;
+  const bool ring0 = (x == 0) || (x == nxp2 - 1);
+  const bool ring1 = (x + 1 == nxp2 - 1);
+  const double* sp = src + (has_pair ? x : 0);
+
+  // first/last input rows the pipeline reads; rows beyond are never loaded
+  const int64_t r_first = max(max(ring_lo, (int64_t)0), yc0 - T);
+  const int64_t r_load_last = min(min(ring_hi, nrows_buf - 1), yc1 + T);
+  const int64_t r_end = yc1 + T;  // steps continue past ring_hi (the ring row propagates)
+
+  double2 n_[T], c_[T];  // level j: rows r-j-2 (n_) and r-j-1 (c_) before step r
+#pragma unroll
+  for (int j = 0; j < T; ++j) n_[j] = c_[j] = make_double2(0.0, 0.0);
+
+  constexpr int U = 4;
+  double2 pf[U];
+  auto load = [&](int64_t r) -> double2 {
+    return (has_pair && r <= r_load_last) ? ldg2(sp + r * ld) : make_double2(0.0, 0.0);
+  };
+#pragma unroll
+  for (int k = 0; k < U; ++k) pf[k] = load(r_first + k);
+
+  for (int64_t r0 = r_first; r0 <= r_end; r0 += U) {
+    double2 nx_[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) nx_[k] = load(r0 + U + k);
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t r = r0 + k;
+      if (r <= r_end) {
+        double2 s = pf[k];  // level 0, row r
+#pragma unroll
+        for (int j = 0; j < T; ++j) {
+          // level j+1, row r-j-1 from level j rows r-j-2 (n), r-j-1 (c), r-j (s)
+          const int64_t row = r - j - 1;
+          const double2 c = c_[j];
+          double w = __shfl_up_sync(0xffffffffu, c.y, 1);
+          double e = __shfl_down_sync(0xffffffffu, c.x, 1);
+          double2 o;
+          o.x = dmul(dadd(dadd(dadd(n_[j].x, s.x), w), c.y), 0.25);
+          o.y = dmul(dadd(dadd(dadd(n_[j].y, s.y), c.x), e), 0.25);
+          if (ring0) o.x = c.x;
+          if (ring1) o.y = c.y;
+          if (row <= ring_lo || row >= ring_hi) o = c;  // Dirichlet rows never change
+          n_[j] = c;
+          c_[j] = s;
+          s = o;
+        }
+        const int64_t orow = r - T;  // s = level T, row r-T
+        if (orow >= yc0 && orow <= yc1) {
+          double* dp = dst + orow * ld + x;
+          if (st0 && st1) stg2(dp, s);
+          else if (st0) dp[0] = s.x;
+          else if (st1) dp[1] = s.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) pf[k] = nx_[k];
+  }
+}
+
+template <int T>
+st_status launch_tb(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
+                    int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s) {
+  const int64_t nxp2 = nx + 2;
+  constexpr int kStride = kStripCols - 2 * T;
+  const int64_t nstrips = (nxp2 + kStride - 1) / kStride;
+  const int64_t rows = y_hi - y_lo + 1;
+  static const int kRows = env_int("ST_JACOBI_TB_ROWS", 512);
+  const int64_t rpc = std::max<int64_t>(1, std::min<int64_t>(kRows, rows));
+  const int64_t nchunks = (rows + rpc - 1) / rpc;
+  ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d tb: too many row chunks");
+  dim3 grid((unsigned)((nstrips + kStreamWarps - 1) / kStreamWarps), (unsigned)nchunks);
+  jacobi2d_tb_kernel<T><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
+                                                        ring_hi, nrows_buf);
+  ST_LAUNCHED();
+  return ST_OK;
+}
+
+}  // namespace
+
+bool jacobi2d_tb_supported(int t) { return t == 2 || t == 4 || t == 6 || t == 8; }
+
+st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
+                           int t, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s) {
+  if (y_hi < y_lo) return ST_OK;
+  switch (t) {
+    case 2: return launch_tb<2>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
+    case 4: return launch_tb<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
+    case 6: return launch_tb<6>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
+    case 8: return launch_tb<8>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
+    default: set_error("jacobi2d: tblock=%d not supported (2, 4, 6, 8)", t); return ST_ENOTSUP;
+  }
 }
 
 }  // namespace st

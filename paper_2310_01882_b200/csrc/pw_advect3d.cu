@@ -27,6 +27,7 @@ namespace {
 
 constexpr int kBX = 64;       // interior columns per tile (32 lanes x 2)
 constexpr int kSX = kBX + 4;  // smem row: 2-column apron each side (keeps pairs 16-byte aligned)
+constexpr int kMaxPlanesPerChunk = 256;
 
 template <int BY>
 struct PwTile {
@@ -100,12 +101,16 @@ __global__ void __launch_bounds__(32 * BY)
                        const double* __restrict__ tzd2, int64_t z_lo, int64_t z_hi,
                        int64_t planes_per_chunk) {
   using T = PwTile<BY>;
+  static_assert(S >= 4, "ring needs planes z-1, z, z+1 and at least one in flight");
   extern __shared__ __align__(128) double ring[];
   __shared__ __align__(8) uint64_t full[S];
+  __shared__ double4 coef[kMaxPlanesPerChunk];  // (tzc1, tzc2, tzd1, tzd2) per output plane
 
   const int lane = threadIdx.x & 31;
   const int wy = threadIdx.x >> 5;
-  const int64_t x0 = (int64_t)blockIdx.x * kBX;  // padded x of the tile's first pair
+  // Tiles are aligned to the INTERIOR: tile bx owns x in [1+64bx, 64bx+64], so
+  // nx = 512 needs exactly 8 tiles. A thread owns the pair (x, x+1), x odd.
+  const int64_t x0 = 1 + (int64_t)blockIdx.x * kBX;
   const int64_t y0 = 1 + (int64_t)blockIdx.y * BY;
   const int64_t za = z_lo + (int64_t)blockIdx.z * planes_per_chunk;
   const int64_t zb = min(z_hi, za + planes_per_chunk - 1);
@@ -118,51 +123,60 @@ __global__ void __launch_bounds__(32 * BY)
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
+  for (int j = threadIdx.x; j < np - 2; j += blockDim.x)
+    coef[j] = make_double4(__ldg(tzc1 + za + j), __ldg(tzc2 + za + j), __ldg(tzd1 + za + j),
+                           __ldg(tzd2 + za + j));
   __syncthreads();
 
-  auto issue = [&](int p) {  // input plane za-1+p -> slot p % S
-    double* slot = ring + (p % S) * T::kSlotStride;
-    uint64_t* bar = &full[p % S];
+  const int32_t cx = (int32_t)(x0 - 2), cy = (int32_t)(y0 - 1);
+  auto issue = [&](int p, int slot) {  // input plane za-1+p -> ring slot
+    double* dstp = ring + slot * T::kSlotStride;
+    uint64_t* bar = &full[slot];
     mbar_arrive_expect_tx(bar, T::kTxBytes);
-    const int32_t cx = (int32_t)(x0 - 2), cy = (int32_t)(y0 - 1), cz = (int32_t)(za - 1 + p);
-    tma_load_3d(slot, &tm_u, cx, cy, cz, bar);
-    tma_load_3d(slot + T::kPlaneStride, &tm_v, cx, cy, cz, bar);
-    tma_load_3d(slot + 2 * T::kPlaneStride, &tm_w, cx, cy, cz, bar);
+    const int32_t cz = (int32_t)(za - 1 + p);
+    tma_load_3d(dstp, &tm_u, cx, cy, cz, bar);
+    tma_load_3d(dstp + T::kPlaneStride, &tm_v, cx, cy, cz, bar);
+    tma_load_3d(dstp + 2 * T::kPlaneStride, &tm_w, cx, cy, cz, bar);
   };
   if (threadIdx.x == 0)
-    for (int p = 0; p < S && p < np; ++p) issue(p);
+    for (int p = 0; p < S && p < np; ++p) issue(p, p);
 
-  // Thread geometry inside a plane slot: smem row r = wy+1, column c = 2*lane+2.
-  const int r = wy + 1;
-  const int c = 2 * lane + 2;
-  const int oc = r * kSX + c;  // own pair offset inside a field plane
+  // Thread geometry inside a plane slot: smem row wy+1, column 2*lane+2.
+  const int oc = (wy + 1) * kSX + 2 * lane + 2;
   const int64_t y = y0 + wy;
   const int64_t x = x0 + 2 * lane;
   const bool row_ok = y <= ny;
-  const bool ok0 = x >= 1 && x <= nx;
-  const bool ok1 = x + 1 >= 1 && x + 1 <= nx;
+  const bool ok0 = x <= nx;      // x >= 1 by construction
+  const bool ok1 = x + 1 <= nx;
+  // Stores are re-paired across lanes so they are 16-byte aligned: lane l>0
+  // writes (x-1, x) = (lane l-1's .y, own .x); lane 0 writes x alone and lane 31
+  // also writes x+1 alone.
+  const bool okm = x - 1 <= nx;  // x-1 >= 1 for lane > 0
+  const int64_t plane_elems = (ny + 2) * ldx;
+  const int64_t g0 = (za * (ny + 2) + y) * ldx + x;
+  double* pu = su + g0;
+  double* pv = sv + g0;
+  double* pw = sw + g0;
 
-  auto field = [&](int p, int f) -> const double* {
-    return ring + (p % S) * T::kSlotStride + f * T::kPlaneStride;
-  };
-  auto wait = [&](int p) { mbar_wait_parity(&full[p % S], (uint32_t)((p / S) & 1)); };
+  // ring slots of input planes j (m), j+1 (c), j+2 (p) and their phase parities
+  int sm_ = 0, sc = 1, sp = 2;
+  uint32_t par_p = 0;  // parity of slot sp's next completion
+  mbar_wait_parity(&full[0], 0);
+  mbar_wait_parity(&full[1], 0);
+  const double* F = ring;
+  double2 um = lds2(F + oc), vm = lds2(F + T::kPlaneStride + oc), wm = lds2(F + 2 * T::kPlaneStride + oc);
+  F = ring + T::kSlotStride;
+  double2 uc = lds2(F + oc), vc = lds2(F + T::kPlaneStride + oc), wc = lds2(F + 2 * T::kPlaneStride + oc);
 
-  // register queue: own pairs at planes z-1 (m) and z (c)
-  wait(0);
-  wait(1);
-  double2 um = lds2(field(0, 0) + oc), vm = lds2(field(0, 1) + oc), wm = lds2(field(0, 2) + oc);
-  double2 uc = lds2(field(1, 0) + oc), vc = lds2(field(1, 1) + oc), wc = lds2(field(1, 2) + oc);
-
-  for (int j = 0; j + 2 < np; ++j) {  // output plane z = za + j, input planes j, j+1, j+2
-    const int64_t z = za + j;
-    wait(j + 2);
-    const double* U0 = field(j + 1, 0);
-    const double* V0 = field(j + 1, 1);
-    const double* W0 = field(j + 1, 2);
-    const double* Up = field(j + 2, 0);
-    const double* Vp = field(j + 2, 1);
-    const double* Wp = field(j + 2, 2);
-    const double* Wm = field(j, 2);
+  for (int j = 0; j + 2 < np; ++j) {  // output plane za+j from input planes j, j+1, j+2
+    mbar_wait_parity(&full[sp], par_p);
+    const double* U0 = ring + sc * T::kSlotStride;
+    const double* V0 = U0 + T::kPlaneStride;
+    const double* W0 = U0 + 2 * T::kPlaneStride;
+    const double* Up = ring + sp * T::kSlotStride;
+    const double* Vp = Up + T::kPlaneStride;
+    const double* Wp = Up + 2 * T::kPlaneStride;
+    const double* Wm = ring + sm_ * T::kSlotStride + 2 * T::kPlaneStride;
 
     const double2 up = lds2(Up + oc), vp = lds2(Vp + oc), wp = lds2(Wp + oc);
     const double2 un = lds2(U0 + oc - kSX), us = lds2(U0 + oc + kSX);
@@ -171,14 +185,15 @@ __global__ void __launch_bounds__(32 * BY)
     const double u_xw = U0[oc - 1], u_xe = U0[oc + 2];
     const double v_xw = V0[oc - 1], v_xe = V0[oc + 2];
     const double w_xw = W0[oc - 1], w_xe = W0[oc + 2];
-    const double u_sw0 = U0[oc + kSX - 1];   // U(0,+1,-1) for point 0
-    const double v_ne1 = V0[oc - kSX + 2];   // V(0,-1,+1) for point 1
-    const double u_pw0 = Up[oc - 1];         // U(+1,0,-1) for point 0
-    const double2 vpn = lds2(Vp + oc - kSX); // V(+1,-1,0)
-    const double w_me1 = Wm[oc + 2];         // W(-1,0,+1) for point 1
-    const double2 wms = lds2(Wm + oc + kSX); // W(-1,+1,0)
+    const double u_sw0 = U0[oc + kSX - 1];    // U(0,+1,-1) for point 0
+    const double v_ne1 = V0[oc - kSX + 2];    // V(0,-1,+1) for point 1
+    const double u_pw0 = Up[oc - 1];          // U(+1,0,-1) for point 0
+    const double2 vpn = lds2(Vp + oc - kSX);  // V(+1,-1,0)
+    const double w_me1 = Wm[oc + 2];          // W(-1,0,+1) for point 1
+    const double2 wms = lds2(Wm + oc + kSX);  // W(-1,+1,0)
 
-    const PwCoef k = {tcx, tcy, __ldg(tzc1 + z), __ldg(tzc2 + z), __ldg(tzd1 + z), __ldg(tzd2 + z)};
+    const double4 cz = coef[j];
+    const PwCoef k = {tcx, tcy, cz.x, cz.y, cz.z, cz.w};
     PwPoint p0, p1;
     p0.uc = uc.x; p0.uw = u_xw; p0.ue = uc.y; p0.un = un.x; p0.us = us.x; p0.um = um.x; p0.up = up.x;
     p0.u_sw = u_sw0; p0.u_pw = u_pw0;
@@ -198,28 +213,44 @@ __global__ void __launch_bounds__(32 * BY)
     pw_point(p0, k, ou.x, ov.x, ow.x);
     pw_point(p1, k, ou.y, ov.y, ow.y);
 
+    // re-pair for aligned stores: (x-1, x) <- (left lane's .y, own .x)
+    const double lu = __shfl_up_sync(0xffffffffu, ou.y, 1);
+    const double lv = __shfl_up_sync(0xffffffffu, ov.y, 1);
+    const double lw = __shfl_up_sync(0xffffffffu, ow.y, 1);
     if (row_ok) {
-      const int64_t g = (z * (ny + 2) + y) * ldx + x;
-      if (ok0 && ok1) {
-        stg2(su + g, ou);
-        stg2(sv + g, ov);
-        stg2(sw + g, ow);
+      if (lane > 0) {
+        if (ok0) {
+          stg2(pu - 1, make_double2(lu, ou.x));
+          stg2(pv - 1, make_double2(lv, ov.x));
+          stg2(pw - 1, make_double2(lw, ow.x));
+        } else if (okm) {
+          pu[-1] = lu; pv[-1] = lv; pw[-1] = lw;
+        }
       } else if (ok0) {
-        su[g] = ou.x; sv[g] = ov.x; sw[g] = ow.x;
-      } else if (ok1) {
-        su[g + 1] = ou.y; sv[g + 1] = ov.y; sw[g + 1] = ow.y;
+        pu[0] = ou.x; pv[0] = ov.x; pw[0] = ow.x;
+      }
+      if (lane == 31 && ok1) {
+        pu[1] = ou.y; pv[1] = ov.y; pw[1] = ow.y;
       }
     }
+    pu += plane_elems;
+    pv += plane_elems;
+    pw += plane_elems;
 
     um = uc; vm = vc; wm = wc;
     uc = up; vc = vp; wc = wp;
 
-    // all reads of input plane j are done -> refill its slot with plane j+S
+    // every read of input plane j (slot sm_) is done -> refill it with plane j+S
     __syncthreads();
     if (threadIdx.x == 0 && j + S < np) {
       fence_proxy_async_smem();
-      issue(j + S);
+      issue(j + S, sm_);
     }
+    const int nsp = (sp + 1 == S) ? 0 : sp + 1;
+    if (nsp == 0) par_p ^= 1u;
+    sm_ = sc;
+    sc = sp;
+    sp = nsp;
   }
 }
 
@@ -236,11 +267,11 @@ st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s)
   const size_t smem = (size_t)S * T::kSlotStride * sizeof(double);
   ST_CHECK_CUDA(cudaFuncSetAttribute(pw_advect3d_kernel<BY, S>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t ntx = (a.nx + 2 + kBX - 1) / kBX;
+  const int64_t ntx = (a.nx + kBX - 1) / kBX;
   const int64_t nty = (a.ny + BY - 1) / BY;
   const int64_t nz = z_hi - z_lo + 1;
   static const int kPpc = env_int("ST_PW_PLANES", 64);
-  const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(kPpc, nz));
+  const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(std::min(kPpc, kMaxPlanesPerChunk), nz));
   const int64_t nzc = (nz + ppc - 1) / ppc;
   ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "pw_advect3d: grid too large");
   dim3 grid((unsigned)ntx, (unsigned)nty, (unsigned)nzc);
@@ -257,10 +288,11 @@ st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaSt
   if (z_hi < z_lo) return ST_OK;
   static const int kVariant = env_int("ST_PW_VARIANT", 0);
   switch (kVariant) {
-    case 1: return launch_pw<8, 5>(a, z_lo, z_hi, s);
-    case 2: return launch_pw<16, 4>(a, z_lo, z_hi, s);
-    case 3: return launch_pw<4, 5>(a, z_lo, z_hi, s);
-    default: return launch_pw<8, 4>(a, z_lo, z_hi, s);
+    case 1: return launch_pw<8, 4>(a, z_lo, z_hi, s);
+    case 2: return launch_pw<16, 5>(a, z_lo, z_hi, s);
+    case 3: return launch_pw<4, 8>(a, z_lo, z_hi, s);
+    case 4: return launch_pw<8, 5>(a, z_lo, z_hi, s);
+    default: return launch_pw<8, 6>(a, z_lo, z_hi, s);
   }
 }
 

@@ -12,14 +12,15 @@ import stencil_inputs as si
 pytestmark = pytest.mark.gpu
 
 
-def run_gpu(st, a_np, iters, tblock=0, nx=None):
+def run_gpu(st, a_np, iters, tblock=0, nx=None, which=False):
     import torch
     a = torch.from_numpy(a_np).cuda()
     b = torch.empty_like(a)
     b.fill_(float("nan"))  # the library must copy the ring itself
     r = st.st_jacobi2d_run(a, b, iters, tblock=tblock, nx=nx)
     torch.cuda.synchronize()
-    return r.cpu().numpy()
+    assert (r is b) == bool(iters & 1)  # result in b iff iters odd
+    return (r.cpu().numpy(), r is b) if which else r.cpu().numpy()
 
 
 def assert_bitwise(got, want):
@@ -43,14 +44,34 @@ SHAPES = [  # (nx, ny, ld, iters): odd/even nx, nx not a multiple of the 64-col 
 
 
 @pytest.mark.parametrize("nx,ny,ld,iters", SHAPES)
-@pytest.mark.parametrize("tblock", [0, 1])
+@pytest.mark.parametrize("tblock", [0, 1, 2, 4, 6, 8])
 def test_ragged_shapes(cuda_lib, nx, ny, ld, iters, tblock):
     a = si.jacobi2d_grid(nx, ny, ld=ld)
     want = oracle.jacobi2d(a, iters, nx=nx)
+    got, in_b = run_gpu(cuda_lib, a, iters, tblock, nx=nx, which=True)
+    assert_bitwise(got[:, : nx + 2], want[:, : nx + 2])
+    # pitch padding of the result buffer is never written (b starts NaN-filled)
+    pad = got[:, nx + 2:]
+    assert np.all(np.isnan(pad)) if in_b else np.array_equal(pad, a[:, nx + 2:])
+
+
+@pytest.mark.parametrize("tblock", [2, 4, 6, 8])
+@pytest.mark.parametrize("iters", [1, 2, 3, 5, 8, 13, 17, 33])
+def test_temporal_blocking_equals_single_sweeps(cuda_lib, tblock, iters):
+    # T sweeps per HBM pass is bitwise T single sweeps, for every remainder/parity
+    nx, ny = 250, 1100  # several strips and several 512-row chunks
+    a = si.jacobi2d_grid(nx, ny, ld=256)
+    want = oracle.jacobi2d(a, iters, nx=nx)
     got = run_gpu(cuda_lib, a, iters, tblock, nx=nx)
     assert_bitwise(got[:, : nx + 2], want[:, : nx + 2])
-    # pitch padding is never written
-    assert np.array_equal(got[:, nx + 2:], a[:, nx + 2:])
+
+
+def test_tblock_rejects_unsupported(cuda_lib):
+    import torch
+    a = torch.zeros(20, 20, dtype=torch.float64, device="cuda")
+    with pytest.raises(cuda_lib.StencilError) as e:
+        cuda_lib.st_jacobi2d_run(a, a.clone(), 5, tblock=3)
+    assert e.value.code == cuda_lib.ST_ENOTSUP
 
 
 def test_iters_zero_is_identity(cuda_lib):
@@ -79,11 +100,19 @@ def test_linear_field_fixed_point_1000_sweeps(cuda_lib):
     assert_bitwise(got, a)
 
 
-@pytest.mark.slow
-def test_C2_full_size_10_sweeps(cuda_lib):
-    # configs[1] grid (16384^2 interior), 10 sweeps, every element vs the oracle
+@pytest.fixture(scope="module")
+def c2_case():
     a = si.jacobi2d_grid(16384, 16384)
-    assert_bitwise(run_gpu(cuda_lib, a, 10, 1), oracle.jacobi2d(a, 10))
+    return a, oracle.jacobi2d(a, 10)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("tblock", [1, 0, 4, 8])
+def test_C2_full_size_10_sweeps(cuda_lib, c2_case, tblock):
+    # configs[1] grid (16384^2 interior), 10 sweeps, every element vs the oracle,
+    # in the launch configurations bench.py times (tblock=0 = auto)
+    a, want = c2_case
+    assert_bitwise(run_gpu(cuda_lib, a, 10, tblock), want)
 
 
 def test_stream_and_sync_semantics(cuda_lib):
