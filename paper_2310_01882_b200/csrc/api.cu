@@ -84,7 +84,9 @@ st_status make_tmap_2d_f64(CUtensorMap* map, const double* base, const uint64_t 
 // ------------------------------------------------------- Jacobi driver ---
 namespace {
 
-constexpr int kAutoTblock = 1;  // tblock=0 on large grids (tuned on B200)
+// tblock=0 on grids of at least kAutoMin^2: T sweeps per pass (tuned on B200)
+constexpr int kAutoTblock = 6;
+constexpr int64_t kAutoMin = 128;
 
 st_status check_device_ptr(const void* p, const char* what) {
   cudaPointerAttributes at;
@@ -136,12 +138,12 @@ st_status one_pass(const double* src, double* dst, int64_t nx, int64_t ld, int64
 st_status jacobi2d_single(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t iters,
                           int32_t tblock, cudaStream_t s) {
   if (tblock == 0 && jacobi2d_resident_fits(nx, ny)) return jacobi2d_resident(a, b, nx, ny, ld, iters, s);
-  // halo rows a -> b (ring columns are passed through by every sweep)
-  ST_CHECK_CUDA(cudaMemcpyAsync(b, a, (size_t)ld * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  ST_CHECK_CUDA(cudaMemcpyAsync(b + (ny + 1) * ld, a + (ny + 1) * ld, (size_t)ld * sizeof(double),
+  // halo rows a -> b (ring columns are passed through by every sweep); pitch padding untouched
+  ST_CHECK_CUDA(cudaMemcpyAsync(b, a, (size_t)(nx + 2) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  ST_CHECK_CUDA(cudaMemcpyAsync(b + (ny + 1) * ld, a + (ny + 1) * ld, (size_t)(nx + 2) * sizeof(double),
                                 cudaMemcpyDeviceToDevice, s));
   int t = tblock;
-  if (t == 0) t = env_int("ST_JACOBI_T", kAutoTblock);
+  if (t == 0) t = (nx >= kAutoMin && ny >= kAutoMin) ? env_int("ST_JACOBI_T", kAutoTblock) : 1;
   if (t > 1 && !jacobi2d_tb_supported(t)) {
     ST_RETURN_IF(tblock != 0, ST_ENOTSUP, "jacobi2d: tblock=%d not supported (1, 2, 4, 6, 8)", tblock);
     t = 1;
@@ -175,10 +177,11 @@ st_status jacobi2d_single(double* a, double* b, int64_t nx, int64_t ny, int64_t 
 st_status jacobi2d_slab(st_comm* comm, double* a, double* b, int64_t nx, int64_t n, int64_t ld,
                         int32_t h, int64_t iters, cudaStream_t s) {
   const bool lo_edge = comm->rank == 0, hi_edge = comm->rank == comm->nranks - 1;
-  const size_t hbytes = (size_t)h * (size_t)ld * sizeof(double);
-  // all ghost rows (incl. the edge ranks' Dirichlet row) a -> b
-  ST_CHECK_CUDA(cudaMemcpyAsync(b, a, hbytes, cudaMemcpyDeviceToDevice, s));
-  ST_CHECK_CUDA(cudaMemcpyAsync(b + (h + n) * ld, a + (h + n) * ld, hbytes, cudaMemcpyDeviceToDevice, s));
+  const size_t pitch = (size_t)ld * sizeof(double), width = (size_t)(nx + 2) * sizeof(double);
+  // all ghost rows (incl. the edge ranks' Dirichlet row) a -> b; pitch padding untouched
+  ST_CHECK_CUDA(cudaMemcpy2DAsync(b, pitch, a, pitch, width, (size_t)h, cudaMemcpyDeviceToDevice, s));
+  ST_CHECK_CUDA(cudaMemcpy2DAsync(b + (h + n) * ld, pitch, a + (h + n) * ld, pitch, width, (size_t)h,
+                                  cudaMemcpyDeviceToDevice, s));
   double* src = a;
   double* dst = b;
   // the initial state's ghosts come from the neighbours

@@ -6,15 +6,19 @@
 // pwadvection form); every binary op rounds once.
 //
 // Design (HBM-bound: 48 algorithmic bytes per point, 63 fp64 flops):
-//  * A CTA owns a 64(x) x BY(y) column of the domain and streams a chunk of
-//    z planes. Each input plane (u, v, w with a 1-row / 2-column apron) is
-//    brought into a shared-memory ring of S plane slots by three TMA tile loads
-//    (cp.async.bulk.tensor.3d) issued by one thread and completed on an
-//    mbarrier; S-3 planes are in flight while the CTA computes.
-//  * A thread owns a 16-byte column pair at one row; its own column of u, v, w
-//    at planes z-1, z, z+1 rides in a register queue, in-plane and cross-plane
-//    neighbours are read from the ring. Outputs go straight to HBM as 16-byte
-//    stores (halo cells of su, sv, sw are never written).
+//  * A CTA owns a 32(x) x BY(y) column of the interior and streams a chunk of z
+//    planes. Each input plane of u, v, w (with a 1-cell x/y apron) is brought
+//    into a shared-memory ring of S plane slots by three TMA tile loads
+//    (cp.async.bulk.tensor.3d, issued by one thread, completed on an
+//    mbarrier), so S-3 planes are in flight while the CTA computes.
+//  * Tiles are aligned to the interior (x0 = 1 + 32*bx): the TMA box then starts
+//    at the even coordinate x0-1, which TMA requires (the innermost start
+//    coordinate must be a multiple of 16 bytes; odd fp64 coordinates fault),
+//    and nx = 512 splits into 16 full tiles with no ragged tile.
+//  * A thread owns one point per plane; its own column of u, v, w at planes
+//    z-1, z rides in registers, all other neighbours are 8-byte shared loads
+//    (a warp's 32 consecutive doubles = 2 wavefronts). Outputs are coalesced
+//    8-byte stores straight to HBM; halo cells of su, sv, sw are never written.
 #include <algorithm>
 
 #include "common.cuh"
@@ -25,8 +29,8 @@ namespace st {
 
 namespace {
 
-constexpr int kBX = 64;       // interior columns per tile (32 lanes x 2)
-constexpr int kSX = kBX + 4;  // smem row: 2-column apron each side (keeps pairs 16-byte aligned)
+constexpr int kBX = 32;       // interior columns per tile (one per lane)
+constexpr int kSX = kBX + 2;  // smem row: 1-column apron each side
 constexpr int kMaxPlanesPerChunk = 256;
 
 template <int BY>
@@ -89,8 +93,6 @@ __device__ __forceinline__ void pw_point(const PwPoint& p, const PwCoef& k, doub
   sw = dadd(dadd(xs, ys), zs);
 }
 
-__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
-
 template <int BY, int S>
 __global__ void __launch_bounds__(32 * BY)
     pw_advect3d_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_v,
@@ -102,14 +104,14 @@ __global__ void __launch_bounds__(32 * BY)
                        int64_t planes_per_chunk) {
   using T = PwTile<BY>;
   static_assert(S >= 4, "ring needs planes z-1, z, z+1 and at least one in flight");
-  extern __shared__ __align__(128) double ring[];
-  __shared__ __align__(8) uint64_t full[S];
-  __shared__ double4 coef[kMaxPlanesPerChunk];  // (tzc1, tzc2, tzd1, tzd2) per output plane
+  // Dynamic smem only (TMA destinations at an aligned base):
+  // [ring: S slots x (u, v, w)][coef: (tzc1,tzc2,tzd1,tzd2) per output plane][S mbarriers]
+  extern __shared__ __align__(1024) double ring[];
+  double4* coef = reinterpret_cast<double4*>(ring + S * T::kSlotStride);
+  uint64_t* full = reinterpret_cast<uint64_t*>(coef + kMaxPlanesPerChunk);
 
   const int lane = threadIdx.x & 31;
   const int wy = threadIdx.x >> 5;
-  // Tiles are aligned to the INTERIOR: tile bx owns x in [1+64bx, 64bx+64], so
-  // nx = 512 needs exactly 8 tiles. A thread owns the pair (x, x+1), x odd.
   const int64_t x0 = 1 + (int64_t)blockIdx.x * kBX;
   const int64_t y0 = 1 + (int64_t)blockIdx.y * BY;
   const int64_t za = z_lo + (int64_t)blockIdx.z * planes_per_chunk;
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(32 * BY)
                            __ldg(tzd2 + za + j));
   __syncthreads();
 
-  const int32_t cx = (int32_t)(x0 - 2), cy = (int32_t)(y0 - 1);
+  const int32_t cx = (int32_t)(x0 - 1), cy = (int32_t)(y0 - 1);  // cx even: TMA alignment rule
   auto issue = [&](int p, int slot) {  // input plane za-1+p -> ring slot
     double* dstp = ring + slot * T::kSlotStride;
     uint64_t* bar = &full[slot];
@@ -141,104 +143,67 @@ __global__ void __launch_bounds__(32 * BY)
   if (threadIdx.x == 0)
     for (int p = 0; p < S && p < np; ++p) issue(p, p);
 
-  // Thread geometry inside a plane slot: smem row wy+1, column 2*lane+2.
-  const int oc = (wy + 1) * kSX + 2 * lane + 2;
+  constexpr int PS = T::kPlaneStride;
+  const int oc = (wy + 1) * kSX + 1 + lane;  // own cell inside a field plane
   const int64_t y = y0 + wy;
-  const int64_t x = x0 + 2 * lane;
-  const bool row_ok = y <= ny;
-  const bool ok0 = x <= nx;      // x >= 1 by construction
-  const bool ok1 = x + 1 <= nx;
-  // Stores are re-paired across lanes so they are 16-byte aligned: lane l>0
-  // writes (x-1, x) = (lane l-1's .y, own .x); lane 0 writes x alone and lane 31
-  // also writes x+1 alone.
-  const bool okm = x - 1 <= nx;  // x-1 >= 1 for lane > 0
+  const int64_t x = x0 + lane;
+  const bool ok = (y <= ny) && (x <= nx);
   const int64_t plane_elems = (ny + 2) * ldx;
   const int64_t g0 = (za * (ny + 2) + y) * ldx + x;
   double* pu = su + g0;
   double* pv = sv + g0;
   double* pw = sw + g0;
 
-  // ring slots of input planes j (m), j+1 (c), j+2 (p) and their phase parities
+  // ring slots of input planes j (m), j+1 (c), j+2 (p); parity of slot sp's next phase
   int sm_ = 0, sc = 1, sp = 2;
-  uint32_t par_p = 0;  // parity of slot sp's next completion
+  uint32_t par_p = 0;
   mbar_wait_parity(&full[0], 0);
   mbar_wait_parity(&full[1], 0);
-  const double* F = ring;
-  double2 um = lds2(F + oc), vm = lds2(F + T::kPlaneStride + oc), wm = lds2(F + 2 * T::kPlaneStride + oc);
-  F = ring + T::kSlotStride;
-  double2 uc = lds2(F + oc), vc = lds2(F + T::kPlaneStride + oc), wc = lds2(F + 2 * T::kPlaneStride + oc);
+  double um = ring[oc], vm = ring[PS + oc], wm = ring[2 * PS + oc];
+  double uc = ring[T::kSlotStride + oc], vc = ring[T::kSlotStride + PS + oc], wc = ring[T::kSlotStride + 2 * PS + oc];
 
   for (int j = 0; j + 2 < np; ++j) {  // output plane za+j from input planes j, j+1, j+2
     mbar_wait_parity(&full[sp], par_p);
     const double* U0 = ring + sc * T::kSlotStride;
-    const double* V0 = U0 + T::kPlaneStride;
-    const double* W0 = U0 + 2 * T::kPlaneStride;
+    const double* V0 = U0 + PS;
+    const double* W0 = U0 + 2 * PS;
     const double* Up = ring + sp * T::kSlotStride;
-    const double* Vp = Up + T::kPlaneStride;
-    const double* Wp = Up + 2 * T::kPlaneStride;
-    const double* Wm = ring + sm_ * T::kSlotStride + 2 * T::kPlaneStride;
+    const double* Vp = Up + PS;
+    const double* Wp = Up + 2 * PS;
+    const double* Wm = ring + sm_ * T::kSlotStride + 2 * PS;
 
-    const double2 up = lds2(Up + oc), vp = lds2(Vp + oc), wp = lds2(Wp + oc);
-    const double2 un = lds2(U0 + oc - kSX), us = lds2(U0 + oc + kSX);
-    const double2 vn = lds2(V0 + oc - kSX), vs = lds2(V0 + oc + kSX);
-    const double2 wn = lds2(W0 + oc - kSX), ws = lds2(W0 + oc + kSX);
-    const double u_xw = U0[oc - 1], u_xe = U0[oc + 2];
-    const double v_xw = V0[oc - 1], v_xe = V0[oc + 2];
-    const double w_xw = W0[oc - 1], w_xe = W0[oc + 2];
-    const double u_sw0 = U0[oc + kSX - 1];    // U(0,+1,-1) for point 0
-    const double v_ne1 = V0[oc - kSX + 2];    // V(0,-1,+1) for point 1
-    const double u_pw0 = Up[oc - 1];          // U(+1,0,-1) for point 0
-    const double2 vpn = lds2(Vp + oc - kSX);  // V(+1,-1,0)
-    const double w_me1 = Wm[oc + 2];          // W(-1,0,+1) for point 1
-    const double2 wms = lds2(Wm + oc + kSX);  // W(-1,+1,0)
+    PwPoint q;
+    q.up = Up[oc]; q.vp = Vp[oc]; q.wp = Wp[oc];
+    q.uc = uc; q.vc = vc; q.wc = wc;
+    q.um = um; q.vm = vm; q.wm = wm;
+    q.uw = U0[oc - 1]; q.ue = U0[oc + 1];
+    q.vw = V0[oc - 1]; q.ve = V0[oc + 1];
+    q.ww = W0[oc - 1]; q.we = W0[oc + 1];
+    q.un = U0[oc - kSX]; q.us = U0[oc + kSX];
+    q.vn = V0[oc - kSX]; q.vs = V0[oc + kSX];
+    q.wn = W0[oc - kSX]; q.ws = W0[oc + kSX];
+    q.u_sw = U0[oc + kSX - 1];  // U(0,+1,-1)
+    q.v_ne = V0[oc - kSX + 1];  // V(0,-1,+1)
+    q.u_pw = Up[oc - 1];        // U(+1,0,-1)
+    q.v_pn = Vp[oc - kSX];      // V(+1,-1,0)
+    q.w_me = Wm[oc + 1];        // W(-1,0,+1)
+    q.w_ms = Wm[oc + kSX];      // W(-1,+1,0)
 
     const double4 cz = coef[j];
     const PwCoef k = {tcx, tcy, cz.x, cz.y, cz.z, cz.w};
-    PwPoint p0, p1;
-    p0.uc = uc.x; p0.uw = u_xw; p0.ue = uc.y; p0.un = un.x; p0.us = us.x; p0.um = um.x; p0.up = up.x;
-    p0.u_sw = u_sw0; p0.u_pw = u_pw0;
-    p0.vc = vc.x; p0.vw = v_xw; p0.ve = vc.y; p0.vn = vn.x; p0.vs = vs.x; p0.vm = vm.x; p0.vp = vp.x;
-    p0.v_ne = vn.y; p0.v_pn = vpn.x;
-    p0.wc = wc.x; p0.ww = w_xw; p0.we = wc.y; p0.wn = wn.x; p0.ws = ws.x; p0.wm = wm.x; p0.wp = wp.x;
-    p0.w_me = wm.y; p0.w_ms = wms.x;
-
-    p1.uc = uc.y; p1.uw = uc.x; p1.ue = u_xe; p1.un = un.y; p1.us = us.y; p1.um = um.y; p1.up = up.y;
-    p1.u_sw = us.x; p1.u_pw = up.x;
-    p1.vc = vc.y; p1.vw = vc.x; p1.ve = v_xe; p1.vn = vn.y; p1.vs = vs.y; p1.vm = vm.y; p1.vp = vp.y;
-    p1.v_ne = v_ne1; p1.v_pn = vpn.y;
-    p1.wc = wc.y; p1.ww = wc.x; p1.we = w_xe; p1.wn = wn.y; p1.ws = ws.y; p1.wm = wm.y; p1.wp = wp.y;
-    p1.w_me = w_me1; p1.w_ms = wms.y;
-
-    double2 ou, ov, ow;
-    pw_point(p0, k, ou.x, ov.x, ow.x);
-    pw_point(p1, k, ou.y, ov.y, ow.y);
-
-    // re-pair for aligned stores: (x-1, x) <- (left lane's .y, own .x)
-    const double lu = __shfl_up_sync(0xffffffffu, ou.y, 1);
-    const double lv = __shfl_up_sync(0xffffffffu, ov.y, 1);
-    const double lw = __shfl_up_sync(0xffffffffu, ow.y, 1);
-    if (row_ok) {
-      if (lane > 0) {
-        if (ok0) {
-          stg2(pu - 1, make_double2(lu, ou.x));
-          stg2(pv - 1, make_double2(lv, ov.x));
-          stg2(pw - 1, make_double2(lw, ow.x));
-        } else if (okm) {
-          pu[-1] = lu; pv[-1] = lv; pw[-1] = lw;
-        }
-      } else if (ok0) {
-        pu[0] = ou.x; pv[0] = ov.x; pw[0] = ow.x;
-      }
-      if (lane == 31 && ok1) {
-        pu[1] = ou.y; pv[1] = ov.y; pw[1] = ow.y;
-      }
+    double ou, ov, ow;
+    pw_point(q, k, ou, ov, ow);
+    if (ok) {
+      *pu = ou;
+      *pv = ov;
+      *pw = ow;
     }
     pu += plane_elems;
     pv += plane_elems;
     pw += plane_elems;
 
     um = uc; vm = vc; wm = wc;
-    uc = up; vc = vp; wc = wp;
+    uc = q.up; vc = q.vp; wc = q.wp;
 
     // every read of input plane j (slot sm_) is done -> refill it with plane j+S
     __syncthreads();
@@ -264,7 +229,8 @@ st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s)
   for (int i = 0; i < 3; ++i)
     ST_TRY(make_tmap_3d_f64(&tm[i], f[i], dims, (uint64_t)a.ldx * 8,
                             (uint64_t)a.ldx * 8 * (uint64_t)(a.ny + 2), box));
-  const size_t smem = (size_t)S * T::kSlotStride * sizeof(double);
+  const size_t smem = (size_t)S * T::kSlotStride * sizeof(double) + kMaxPlanesPerChunk * sizeof(double4) +
+                      S * sizeof(uint64_t);
   ST_CHECK_CUDA(cudaFuncSetAttribute(pw_advect3d_kernel<BY, S>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t ntx = (a.nx + kBX - 1) / kBX;
@@ -288,11 +254,12 @@ st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaSt
   if (z_hi < z_lo) return ST_OK;
   static const int kVariant = env_int("ST_PW_VARIANT", 0);
   switch (kVariant) {
-    case 1: return launch_pw<8, 4>(a, z_lo, z_hi, s);
+    case 1: return launch_pw<8, 8>(a, z_lo, z_hi, s);
     case 2: return launch_pw<16, 5>(a, z_lo, z_hi, s);
-    case 3: return launch_pw<4, 8>(a, z_lo, z_hi, s);
-    case 4: return launch_pw<8, 5>(a, z_lo, z_hi, s);
-    default: return launch_pw<8, 6>(a, z_lo, z_hi, s);
+    case 3: return launch_pw<32, 4>(a, z_lo, z_hi, s);
+    case 4: return launch_pw<8, 6>(a, z_lo, z_hi, s);
+    case 5: return launch_pw<16, 8>(a, z_lo, z_hi, s);
+    default: return launch_pw<16, 6>(a, z_lo, z_hi, s);
   }
 }
 

@@ -17,6 +17,9 @@ for w in $WHAT; do
         python bench.py --steps 2 --warmup 1 --sweeps 100 --pw-apps 4 --no-e2e --no-cpu > $OUT/launches_bench.log 2>&1; echo "launches rc=$?" ;;
     ncu) timeout 900 $NCU --set full --clock-control none --import-source on -k regex:'jacobi2d_stream|pw_advect3d_kernel' -s 2 -c 4 \
         -o $OUT/prof python tools/prof_kernels.py --sweeps 4 --apps 3 > $OUT/ncu.log 2>&1; echo "ncu rc=$?"; tail -3 $OUT/ncu.log ;;
+    sanitize) for tool in memcheck racecheck synccheck; do
+        timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_cases.py > $OUT/sanitize_$tool.log 2>&1
+        echo "sanitize $tool rc=$?"; tail -3 $OUT/sanitize_$tool.log; done ;;
   esac
 done
 # tuning sweeps (quick bench lines, no e2e / cpu legs)

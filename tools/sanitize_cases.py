@@ -1,0 +1,22 @@
+"""Small invocations of every kernel for compute-sanitizer (memcheck/racecheck/synccheck/initcheck)."""
+import sys
+import pathlib
+
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+import numpy as np
+import torch
+
+import paper_2310_01882_b200 as st
+import stencil_inputs as si
+
+for nx, ny, iters, tb in ((64, 64, 5, 0), (130, 70, 3, 1), (130, 70, 5, 2), (130, 1100, 9, 4), (61, 37, 8, 8)):
+    a = torch.from_numpy(si.jacobi2d_grid(nx, ny)).cuda()
+    b = torch.empty_like(a)
+    st.st_jacobi2d_run(a, b, iters, tblock=tb)
+for nx, ny, nz in ((70, 13, 9), (129, 17, 70)):
+    d = si.pw_inputs(nx, ny, nz)
+    g = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in d.items()}
+    outs = [torch.zeros_like(g["u"]) for _ in range(3)]
+    st.st_pw_advect3d(g["u"], g["v"], g["w"], *outs, g["tcx"], g["tcy"], g["tzc1"], g["tzc2"], g["tzd1"], g["tzd2"])
+torch.cuda.synchronize()
+print("sanitize cases done")
