@@ -85,7 +85,7 @@ st_status make_tmap_2d_f64(CUtensorMap* map, const double* base, const uint64_t 
 namespace {
 
 // tblock=0 on grids of at least kAutoMin^2: T sweeps per pass (tuned on B200)
-constexpr int kAutoTblock = 6;
+constexpr int kAutoTblock = 4;
 constexpr int64_t kAutoMin = 128;
 
 st_status check_device_ptr(const void* p, const char* what) {

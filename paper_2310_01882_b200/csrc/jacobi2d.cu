@@ -178,10 +178,68 @@ namespace {
 // neighbours by 2T columns: after T levels only the centre 64-2T columns are
 // exact, so strips advance by 64-2T. Rows stream through a T-level software
 // pipeline held entirely in registers: level j keeps its two most recent rows
-// (N, C); when level j produces a new row S, level j+1 produces row C. W/E
+// (N, C); when level j-1 delivers a new row S, level j produces row C. W/E
 // neighbours at every level come from warp shuffles. Dirichlet rows/columns are
 // passed through unchanged at every level, so every level is exactly one Jacobi
-// sweep and the result is bitwise the same as T single sweeps.
+// sweep and the result is bitwise T single sweeps.
+//
+// Instruction diet (the kernel is issue-bound once T >= 4): each level keeps two
+// row slots; N is slot k%2 and C slot (k+1)%2, and the new row S overwrites the
+// N slot once N has been consumed, so with steps unrolled in groups of
+// kTbGroup (even) the rotation is register renaming, not moves. Groups that
+// touch no Dirichlet row, no chunk edge and no out-of-range load run a
+// check-free body (block-uniform branch); Dirichlet-column selects run only in
+// the strips that contain a ring column (warp-uniform branch). Load and store
+// addresses advance by one pitch per step instead of being recomputed.
+constexpr int kTbGroup = 4;  // steps per unrolled group (even: the slot rotation period is 2)
+
+template <int T, bool kChecked>
+__device__ __forceinline__ void tb_group(double2 (&st)[T][2], double2 (&buf)[kTbGroup], int64_t r0,
+                                         int64_t r_end, int64_t r_load_last, const double*& lp, double*& sp_out,
+                                         int64_t ld, bool has_pair, bool col_ring, bool ring0, bool ring1,
+                                         int64_t ring_lo, int64_t ring_hi, int64_t yc0, int64_t yc1, bool st0,
+                                         bool st1) {
+#pragma unroll
+  for (int k = 0; k < kTbGroup; ++k) {
+    const int64_t r = r0 + k;
+    if (kChecked && r > r_end) break;
+    double2 s = buf[k];  // level 0, row r
+    {                    // refill the slot with row r + kTbGroup (consumed one group later)
+      if (!kChecked || (has_pair && r + kTbGroup <= r_load_last)) buf[k] = ldg2(lp);
+      else buf[k] = make_double2(0.0, 0.0);
+      lp += ld;
+    }
+#pragma unroll
+    for (int j = 0; j < T; ++j) {
+      // level j: N = slot k%2, C = slot (k+1)%2; S (from level j-1) replaces N afterwards
+      const double2 n = st[j][k & 1];
+      const double2 c = st[j][(k + 1) & 1];
+      const double w = __shfl_up_sync(0xffffffffu, c.y, 1);
+      const double e = __shfl_down_sync(0xffffffffu, c.x, 1);
+      double2 o;
+      o.x = dmul(dadd(dadd(dadd(n.x, s.x), w), c.y), 0.25);
+      o.y = dmul(dadd(dadd(dadd(n.y, s.y), c.x), e), 0.25);
+      if (col_ring) {  // Dirichlet columns pass through
+        if (ring0) o.x = c.x;
+        if (ring1) o.y = c.y;
+      }
+      if (kChecked) {
+        const int64_t row = r - j - 1;
+        if (row <= ring_lo || row >= ring_hi) o = c;  // Dirichlet rows never change
+      }
+      st[j][k & 1] = s;
+      s = o;
+    }
+    // s = level T, row r-T
+    if (!kChecked || (r - T >= yc0 && r - T <= yc1)) {
+      if (st0 && st1) stg2(sp_out, s);
+      else if (st0) sp_out[0] = s.x;
+      else if (st1) sp_out[1] = s.y;
+    }
+    sp_out += ld;
+  }
+}
+
 template <int T>
 __global__ void __launch_bounds__(kStreamThreads)
     jacobi2d_tb_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
@@ -203,62 +261,37 @@ __global__ void __launch_bounds__(kStreamThreads)
   const bool st1 = st_lane && x + 1 >= 0 && x + 1 < nxp2;
   const bool ring0 = (x == 0) || (x == nxp2 - 1);
   const bool ring1 = (x + 1 == nxp2 - 1);
+  const int64_t x_first = strip * kStride - T;
+  const bool col_ring = x_first <= 0 || x_first + kStripCols >= nxp2 - 1;  // warp-uniform
   const double* sp = src + (has_pair ? x : 0);
 
-  // first/last input rows the pipeline reads; rows beyond are never loaded
+  // input rows the pipeline reads: [r_first, r_load_last]; steps run to r_end
   const int64_t r_first = max(max(ring_lo, (int64_t)0), yc0 - T);
   const int64_t r_load_last = min(min(ring_hi, nrows_buf - 1), yc1 + T);
-  const int64_t r_end = yc1 + T;  // steps continue past ring_hi (the ring row propagates)
+  const int64_t r_end = yc1 + T;
+  // steps r in [safe_lo, safe_hi] touch no Dirichlet row at any level, store an
+  // in-chunk row and (with their refill loads) read only existing rows
+  const int64_t safe_lo = max(ring_lo + T + 1, yc0 + T);
+  const int64_t safe_hi = min(min(ring_hi, yc1 + T), r_load_last - kTbGroup);
 
-  double2 n_[T], c_[T];  // level j: rows r-j-2 (n_) and r-j-1 (c_) before step r
+  double2 st[T][2];
 #pragma unroll
-  for (int j = 0; j < T; ++j) n_[j] = c_[j] = make_double2(0.0, 0.0);
-
-  constexpr int U = 4;
-  double2 pf[U];
-  auto load = [&](int64_t r) -> double2 {
-    return (has_pair && r <= r_load_last) ? ldg2(sp + r * ld) : make_double2(0.0, 0.0);
-  };
+  for (int j = 0; j < T; ++j) st[j][0] = st[j][1] = make_double2(0.0, 0.0);
+  double2 buf[kTbGroup];
 #pragma unroll
-  for (int k = 0; k < U; ++k) pf[k] = load(r_first + k);
-
-  for (int64_t r0 = r_first; r0 <= r_end; r0 += U) {
-    double2 nx_[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) nx_[k] = load(r0 + U + k);
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t r = r0 + k;
-      if (r <= r_end) {
-        double2 s = pf[k];  // level 0, row r
-#pragma unroll
-        for (int j = 0; j < T; ++j) {
-          // level j+1, row r-j-1 from level j rows r-j-2 (n), r-j-1 (c), r-j (s)
-          const int64_t row = r - j - 1;
-          const double2 c = c_[j];
-          double w = __shfl_up_sync(0xffffffffu, c.y, 1);
-          double e = __shfl_down_sync(0xffffffffu, c.x, 1);
-          double2 o;
-          o.x = dmul(dadd(dadd(dadd(n_[j].x, s.x), w), c.y), 0.25);
-          o.y = dmul(dadd(dadd(dadd(n_[j].y, s.y), c.x), e), 0.25);
-          if (ring0) o.x = c.x;
-          if (ring1) o.y = c.y;
-          if (row <= ring_lo || row >= ring_hi) o = c;  // Dirichlet rows never change
-          n_[j] = c;
-          c_[j] = s;
-          s = o;
-        }
-        const int64_t orow = r - T;  // s = level T, row r-T
-        if (orow >= yc0 && orow <= yc1) {
-          double* dp = dst + orow * ld + x;
-          if (st0 && st1) stg2(dp, s);
-          else if (st0) dp[0] = s.x;
-          else if (st1) dp[1] = s.y;
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) pf[k] = nx_[k];
+  for (int k = 0; k < kTbGroup; ++k) {
+    const int64_t rr = r_first + k;
+    buf[k] = (has_pair && rr <= r_load_last) ? ldg2(sp + rr * ld) : make_double2(0.0, 0.0);
+  }
+  const double* lp = sp + (r_first + kTbGroup) * ld;  // next row to load
+  double* sp_out = dst + x + (r_first - T) * ld;      // row the next step stores
+  for (int64_t r0 = r_first; r0 <= r_end; r0 += kTbGroup) {
+    if (r0 >= safe_lo && r0 + kTbGroup - 1 <= safe_hi)
+      tb_group<T, false>(st, buf, r0, r_end, r_load_last, lp, sp_out, ld, has_pair, col_ring, ring0, ring1,
+                         ring_lo, ring_hi, yc0, yc1, st0, st1);
+    else
+      tb_group<T, true>(st, buf, r0, r_end, r_load_last, lp, sp_out, ld, has_pair, col_ring, ring0, ring1,
+                        ring_lo, ring_hi, yc0, yc1, st0, st1);
   }
 }
 
