@@ -123,6 +123,40 @@ st_status st_halo_exchange(st_comm* comm, double* const* fields, int32_t nfields
 /* 2-D Jacobi 5-point sweep (Listing 1)                      */
 /* ------------------------------------------------------------------------ */
 
+/* One step of the per-rank schedule st_jacobi2d_run executes (host-only, so
+ * the decomposition / halo-swap / temporal-blocking logic is testable without
+ * a GPU). Buffers: 0 = a, 1 = b.
+ *   ST_OP_SWEEP     dst = buffer 1-buf gets rows [y_lo, y_hi] (buffer rows) of
+ *                   the state `sweeps` Jacobi sweeps after buffer `buf`; rows
+ *                   <= ring_lo and >= ring_hi are Dirichlet (unchanged at every
+ *                   level). sweeps == 1: one sweep; sweeps >= 2 (even): one
+ *                   temporally blocked pass.
+ *   ST_OP_EXCHANGE  halo swap (st_halo_plan, width `sweeps`) of buffer `buf`;
+ *                   flag = 1: asynchronous (overlaps the following sweeps and
+ *                   must be joined by ST_OP_JOIN), 0: joined immediately.
+ *   ST_OP_JOIN      the main stream waits for the pending exchange.
+ *   ST_OP_SWAP      the roles of the buffers swap (the next state lives in 1-buf). */
+enum { ST_OP_SWEEP = 1, ST_OP_EXCHANGE = 2, ST_OP_JOIN = 3, ST_OP_SWAP = 4 };
+
+typedef struct {
+  int32_t kind;
+  int32_t buf;
+  int32_t sweeps;
+  int32_t flag;
+  int64_t y_lo, y_hi;
+  int64_t ring_lo, ring_hi;
+} st_op;
+
+/* Builds the schedule of st_jacobi2d_run for one rank: `iters` sweeps of a
+ * slab of ny_local owned rows with `halo` ghost rows per side (nranks == 1:
+ * halo must be 1 and the ghost rows are the Dirichlet rows), temporal
+ * blocking depth `tblock` (1, or even T <= halo; 0 = auto). Writes up to `cap`
+ * ops and the total count to *nops (call with cap = 0 to size the buffer).
+ * Host-only; no device needed. */
+st_status st_jacobi2d_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_t ny_local,
+                               int32_t halo, int64_t iters, int32_t tblock, st_op* ops,
+                               int64_t cap, int64_t* nops);
+
 /* `iters` sweeps of
  *     B[y][x] = (((A[y-1][x] + A[y+1][x]) + A[y][x-1]) + A[y][x+1]) * 0.25
  * over the interior 1 <= y <= ny_local, 1 <= x <= nx, with value semantics
@@ -136,9 +170,12 @@ st_status st_halo_exchange(st_comm* comm, double* const* fields, int32_t nfields
  *   comm NULL halo must be 1; rows 0 and ny_local+1 are the Dirichlet ring.
  *   comm set  rank-local row slab of a global grid; halo = ghost depth
  *             (>= max(1, tblock)); ghost rows are refreshed from the
- *             neighbouring ranks every `halo` sweeps, overlapped with interior
- *             rows. On the first/last rank the ghost row adjacent to the owned
- *             rows holds the global Dirichlet row. Requires ny_local >= halo.
+ *             neighbouring ranks whenever the sweeps since the last swap
+ *             would exceed `halo`, and the swap of a pass's boundary rows
+ *             overlaps that pass's interior rows. On the first/last rank the
+ *             ghost row adjacent to the owned rows holds the global Dirichlet
+ *             row. Requires ny_local >= halo. The exact step sequence is
+ *             st_jacobi2d_schedule's.
  *   iters     >= 0; 0 is a no-op.
  *   tblock    0 = auto; 1 = one sweep per pass over HBM; T >= 2 = temporal
  *             blocking (T sweeps per pass). Any choice gives bitwise the same

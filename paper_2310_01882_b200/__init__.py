@@ -12,6 +12,7 @@ Entry points (same names as the C ABI, tensors instead of raw pointers):
     st_pw_advect3d(u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, tzd1, tzd2, comm=None, nx=None)
     st_halo_exchange(comm, fields, n_slow_local, slab_pitch, width)
     st_halo_plan(rank, nranks, n_slow_local, slab_pitch, width) -> (sends, recvs)   [host only]
+    st_jacobi2d_schedule(rank, nranks, nx, ny_local, halo, iters, tblock) -> [ops]   [host only]
     st_block_split(n, nranks, rank) -> (start, count)                                [host only]
     Comm.create(rank, nranks, unique_id, device) / Comm.from_process_group(pg, device)
 """
@@ -40,6 +41,14 @@ class Xfer(ctypes.Structure):
     _fields_ = [("peer", ctypes.c_int32), ("offset", ctypes.c_int64), ("count", ctypes.c_int64)]
 
 
+class Op(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("buf", ctypes.c_int32), ("sweeps", ctypes.c_int32),
+                ("flag", ctypes.c_int32), ("y_lo", ctypes.c_int64), ("y_hi", ctypes.c_int64),
+                ("ring_lo", ctypes.c_int64), ("ring_hi", ctypes.c_int64)]
+
+
+OP_SWEEP, OP_EXCHANGE, OP_JOIN, OP_SWAP = 1, 2, 3, 4
+
 _vp, _i64, _i32, _dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
 
 _SIGS = {
@@ -54,6 +63,8 @@ _SIGS = {
     "st_halo_plan": (ctypes.c_int, [_i32, _i32, _i64, _i64, _i32, ctypes.POINTER(Xfer),
                                     ctypes.POINTER(_i32), ctypes.POINTER(Xfer), ctypes.POINTER(_i32)]),
     "st_halo_exchange": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), _i32, _i64, _i64, _i32, _vp]),
+    "st_jacobi2d_schedule": (ctypes.c_int, [_i32, _i32, _i64, _i64, _i32, _i64, _i32, ctypes.POINTER(Op), _i64,
+                                            ctypes.POINTER(_i64)]),
     "st_jacobi2d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i32, _i64, _i32, _vp, _vp,
                                        ctypes.POINTER(_i32)]),
     "st_pw_advect3d": (ctypes.c_int, [_vp] * 6 + [_i64] * 4 + [_dbl, _dbl] + [_vp] * 4 + [_vp, _vp]),
@@ -166,6 +177,18 @@ def st_halo_plan(rank: int, nranks: int, n_slow_local: int, slab_pitch: int, wid
                               recvs, ctypes.byref(nr)), "st_halo_plan")
     conv = lambda x: (x.peer, x.offset, x.count)
     return [conv(sends[i]) for i in range(ns.value)], [conv(recvs[i]) for i in range(nr.value)]
+
+
+def st_jacobi2d_schedule(rank: int, nranks: int, nx: int, ny_local: int, halo: int, iters: int,
+                         tblock: int = 0) -> list[dict]:
+    """The step schedule st_jacobi2d_run executes for one rank (host only)."""
+    n = _i64()
+    _check(lib().st_jacobi2d_schedule(rank, nranks, nx, ny_local, halo, iters, tblock, None, 0, ctypes.byref(n)),
+           "st_jacobi2d_schedule")
+    arr = (Op * max(1, n.value))()
+    _check(lib().st_jacobi2d_schedule(rank, nranks, nx, ny_local, halo, iters, tblock, arr, n.value,
+                                      ctypes.byref(n)), "st_jacobi2d_schedule")
+    return [{f: getattr(arr[i], f) for f, _ in Op._fields_} for i in range(n.value)]
 
 
 # ------------------------------------------------------------- compute ---

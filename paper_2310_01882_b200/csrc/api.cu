@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "comm.h"
 #include "common.cuh"
@@ -84,10 +85,6 @@ st_status make_tmap_2d_f64(CUtensorMap* map, const double* base, const uint64_t 
 // ------------------------------------------------------- Jacobi driver ---
 namespace {
 
-// tblock=0 on grids of at least kAutoMin^2: T sweeps per pass (tuned on B200)
-constexpr int kAutoTblock = 4;
-constexpr int64_t kAutoMin = 128;
-
 st_status check_device_ptr(const void* p, const char* what) {
   cudaPointerAttributes at;
   cudaError_t e = cudaPointerGetAttributes(&at, p);
@@ -101,110 +98,31 @@ st_status check_device_ptr(const void* p, const char* what) {
   return ST_OK;
 }
 
-// Split `iters` sweeps into passes of at most T (even) sweeps such that the
-// number of passes has the parity of `iters`: every pass reads one buffer and
-// writes the other, so the result lands where plain Jacobi ping-pong puts it
-// (b iff iters odd). Passes are even-sized (temporal-blocking kernel) or 1
-// (single-sweep kernel).
-int plan_passes(int64_t iters, int t, int64_t* out, int cap) {
-  if (t < 2 || (t & 1)) return -1;
-  int n = 0;
-  int64_t left = iters;
-  while (left >= t && n < cap) { out[n++] = t; left -= t; }
-  if (left >= 2 && n < cap) { out[n++] = left & ~int64_t(1); left &= 1; }
-  if (left == 1 && n < cap) { out[n++] = 1; left = 0; }
-  if (left != 0) return -1;
-  if ((n & 1) != (int)(iters & 1)) {
-    for (int i = 0; i < n; ++i) {
-      if (out[i] >= 2 && n < cap) {
-        for (int j = n; j > i + 1; --j) out[j] = out[j - 1];
-        if (out[i] >= 4) { out[i + 1] = 2; out[i] -= 2; }
-        else { out[i + 1] = 1; out[i] = 1; }
-        ++n;
+// Executes the schedule of build_jacobi_schedule (schedule.cu) on the GPU.
+st_status run_schedule(const std::vector<st_op>& ops, st_comm* comm, double* a, double* b, int64_t nx,
+                       int64_t n, int64_t ld, int32_t h, cudaStream_t s) {
+  double* buf[2] = {a, b};
+  const int64_t nrows = n + 2 * (int64_t)h;
+  for (const st_op& o : ops) {
+    switch (o.kind) {
+      case ST_OP_SWEEP:
+        if (o.sweeps == 1)
+          ST_TRY(jacobi2d_sweep_rows(buf[o.buf], buf[1 - o.buf], nx, ld, o.y_lo, o.y_hi, s));
+        else
+          ST_TRY(jacobi2d_tb_rows(buf[o.buf], buf[1 - o.buf], nx, ld, o.y_lo, o.y_hi, o.sweeps, o.ring_lo,
+                                  o.ring_hi, nrows, s));
         break;
-      }
+      case ST_OP_EXCHANGE:
+        ST_TRY(halo_exchange_async(comm, &buf[o.buf], 1, n, ld, o.sweeps, s, o.flag == 0));
+        break;
+      case ST_OP_JOIN:
+        if (comm && comm->nranks > 1) ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
+        break;
+      case ST_OP_SWAP:
+        break;
+      default:
+        ST_RETURN_IF(true, ST_EINTERNAL, "jacobi2d: bad schedule op %d", o.kind);
     }
-  }
-  return n;
-}
-
-st_status one_pass(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
-                   int64_t sweeps, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s) {
-  if (sweeps == 1) return jacobi2d_sweep_rows(src, dst, nx, ld, y_lo, y_hi, s);
-  return jacobi2d_tb_rows(src, dst, nx, ld, y_lo, y_hi, (int)sweeps, ring_lo, ring_hi, nrows_buf, s);
-}
-
-// Single-domain run (no comm): halo == 1, rows 0 and ny+1 Dirichlet.
-st_status jacobi2d_single(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t iters,
-                          int32_t tblock, cudaStream_t s) {
-  if (tblock == 0 && jacobi2d_resident_fits(nx, ny)) return jacobi2d_resident(a, b, nx, ny, ld, iters, s);
-  // halo rows a -> b (ring columns are passed through by every sweep); pitch padding untouched
-  ST_CHECK_CUDA(cudaMemcpyAsync(b, a, (size_t)(nx + 2) * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  ST_CHECK_CUDA(cudaMemcpyAsync(b + (ny + 1) * ld, a + (ny + 1) * ld, (size_t)(nx + 2) * sizeof(double),
-                                cudaMemcpyDeviceToDevice, s));
-  int t = tblock;
-  if (t == 0) t = (nx >= kAutoMin && ny >= kAutoMin) ? env_int("ST_JACOBI_T", kAutoTblock) : 1;
-  if (t > 1 && !jacobi2d_tb_supported(t)) {
-    ST_RETURN_IF(tblock != 0, ST_ENOTSUP, "jacobi2d: tblock=%d not supported (1, 2, 4, 6, 8)", tblock);
-    t = 1;
-  }
-  double* src = a;
-  double* dst = b;
-  if (t <= 1) {
-    for (int64_t it = 0; it < iters; ++it) {
-      ST_TRY(jacobi2d_sweep_rows(src, dst, nx, ld, 1, ny, s));
-      double* tmp = src; src = dst; dst = tmp;
-    }
-    return ST_OK;
-  }
-  int64_t pass[64];
-  int64_t done = 0;
-  while (done < iters) {
-    // plan in blocks so the pass list stays bounded; each block keeps parity
-    const int64_t blk = std::min<int64_t>(iters - done, (int64_t)t * 48);
-    const int n = plan_passes(blk, t, pass, 64);
-    ST_RETURN_IF(n < 0, ST_EINTERNAL, "jacobi2d: pass planning failed");
-    for (int i = 0; i < n; ++i) {
-      ST_TRY(one_pass(src, dst, nx, ld, 1, ny, pass[i], 0, ny + 1, ny + 2, s));
-      double* tmp = src; src = dst; dst = tmp;
-    }
-    done += blk;
-  }
-  return ST_OK;
-}
-
-// Rank-local slab run: ghost depth h, ghosts swapped every h sweeps.
-st_status jacobi2d_slab(st_comm* comm, double* a, double* b, int64_t nx, int64_t n, int64_t ld,
-                        int32_t h, int64_t iters, cudaStream_t s) {
-  const bool lo_edge = comm->rank == 0, hi_edge = comm->rank == comm->nranks - 1;
-  const size_t pitch = (size_t)ld * sizeof(double), width = (size_t)(nx + 2) * sizeof(double);
-  // all ghost rows (incl. the edge ranks' Dirichlet row) a -> b; pitch padding untouched
-  ST_CHECK_CUDA(cudaMemcpy2DAsync(b, pitch, a, pitch, width, (size_t)h, cudaMemcpyDeviceToDevice, s));
-  ST_CHECK_CUDA(cudaMemcpy2DAsync(b + (h + n) * ld, pitch, a + (h + n) * ld, pitch, width, (size_t)h,
-                                  cudaMemcpyDeviceToDevice, s));
-  double* src = a;
-  double* dst = b;
-  // the initial state's ghosts come from the neighbours
-  ST_TRY(halo_exchange_async(comm, &src, 1, n, ld, h, s, true));
-  if (h == 1) {
-    // boundary rows first, their swap overlaps the interior rows
-    for (int64_t it = 0; it < iters; ++it) {
-      ST_TRY(jacobi2d_sweep_rows(src, dst, nx, ld, 1, 1, s));
-      if (n >= 2) ST_TRY(jacobi2d_sweep_rows(src, dst, nx, ld, n, n, s));
-      ST_TRY(halo_exchange_async(comm, &dst, 1, n, ld, 1, s, false));
-      ST_TRY(jacobi2d_sweep_rows(src, dst, nx, ld, 2, n - 1, s));
-      if (comm->nranks > 1) ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
-      double* tmp = src; src = dst; dst = tmp;
-    }
-    return ST_OK;
-  }
-  for (int64_t it = 0; it < iters; ++it) {
-    const int64_t k = it % h;
-    if (k == 0 && it > 0) ST_TRY(halo_exchange_async(comm, &src, 1, n, ld, h, s, true));
-    const int64_t lo = lo_edge ? h : k + 1;
-    const int64_t hi = hi_edge ? h + n - 1 : 2 * h + n - 2 - k;
-    ST_TRY(jacobi2d_sweep_rows(src, dst, nx, ld, lo, hi, s));
-    double* tmp = src; src = dst; dst = tmp;
   }
   return ST_OK;
 }
@@ -237,7 +155,6 @@ st_status st_jacobi2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
   ST_RETURN_IF(!comm && halo != 1, ST_EINVAL, "st_jacobi2d_run: halo must be 1 without a comm");
   ST_RETURN_IF(comm && ny < halo, ST_EINVAL, "st_jacobi2d_run: slab of %lld rows < halo %d",
                (long long)ny, halo);
-  ST_RETURN_IF(comm && tblock > 1, ST_ENOTSUP, "st_jacobi2d_run: temporal blocking across ranks not built");
   const size_t bytes = (size_t)(ny + 2 * halo) * (size_t)ld * sizeof(double);
   ST_RETURN_IF(overlaps(a, bytes, b, bytes), ST_EINVAL, "st_jacobi2d_run: a and b overlap");
   ST_TRY(check_device_ptr(a, "a"));
@@ -245,9 +162,19 @@ st_status st_jacobi2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
   if (result_in_b) *result_in_b = (int32_t)(iters & 1);
   if (iters == 0) return ST_OK;
   cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
-  if (!comm) return jacobi2d_single(a, b, nx, ny, ld, iters, tblock, s);
-  ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier NCCL error");
-  return jacobi2d_slab(comm, a, b, nx, ny, ld, halo, iters, s);
+  const int32_t nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
+  if (comm) ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier NCCL error");
+  // launch-bound small grids: every sweep inside one CTA's shared memory
+  if (nranks == 1 && tblock == 0 && halo == 1 && jacobi2d_resident_fits(nx, ny))
+    return jacobi2d_resident(a, b, nx, ny, ld, iters, s);
+  std::vector<st_op> ops;
+  ST_TRY(build_jacobi_schedule(rank, nranks, nx, ny, halo, iters, tblock, ops));
+  // ghost / Dirichlet rows a -> b (ring columns are passed through by every sweep); pitch padding untouched
+  const size_t pitch = (size_t)ld * sizeof(double), width = (size_t)(nx + 2) * sizeof(double);
+  ST_CHECK_CUDA(cudaMemcpy2DAsync(b, pitch, a, pitch, width, (size_t)halo, cudaMemcpyDeviceToDevice, s));
+  ST_CHECK_CUDA(cudaMemcpy2DAsync(b + (halo + ny) * ld, pitch, a + (halo + ny) * ld, pitch, width, (size_t)halo,
+                                  cudaMemcpyDeviceToDevice, s));
+  return run_schedule(ops, comm, a, b, nx, ny, ld, halo, s);
 }
 
 st_status st_pw_advect3d(double* u, double* v, double* w, double* su, double* sv, double* sw,

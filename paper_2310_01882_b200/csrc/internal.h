@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "libstencil.h"
 
 namespace st {
@@ -45,6 +47,11 @@ struct PwArgs {
 };
 // Computes output planes [z_lo, z_hi] (local plane indices, 1-based interior).
 st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s);
+
+// ------------------------------------------------------------ schedule ---
+int choose_tblock(int32_t nranks, int64_t nx, int64_t n, int32_t h, int32_t tblock);
+st_status build_jacobi_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_t n, int32_t h,
+                                int64_t iters, int32_t tblock, std::vector<st_op>& ops);
 
 // --------------------------------------------------------------- misc ---
 int env_int(const char* name, int dflt);
