@@ -186,62 +186,43 @@ namespace {
 // Instruction diet (the kernel is issue-bound once T >= 4): each level keeps two
 // row slots; N is slot k%2 and C slot (k+1)%2, and the new row S overwrites the
 // N slot once N has been consumed, so with steps unrolled in groups of
-// kTbGroup (even) the rotation is register renaming, not moves. Groups that
-// touch no Dirichlet row, no chunk edge and no out-of-range load run a
-// check-free body (block-uniform branch); Dirichlet-column selects run only in
-// the strips that contain a ring column (warp-uniform branch). Load and store
-// addresses advance by one pitch per step instead of being recomputed.
+// kTbGroup (even) the rotation is register renaming, not moves. The refill
+// load of every step is unconditional (its address is clamped to a valid row),
+// so no select ever waits on an in-flight load; the per-level Dirichlet-row and
+// Dirichlet-column handling is compiled into separate level bodies chosen per
+// step by a block-/warp-uniform branch, so steady-state steps carry no checks.
+// Load and store addresses advance by one pitch per step.
 constexpr int kTbGroup = 4;  // steps per unrolled group (even: the slot rotation period is 2)
 
-template <int T, bool kChecked>
-__device__ __forceinline__ void tb_group(double2 (&st)[T][2], double2 (&buf)[kTbGroup], int64_t r0,
-                                         int64_t r_end, int64_t r_load_last, const double*& lp, double*& sp_out,
-                                         int64_t ld, bool has_pair, bool col_ring, bool ring0, bool ring1,
-                                         int64_t ring_lo, int64_t ring_hi, int64_t yc0, int64_t yc1, bool st0,
-                                         bool st1) {
+template <int T, bool kRows, bool kCols>
+__device__ __forceinline__ double2 tb_levels(double2 (&st)[T][2], const int k, double2 s, int64_t r,
+                                             bool ring0, bool ring1, int64_t ring_lo, int64_t ring_hi) {
 #pragma unroll
-  for (int k = 0; k < kTbGroup; ++k) {
-    const int64_t r = r0 + k;
-    if (kChecked && r > r_end) break;
-    double2 s = buf[k];  // level 0, row r
-    {                    // refill the slot with row r + kTbGroup (consumed one group later)
-      if (!kChecked || (has_pair && r + kTbGroup <= r_load_last)) buf[k] = ldg2(lp);
-      else buf[k] = make_double2(0.0, 0.0);
-      lp += ld;
+  for (int j = 0; j < T; ++j) {
+    // level j: N = slot k%2, C = slot (k+1)%2; S (from level j-1) replaces N afterwards
+    const double2 n = st[j][k & 1];
+    const double2 c = st[j][(k + 1) & 1];
+    const double w = __shfl_up_sync(0xffffffffu, c.y, 1);
+    const double e = __shfl_down_sync(0xffffffffu, c.x, 1);
+    double2 o;
+    o.x = dmul(dadd(dadd(dadd(n.x, s.x), w), c.y), 0.25);
+    o.y = dmul(dadd(dadd(dadd(n.y, s.y), c.x), e), 0.25);
+    if (kCols) {  // Dirichlet columns pass through
+      if (ring0) o.x = c.x;
+      if (ring1) o.y = c.y;
     }
-#pragma unroll
-    for (int j = 0; j < T; ++j) {
-      // level j: N = slot k%2, C = slot (k+1)%2; S (from level j-1) replaces N afterwards
-      const double2 n = st[j][k & 1];
-      const double2 c = st[j][(k + 1) & 1];
-      const double w = __shfl_up_sync(0xffffffffu, c.y, 1);
-      const double e = __shfl_down_sync(0xffffffffu, c.x, 1);
-      double2 o;
-      o.x = dmul(dadd(dadd(dadd(n.x, s.x), w), c.y), 0.25);
-      o.y = dmul(dadd(dadd(dadd(n.y, s.y), c.x), e), 0.25);
-      if (col_ring) {  // Dirichlet columns pass through
-        if (ring0) o.x = c.x;
-        if (ring1) o.y = c.y;
-      }
-      if (kChecked) {
-        const int64_t row = r - j - 1;
-        if (row <= ring_lo || row >= ring_hi) o = c;  // Dirichlet rows never change
-      }
-      st[j][k & 1] = s;
-      s = o;
+    if (kRows) {
+      const int64_t row = r - j - 1;
+      if (row <= ring_lo || row >= ring_hi) o = c;  // Dirichlet rows never change
     }
-    // s = level T, row r-T
-    if (!kChecked || (r - T >= yc0 && r - T <= yc1)) {
-      if (st0 && st1) stg2(sp_out, s);
-      else if (st0) sp_out[0] = s.x;
-      else if (st1) sp_out[1] = s.y;
-    }
-    sp_out += ld;
+    st[j][k & 1] = s;
+    s = o;
   }
+  return s;
 }
 
-template <int T>
-__global__ void __launch_bounds__(kStreamThreads)
+template <int T, int kMinBlocks>
+__global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
     jacobi2d_tb_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
                        int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk, int64_t nstrips, int64_t ring_lo,
                        int64_t ring_hi, int64_t nrows_buf) {
@@ -263,35 +244,49 @@ __global__ void __launch_bounds__(kStreamThreads)
   const bool ring1 = (x + 1 == nxp2 - 1);
   const int64_t x_first = strip * kStride - T;
   const bool col_ring = x_first <= 0 || x_first + kStripCols >= nxp2 - 1;  // warp-uniform
-  const double* sp = src + (has_pair ? x : 0);
+  const double* sp = src + (has_pair ? x : 0);  // every lane loads from a valid column
 
   // input rows the pipeline reads: [r_first, r_load_last]; steps run to r_end
   const int64_t r_first = max(max(ring_lo, (int64_t)0), yc0 - T);
   const int64_t r_load_last = min(min(ring_hi, nrows_buf - 1), yc1 + T);
   const int64_t r_end = yc1 + T;
-  // steps r in [safe_lo, safe_hi] touch no Dirichlet row at any level, store an
-  // in-chunk row and (with their refill loads) read only existing rows
-  const int64_t safe_lo = max(ring_lo + T + 1, yc0 + T);
-  const int64_t safe_hi = min(min(ring_hi, yc1 + T), r_load_last - kTbGroup);
 
   double2 st[T][2];
 #pragma unroll
   for (int j = 0; j < T; ++j) st[j][0] = st[j][1] = make_double2(0.0, 0.0);
-  double2 buf[kTbGroup];
+  double2 buf[kTbGroup];  // input rows r0..r0+G-1; slot k is refilled with row r0+k+G after use
+  const double* safe = sp + r_first * ld;
 #pragma unroll
-  for (int k = 0; k < kTbGroup; ++k) {
-    const int64_t rr = r_first + k;
-    buf[k] = (has_pair && rr <= r_load_last) ? ldg2(sp + rr * ld) : make_double2(0.0, 0.0);
-  }
+  for (int k = 0; k < kTbGroup; ++k) buf[k] = ldg2(r_first + k <= r_load_last ? sp + (r_first + k) * ld : safe);
   const double* lp = sp + (r_first + kTbGroup) * ld;  // next row to load
   double* sp_out = dst + x + (r_first - T) * ld;      // row the next step stores
+
   for (int64_t r0 = r_first; r0 <= r_end; r0 += kTbGroup) {
-    if (r0 >= safe_lo && r0 + kTbGroup - 1 <= safe_hi)
-      tb_group<T, false>(st, buf, r0, r_end, r_load_last, lp, sp_out, ld, has_pair, col_ring, ring0, ring1,
-                         ring_lo, ring_hi, yc0, yc1, st0, st1);
-    else
-      tb_group<T, true>(st, buf, r0, r_end, r_load_last, lp, sp_out, ld, has_pair, col_ring, ring0, ring1,
-                        ring_lo, ring_hi, yc0, yc1, st0, st1);
+#pragma unroll
+    for (int k = 0; k < kTbGroup; ++k) {
+      const int64_t r = r0 + k;
+      if (r > r_end) break;
+      const double2 s0 = buf[k];
+      buf[k] = ldg2(r + kTbGroup <= r_load_last ? lp : safe);
+      lp += ld;
+      // does any level of this step touch a Dirichlet row (rows r-1 .. r-T)?
+      const bool rows_chk = (r - T <= ring_lo) || (r - 1 >= ring_hi);
+      double2 o;
+      if (rows_chk) {
+        o = col_ring ? tb_levels<T, true, true>(st, k, s0, r, ring0, ring1, ring_lo, ring_hi)
+                     : tb_levels<T, true, false>(st, k, s0, r, ring0, ring1, ring_lo, ring_hi);
+      } else {
+        o = col_ring ? tb_levels<T, false, true>(st, k, s0, r, ring0, ring1, ring_lo, ring_hi)
+                     : tb_levels<T, false, false>(st, k, s0, r, ring0, ring1, ring_lo, ring_hi);
+      }
+      // o = level T, row r-T
+      if (r - T >= yc0 && r - T <= yc1) {
+        if (st0 && st1) stg2(sp_out, o);
+        else if (st0) sp_out[0] = o.x;
+        else if (st1) sp_out[1] = o.y;
+      }
+      sp_out += ld;
+    }
   }
 }
 
@@ -307,8 +302,16 @@ st_status launch_tb(const double* src, double* dst, int64_t nx, int64_t ld, int6
   const int64_t nchunks = (rows + rpc - 1) / rpc;
   ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d tb: too many row chunks");
   dim3 grid((unsigned)((nstrips + kStreamWarps - 1) / kStreamWarps), (unsigned)nchunks);
-  jacobi2d_tb_kernel<T><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
-                                                        ring_hi, nrows_buf);
+  static const int kOcc = env_int("ST_JACOBI_TB_OCC", 2);
+  if (kOcc == 3)
+    jacobi2d_tb_kernel<T, 3><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
+                                                             ring_hi, nrows_buf);
+  else if (kOcc == 2)
+    jacobi2d_tb_kernel<T, 2><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
+                                                             ring_hi, nrows_buf);
+  else
+    jacobi2d_tb_kernel<T, 1><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
+                                                             ring_hi, nrows_buf);
   ST_LAUNCHED();
   return ST_OK;
 }
