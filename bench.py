@@ -109,6 +109,12 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def pitch(n: int, align: int) -> int:
+    """Row pitch in doubles: n rounded up to a multiple of `align` (even)."""
+    align = max(2, align + (align & 1))
+    return (n + align - 1) // align * align
+
+
 def host_info():
     model = ""
     try:
@@ -193,7 +199,8 @@ def main():
     ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
     ap.add_argument("--sweeps", type=int, default=1000, help="Jacobi sweeps per step (configs[1]: 1000)")
     ap.add_argument("--tblock", type=int, default=0)
-    ap.add_argument("--halo", type=int, default=4, help="ghost rows per side across ranks (N>1)")
+    ap.add_argument("--halo", type=int, default=6, help="ghost rows per side across ranks (N>1)")
+    ap.add_argument("--align", type=int, default=2, help="row pitch multiple in doubles (2 = 16-byte rows)")
     ap.add_argument("--pw-apps", type=int, default=20, help="PW applications timed")
     ap.add_argument("--no-pw", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -241,7 +248,7 @@ def main():
     n_glob = 16384 if world == 1 else 32768
     halo = 1 if world == 1 else args.halo  # ghost depth across ranks (>= the temporal-blocking depth)
     ny0, ny_loc = st.st_block_split(n_glob, world, rank)
-    ld = n_glob + 2
+    ld = pitch(n_glob + 2, args.align)
     rows = ny_loc + 2 * halo
     # rank slab: buffer row l <-> global padded row ny0 + 1 + (l - halo); rows beyond the grid stay 0
     g_lo = max(0, ny0 + 1 - halo)
@@ -329,7 +336,7 @@ def main():
         nxy = 512 if world == 1 else 1024
         nz_glob = 512
         z0, nz_loc = st.st_block_split(nz_glob, world, rank)
-        d = si.pw_inputs(nxy, nxy, nz_glob, plane0=z0, planes=nz_loc + 2)
+        d = si.pw_inputs(nxy, nxy, nz_glob, ldx=pitch(nxy + 2, args.align), plane0=z0, planes=nz_loc + 2)
         g = {k: (torch.from_numpy(v).to(dev) if hasattr(v, "shape") else v) for k, v in d.items()}
         outs = [torch.empty_like(g["u"]) for _ in range(3)]
 
@@ -351,6 +358,7 @@ def main():
         pts = nxy * nxy * nz_glob
         pw_gbs = PW_BYTES_PER_PT * nxy * nxy * nz_loc / (app_ms / 1e3) / 1e9
         pw = {"workload": f"pw_advect3d_{nxy}x{nxy}x{nz_glob}_fp64" + ("" if world == 1 else f"_zslabs{world}"),
+              "ldx": pitch(nxy + 2, args.align),
               "value": round(pts / (app_ms / 1e3) / 1e9, 3), "unit": UNIT, "ms_per_app": round(app_ms, 4),
               "apps": args.pw_apps, "gpu_launches": pw_launches,
               "roofline": {"bound": "hbm", "achieved": round(pw_gbs, 1), "peak": hbm_peak, "unit": "GB/s",

@@ -93,8 +93,11 @@ __device__ __forceinline__ void pw_point(const PwPoint& p, const PwCoef& k, doub
   sw = dadd(dadd(xs, ys), zs);
 }
 
-template <int BY, int S>
-__global__ void __launch_bounds__(32 * BY)
+// R consecutive rows per thread (BY = R x warps): neighbours shared by the
+// thread's own points come from registers, so shared loads per point drop from
+// 21 (R=1) to 11 + 10/R, and the R points give the scheduler independent work.
+template <int BY, int S, int R>
+__global__ void __launch_bounds__(32 * (BY / R))
     pw_advect3d_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_v,
                        const __grid_constant__ CUtensorMap tm_w, double* __restrict__ su,
                        double* __restrict__ sv, double* __restrict__ sw, int64_t nx, int64_t ny,
@@ -104,6 +107,7 @@ __global__ void __launch_bounds__(32 * BY)
                        int64_t planes_per_chunk) {
   using T = PwTile<BY>;
   static_assert(S >= 4, "ring needs planes z-1, z, z+1 and at least one in flight");
+  static_assert(BY % R == 0, "BY = R x warps");
   // Dynamic smem only (TMA destinations at an aligned base):
   // [ring: S slots x (u, v, w)][coef: (tzc1,tzc2,tzd1,tzd2) per output plane][S mbarriers]
   extern __shared__ __align__(1024) double ring[];
@@ -144,12 +148,14 @@ __global__ void __launch_bounds__(32 * BY)
     for (int p = 0; p < S && p < np; ++p) issue(p, p);
 
   constexpr int PS = T::kPlaneStride;
-  const int oc = (wy + 1) * kSX + 1 + lane;  // own cell inside a field plane
-  const int64_t y = y0 + wy;
+  const int oc = (wy * R + 1) * kSX + 1 + lane;  // first own cell inside a field plane
+  const int64_t yb = y0 + (int64_t)wy * R;
   const int64_t x = x0 + lane;
-  const bool ok = (y <= ny) && (x <= nx);
+  bool ok[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) ok[i] = (yb + i <= ny) && (x <= nx);
   const int64_t plane_elems = (ny + 2) * ldx;
-  const int64_t g0 = (za * (ny + 2) + y) * ldx + x;
+  const int64_t g0 = (za * (ny + 2) + yb) * ldx + x;
   double* pu = su + g0;
   double* pv = sv + g0;
   double* pw = sw + g0;
@@ -159,51 +165,81 @@ __global__ void __launch_bounds__(32 * BY)
   uint32_t par_p = 0;
   mbar_wait_parity(&full[0], 0);
   mbar_wait_parity(&full[1], 0);
-  double um = ring[oc], vm = ring[PS + oc], wm = ring[2 * PS + oc];
-  double uc = ring[T::kSlotStride + oc], vc = ring[T::kSlotStride + PS + oc], wc = ring[T::kSlotStride + 2 * PS + oc];
+  double um[R], vm[R], wm[R], uc[R], vc[R], wc[R];  // own column at planes z-1, z
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int o = oc + i * kSX;
+    um[i] = ring[o]; vm[i] = ring[PS + o]; wm[i] = ring[2 * PS + o];
+    uc[i] = ring[T::kSlotStride + o]; vc[i] = ring[T::kSlotStride + PS + o]; wc[i] = ring[T::kSlotStride + 2 * PS + o];
+  }
 
   for (int j = 0; j + 2 < np; ++j) {  // output plane za+j from input planes j, j+1, j+2
     mbar_wait_parity(&full[sp], par_p);
-    const double* U0 = ring + sc * T::kSlotStride;
+    const double* U0 = ring + sc * T::kSlotStride + oc;
     const double* V0 = U0 + PS;
     const double* W0 = U0 + 2 * PS;
-    const double* Up = ring + sp * T::kSlotStride;
+    const double* Up = ring + sp * T::kSlotStride + oc;
     const double* Vp = Up + PS;
     const double* Wp = Up + 2 * PS;
-    const double* Wm = ring + sm_ * T::kSlotStride + 2 * PS;
+    const double* Wm = ring + sm_ * T::kSlotStride + 2 * PS + oc;
 
-    PwPoint q;
-    q.up = Up[oc]; q.vp = Vp[oc]; q.wp = Wp[oc];
-    q.uc = uc; q.vc = vc; q.wc = wc;
-    q.um = um; q.vm = vm; q.wm = wm;
-    q.uw = U0[oc - 1]; q.ue = U0[oc + 1];
-    q.vw = V0[oc - 1]; q.ve = V0[oc + 1];
-    q.ww = W0[oc - 1]; q.we = W0[oc + 1];
-    q.un = U0[oc - kSX]; q.us = U0[oc + kSX];
-    q.vn = V0[oc - kSX]; q.vs = V0[oc + kSX];
-    q.wn = W0[oc - kSX]; q.ws = W0[oc + kSX];
-    q.u_sw = U0[oc + kSX - 1];  // U(0,+1,-1)
-    q.v_ne = V0[oc - kSX + 1];  // V(0,-1,+1)
-    q.u_pw = Up[oc - 1];        // U(+1,0,-1)
-    q.v_pn = Vp[oc - kSX];      // V(+1,-1,0)
-    q.w_me = Wm[oc + 1];        // W(-1,0,+1)
-    q.w_ms = Wm[oc + kSX];      // W(-1,+1,0)
-
+    double up[R], vp[R], wp[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) { up[i] = Up[i * kSX]; vp[i] = Vp[i * kSX]; wp[i] = Wp[i * kSX]; }
+    // centre column of plane z at the apron rows -1 and R
+    const double u_n0 = U0[-kSX], u_sR = U0[R * kSX];
+    const double v_n0 = V0[-kSX], v_sR = V0[R * kSX];
+    const double w_n0 = W0[-kSX], w_sR = W0[R * kSX];
+    const double vp_n0 = Vp[-kSX];          // V(+1,-1,0) of row 0
+    const double u_wR = U0[R * kSX - 1];    // U(0,+1,-1) of row R-1
+    const double v_e_1 = V0[-kSX + 1];      // V(0,-1,+1) of row 0
+    const double wm_sR = Wm[R * kSX];       // W(-1,+1,0) of row R-1
     const double4 cz = coef[j];
     const PwCoef k = {tcx, tcy, cz.x, cz.y, cz.z, cz.w};
-    double ou, ov, ow;
-    pw_point(q, k, ou, ov, ow);
-    if (ok) {
-      *pu = ou;
-      *pv = ov;
-      *pw = ow;
+    double uw[R], ue[R], vw[R], ve[R], ww[R], we[R], upw[R], wme[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      uw[i] = U0[i * kSX - 1]; ue[i] = U0[i * kSX + 1];
+      vw[i] = V0[i * kSX - 1]; ve[i] = V0[i * kSX + 1];
+      ww[i] = W0[i * kSX - 1]; we[i] = W0[i * kSX + 1];
+      upw[i] = Up[i * kSX - 1];  // U(+1,0,-1)
+      wme[i] = Wm[i * kSX + 1];  // W(-1,0,+1)
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      PwPoint q;
+      q.uc = uc[i]; q.vc = vc[i]; q.wc = wc[i];
+      q.um = um[i]; q.vm = vm[i]; q.wm = wm[i];
+      q.up = up[i]; q.vp = vp[i]; q.wp = wp[i];
+      q.uw = uw[i]; q.ue = ue[i]; q.vw = vw[i]; q.ve = ve[i]; q.ww = ww[i]; q.we = we[i];
+      q.un = i > 0 ? uc[i - 1] : u_n0;
+      q.vn = i > 0 ? vc[i - 1] : v_n0;
+      q.wn = i > 0 ? wc[i - 1] : w_n0;
+      q.us = i + 1 < R ? uc[i + 1] : u_sR;
+      q.vs = i + 1 < R ? vc[i + 1] : v_sR;
+      q.ws = i + 1 < R ? wc[i + 1] : w_sR;
+      q.u_sw = i + 1 < R ? uw[i + 1] : u_wR;   // U(0,+1,-1)
+      q.v_ne = i > 0 ? ve[i - 1] : v_e_1;      // V(0,-1,+1)
+      q.u_pw = upw[i];                          // U(+1,0,-1)
+      q.v_pn = i > 0 ? vp[i - 1] : vp_n0;      // V(+1,-1,0)
+      q.w_me = wme[i];                          // W(-1,0,+1)
+      q.w_ms = i + 1 < R ? wm[i + 1] : wm_sR;  // W(-1,+1,0)
+      double ou, ov, ow;
+      pw_point(q, k, ou, ov, ow);
+      if (ok[i]) {
+        pu[i * ldx] = ou;
+        pv[i * ldx] = ov;
+        pw[i * ldx] = ow;
+      }
     }
     pu += plane_elems;
     pv += plane_elems;
     pw += plane_elems;
-
-    um = uc; vm = vc; wm = wc;
-    uc = q.up; vc = q.vp; wc = q.wp;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      um[i] = uc[i]; vm[i] = vc[i]; wm[i] = wc[i];
+      uc[i] = up[i]; vc[i] = vp[i]; wc[i] = wp[i];
+    }
 
     // every read of input plane j (slot sm_) is done -> refill it with plane j+S
     __syncthreads();
@@ -219,7 +255,7 @@ __global__ void __launch_bounds__(32 * BY)
   }
 }
 
-template <int BY, int S>
+template <int BY, int S, int R>
 st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s) {
   using T = PwTile<BY>;
   CUtensorMap tm[3];
@@ -231,7 +267,7 @@ st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s)
                             (uint64_t)a.ldx * 8 * (uint64_t)(a.ny + 2), box));
   const size_t smem = (size_t)S * T::kSlotStride * sizeof(double) + kMaxPlanesPerChunk * sizeof(double4) +
                       S * sizeof(uint64_t);
-  ST_CHECK_CUDA(cudaFuncSetAttribute(pw_advect3d_kernel<BY, S>,
+  ST_CHECK_CUDA(cudaFuncSetAttribute(pw_advect3d_kernel<BY, S, R>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t ntx = (a.nx + kBX - 1) / kBX;
   const int64_t nty = (a.ny + BY - 1) / BY;
@@ -241,7 +277,7 @@ st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s)
   const int64_t nzc = (nz + ppc - 1) / ppc;
   ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "pw_advect3d: grid too large");
   dim3 grid((unsigned)ntx, (unsigned)nty, (unsigned)nzc);
-  pw_advect3d_kernel<BY, S><<<grid, 32 * BY, smem, s>>>(tm[0], tm[1], tm[2], a.su, a.sv, a.sw, a.nx,
+  pw_advect3d_kernel<BY, S, R><<<grid, 32 * (BY / R), smem, s>>>(tm[0], tm[1], tm[2], a.su, a.sv, a.sw, a.nx,
                                                         a.ny, a.ldx, a.tcx, a.tcy, a.tzc1, a.tzc2,
                                                         a.tzd1, a.tzd2, z_lo, z_hi, ppc);
   ST_LAUNCHED();
@@ -254,12 +290,13 @@ st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaSt
   if (z_hi < z_lo) return ST_OK;
   static const int kVariant = env_int("ST_PW_VARIANT", 0);
   switch (kVariant) {
-    case 1: return launch_pw<8, 8>(a, z_lo, z_hi, s);
-    case 2: return launch_pw<16, 5>(a, z_lo, z_hi, s);
-    case 3: return launch_pw<32, 4>(a, z_lo, z_hi, s);
-    case 4: return launch_pw<8, 6>(a, z_lo, z_hi, s);
-    case 5: return launch_pw<16, 8>(a, z_lo, z_hi, s);
-    default: return launch_pw<16, 6>(a, z_lo, z_hi, s);
+    case 1: return launch_pw<16, 5, 1>(a, z_lo, z_hi, s);
+    case 2: return launch_pw<16, 5, 2>(a, z_lo, z_hi, s);
+    case 3: return launch_pw<32, 4, 4>(a, z_lo, z_hi, s);
+    case 4: return launch_pw<16, 6, 2>(a, z_lo, z_hi, s);
+    case 5: return launch_pw<32, 5, 4>(a, z_lo, z_hi, s);
+    case 6: return launch_pw<16, 8, 4>(a, z_lo, z_hi, s);
+    default: return launch_pw<32, 5, 2>(a, z_lo, z_hi, s);  // tuned on B200
   }
 }
 
