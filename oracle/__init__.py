@@ -47,6 +47,10 @@ def _load():
     lib.or_pw_advect3d.argtypes = pw + [ctypes.c_int]
     lib.or_pw_slabs.restype = ctypes.c_int
     lib.or_pw_slabs.argtypes = pw + [ctypes.c_int]
+    lib.or_jacobi3d.restype = ctypes.c_int
+    lib.or_jacobi3d.argtypes = [_dp, _dp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
+    lib.or_jacobi3d_slabs.restype = ctypes.c_int
+    lib.or_jacobi3d_slabs.argtypes = [_dp, _dp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
     lib.or_pw_points.restype = ctypes.c_int
     lib.or_pw_points.argtypes = [_dp] * 3 + [_i64] * 4 + [_dbl, _dbl] + [_dp] * 4 + [_dp, _i64, _dp]
     _lib = lib
@@ -91,6 +95,31 @@ def jacobi2d_slabs(a0: np.ndarray, iters: int, p: int, h: int = 1, nx: int | Non
                                    nx, ny, ld, iters, p, h)
     if rc < 0:
         raise ValueError("or_jacobi2d_slabs: bad arguments")
+    return out
+
+
+def jacobi3d(a0: np.ndarray, iters: int, nx: int | None = None, threads: int | None = None) -> np.ndarray:
+    """`iters` sweeps of the 3-D 7-point Jacobi (R20/R21) of a
+    padded (nz+2, ny+2, ldx) field; a0 is not modified."""
+    assert a0.dtype == np.float64 and a0.ndim == 3 and a0.flags.c_contiguous
+    nz, ny, ldx = a0.shape[0] - 2, a0.shape[1] - 2, a0.shape[2]
+    nx = ldx - 2 if nx is None else nx
+    a = a0.copy()
+    b = np.empty_like(a)
+    rc = _load().or_jacobi3d(a.ctypes.data, b.ctypes.data, nx, ny, nz, ldx, iters, threads or default_threads())
+    if rc < 0:
+        raise ValueError("or_jacobi3d: bad arguments")
+    return b if rc == 1 else a
+
+
+def jacobi3d_slabs(a0: np.ndarray, iters: int, p: int, nx: int | None = None) -> np.ndarray:
+    """z-slab decomposed 3-D Jacobi (1 ghost plane swapped before every sweep)."""
+    nz, ny, ldx = a0.shape[0] - 2, a0.shape[1] - 2, a0.shape[2]
+    nx = ldx - 2 if nx is None else nx
+    out = np.zeros_like(a0)
+    rc = _load().or_jacobi3d_slabs(np.ascontiguousarray(a0).ctypes.data, out.ctypes.data, nx, ny, nz, ldx, iters, p)
+    if rc < 0:
+        raise ValueError("or_jacobi3d_slabs: bad arguments")
     return out
 
 

@@ -73,3 +73,19 @@ def pw_advect3d(u, v, w, co, nx: int | None = None):
         s[1:nz + 1, 1:ny + 1, 1:nx + 1] = (xs + ys) + zs
         out.append(s)
     return tuple(out)
+
+
+def jacobi3d(a0: np.ndarray, iters: int, nx: int | None = None) -> np.ndarray:
+    """3-D 7-point Jacobi by slicing (order z-, z+, y-, y+, x-, x+, then / 6.0)."""
+    nx = a0.shape[2] - 2 if nx is None else nx
+    a = a0.copy()
+    for _ in range(iters):
+        b = a.copy()
+        s = a[:-2, 1:-1, 1:nx + 1] + a[2:, 1:-1, 1:nx + 1]
+        s = s + a[1:-1, :-2, 1:nx + 1]
+        s = s + a[1:-1, 2:, 1:nx + 1]
+        s = s + a[1:-1, 1:-1, 0:nx]
+        s = s + a[1:-1, 1:-1, 2:nx + 2]
+        b[1:-1, 1:-1, 1:nx + 1] = s / 6.0
+        a = b
+    return a

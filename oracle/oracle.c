@@ -28,6 +28,13 @@
  *                      decomposed domain); SPEC.md:399 block split, remainder to
  *                      high ranks. Ghost depth H, exchange every H sweeps.
  *   or_pw_slabs        PAPER.md:268 (PW halo swapped before the time step).
+ *   or_jacobi3d        PAPER.md:214 (benchmark 1: Laplace by a 7-point stencil,
+ *                      "averages values across the six neighbouring cells", six
+ *                      flops per cell) under the value semantics of PAPER.md:126;
+ *                      readings R20/R21 of DESIGN.md: sum order z-,z+,y-,y+,x-,x+
+ *                      (slowest index first, as Listing 1 orders i before j),
+ *                      then / 6.0 (5 adds + 1 divide = 6 flops).
+ *   or_jacobi3d_slabs  z-slab decomposition of or_jacobi3d (1 ghost plane).
  *
  * Pins (tests/test_oracle_*.py): J1-J10, P1-P9, D1 of SURVEY.md §8(c5).
  */
@@ -310,4 +317,85 @@ int or_pw_slabs(const double* u, const double* v, const double* w, double* su, d
   for (int i = 0; f && i < 6 * p; ++i) free(f[i]);
   free(f); free(st); free(nr);
   return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* 3-D 7-point Jacobi (the paper's benchmark 1)       */
+/* ------------------------------------------------------------------------- */
+
+/* One sweep over planes [zlo, zhi] (inclusive), all interior rows/columns:
+ * dst = (((((Zm + Zp) + Ym) + Yp) + Xm) + Xp) / 6.0 */
+static void jacobi3d_sweep_planes(const double* src, double* dst, int64_t nx, int64_t ny, int64_t ldx,
+                                  int64_t zlo, int64_t zhi, int nthreads) {
+  const int64_t ny2 = ny + 2;
+#pragma omp parallel for schedule(static) num_threads(nthreads) collapse(2)
+  for (int64_t z = zlo; z <= zhi; ++z) {
+    for (int64_t y = 1; y <= ny; ++y) {
+      for (int64_t x = 1; x <= nx; ++x) {
+        double sum = src[IDX3(z - 1, y, x, ny2, ldx)] + src[IDX3(z + 1, y, x, ny2, ldx)];
+        sum = sum + src[IDX3(z, y - 1, x, ny2, ldx)];
+        sum = sum + src[IDX3(z, y + 1, x, ny2, ldx)];
+        sum = sum + src[IDX3(z, y, x - 1, ny2, ldx)];
+        sum = sum + src[IDX3(z, y, x + 1, ny2, ldx)];
+        dst[IDX3(z, y, x, ny2, ldx)] = sum / 6.0;
+      }
+    }
+  }
+}
+
+/* B := copy(A); repeat iters: B = sweep(A); swap. Returns 1 if the result is in b. */
+int or_jacobi3d(double* a, double* b, int64_t nx, int64_t ny, int64_t nz, int64_t ldx, int64_t iters,
+                int nthreads) {
+  if (!a || !b || nx < 1 || ny < 1 || nz < 1 || ldx < nx + 2 || iters < 0) return -1;
+  if (nthreads < 1) nthreads = 1;
+  memcpy(b, a, sizeof(double) * (size_t)((nz + 2) * (ny + 2) * ldx));
+  double* src = a;
+  double* dst = b;
+  for (int64_t it = 0; it < iters; ++it) {
+    jacobi3d_sweep_planes(src, dst, nx, ny, ldx, 1, nz, nthreads);
+    double* t = src; src = dst; dst = t;
+  }
+  return (int)(iters & 1);
+}
+
+/* z-slab decomposition with one ghost plane per side, swapped before every
+ * sweep; gathered into `out`. Must equal or_jacobi3d bitwise. */
+int or_jacobi3d_slabs(const double* a, double* out, int64_t nx, int64_t ny, int64_t nz, int64_t ldx,
+                      int64_t iters, int p) {
+  if (!a || !out || nx < 1 || ny < 1 || nz < 1 || ldx < nx + 2 || iters < 0 || p < 1 || nz / p < 1) return -1;
+  const int64_t plane = (ny + 2) * ldx;
+  double** A = calloc((size_t)p, sizeof(double*));
+  double** B = calloc((size_t)p, sizeof(double*));
+  int64_t* st = calloc((size_t)p, sizeof(int64_t));
+  int64_t* nr = calloc((size_t)p, sizeof(int64_t));
+  int ok = A && B && st && nr;
+  for (int r = 0; ok && r < p; ++r) {
+    block_split(nz, p, r, &st[r], &nr[r]);
+    A[r] = malloc(sizeof(double) * (size_t)((nr[r] + 2) * plane));
+    B[r] = malloc(sizeof(double) * (size_t)((nr[r] + 2) * plane));
+    ok = A[r] && B[r];
+    if (!ok) break;
+    /* local plane k <-> global plane st + k, k = 0..n+1 */
+    memcpy(A[r], a + st[r] * plane, sizeof(double) * (size_t)((nr[r] + 2) * plane));
+    memcpy(B[r], A[r], sizeof(double) * (size_t)((nr[r] + 2) * plane));
+  }
+  for (int64_t it = 0; ok && it < iters; ++it) {
+    for (int r = 0; r < p; ++r) {
+      if (r > 0) memcpy(A[r], A[r - 1] + nr[r - 1] * plane, sizeof(double) * (size_t)plane);
+      if (r < p - 1) memcpy(A[r] + (nr[r] + 1) * plane, A[r + 1] + plane, sizeof(double) * (size_t)plane);
+    }
+    for (int r = 0; r < p; ++r) {
+      jacobi3d_sweep_planes(A[r], B[r], nx, ny, ldx, 1, nr[r], 1);
+      double* t = A[r]; A[r] = B[r]; B[r] = t;
+    }
+  }
+  if (ok) {
+    for (int r = 0; r < p; ++r)
+      memcpy(out + (st[r] + 1) * plane, A[r] + plane, sizeof(double) * (size_t)(nr[r] * plane));
+    memcpy(out, A[0], sizeof(double) * (size_t)plane);
+    memcpy(out + (nz + 1) * plane, A[p - 1] + (nr[p - 1] + 1) * plane, sizeof(double) * (size_t)plane);
+  }
+  for (int r = 0; r < p && A && B; ++r) { free(A[r]); free(B[r]); }
+  free(A); free(B); free(st); free(nr);
+  return ok ? 0 : -1;
 }

@@ -38,6 +38,26 @@ def jacobi_point(n, s, w, e, quarter):
     return (((n + s) + w) + e) * quarter
 
 
+def jacobi3d_point(zm, zp, ym, yp, xm, xp, six):
+    """average of the six orthogonal neighbours (R20/R21)."""
+    return (((((zm + zp) + ym) + yp) + xm) + xp) / six
+
+
+def jacobi3d(a, iters, six):
+    """Exact/generic 3-D Jacobi on nested lists a[z][y][x]."""
+    nz, ny, nx = len(a) - 2, len(a[0]) - 2, len(a[0][0]) - 2
+    cur = [[row[:] for row in pl] for pl in a]
+    for _ in range(iters):
+        nxt = [[row[:] for row in pl] for pl in cur]
+        for z in range(1, nz + 1):
+            for y in range(1, ny + 1):
+                for x in range(1, nx + 1):
+                    nxt[z][y][x] = jacobi3d_point(cur[z - 1][y][x], cur[z + 1][y][x], cur[z][y - 1][x],
+                                                  cur[z][y + 1][x], cur[z][y][x - 1], cur[z][y][x + 1], six)
+        cur = nxt
+    return cur
+
+
 def jacobi2d(a, iters, quarter):
     """Exact/generic Jacobi on a list-of-lists padded grid (value semantics)."""
     ny, nx = len(a) - 2, len(a[0]) - 2

@@ -31,6 +31,7 @@ SEED = 42
 STREAM_JACOBI = 0
 STREAM_U, STREAM_V, STREAM_W = 1, 2, 3
 STREAM_TZC1, STREAM_TZC2, STREAM_TZD1, STREAM_TZD2 = 4, 5, 6, 7
+STREAM_JACOBI3D = 8
 PW_TCX = 0.25 / 3.0
 PW_TCY = 0.25 / 5.0
 
@@ -126,6 +127,20 @@ def pw_field(nx: int, ny: int, nz: int, stream: int, ldx: int | None = None, *,
     out = np.zeros((planes, ny + 2, ldx), dtype=np.float64)
     fill_affine(out, planes * (ny + 2), nx + 2, ldx, plane0 * (ny + 2) * (nx + 2), nx + 2,
                 seed, stream, 2.0, -1.0)
+    return out
+
+
+def jacobi3d_grid(nx: int, ny: int, nz: int, ldx: int | None = None, *, seed: int = SEED,
+                  stream: int = STREAM_JACOBI3D, plane0: int = 0, planes: int | None = None) -> np.ndarray:
+    """Padded 3-D field (planes x (ny+2) x ldx) for the 7-point Jacobi (NEXT #1):
+    value(z, y, x) = 0.5 + U01(seed, 8, (z*(ny+2)+y)*(nx+2)+x), ring included."""
+    ldx = even_ld(nx + 2) if ldx is None else ldx
+    if ldx < nx + 2:
+        raise ValueError(f"ldx={ldx} < nx+2={nx + 2}")
+    planes = (nz + 2 - plane0) if planes is None else planes
+    out = np.zeros((planes, ny + 2, ldx), dtype=np.float64)
+    fill_affine(out, planes * (ny + 2), nx + 2, ldx, plane0 * (ny + 2) * (nx + 2), nx + 2,
+                seed, stream, 1.0, 0.5)
     return out
 
 
