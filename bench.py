@@ -203,6 +203,8 @@ def main():
     ap.add_argument("--align", type=int, default=2, help="row pitch multiple in doubles (2 = 16-byte rows)")
     ap.add_argument("--pw-apps", type=int, default=20, help="PW applications timed")
     ap.add_argument("--no-pw", action="store_true")
+    ap.add_argument("--no-j3", action="store_true")
+    ap.add_argument("--j3-sweeps", type=int, default=100, help="3-D 7-point Jacobi sweeps timed (512^3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-sweeps", type=int, default=20)
@@ -368,6 +370,52 @@ def main():
             pw["cpu_baseline"] = cpu_baseline_pw()
         del g, outs
 
+    # ------------------------------------------------------------------ 3-D 7-point Jacobi (NEXT #1)
+    j3 = None
+    if not args.no_j3:
+        n3 = 512
+        z0, nz3 = st.st_block_split(n3, world, rank)
+        h3 = 1
+        ldx3 = pitch(n3 + 2, args.align)
+        g3 = si.jacobi3d_grid(n3, n3, n3, ldx=ldx3, plane0=z0, planes=nz3 + 2)
+        A3 = torch.from_numpy(g3).to(dev)
+        B3 = torch.empty_like(A3)
+        j3_sweeps = args.j3_sweeps
+
+        def j3_step():
+            r3 = st.st_jacobi3d_run(A3, B3, j3_sweeps, halo=h3, comm=comm)
+            if r3 is not A3:
+                A3.copy_(r3)
+
+        for _ in range(args.warmup):
+            j3_step()
+        barrier()
+        jl0 = st.launch_count()
+        ev0.record(stream)
+        j3_step()
+        ev1.record(stream)
+        ev1.synchronize()
+        j3_launches = st.launch_count() - jl0
+        j3_ms = max_over_ranks(ev0.elapsed_time(ev1))
+        j3_launch_ms = j3_ms / max(1, j3_launches - 1)  # minus the one-off face copy
+        j3_gbs = JACOBI_BYTES_PER_PT * n3 * n3 * nz3 / (j3_launch_ms / 1e3) / 1e9
+        j3 = {"workload": f"jacobi3d_{n3}^3_fp64_{j3_sweeps}sweeps" + ("" if world == 1 else f"_zslabs{world}"),
+              "value": round(n3 ** 3 * j3_sweeps / (j3_ms / 1e3) / 1e9, 3), "unit": UNIT,
+              "ms_per_step": round(j3_ms, 3), "gpu_launches": j3_launches,
+              "roofline": {"bound": "hbm", "kernel": "jacobi3d_kernel", "achieved": round(j3_gbs, 1),
+                           "peak": hbm_peak, "unit": "GB/s", "frac": round(j3_gbs / hbm_peak, 4),
+                           "traffic": ncu_traffic("jacobi3d_kernel"), "bytes_per_pt": JACOBI_BYTES_PER_PT,
+                           "peak_source": peak_src}}
+        if world == 1 and not args.no_cpu:
+            import oracle
+            _, cores = host_info()
+            t0 = time.perf_counter()
+            oracle.jacobi3d(g3, 2, threads=cores)
+            dt = time.perf_counter() - t0
+            j3["cpu_baseline"] = {"value": round(n3 ** 3 * 2 / dt / 1e9, 4), "unit": UNIT, "cores": cores,
+                                  "kind": "oracle", "sample": f"2 sweeps of the 512^3 grid; {dt:.2f} s"}
+        del A3, B3
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_jacobi(args.cpu_sweeps)
@@ -395,6 +443,7 @@ def main():
             "clocks": clocks,
             "cpu_baseline": cpu,
             "pw_advect3d": pw,
+            "jacobi3d": j3,
         }
         print(json.dumps(out), flush=True)
     if dist is not None:

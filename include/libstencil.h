@@ -188,6 +188,33 @@ st_status st_jacobi2d_run(double* a, double* b, int64_t nx, int64_t ny_local, in
                           void* cuda_stream, int32_t* result_in_b);
 
 /* ------------------------------------------------------------------------ */
+/* 3-D 7-point Jacobi (the paper's benchmark 1)                 */
+/* ------------------------------------------------------------------------ */
+
+/* `iters` sweeps of the 7-point average
+ *     B = (((((A[z-1] + A[z+1]) + A[y-1]) + A[y+1]) + A[x-1]) + A[x+1]) / 6.0
+ * ("averages values across the six neighbouring cells", six flops per cell,
+ * PAPER.md:214; R20/R21) over the interior with value semantics
+ * (Jacobi double buffering, as st_jacobi2d_run).
+ *
+ *   a, b      (nz_local + 2*halo) planes x (ny+2) rows x ldx doubles, x fastest,
+ *             ldx even >= nx+2, 16-byte aligned, non-overlapping. `a` holds the
+ *             initial state including every Dirichlet face; the library copies
+ *             the faces and ghost planes a -> b. The side faces (x = 0, nx+1;
+ *             y = 0, ny+1) and, without a comm, planes 0 and nz_local+1 are
+ *             Dirichlet and never change.
+ *   comm      NULL: halo must be 1. Set: rank-local z-slab, halo = ghost-plane
+ *             depth; planes are swapped with rank -/+ 1 every `halo` sweeps
+ *             (boundary planes first, swap overlapped with the interior
+ *             planes); edge ranks keep the global Dirichlet plane next to their
+ *             owned planes. Requires nz_local >= halo.
+ *   tblock    0 or 1 (one sweep per pass over HBM); others -> ST_ENOTSUP.
+ *   *result_in_b (may be NULL) = iters & 1. */
+st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t nz_local, int64_t ldx,
+                          int32_t halo, int64_t iters, int32_t tblock, st_comm* comm,
+                          void* cuda_stream, int32_t* result_in_b);
+
+/* ------------------------------------------------------------------------ */
 /* 3-D Piacsek-Williams advection                              */
 /* ------------------------------------------------------------------------ */
 

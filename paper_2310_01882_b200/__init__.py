@@ -9,6 +9,7 @@ every entry point raises. It never imports the CPU oracle.
 
 Entry points (same names as the C ABI, tensors instead of raw pointers):
     st_jacobi2d_run(a, b, iters, tblock=0, halo=1, comm=None, nx=None) -> result tensor
+    st_jacobi3d_run(a, b, iters, tblock=0, halo=1, comm=None, nx=None) -> result tensor
     st_pw_advect3d(u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, tzd1, tzd2, comm=None, nx=None)
     st_halo_exchange(comm, fields, n_slow_local, slab_pitch, width)
     st_halo_plan(rank, nranks, n_slow_local, slab_pitch, width) -> (sends, recvs)   [host only]
@@ -66,6 +67,8 @@ _SIGS = {
     "st_jacobi2d_schedule": (ctypes.c_int, [_i32, _i32, _i64, _i64, _i32, _i64, _i32, ctypes.POINTER(Op), _i64,
                                             ctypes.POINTER(_i64)]),
     "st_jacobi2d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i32, _i64, _i32, _vp, _vp,
+                                       ctypes.POINTER(_i32)]),
+    "st_jacobi3d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i64, _i32, _vp, _vp,
                                        ctypes.POINTER(_i32)]),
     "st_pw_advect3d": (ctypes.c_int, [_vp] * 6 + [_i64] * 4 + [_dbl, _dbl] + [_vp] * 4 + [_vp, _vp]),
 }
@@ -211,6 +214,26 @@ def st_jacobi2d_run(a, b, iters: int, tblock: int = 0, halo: int = 1, comm: Comm
     return b if rib.value else a
 
 
+def st_jacobi3d_run(a, b, iters: int, tblock: int = 0, halo: int = 1, comm: Comm | None = None,
+                    nx: int | None = None, stream=None):
+    """`iters` 7-point Jacobi sweeps on (planes, ny+2, ldx) float64 CUDA tensors.
+
+    a, b: (nz_local + 2*halo, ny+2, ldx), contiguous; nx defaults to ldx - 2.
+    Returns the tensor holding the result (b iff iters is odd)."""
+    _f64_cuda(a, "a")
+    _f64_cuda(b, "b")
+    if a.dim() != 3 or a.shape != b.shape or not a.is_contiguous() or not b.is_contiguous():
+        raise ValueError("a, b: contiguous 3-D tensors of equal shape")
+    ldx = a.shape[2]
+    nx = ldx - 2 if nx is None else nx
+    ny = a.shape[1] - 2
+    nz = a.shape[0] - 2 * halo
+    rib = _i32()
+    _check(lib().st_jacobi3d_run(a.data_ptr(), b.data_ptr(), nx, ny, nz, ldx, halo, iters, tblock,
+                                 _comm_ptr(comm), _stream_ptr(stream), ctypes.byref(rib)), "st_jacobi3d_run")
+    return b if rib.value else a
+
+
 def st_pw_advect3d(u, v, w, su, sv, sw, tcx: float, tcy: float, tzc1, tzc2, tzd1, tzd2,
                    comm: Comm | None = None, nx: int | None = None, stream=None) -> None:
     """Fused PW advection on (nz+2, ny+2, ldx) float64 CUDA tensors."""
@@ -243,5 +266,6 @@ def st_halo_exchange(comm: Comm, fields, n_slow_local: int, slab_pitch: int, wid
 
 # Friendlier aliases
 jacobi2d = st_jacobi2d_run
+jacobi3d = st_jacobi3d_run
 pw_advect3d = st_pw_advect3d
 halo_exchange = st_halo_exchange

@@ -127,6 +127,32 @@ st_status run_schedule(const std::vector<st_op>& ops, st_comm* comm, double* a, 
   return ST_OK;
 }
 
+// Executes a dims=3 schedule: sweeps of planes, swaps of whole planes.
+st_status run_schedule3d(const std::vector<st_op>& ops, st_comm* comm, double* a, double* b, int64_t nx,
+                         int64_t ny, int64_t n, int64_t ldx, int32_t h, cudaStream_t s) {
+  double* buf[2] = {a, b};
+  const int64_t nplanes = n + 2 * (int64_t)h, plane = (ny + 2) * ldx;
+  for (const st_op& o : ops) {
+    switch (o.kind) {
+      case ST_OP_SWEEP:
+        ST_RETURN_IF(o.sweeps != 1, ST_EINTERNAL, "jacobi3d: pass of %d sweeps", o.sweeps);
+        ST_TRY(jacobi3d_sweep_planes(buf[o.buf], buf[1 - o.buf], nx, ny, nplanes, ldx, o.y_lo, o.y_hi, s));
+        break;
+      case ST_OP_EXCHANGE:
+        ST_TRY(halo_exchange_async(comm, &buf[o.buf], 1, n, plane, o.sweeps, s, o.flag == 0));
+        break;
+      case ST_OP_JOIN:
+        if (comm && comm->nranks > 1) ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
+        break;
+      case ST_OP_SWAP:
+        break;
+      default:
+        ST_RETURN_IF(true, ST_EINTERNAL, "jacobi3d: bad schedule op %d", o.kind);
+    }
+  }
+  return ST_OK;
+}
+
 }  // namespace
 }  // namespace st
 
@@ -175,6 +201,43 @@ st_status st_jacobi2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
   ST_CHECK_CUDA(cudaMemcpy2DAsync(b + (halo + ny) * ld, pitch, a + (halo + ny) * ld, pitch, width, (size_t)halo,
                                   cudaMemcpyDeviceToDevice, s));
   return run_schedule(ops, comm, a, b, nx, ny, ld, halo, s);
+}
+
+st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t nz, int64_t ldx, int32_t halo,
+                          int64_t iters, int32_t tblock, st_comm* comm, void* cuda_stream, int32_t* result_in_b) {
+  clear_error();
+  ST_RETURN_IF(!a || !b, ST_EINVAL, "st_jacobi3d_run: null field pointer");
+  ST_RETURN_IF(nx < 1 || ny < 1 || nz < 1, ST_EINVAL, "st_jacobi3d_run: empty interior");
+  ST_RETURN_IF(ldx < nx + 2 || (ldx & 1), ST_EINVAL, "st_jacobi3d_run: ldx=%lld must be even and >= nx+2",
+               (long long)ldx);
+  ST_RETURN_IF(!aligned16(a) || !aligned16(b), ST_EINVAL, "st_jacobi3d_run: fields must be 16-byte aligned");
+  ST_RETURN_IF(iters < 0 || tblock < 0 || halo < 1, ST_EINVAL, "st_jacobi3d_run: iters=%lld tblock=%d halo=%d",
+               (long long)iters, tblock, halo);
+  ST_RETURN_IF(tblock > 1, ST_ENOTSUP, "st_jacobi3d_run: tblock=%d not supported (0, 1)", tblock);
+  ST_RETURN_IF(!comm && halo != 1, ST_EINVAL, "st_jacobi3d_run: halo must be 1 without a comm");
+  ST_RETURN_IF(comm && nz < halo, ST_EINVAL, "st_jacobi3d_run: slab of %lld planes < halo %d", (long long)nz, halo);
+  ST_RETURN_IF(nx + 2 > (int64_t)INT32_MAX || ny + 2 > (int64_t)INT32_MAX || nz + 2 * halo > (int64_t)INT32_MAX,
+               ST_EINVAL, "st_jacobi3d_run: extents exceed TMA coordinate range");
+  const size_t bytes = (size_t)(nz + 2 * halo) * (size_t)(ny + 2) * (size_t)ldx * sizeof(double);
+  ST_RETURN_IF(overlaps(a, bytes, b, bytes), ST_EINVAL, "st_jacobi3d_run: a and b overlap");
+  ST_TRY(check_device_ptr(a, "a"));
+  ST_TRY(check_device_ptr(b, "b"));
+  if (result_in_b) *result_in_b = (int32_t)(iters & 1);
+  if (iters == 0) return ST_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  const int32_t nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
+  if (comm) ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier NCCL error");
+  std::vector<st_op> ops;
+  ST_TRY(build_jacobi_schedule(rank, nranks, nx, nz, halo, iters, 1, ops, 3));
+  // ghost / Dirichlet planes and the side faces of the owned planes a -> b (pitch padding untouched)
+  const size_t pitch = (size_t)ldx * sizeof(double), width = (size_t)(nx + 2) * sizeof(double);
+  const int64_t plane = (ny + 2) * ldx;
+  ST_CHECK_CUDA(cudaMemcpy2DAsync(b, pitch, a, pitch, width, (size_t)halo * (size_t)(ny + 2),
+                                  cudaMemcpyDeviceToDevice, s));
+  ST_CHECK_CUDA(cudaMemcpy2DAsync(b + (halo + nz) * plane, pitch, a + (halo + nz) * plane, pitch, width,
+                                  (size_t)halo * (size_t)(ny + 2), cudaMemcpyDeviceToDevice, s));
+  ST_TRY(jacobi3d_copy_faces(a, b, nx, ny, ldx, halo, halo + nz - 1, s));
+  return run_schedule3d(ops, comm, a, b, nx, ny, nz, ldx, halo, s);
 }
 
 st_status st_pw_advect3d(double* u, double* v, double* w, double* su, double* sv, double* sw,

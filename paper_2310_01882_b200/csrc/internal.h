@@ -37,6 +37,16 @@ st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t l
                            int64_t y_lo, int64_t y_hi, int t, int64_t ring_lo,
                            int64_t ring_hi, int64_t nrows_buf, cudaStream_t s);
 
+// ------------------------------------------------------------ Jacobi 3-D ---
+// One 7-point sweep dst = J(src) over planes [z_lo, z_hi] (buffer plane indices)
+// and the interior rows/columns; reads planes z_lo-1 .. z_hi+1. nplanes_buf =
+// planes in the buffer (TMA extent).
+st_status jacobi3d_sweep_planes(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
+                                int64_t ldx, int64_t z_lo, int64_t z_hi, cudaStream_t s);
+// dst's side faces (x = 0, nx+1; y = 0, ny+1) of planes [z_lo, z_hi] <- src.
+st_status jacobi3d_copy_faces(const double* src, double* dst, int64_t nx, int64_t ny, int64_t ldx, int64_t z_lo,
+                              int64_t z_hi, cudaStream_t s);
+
 // ------------------------------------------------------------ PW 3-D ---
 struct PwArgs {
   const double *u, *v, *w;
@@ -49,9 +59,11 @@ struct PwArgs {
 st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s);
 
 // ------------------------------------------------------------ schedule ---
+// dims = 2: rows of a 2-D grid (temporal blocking T in {1,2,4,6,8});
+// dims = 3: planes of a 3-D grid (T = 1).
 int choose_tblock(int32_t nranks, int64_t nx, int64_t n, int32_t h, int32_t tblock);
 st_status build_jacobi_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_t n, int32_t h,
-                                int64_t iters, int32_t tblock, std::vector<st_op>& ops);
+                                int64_t iters, int32_t tblock, std::vector<st_op>& ops, int dims = 2);
 
 // --------------------------------------------------------------- misc ---
 int env_int(const char* name, int dflt);

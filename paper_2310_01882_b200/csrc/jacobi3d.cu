@@ -1,0 +1,187 @@
+// jacobi3d.cu — 3-D 7-point Jacobi sweep (the paper's benchmark 1), sm_100a.
+//
+// Operation ("a 7-point stencil, the orthogonal neighbours in
+// three dimensions, and averages values across the six neighbouring cells";
+// value semantics PAPER.md:126; readings R20/R21 of DESIGN.md):
+//     dst = (((((Zm + Zp) + Ym) + Yp) + Xm) + Xp) / 6.0
+// 5 adds + 1 correctly rounded divide = the paper's 6 flops per cell.
+//
+// HBM-bound (16 algorithmic bytes per point per sweep). Design = the PW
+// kernel's 2.5-D z-streaming skeleton with one field: a CTA owns a 32 x BY
+// interior column and a chunk of planes; input planes (tile + 1-cell apron)
+// stream through an S-slot shared-memory ring filled by TMA
+// (cp.async.bulk.tensor.3d, one elected thread, mbarrier completion); a thread
+// owns R consecutive rows of one column, keeps its own column at z-1 and z in
+// registers, and reads the four in-plane neighbours from shared memory.
+// Dirichlet faces are never written by the sweep kernel; the side faces are
+// copied a -> b once per call (jacobi3d_copy_faces).
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+#include "tma.cuh"
+
+namespace st {
+
+namespace {
+
+constexpr int kBX = 32;
+constexpr int kSX = kBX + 2;
+
+template <int BY>
+struct J3Tile {
+  static constexpr int SY = BY + 2;
+  static constexpr int kPlaneBytes = kSX * SY * 8;
+  static constexpr int kPlaneStride = ((kPlaneBytes + 127) / 128) * 128 / 8;  // doubles, 128-B aligned
+  static constexpr uint32_t kTxBytes = kPlaneBytes;
+};
+
+template <int BY, int S, int R>
+__global__ void __launch_bounds__(32 * (BY / R))
+    jacobi3d_kernel(const __grid_constant__ CUtensorMap tm, double* __restrict__ dst, int64_t nx, int64_t ny,
+                    int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t planes_per_chunk) {
+  using T = J3Tile<BY>;
+  static_assert(S >= 4 && BY % R == 0, "ring depth / rows per thread");
+  extern __shared__ __align__(1024) double ring[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * T::kPlaneStride);
+
+  const int lane = threadIdx.x & 31;
+  const int wy = threadIdx.x >> 5;
+  const int64_t x0 = 1 + (int64_t)blockIdx.x * kBX;
+  const int64_t y0 = 1 + (int64_t)blockIdx.y * BY;
+  const int64_t za = z_lo + (int64_t)blockIdx.z * planes_per_chunk;
+  const int64_t zb = min(z_hi, za + planes_per_chunk - 1);
+  const int np = (int)(zb - za + 3);
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm);
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int32_t cx = (int32_t)(x0 - 1), cy = (int32_t)(y0 - 1);  // even x start (TMA rule)
+  auto issue = [&](int p, int slot) {
+    mbar_arrive_expect_tx(&full[slot], T::kTxBytes);
+    tma_load_3d(ring + slot * T::kPlaneStride, &tm, cx, cy, (int32_t)(za - 1 + p), &full[slot]);
+  };
+  if (threadIdx.x == 0)
+    for (int p = 0; p < S && p < np; ++p) issue(p, p);
+
+  const int oc = (wy * R + 1) * kSX + 1 + lane;
+  const int64_t yb = y0 + (int64_t)wy * R;
+  const int64_t x = x0 + lane;
+  bool ok[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) ok[i] = (yb + i <= ny) && (x <= nx);
+  const int64_t plane_elems = (ny + 2) * ldx;
+  double* out = dst + (za * (ny + 2) + yb) * ldx + x;
+
+  int sm_ = 0, sc = 1, sp = 2;
+  uint32_t par_p = 0;
+  mbar_wait_parity(&full[0], 0);
+  mbar_wait_parity(&full[1], 0);
+  double m[R], c[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    m[i] = ring[oc + i * kSX];
+    c[i] = ring[T::kPlaneStride + oc + i * kSX];
+  }
+  for (int j = 0; j + 2 < np; ++j) {
+    mbar_wait_parity(&full[sp], par_p);
+    const double* C = ring + sc * T::kPlaneStride + oc;
+    const double* P = ring + sp * T::kPlaneStride + oc;
+    double p[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) p[i] = P[i * kSX];
+    const double n0 = C[-kSX], sR = C[R * kSX];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const double ym = i > 0 ? c[i - 1] : n0;
+      const double yp = i + 1 < R ? c[i + 1] : sR;
+      const double xm = C[i * kSX - 1], xp = C[i * kSX + 1];
+      const double sum = dadd(dadd(dadd(dadd(dadd(m[i], p[i]), ym), yp), xm), xp);
+      const double v = __ddiv_rn(sum, 6.0);
+      if (ok[i]) out[i * ldx] = v;
+    }
+    out += plane_elems;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      m[i] = c[i];
+      c[i] = p[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && j + S < np) {
+      fence_proxy_async_smem();
+      issue(j + S, sm_);
+    }
+    const int nsp = (sp + 1 == S) ? 0 : sp + 1;
+    if (nsp == 0) par_p ^= 1u;
+    sm_ = sc;
+    sc = sp;
+    sp = nsp;
+  }
+}
+
+// dst's side faces (x = 0, nx+1 and y = 0, ny+1) of planes [z_lo, z_hi] <- src
+__global__ void jacobi3d_copy_faces_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nx,
+                                           int64_t ny, int64_t ldx, int64_t z_lo, int64_t z_hi) {
+  const int64_t per_plane = 2 * (nx + 2) + 2 * ny;
+  const int64_t total = per_plane * (z_hi - z_lo + 1);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = z_lo + t / per_plane;
+    int64_t k = t % per_plane, y, x;
+    if (k < nx + 2) { y = 0; x = k; }
+    else if (k < 2 * (nx + 2)) { y = ny + 1; x = k - (nx + 2); }
+    else { k -= 2 * (nx + 2); y = 1 + (k >> 1); x = (k & 1) ? nx + 1 : 0; }
+    const int64_t g = (z * (ny + 2) + y) * ldx + x;
+    dst[g] = src[g];
+  }
+}
+
+template <int BY, int S, int R>
+st_status launch_j3(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf, int64_t ldx,
+                    int64_t z_lo, int64_t z_hi, cudaStream_t s) {
+  using T = J3Tile<BY>;
+  CUtensorMap tm;
+  const uint64_t dims[3] = {(uint64_t)(nx + 2), (uint64_t)(ny + 2), (uint64_t)nplanes_buf};
+  const uint32_t box[3] = {(uint32_t)kSX, (uint32_t)T::SY, 1u};
+  ST_TRY(make_tmap_3d_f64(&tm, src, dims, (uint64_t)ldx * 8, (uint64_t)ldx * 8 * (uint64_t)(ny + 2), box));
+  const size_t smem = (size_t)S * T::kPlaneStride * sizeof(double) + S * sizeof(uint64_t);
+  ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi3d_kernel<BY, S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  const int64_t ntx = (nx + kBX - 1) / kBX, nty = (ny + BY - 1) / BY, nz = z_hi - z_lo + 1;
+  static const int kPpc = env_int("ST_J3_PLANES", 64);
+  const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(kPpc, nz));
+  const int64_t nzc = (nz + ppc - 1) / ppc;
+  ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "jacobi3d: grid too large");
+  jacobi3d_kernel<BY, S, R><<<dim3((unsigned)ntx, (unsigned)nty, (unsigned)nzc), 32 * (BY / R), smem, s>>>(
+      tm, dst, nx, ny, ldx, z_lo, z_hi, ppc);
+  ST_LAUNCHED();
+  return ST_OK;
+}
+
+}  // namespace
+
+st_status jacobi3d_sweep_planes(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
+                                int64_t ldx, int64_t z_lo, int64_t z_hi, cudaStream_t s) {
+  if (z_hi < z_lo) return ST_OK;
+  static const int kVariant = env_int("ST_J3_VARIANT", 0);
+  switch (kVariant) {
+    case 1: return launch_j3<16, 6, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 2: return launch_j3<32, 6, 4>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 3: return launch_j3<16, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    default: return launch_j3<32, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+  }
+}
+
+st_status jacobi3d_copy_faces(const double* src, double* dst, int64_t nx, int64_t ny, int64_t ldx, int64_t z_lo,
+                              int64_t z_hi, cudaStream_t s) {
+  if (z_hi < z_lo) return ST_OK;
+  const int64_t total = (2 * (nx + 2) + 2 * ny) * (z_hi - z_lo + 1);
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  jacobi3d_copy_faces_kernel<<<blocks, 256, 0, s>>>(src, dst, nx, ny, ldx, z_lo, z_hi);
+  ST_LAUNCHED();
+  return ST_OK;
+}
+
+}  // namespace st

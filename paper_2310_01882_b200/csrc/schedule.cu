@@ -47,11 +47,12 @@ int choose_tblock(int32_t nranks, int64_t nx, int64_t n, int32_t h, int32_t tblo
 }
 
 st_status build_jacobi_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_t n, int32_t h,
-                                int64_t iters, int32_t tblock, std::vector<st_op>& ops) {
+                                int64_t iters, int32_t tblock, std::vector<st_op>& ops, int dims) {
   ST_RETURN_IF(nranks < 1 || rank < 0 || rank >= nranks, ST_EINVAL, "schedule: rank %d of %d", rank, nranks);
   ST_RETURN_IF(nx < 1 || n < 1 || h < 1 || iters < 0 || tblock < 0, ST_EINVAL, "schedule: bad extents/counts");
   ST_RETURN_IF(nranks > 1 && n < h, ST_EINVAL, "schedule: slab of %lld rows < halo %d", (long long)n, h);
-  const int T = choose_tblock(nranks, nx, n, h, tblock);
+  ST_RETURN_IF(dims == 3 && tblock > 1, ST_ENOTSUP, "jacobi3d: tblock=%d not supported (0, 1)", tblock);
+  const int T = dims == 3 ? 1 : choose_tblock(nranks, nx, n, h, tblock);
   ST_RETURN_IF(T > 1 && !jacobi2d_tb_supported(T), ST_ENOTSUP,
                "jacobi2d: tblock=%d not supported (1, 2, 4, 6, 8)", T);
   ST_RETURN_IF(nranks > 1 && T > h, ST_EINVAL, "jacobi2d: tblock=%d needs halo >= %d", T, T);

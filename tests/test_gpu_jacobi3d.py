@@ -1,0 +1,72 @@
+"""GPU parity of st_jacobi3d_run (the paper's 7-point benchmark, PAPER.md:214;
+SURVEY.md §8(f) NEXT #1) against the CPU oracle — bitwise."""
+import numpy as np
+import pytest
+
+import oracle
+import stencil_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+
+def run_gpu(st, a_np, iters, tblock=0, nx=None, halo=1, comm=None):
+    import torch
+    a = torch.from_numpy(a_np).cuda()
+    b = torch.full_like(a, float("nan"))
+    r = st.st_jacobi3d_run(a, b, iters, tblock=tblock, nx=nx, halo=halo, comm=comm)
+    torch.cuda.synchronize()
+    assert (r is b) == bool(iters & 1)
+    return r.cpu().numpy()
+
+
+SHAPES = [  # (nx, ny, nz, ldx, iters): tiles of 32 x 32 (2 rows/thread), ragged in every dim
+    (1, 1, 1, 4, 3), (2, 3, 5, 4, 2), (31, 33, 7, 34, 5), (32, 32, 64, 34, 4), (33, 31, 65, 36, 3),
+    (64, 70, 9, 66, 6), (100, 45, 130, 102, 7), (257, 9, 11, 260, 2),
+]
+
+
+@pytest.mark.parametrize("nx,ny,nz,ldx,iters", SHAPES)
+def test_ragged_shapes_bitwise(cuda_lib, nx, ny, nz, ldx, iters):
+    a = si.jacobi3d_grid(nx, ny, nz, ldx=ldx)
+    want = oracle.jacobi3d(a, iters, nx=nx)
+    got = run_gpu(cuda_lib, a, iters, nx=nx)
+    assert np.array_equal(got[:, :, :nx + 2], want[:, :, :nx + 2])
+    if iters & 1:  # result in b: its pitch padding was never written
+        assert np.all(np.isnan(got[:, :, nx + 2:]))
+
+
+def test_integer_linear_fixed_point_many_sweeps(cuda_lib):
+    nz, ny, nx = 40, 66, 70
+    z, y, x = np.meshgrid(np.arange(nz + 2), np.arange(ny + 2), np.arange(nx + 2), indexing="ij")
+    a = np.ascontiguousarray((3 * x + 2 * y + 5 * z + 7).astype(np.float64))
+    assert np.array_equal(run_gpu(cuda_lib, a, 200), a)
+
+
+@pytest.mark.slow
+def test_512cubed_5_sweeps_bitwise(cuda_lib):
+    a = si.jacobi3d_grid(512, 512, 512)
+    assert np.array_equal(run_gpu(cuda_lib, a, 5), oracle.jacobi3d(a, 5))
+
+
+def test_tblock_rejected(cuda_lib):
+    import torch
+    a = torch.zeros(6, 6, 6, dtype=torch.float64, device="cuda")
+    with pytest.raises(cuda_lib.StencilError) as e:
+        cuda_lib.st_jacobi3d_run(a, a.clone(), 3, tblock=2)
+    assert e.value.code == cuda_lib.ST_ENOTSUP
+
+
+@pytest.mark.parametrize("h", [1, 3])
+def test_single_rank_comm(cuda_lib, h):
+    import torch
+    torch.cuda.set_device(0)
+    comm = cuda_lib.Comm.create(0, 1, cuda_lib.Comm.unique_id(), 0)
+    try:
+        nx, ny, nz, iters = 40, 30, 20, 7
+        g = si.jacobi3d_grid(nx, ny, nz)
+        loc = np.zeros((nz + 2 * h, ny + 2, g.shape[2]))
+        loc[h - 1:h + nz + 1] = g
+        got = run_gpu(cuda_lib, loc, iters, halo=h, comm=comm)
+        assert np.array_equal(got[h - 1:h + nz + 1], oracle.jacobi3d(g, iters))
+    finally:
+        comm.close()
