@@ -18,5 +18,9 @@ for nx, ny, nz in ((70, 13, 9), (129, 17, 70)):
     g = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in d.items()}
     outs = [torch.zeros_like(g["u"]) for _ in range(3)]
     st.st_pw_advect3d(g["u"], g["v"], g["w"], *outs, g["tcx"], g["tcy"], g["tzc1"], g["tzc2"], g["tzd1"], g["tzd2"])
+for nx, ny, nz in ((33, 31, 9), (70, 40, 66)):
+    a = torch.from_numpy(si.jacobi3d_grid(nx, ny, nz)).cuda()
+    b = torch.empty_like(a)
+    st.st_jacobi3d_run(a, b, 3)
 torch.cuda.synchronize()
 print("sanitize cases done")
