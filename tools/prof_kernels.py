@@ -30,4 +30,9 @@ outs = [torch.empty_like(g["u"]) for _ in range(3)]
 for _ in range(args.apps):
     st.st_pw_advect3d(g["u"], g["v"], g["w"], *outs, g["tcx"], g["tcy"], g["tzc1"], g["tzc2"], g["tzd1"], g["tzd2"])
 torch.cuda.synchronize()
+del g, outs
+a3 = torch.from_numpy(si.jacobi3d_grid(m, m, m)).cuda()
+b3 = torch.empty_like(a3)
+st.st_jacobi3d_run(a3, b3, args.apps)
+torch.cuda.synchronize()
 print("done")
