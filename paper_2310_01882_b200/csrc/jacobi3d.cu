@@ -7,8 +7,9 @@
 // 5 adds + 1 correctly rounded divide = the paper's 6 flops per cell.
 //
 // HBM-bound (16 algorithmic bytes per point per sweep). Design = the PW
-// kernel's 2.5-D z-streaming skeleton with one field: a CTA owns a 32 x BY
-// interior column and a chunk of planes; input planes (tile + 1-cell apron)
+// kernel's 2.5-D z-streaming skeleton with one field: a CTA owns a BX x BY
+// interior column (BX = 128 measured best: longer TMA row segments) and a chunk
+// of planes; input planes (tile + 1-cell apron)
 // stream through an S-slot shared-memory ring filled by TMA
 // (cp.async.bulk.tensor.3d, one elected thread, mbarrier completion); a thread
 // owns R consecutive rows of one column, keeps its own column at z-1 and z in
@@ -25,29 +26,29 @@ namespace st {
 
 namespace {
 
-constexpr int kBX = 32;
-constexpr int kSX = kBX + 2;
-
-template <int BY>
+template <int BX, int BY>
 struct J3Tile {
+  static constexpr int SX = BX + 2;  // smem row: 1-column apron each side
   static constexpr int SY = BY + 2;
-  static constexpr int kPlaneBytes = kSX * SY * 8;
+  static constexpr int kPlaneBytes = SX * SY * 8;
   static constexpr int kPlaneStride = ((kPlaneBytes + 127) / 128) * 128 / 8;  // doubles, 128-B aligned
   static constexpr uint32_t kTxBytes = kPlaneBytes;
 };
 
-template <int BY, int S, int R>
-__global__ void __launch_bounds__(32 * (BY / R))
+template <int BX, int BY, int S, int R>
+__global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
     jacobi3d_kernel(const __grid_constant__ CUtensorMap tm, double* __restrict__ dst, int64_t nx, int64_t ny,
                     int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t planes_per_chunk) {
-  using T = J3Tile<BY>;
-  static_assert(S >= 4 && BY % R == 0, "ring depth / rows per thread");
+  using T = J3Tile<BX, BY>;
+  constexpr int kSX = T::SX, WX = BX / 32;
+  static_assert(S >= 4 && BY % R == 0 && BX % 32 == 0, "ring depth / rows per thread / tile width");
   extern __shared__ __align__(1024) double ring[];
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * T::kPlaneStride);
 
   const int lane = threadIdx.x & 31;
-  const int wy = threadIdx.x >> 5;
-  const int64_t x0 = 1 + (int64_t)blockIdx.x * kBX;
+  const int wx = (threadIdx.x >> 5) % WX;
+  const int wy = (threadIdx.x >> 5) / WX;
+  const int64_t x0 = 1 + (int64_t)blockIdx.x * BX;
   const int64_t y0 = 1 + (int64_t)blockIdx.y * BY;
   const int64_t za = z_lo + (int64_t)blockIdx.z * planes_per_chunk;
   const int64_t zb = min(z_hi, za + planes_per_chunk - 1);
@@ -67,9 +68,9 @@ __global__ void __launch_bounds__(32 * (BY / R))
   if (threadIdx.x == 0)
     for (int p = 0; p < S && p < np; ++p) issue(p, p);
 
-  const int oc = (wy * R + 1) * kSX + 1 + lane;
+  const int oc = (wy * R + 1) * kSX + 1 + wx * 32 + lane;
   const int64_t yb = y0 + (int64_t)wy * R;
-  const int64_t x = x0 + lane;
+  const int64_t x = x0 + wx * 32 + lane;
   bool ok[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) ok[i] = (yb + i <= ny) && (x <= nx);
@@ -138,23 +139,24 @@ __global__ void jacobi3d_copy_faces_kernel(const double* __restrict__ src, doubl
   }
 }
 
-template <int BY, int S, int R>
+template <int BX, int BY, int S, int R>
 st_status launch_j3(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf, int64_t ldx,
                     int64_t z_lo, int64_t z_hi, cudaStream_t s) {
-  using T = J3Tile<BY>;
+  using T = J3Tile<BX, BY>;
   CUtensorMap tm;
   const uint64_t dims[3] = {(uint64_t)(nx + 2), (uint64_t)(ny + 2), (uint64_t)nplanes_buf};
-  const uint32_t box[3] = {(uint32_t)kSX, (uint32_t)T::SY, 1u};
+  const uint32_t box[3] = {(uint32_t)T::SX, (uint32_t)T::SY, 1u};
   ST_TRY(make_tmap_3d_f64(&tm, src, dims, (uint64_t)ldx * 8, (uint64_t)ldx * 8 * (uint64_t)(ny + 2), box));
   const size_t smem = (size_t)S * T::kPlaneStride * sizeof(double) + S * sizeof(uint64_t);
-  ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi3d_kernel<BY, S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi3d_kernel<BX, BY, S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-  const int64_t ntx = (nx + kBX - 1) / kBX, nty = (ny + BY - 1) / BY, nz = z_hi - z_lo + 1;
+  const int64_t ntx = (nx + BX - 1) / BX, nty = (ny + BY - 1) / BY, nz = z_hi - z_lo + 1;
   static const int kPpc = env_int("ST_J3_PLANES", 64);
   const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(kPpc, nz));
   const int64_t nzc = (nz + ppc - 1) / ppc;
   ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "jacobi3d: grid too large");
-  jacobi3d_kernel<BY, S, R><<<dim3((unsigned)ntx, (unsigned)nty, (unsigned)nzc), 32 * (BY / R), smem, s>>>(
+  jacobi3d_kernel<BX, BY, S, R><<<dim3((unsigned)ntx, (unsigned)nty, (unsigned)nzc), (BX / 32) * (BY / R) * 32,
+                                  smem, s>>>(
       tm, dst, nx, ny, ldx, z_lo, z_hi, ppc);
   ST_LAUNCHED();
   return ST_OK;
@@ -167,10 +169,20 @@ st_status jacobi3d_sweep_planes(const double* src, double* dst, int64_t nx, int6
   if (z_hi < z_lo) return ST_OK;
   static const int kVariant = env_int("ST_J3_VARIANT", 0);
   switch (kVariant) {
-    case 1: return launch_j3<16, 6, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 2: return launch_j3<32, 6, 4>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 3: return launch_j3<16, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    default: return launch_j3<32, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 1: return launch_j3<32, 32, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 2: return launch_j3<64, 16, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 3: return launch_j3<128, 16, 4, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 4: return launch_j3<64, 16, 8, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 5: return launch_j3<128, 16, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 6: return launch_j3<192, 8, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 7: return launch_j3<128, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 8: return launch_j3<128, 4, 8, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 9: return launch_j3<32, 16, 6, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 10: return launch_j3<128, 8, 12, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 11: return launch_j3<192, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 12: return launch_j3<128, 16, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    case 13: return launch_j3<128, 8, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
+    default: return launch_j3<128, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);  // tuned
   }
 }
 

@@ -29,14 +29,13 @@ namespace st {
 
 namespace {
 
-constexpr int kBX = 32;       // interior columns per tile (one per lane)
-constexpr int kSX = kBX + 2;  // smem row: 1-column apron each side
 constexpr int kMaxPlanesPerChunk = 256;
 
-template <int BY>
+template <int BX, int BY>
 struct PwTile {
+  static constexpr int SX = BX + 2;  // smem row: 1-column apron each side
   static constexpr int SY = BY + 2;
-  static constexpr int kPlaneElems = kSX * SY;
+  static constexpr int kPlaneElems = SX * SY;
   static constexpr int kPlaneBytes = kPlaneElems * 8;
   static constexpr int kPlaneStride = ((kPlaneBytes + 127) / 128) * 128 / 8;  // doubles
   static constexpr int kSlotStride = 3 * kPlaneStride;                        // u, v, w
@@ -96,8 +95,8 @@ __device__ __forceinline__ void pw_point(const PwPoint& p, const PwCoef& k, doub
 // R consecutive rows per thread (BY = R x warps): neighbours shared by the
 // thread's own points come from registers, so shared loads per point drop from
 // 21 (R=1) to 11 + 10/R, and the R points give the scheduler independent work.
-template <int BY, int S, int R>
-__global__ void __launch_bounds__(32 * (BY / R))
+template <int BX, int BY, int S, int R>
+__global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
     pw_advect3d_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_v,
                        const __grid_constant__ CUtensorMap tm_w, double* __restrict__ su,
                        double* __restrict__ sv, double* __restrict__ sw, int64_t nx, int64_t ny,
@@ -105,9 +104,10 @@ __global__ void __launch_bounds__(32 * (BY / R))
                        const double* __restrict__ tzc2, const double* __restrict__ tzd1,
                        const double* __restrict__ tzd2, int64_t z_lo, int64_t z_hi,
                        int64_t planes_per_chunk) {
-  using T = PwTile<BY>;
+  using T = PwTile<BX, BY>;
+  constexpr int kSX = T::SX, WX = BX / 32;
   static_assert(S >= 4, "ring needs planes z-1, z, z+1 and at least one in flight");
-  static_assert(BY % R == 0, "BY = R x warps");
+  static_assert(BY % R == 0 && BX % 32 == 0, "BY = R x warp rows, BX = 32 x warp columns");
   // Dynamic smem only (TMA destinations at an aligned base):
   // [ring: S slots x (u, v, w)][coef: (tzc1,tzc2,tzd1,tzd2) per output plane][S mbarriers]
   extern __shared__ __align__(1024) double ring[];
@@ -115,8 +115,9 @@ __global__ void __launch_bounds__(32 * (BY / R))
   uint64_t* full = reinterpret_cast<uint64_t*>(coef + kMaxPlanesPerChunk);
 
   const int lane = threadIdx.x & 31;
-  const int wy = threadIdx.x >> 5;
-  const int64_t x0 = 1 + (int64_t)blockIdx.x * kBX;
+  const int wx = (threadIdx.x >> 5) % WX;
+  const int wy = (threadIdx.x >> 5) / WX;
+  const int64_t x0 = 1 + (int64_t)blockIdx.x * BX;
   const int64_t y0 = 1 + (int64_t)blockIdx.y * BY;
   const int64_t za = z_lo + (int64_t)blockIdx.z * planes_per_chunk;
   const int64_t zb = min(z_hi, za + planes_per_chunk - 1);
@@ -148,9 +149,9 @@ __global__ void __launch_bounds__(32 * (BY / R))
     for (int p = 0; p < S && p < np; ++p) issue(p, p);
 
   constexpr int PS = T::kPlaneStride;
-  const int oc = (wy * R + 1) * kSX + 1 + lane;  // first own cell inside a field plane
+  const int oc = (wy * R + 1) * kSX + 1 + wx * 32 + lane;  // first own cell inside a field plane
   const int64_t yb = y0 + (int64_t)wy * R;
-  const int64_t x = x0 + lane;
+  const int64_t x = x0 + wx * 32 + lane;
   bool ok[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) ok[i] = (yb + i <= ny) && (x <= nx);
@@ -255,21 +256,21 @@ __global__ void __launch_bounds__(32 * (BY / R))
   }
 }
 
-template <int BY, int S, int R>
+template <int BX, int BY, int S, int R>
 st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s) {
-  using T = PwTile<BY>;
+  using T = PwTile<BX, BY>;
   CUtensorMap tm[3];
   const double* f[3] = {a.u, a.v, a.w};
   const uint64_t dims[3] = {(uint64_t)(a.nx + 2), (uint64_t)(a.ny + 2), (uint64_t)(a.nz + 2)};
-  const uint32_t box[3] = {(uint32_t)kSX, (uint32_t)T::SY, 1u};
+  const uint32_t box[3] = {(uint32_t)T::SX, (uint32_t)T::SY, 1u};
   for (int i = 0; i < 3; ++i)
     ST_TRY(make_tmap_3d_f64(&tm[i], f[i], dims, (uint64_t)a.ldx * 8,
                             (uint64_t)a.ldx * 8 * (uint64_t)(a.ny + 2), box));
   const size_t smem = (size_t)S * T::kSlotStride * sizeof(double) + kMaxPlanesPerChunk * sizeof(double4) +
                       S * sizeof(uint64_t);
-  ST_CHECK_CUDA(cudaFuncSetAttribute(pw_advect3d_kernel<BY, S, R>,
+  ST_CHECK_CUDA(cudaFuncSetAttribute(pw_advect3d_kernel<BX, BY, S, R>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t ntx = (a.nx + kBX - 1) / kBX;
+  const int64_t ntx = (a.nx + BX - 1) / BX;
   const int64_t nty = (a.ny + BY - 1) / BY;
   const int64_t nz = z_hi - z_lo + 1;
   static const int kPpc = env_int("ST_PW_PLANES", 64);
@@ -277,7 +278,7 @@ st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s)
   const int64_t nzc = (nz + ppc - 1) / ppc;
   ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "pw_advect3d: grid too large");
   dim3 grid((unsigned)ntx, (unsigned)nty, (unsigned)nzc);
-  pw_advect3d_kernel<BY, S, R><<<grid, 32 * (BY / R), smem, s>>>(tm[0], tm[1], tm[2], a.su, a.sv, a.sw, a.nx,
+  pw_advect3d_kernel<BX, BY, S, R><<<grid, (BX / 32) * (BY / R) * 32, smem, s>>>(tm[0], tm[1], tm[2], a.su, a.sv, a.sw, a.nx,
                                                         a.ny, a.ldx, a.tcx, a.tcy, a.tzc1, a.tzc2,
                                                         a.tzd1, a.tzd2, z_lo, z_hi, ppc);
   ST_LAUNCHED();
@@ -290,13 +291,18 @@ st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaSt
   if (z_hi < z_lo) return ST_OK;
   static const int kVariant = env_int("ST_PW_VARIANT", 0);
   switch (kVariant) {
-    case 1: return launch_pw<16, 5, 1>(a, z_lo, z_hi, s);
-    case 2: return launch_pw<16, 5, 2>(a, z_lo, z_hi, s);
-    case 3: return launch_pw<32, 4, 4>(a, z_lo, z_hi, s);
-    case 4: return launch_pw<16, 6, 2>(a, z_lo, z_hi, s);
-    case 5: return launch_pw<32, 5, 4>(a, z_lo, z_hi, s);
-    case 6: return launch_pw<16, 8, 4>(a, z_lo, z_hi, s);
-    default: return launch_pw<32, 5, 2>(a, z_lo, z_hi, s);  // tuned on B200
+    case 1: return launch_pw<32, 16, 5, 1>(a, z_lo, z_hi, s);
+    case 2: return launch_pw<64, 16, 5, 2>(a, z_lo, z_hi, s);
+    case 3: return launch_pw<128, 8, 4, 2>(a, z_lo, z_hi, s);
+    case 4: return launch_pw<128, 8, 5, 2>(a, z_lo, z_hi, s);
+    case 5: return launch_pw<128, 4, 5, 1>(a, z_lo, z_hi, s);
+    case 6: return launch_pw<64, 8, 6, 1>(a, z_lo, z_hi, s);
+    case 7: return launch_pw<128, 8, 6, 2>(a, z_lo, z_hi, s);
+    case 8: return launch_pw<64, 16, 6, 2>(a, z_lo, z_hi, s);
+    case 9: return launch_pw<192, 8, 4, 2>(a, z_lo, z_hi, s);
+    case 10: return launch_pw<32, 32, 5, 2>(a, z_lo, z_hi, s);
+    case 11: return launch_pw<128, 8, 5, 1>(a, z_lo, z_hi, s);
+    default: return launch_pw<128, 8, 5, 2>(a, z_lo, z_hi, s);  // tuned on B200
   }
 }
 
