@@ -273,7 +273,7 @@ st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s)
   const int64_t ntx = (a.nx + BX - 1) / BX;
   const int64_t nty = (a.ny + BY - 1) / BY;
   const int64_t nz = z_hi - z_lo + 1;
-  static const int kPpc = env_int("ST_PW_PLANES", 64);
+  static const int kPpc = env_int("ST_PW_PLANES", 128);
   const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(std::min(kPpc, kMaxPlanesPerChunk), nz));
   const int64_t nzc = (nz + ppc - 1) / ppc;
   ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "pw_advect3d: grid too large");
