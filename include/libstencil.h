@@ -84,7 +84,23 @@ st_status st_comm_unique_id(uint8_t id[ST_UNIQUE_ID_BYTES]);
 st_status st_comm_init(st_comm** out, int32_t nranks, int32_t rank,
                        const uint8_t id[ST_UNIQUE_ID_BYTES], int32_t cuda_device);
 
-/* Frees the NCCL communicator, stream and events (waits for pending comm work). */
+/* Single-process group of `nranks` ranks (LOCAL transport): comms[r] is rank r,
+ * on CUDA device devices[r] (devices may repeat; distinct devices get peer
+ * access enabled). The halo swap copies boundary slabs straight into the
+ * neighbour's ghost slabs with the copy engines, ordered by device-side flags
+ * (stream memory operations), so no SM and no host synchronisation is used and
+ * the ranks' st_* calls may be issued sequentially from one host thread.
+ * Every rank must st_comm_bind the buffers it will swap. */
+st_status st_comm_init_local(st_comm** comms, int32_t nranks, const int32_t* devices);
+
+/* Registers the buffers this rank swaps (LOCAL transport; no-op for NCCL): all
+ * ranks bind the same number of buffers in the same order (buffer i of rank r
+ * exchanges with buffer i of its neighbours), each holding n_slow_local owned
+ * slabs. Re-binding replaces the previous set. */
+st_status st_comm_bind(st_comm* comm, double* const* buffers, int32_t nbuffers, int64_t n_slow_local);
+
+/* Frees the communicator's NCCL comm or group slot, stream, events and flags
+ * (waits for pending comm work). */
 st_status st_comm_destroy(st_comm* comm);
 
 st_status st_comm_query(const st_comm* comm, int32_t* rank, int32_t* nranks, int32_t* cuda_device);

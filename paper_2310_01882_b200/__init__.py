@@ -16,6 +16,7 @@ Entry points (same names as the C ABI, tensors instead of raw pointers):
     st_jacobi2d_schedule(rank, nranks, nx, ny_local, halo, iters, tblock) -> [ops]   [host only]
     st_block_split(n, nranks, rank) -> (start, count)                                [host only]
     Comm.create(rank, nranks, unique_id, device) / Comm.from_process_group(pg, device)
+    Comm.local_group(nranks, devices) -> [Comm]; comm.bind(buffers, n_slow_local)
 """
 from __future__ import annotations
 
@@ -59,6 +60,8 @@ _SIGS = {
     "st_comm_unique_id": (ctypes.c_int, [_vp]),
     "st_comm_init": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, _i32, _vp, _i32]),
     "st_comm_destroy": (ctypes.c_int, [_vp]),
+    "st_comm_init_local": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, ctypes.POINTER(_i32)]),
+    "st_comm_bind": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), _i32, _i64]),
     "st_comm_query": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "st_block_split": (ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "st_halo_plan": (ctypes.c_int, [_i32, _i32, _i64, _i64, _i32, ctypes.POINTER(Xfer),
@@ -149,6 +152,23 @@ class Comm:
         obj = [cls.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0, group=group)
         return cls.create(rank, nranks, obj[0], device)
+
+    @classmethod
+    def local_group(cls, nranks: int, devices=None) -> list["Comm"]:
+        """A single-process group of ranks (LOCAL transport: copy-engine swaps ordered by
+        device-side flags). devices[r] is rank r's CUDA device (default: all on device 0)."""
+        devices = [0] * nranks if devices is None else list(devices)
+        hs = (_vp * nranks)()
+        devs = (_i32 * nranks)(*devices)
+        _check(lib().st_comm_init_local(hs, nranks, devs), "st_comm_init_local")
+        return [cls(hs[r], r, nranks, devices[r]) for r in range(nranks)]
+
+    def bind(self, buffers, n_slow_local: int) -> None:
+        """Registers the buffers this rank swaps (LOCAL transport; no-op for NCCL)."""
+        for i, t in enumerate(buffers):
+            _f64_cuda(t, f"buffers[{i}]")
+        arr = (_vp * len(buffers))(*[t.data_ptr() for t in buffers])
+        _check(lib().st_comm_bind(self.handle, arr, len(buffers), n_slow_local), "st_comm_bind")
 
     def close(self) -> None:
         if self.handle:

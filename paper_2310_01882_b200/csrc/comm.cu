@@ -7,7 +7,10 @@
 // every message is one contiguous run of doubles (no pack kernels), sent with
 // ncclSend/ncclRecv inside one group on a dedicated comm stream so the swap of
 // sweep t overlaps the interior rows of sweep t.
+#include <cuda.h>
+
 #include <cstring>
+#include <mutex>
 
 #include "comm.h"
 #include "common.cuh"
@@ -50,6 +53,96 @@ st_status halo_plan(int32_t rank, int32_t nranks, int64_t n_slow_local, int64_t 
   return ST_OK;
 }
 
+// ------------------------------------------------ stream memory operations ---
+namespace {
+using PFN_waitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using PFN_writeValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_waitValue32 g_wait32 = nullptr;
+PFN_writeValue32 g_write32 = nullptr;
+
+st_status load_stream_memops() {
+  static std::once_flag once;
+  static bool ok = false;
+  std::call_once(once, [] {
+    void* pw = nullptr;
+    void* pr = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &pw, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWriteValue32", &pr, cudaEnableDefault, &q2) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && pw && pr) {
+      g_wait32 = reinterpret_cast<PFN_waitValue32>(pw);
+      g_write32 = reinterpret_cast<PFN_writeValue32>(pr);
+      ok = true;
+    }
+  });
+  ST_RETURN_IF(!ok, ST_ECUDA, "stream memory operations (cuStreamWaitValue32) unavailable");
+  return ST_OK;
+}
+
+st_status stream_write(cudaStream_t s, uint32_t* addr, uint32_t v) {
+  CUresult r = g_write32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v, 0);
+  ST_RETURN_IF(r != CUDA_SUCCESS, ST_ECUDA, "cuStreamWriteValue32 failed: %d", (int)r);
+  return ST_OK;
+}
+
+st_status stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t v) {
+  CUresult r = g_wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  ST_RETURN_IF(r != CUDA_SUCCESS, ST_ECUDA, "cuStreamWaitValue32 failed: %d", (int)r);
+  return ST_OK;
+}
+
+constexpr int kFlagReady = 0, kFlagDoneFromLo = 1, kFlagDoneFromHi = 2;
+
+// LOCAL transport: push my boundary slabs into the neighbours' ghost slabs.
+st_status local_exchange(st_comm* c, double* const* fields, int32_t nfields, int64_t n, int64_t pitch,
+                         int32_t width, cudaStream_t main, bool join) {
+  st_local_group* g = c->group;
+  ST_RETURN_IF(c->bound.empty(), ST_EINVAL, "LOCAL comm: st_comm_bind the swapped buffers first");
+  ST_RETURN_IF(n != c->bound_n_slow, ST_EINVAL, "LOCAL comm: %lld owned slabs, bound with %lld",
+               (long long)n, (long long)c->bound_n_slow);
+  int idx[8];
+  ST_RETURN_IF(nfields > 8, ST_EINVAL, "LOCAL comm: at most 8 fields per swap");
+  for (int f = 0; f < nfields; ++f) {
+    idx[f] = -1;
+    for (size_t i = 0; i < c->bound.size(); ++i)
+      if (c->bound[i] == fields[f]) idx[f] = (int)i;
+    ST_RETURN_IF(idx[f] < 0, ST_EINVAL, "LOCAL comm: field %d was not bound", f);
+  }
+  const uint32_t k = ++c->seq;
+  cudaStream_t cs = c->comm_stream;
+  ST_CHECK_CUDA(cudaEventRecord(c->ev_ready, main));
+  ST_CHECK_CUDA(cudaStreamWaitEvent(cs, c->ev_ready, 0));
+  ST_TRY(stream_write(cs, c->flags + kFlagReady, k));  // my ghost slabs may now be overwritten
+  const size_t bytes = (size_t)width * (size_t)pitch * sizeof(double);
+  for (int side = 0; side < 2; ++side) {
+    const int32_t peer = side == 0 ? c->rank - 1 : c->rank + 1;
+    if (peer < 0 || peer >= c->nranks) continue;
+    st_comm* pc = g->ranks[(size_t)peer];
+    ST_RETURN_IF(!pc || pc->bound.size() != c->bound.size(), ST_EINVAL,
+                 "LOCAL comm: rank %d has not bound the same buffers", peer);
+    ST_TRY(stream_wait_geq(cs, pc->flags + kFlagReady, k));
+    for (int f = 0; f < nfields; ++f) {
+      double* src = fields[f];
+      double* dst = pc->bound[(size_t)idx[f]];
+      // to rank-1: my first owned slabs -> its high ghosts; to rank+1: my last owned -> its low ghosts
+      const int64_t soff = side == 0 ? (int64_t)width * pitch : n * pitch;
+      const int64_t doff = side == 0 ? ((int64_t)width + pc->bound_n_slow) * pitch : 0;
+      if (pc->device == c->device)
+        ST_CHECK_CUDA(cudaMemcpyAsync(dst + doff, src + soff, bytes, cudaMemcpyDeviceToDevice, cs));
+      else
+        ST_CHECK_CUDA(cudaMemcpyPeerAsync(dst + doff, pc->device, src + soff, c->device, bytes, cs));
+    }
+    ST_TRY(stream_write(cs, pc->flags + (side == 0 ? kFlagDoneFromHi : kFlagDoneFromLo), k));
+  }
+  if (c->rank > 0) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromLo, k));
+  if (c->rank < c->nranks - 1) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromHi, k));
+  ST_CHECK_CUDA(cudaEventRecord(c->ev_done, cs));
+  if (join) ST_CHECK_CUDA(cudaStreamWaitEvent(main, c->ev_done, 0));
+  return ST_OK;
+}
+}  // namespace
+
 st_status halo_exchange_async(st_comm* comm, double* const* fields, int32_t nfields,
                               int64_t n_slow_local, int64_t slab_pitch, int32_t width,
                               cudaStream_t main, bool join) {
@@ -57,6 +150,8 @@ st_status halo_exchange_async(st_comm* comm, double* const* fields, int32_t nfie
   int32_t ns = 0, nr = 0;
   ST_TRY(halo_plan(comm->rank, comm->nranks, n_slow_local, slab_pitch, width, sends, &ns, recvs, &nr));
   if (comm->nranks == 1) return ST_OK;
+  if (comm->kind == st_comm::LOCAL)
+    return local_exchange(comm, fields, nfields, n_slow_local, slab_pitch, width, main, join);
   ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier NCCL error");
   ST_CHECK_CUDA(cudaEventRecord(comm->ev_ready, main));
   ST_CHECK_CUDA(cudaStreamWaitEvent(comm->comm_stream, comm->ev_ready, 0));
@@ -98,6 +193,7 @@ st_status st_comm_init(st_comm** out, int32_t nranks, int32_t rank,
   ST_RETURN_IF(nranks < 1 || rank < 0 || rank >= nranks, ST_EINVAL, "st_comm_init: rank %d of %d",
                rank, nranks);
   ST_CHECK_CUDA(cudaSetDevice(cuda_device));
+  ST_TRY(preload_kernels());
   st_comm* c = new st_comm();
   c->rank = rank;
   c->nranks = nranks;
@@ -122,6 +218,73 @@ st_status st_comm_init(st_comm** out, int32_t nranks, int32_t rank,
   return ST_OK;
 }
 
+st_status st_comm_init_local(st_comm** comms, int32_t nranks, const int32_t* devices) {
+  clear_error();
+  ST_RETURN_IF(!comms || !devices || nranks < 1, ST_EINVAL, "st_comm_init_local: bad arguments");
+  ST_TRY(load_stream_memops());
+  int ndev = 0;
+  ST_CHECK_CUDA(cudaGetDeviceCount(&ndev));
+  for (int r = 0; r < nranks; ++r)
+    ST_RETURN_IF(devices[r] < 0 || devices[r] >= ndev, ST_EINVAL, "st_comm_init_local: device %d", devices[r]);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  // peer access between the distinct devices of the group (copies and flag writes go device to device)
+  for (int i = 0; i < nranks; ++i)
+    for (int j = 0; j < nranks; ++j)
+      if (devices[i] != devices[j]) {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, devices[i], devices[j]);
+        ST_RETURN_IF(!can, ST_ENOTSUP, "st_comm_init_local: no peer access %d -> %d", devices[i], devices[j]);
+        cudaSetDevice(devices[i]);
+        cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else ST_CHECK_CUDA(e);
+      }
+  for (int r = 0; r < nranks; ++r) {
+    cudaSetDevice(devices[r]);
+    ST_TRY(preload_kernels());
+  }
+  st_local_group* g = new st_local_group();
+  g->nranks = nranks;
+  g->ranks.assign((size_t)nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    st_comm* c = new st_comm();
+    c->kind = st_comm::LOCAL;
+    c->rank = r;
+    c->nranks = nranks;
+    c->device = devices[r];
+    c->group = g;
+    cudaSetDevice(c->device);
+    if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMalloc(&c->flags, 4 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemset(c->flags, 0, 4 * sizeof(uint32_t)) != cudaSuccess) {
+      set_error("st_comm_init_local: stream/event/flag allocation failed");
+      delete c;
+      for (int q = 0; q < r; ++q) st_comm_destroy(comms[q]);
+      cudaSetDevice(prev);
+      return ST_ECUDA;
+    }
+    g->ranks[(size_t)r] = c;
+    g->alive++;
+    comms[r] = c;
+  }
+  ST_CHECK_CUDA(cudaDeviceSynchronize());  // flags are zero before any stream uses them
+  cudaSetDevice(prev);
+  return ST_OK;
+}
+
+st_status st_comm_bind(st_comm* comm, double* const* buffers, int32_t nbuffers, int64_t n_slow_local) {
+  clear_error();
+  ST_RETURN_IF(!comm || nbuffers < 0 || (nbuffers > 0 && !buffers) || n_slow_local < 1, ST_EINVAL,
+               "st_comm_bind: bad arguments");
+  if (comm->kind != st_comm::LOCAL) return ST_OK;
+  comm->bound.assign(buffers, buffers + nbuffers);
+  comm->bound_n_slow = n_slow_local;
+  return ST_OK;
+}
+
 st_status st_comm_destroy(st_comm* c) {
   clear_error();
   if (!c) return ST_OK;
@@ -132,6 +295,12 @@ st_status st_comm_destroy(st_comm* c) {
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->flags) cudaFree(c->flags);
+  if (c->group) {
+    st_local_group* g = c->group;
+    g->ranks[(size_t)c->rank] = nullptr;
+    if (--g->alive == 0) delete g;
+  }
   delete c;
   return s;
 }

@@ -1,21 +1,48 @@
-// comm.h — st_comm: an NCCL communicator plus the streams/events that let the
-// halo swap of one sweep run concurrently with the interior rows of that sweep.
+// comm.h — st_comm: a rank of a slab decomposition plus the streams/events that
+// let the halo swap of one sweep run concurrently with the interior rows.
+//
+// Two transports:
+//  * NCCL  — one process per GPU, ncclSend/ncclRecv on a comm stream.
+//  * LOCAL — a group of ranks inside one process (same or different GPUs):
+//            the swap is a copy-engine cudaMemcpyAsync into the neighbour's
+//            ghost slabs, ordered by device-side flags written/waited with
+//            stream memory operations (cuStreamWriteValue32/WaitValue32), so
+//            no SM and no host synchronisation is involved and the ranks'
+//            calls may be issued one after another from one host thread.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <vector>
+
 #include "libstencil.h"
 
+struct st_local_group;
+
 struct st_comm {
+  enum Kind { NCCL = 0, LOCAL = 1 };
+  Kind kind = NCCL;
   ncclComm_t nccl = nullptr;
   int32_t rank = 0;
   int32_t nranks = 1;
   int32_t device = 0;
-  cudaStream_t comm_stream = nullptr;  // NCCL work runs here
+  cudaStream_t comm_stream = nullptr;  // swap work runs here
   cudaEvent_t ev_ready = nullptr;      // main -> comm: boundary rows are written
   cudaEvent_t ev_done = nullptr;       // comm -> main: ghost rows have arrived
   bool broken = false;                 // set after an NCCL error
+  // LOCAL transport
+  st_local_group* group = nullptr;
+  uint32_t* flags = nullptr;  // device: [0] ready-to-receive, [1] done from rank-1, [2] done from rank+1
+  uint32_t seq = 0;           // swaps issued so far (all ranks issue the same sequence)
+  std::vector<double*> bound;  // buffers registered with st_comm_bind (same order on every rank)
+  int64_t bound_n_slow = 0;    // owned slabs of this rank's bound buffers
+};
+
+struct st_local_group {
+  int32_t nranks = 0;
+  int32_t alive = 0;
+  std::vector<st_comm*> ranks;
 };
 
 namespace st {

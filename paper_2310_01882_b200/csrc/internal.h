@@ -7,6 +7,7 @@
 
 #include <vector>
 
+#include "common.cuh"
 #include "libstencil.h"
 
 namespace st {
@@ -64,6 +65,20 @@ st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaSt
 int choose_tblock(int32_t nranks, int64_t nx, int64_t n, int32_t h, int32_t tblock);
 st_status build_jacobi_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_t n, int32_t h,
                                 int64_t iters, int32_t tblock, std::vector<st_op>& ops, int dims = 2);
+
+// Eagerly loads every kernel of the library on the current device. Under CUDA's
+// lazy module loading, the first launch of a kernel may wait for the device to
+// drain; if another rank's stream is parked on a device-side wait (NCCL, or the
+// LOCAL transport's flag waits) that wait never ends. Communicators therefore
+// preload all kernels at creation.
+st_status jacobi2d_preload();
+st_status jacobi3d_preload();
+st_status pw_advect3d_preload();
+inline st_status preload_kernels() {
+  ST_TRY(jacobi2d_preload());
+  ST_TRY(jacobi3d_preload());
+  return pw_advect3d_preload();
+}
 
 // --------------------------------------------------------------- misc ---
 int env_int(const char* name, int dflt);

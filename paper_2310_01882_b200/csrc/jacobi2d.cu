@@ -320,6 +320,25 @@ st_status launch_tb(const double* src, double* dst, int64_t nx, int64_t ld, int6
 
 bool jacobi2d_tb_supported(int t) { return t == 2 || t == 4 || t == 6 || t == 8; }
 
+st_status jacobi2d_preload() {
+  cudaFuncAttributes fa;
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_stream_kernel<4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_resident_kernel));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<2, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<2, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<2, 3>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<4, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<4, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<4, 3>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<6, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<6, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<6, 3>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 3>));
+  return ST_OK;
+}
+
 st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
                            int t, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s) {
   if (y_hi < y_lo) return ST_OK;

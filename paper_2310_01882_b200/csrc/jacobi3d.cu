@@ -164,6 +164,25 @@ st_status launch_j3(const double* src, double* dst, int64_t nx, int64_t ny, int6
 
 }  // namespace
 
+st_status jacobi3d_preload() {
+  cudaFuncAttributes fa;
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 16, 4, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 16, 6, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 16, 8, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 4, 8, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 8, 12, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 8, 6, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 8, 8, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<192, 8, 6, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<192, 8, 8, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<32, 16, 6, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<32, 32, 6, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<64, 16, 6, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<64, 16, 8, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_copy_faces_kernel));
+  return ST_OK;
+}
+
 st_status jacobi3d_sweep_planes(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
                                 int64_t ldx, int64_t z_lo, int64_t z_hi, cudaStream_t s) {
   if (z_hi < z_lo) return ST_OK;

@@ -287,6 +287,22 @@ st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s)
 
 }  // namespace
 
+st_status pw_advect3d_preload() {
+  cudaFuncAttributes fa;
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 4, 5, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 4, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 5, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 5, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 6, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<192, 8, 4, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<32, 16, 5, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<32, 32, 5, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<64, 16, 5, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<64, 16, 6, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<64, 8, 6, 1>));
+  return ST_OK;
+}
+
 st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s) {
   if (z_hi < z_lo) return ST_OK;
   static const int kVariant = env_int("ST_PW_VARIANT", 0);

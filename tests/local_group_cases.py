@@ -1,0 +1,148 @@
+"""Runs the decomposed CUDA path with a LOCAL rank group on one GPU (P ranks in
+this process) and checks the gathered result against the oracle, bitwise.
+Executed as a subprocess by tests/test_gpu_local_group.py so that
+CUDA_DEVICE_MAX_CONNECTIONS is set before CUDA initialises (each rank uses its
+own main + comm stream; the ranks' calls are issued one after another and
+ordered on the device)."""
+import pathlib
+import sys
+
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+
+import numpy as np
+import torch
+
+import oracle
+import paper_2310_01882_b200 as st
+import stencil_inputs as si
+
+
+def slab2d(g, nranks, r, h):
+    ny = g.shape[0] - 2
+    start, n = st.st_block_split(ny, nranks, r)
+    buf = np.zeros((n + 2 * h, g.shape[1]))
+    for l in range(n + 2 * h):
+        gr = start + 1 + (l - h)
+        if 0 <= gr <= ny + 1:
+            buf[l] = g[gr]
+    return buf, start, n
+
+
+def jacobi2d_case(P, nx, ny, h, iters, tblock, poison=True):
+    g = si.jacobi2d_grid(nx, ny)
+    comms = st.Comm.local_group(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    ranks = []
+    for r in range(P):
+        buf, start, n = slab2d(g, P, r, h)
+        a = torch.from_numpy(buf).cuda()
+        if poison:  # ghosts of middle ranks must come from the swap
+            if r > 0:
+                a[:h] = float("nan")
+            if r < P - 1:
+                a[h + n:] = float("nan")
+        b = torch.full_like(a, float("nan"))
+        comms[r].bind([a, b], n)
+        ranks.append((a, b, start, n))
+    torch.cuda.synchronize()
+    outs = []
+    for r in range(P):
+        a, b, start, n = ranks[r]
+        with torch.cuda.stream(streams[r]):
+            outs.append(st.st_jacobi2d_run(a, b, iters, tblock=tblock, halo=h, comm=comms[r], nx=nx))
+    torch.cuda.synchronize()
+    want = oracle.jacobi2d(g, iters, nx=nx)
+    ok = True
+    for r in range(P):
+        _, _, start, n = ranks[r]
+        got = outs[r].cpu().numpy()[h:h + n, :nx + 2]
+        ok &= bool(np.array_equal(got, want[start + 1:start + 1 + n, :nx + 2]))
+    for c in comms:
+        c.close()
+    return ok
+
+
+def jacobi3d_case(P, nx, ny, nz, h, iters):
+    g = si.jacobi3d_grid(nx, ny, nz)
+    comms = st.Comm.local_group(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    ranks = []
+    for r in range(P):
+        start, n = st.st_block_split(nz, P, r)
+        loc = np.zeros((n + 2 * h, ny + 2, g.shape[2]))
+        for l in range(n + 2 * h):
+            gz = start + 1 + (l - h)
+            if 0 <= gz <= nz + 1:
+                loc[l] = g[gz]
+        a = torch.from_numpy(loc).cuda()
+        b = torch.full_like(a, float("nan"))
+        comms[r].bind([a, b], n)
+        ranks.append((a, b, start, n))
+    torch.cuda.synchronize()
+    outs = []
+    for r in range(P):
+        a, b, start, n = ranks[r]
+        with torch.cuda.stream(streams[r]):
+            outs.append(st.st_jacobi3d_run(a, b, iters, halo=h, comm=comms[r], nx=nx))
+    torch.cuda.synchronize()
+    want = oracle.jacobi3d(g, iters, nx=nx)
+    ok = True
+    for r in range(P):
+        _, _, start, n = ranks[r]
+        ok &= bool(np.array_equal(outs[r].cpu().numpy()[h:h + n], want[start + 1:start + 1 + n]))
+    for c in comms:
+        c.close()
+    return ok
+
+
+def pw_case(P, nx, ny, nz):
+    d = si.pw_inputs(nx, ny, nz)
+    want = oracle.pw_advect3d(d["u"], d["v"], d["w"], d)
+    comms = st.Comm.local_group(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    parts = []
+    for r in range(P):
+        z0, n = st.st_block_split(nz, P, r)
+        dl = si.pw_inputs(nx, ny, nz, plane0=z0, planes=n + 2)
+        g = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in dl.items()}
+        for k in "uvw":
+            if r > 0:
+                g[k][0] = float("nan")
+            if r < P - 1:
+                g[k][-1] = float("nan")
+        outs = [torch.zeros_like(g["u"]) for _ in range(3)]
+        comms[r].bind([g["u"], g["v"], g["w"]], n)
+        parts.append((g, outs, z0, n))
+    torch.cuda.synchronize()
+    for r in range(P):
+        g, outs, _, _ = parts[r]
+        with torch.cuda.stream(streams[r]):
+            st.st_pw_advect3d(g["u"], g["v"], g["w"], *outs, g["tcx"], g["tcy"], g["tzc1"], g["tzc2"], g["tzd1"],
+                              g["tzd2"], comm=comms[r])
+    torch.cuda.synchronize()
+    ok = True
+    for g, outs, z0, n in parts:
+        for o, w in zip(outs, want):
+            ok &= bool(np.array_equal(o.cpu().numpy()[1:n + 1], w[z0 + 1:z0 + 1 + n]))
+    for c in comms:
+        c.close()
+    return ok
+
+
+CASES = {
+    "j2_h1": lambda: jacobi2d_case(2, 130, 200, 1, 9, 1),
+    "j2_p3_h1": lambda: jacobi2d_case(3, 70, 101, 1, 7, 1),
+    "j2_h4_t4": lambda: jacobi2d_case(2, 300, 260, 4, 13, 4),
+    "j2_p4_h6_t6": lambda: jacobi2d_case(4, 260, 520, 6, 25, 6),
+    "j2_p3_h3_t1": lambda: jacobi2d_case(3, 90, 99, 3, 10, 1),
+    "j3_h1": lambda: jacobi3d_case(2, 70, 40, 33, 1, 7),
+    "j3_p3_h2": lambda: jacobi3d_case(3, 40, 30, 31, 2, 6),
+    "pw_p2": lambda: pw_case(2, 140, 20, 41),
+    "pw_p4": lambda: pw_case(4, 70, 17, 40),
+}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(CASES)
+    bad = [n for n in names if not CASES[n]()]
+    print("LOCAL-GROUP CASES", "FAILED: " + ",".join(bad) if bad else "OK", flush=True)
+    sys.exit(1 if bad else 0)

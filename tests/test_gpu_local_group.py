@@ -1,0 +1,22 @@
+"""GPU tests of the decomposed path on ONE B200: P ranks in one process (LOCAL
+transport) run the real kernels, the shared schedule (boundary rows, async
+copy-engine swap, interior rows, join) and temporal blocking across ranks; the
+gathered results equal the oracle bitwise."""
+import os
+import pathlib
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = pathlib.Path(__file__).resolve().parent
+
+
+@pytest.mark.parametrize("case", ["j2_h1", "j2_p3_h1", "j2_h4_t4", "j2_p4_h6_t6", "j2_p3_h3_t1", "j3_h1", "j3_p3_h2",
+                                  "pw_p2", "pw_p4"])
+def test_local_group_equals_oracle(cuda_lib, case):
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    r = subprocess.run([sys.executable, str(HERE / "local_group_cases.py"), case], env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "CASES OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
