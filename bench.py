@@ -416,6 +416,26 @@ def main():
                                   "kind": "oracle", "sample": f"2 sweeps of the 512^3 grid; {dt:.2f} s"}
         del A3, B3
 
+    # ------------------------------------------------------------------ C1: 64^2 + ring, 100 sweeps (latency-bound)
+    c1 = None
+    if world == 1:
+        a1 = torch.from_numpy(si.jacobi2d_grid(64, 64)).to(dev)
+        b1 = torch.empty_like(a1)
+        c1 = {"workload": "jacobi2d_64x64_fp64_100sweeps (configs[0])", "unit": "us per 100 sweeps"}
+        for label, tb in (("resident_single_cta", 0), ("one_launch_per_sweep", 1)):
+            for _ in range(3):
+                st.st_jacobi2d_run(a1, b1, 100, tblock=tb)
+            torch.cuda.synchronize()
+            reps = 20
+            ev0.record(stream)
+            for _ in range(reps):
+                st.st_jacobi2d_run(a1, b1, 100, tblock=tb)
+            ev1.record(stream)
+            ev1.synchronize()
+            c1[label] = round(ev0.elapsed_time(ev1) * 1e3 / reps, 2)
+        c1["value_resident_gpts"] = round(64 * 64 * 100 / (c1["resident_single_cta"] * 1e-6) / 1e9, 3)
+        del a1, b1
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_jacobi(args.cpu_sweeps)
@@ -444,6 +464,7 @@ def main():
             "cpu_baseline": cpu,
             "pw_advect3d": pw,
             "jacobi3d": j3,
+            "c1": c1,
         }
         print(json.dumps(out), flush=True)
     if dist is not None:
