@@ -290,9 +290,12 @@ def main():
     launches = st.launch_count() - l0
     step_ms = max_over_ranks(sum(times) / len(times))
     launches_per_step = launches / args.steps
-    launch_ms = step_ms / launches_per_step  # every launch in the step is a sweep/pass kernel
     ops = st.st_jacobi2d_schedule(rank, world, n_glob, ny_loc, halo, sweeps, args.tblock)
     pass_sweeps = sorted({o["sweeps"] for o in ops if o["kind"] == st.OP_SWEEP})
+    # one pass = one read + one write of the rank's grid (a pass may be split into boundary and
+    # interior launches across ranks); its average duration is the roofline's launch time
+    passes_per_step = sum(1 for o in ops if o["kind"] == st.OP_SWAP)
+    launch_ms = step_ms / passes_per_step
     pts_total = n_glob * n_glob * sweeps
     value = pts_total / (step_ms / 1e3) / 1e9
     pts_rank = ny_loc * n_glob
@@ -456,7 +459,8 @@ def main():
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved_gbs, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(achieved_gbs / hbm_peak, 4), "traffic": ncu_traffic(kname),
                          "bytes_per_pt_per_launch": JACOBI_BYTES_PER_PT, "sweeps_per_launch": pass_sweeps,
-                         "launches_per_step": launches_per_step, "ms_per_launch": round(launch_ms, 5),
+                         "launches_per_step": launches_per_step, "passes_per_step": passes_per_step,
+                         "ms_per_pass": round(launch_ms, 5),
                          "effective_gbs_16B_per_update": round(effective_gbs, 1), "peak_source": peak_src},
             "e2e": e2e,
             "gpu_launches": launches,
