@@ -98,7 +98,9 @@ __global__ void __launch_bounds__(kStreamThreads)
   }
 }
 
-// All sweeps inside one CTA: both buffers live in shared memory, compact pitch nxp2.
+// All sweeps inside one CTA: both buffers live in shared memory, compact pitch
+// nxp2. 2-D thread block (bx columns x by rows): thread (tx, ty) owns the points
+// x = 1+tx+i*bx, y = 1+ty+j*by, so the sweep loop has no integer division.
 __global__ void __launch_bounds__(1024)
     jacobi2d_resident_kernel(double* __restrict__ a, double* __restrict__ b, int nxp2, int nyp2,
                              int64_t ld, int64_t iters) {
@@ -106,22 +108,27 @@ __global__ void __launch_bounds__(1024)
   const int n = nxp2 * nyp2;
   double* s0 = sm;
   double* s1 = sm + n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int y = i / nxp2, x = i - y * nxp2;
-    const double v = a[(int64_t)y * ld + x];
-    s0[i] = v;
-    s1[i] = v;
-  }
+  for (int y = threadIdx.y; y < nyp2; y += blockDim.y)
+    for (int x = threadIdx.x; x < nxp2; x += blockDim.x) {
+      const double v = a[(int64_t)y * ld + x];
+      s0[y * nxp2 + x] = v;
+      s1[y * nxp2 + x] = v;
+    }
   __syncthreads();
   const int nx = nxp2 - 2, ny = nyp2 - 2;
-  const int ni = nx * ny;
   double* cur = s0;
   double* nxt = s1;
   for (int64_t it = 0; it < iters; ++it) {
-    for (int i = threadIdx.x; i < ni; i += blockDim.x) {
-      const int y = 1 + i / nx, x = 1 + (i - (y - 1) * nx);
-      const int c = y * nxp2 + x;
-      nxt[c] = dmul(dadd(dadd(dadd(cur[c - nxp2], cur[c + nxp2]), cur[c - 1]), cur[c + 1]), 0.25);
+    // the two buffers never alias: let the compiler hoist every load of the sweep
+    const double* __restrict__ src = cur;
+    double* __restrict__ dst = nxt;
+#pragma unroll 4
+    for (int y = 1 + threadIdx.y; y <= ny; y += blockDim.y) {
+      const int row = y * nxp2;
+      for (int x = 1 + threadIdx.x; x <= nx; x += blockDim.x) {
+        const int c = row + x;
+        dst[c] = dmul(dadd(dadd(dadd(src[c - nxp2], src[c + nxp2]), src[c - 1]), src[c + 1]), 0.25);
+      }
     }
     __syncthreads();
     double* t = cur;
@@ -129,10 +136,8 @@ __global__ void __launch_bounds__(1024)
     nxt = t;
   }
   double* out = (iters & 1) ? b : a;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int y = i / nxp2, x = i - y * nxp2;
-    out[(int64_t)y * ld + x] = cur[i];
-  }
+  for (int y = threadIdx.y; y < nyp2; y += blockDim.y)
+    for (int x = threadIdx.x; x < nxp2; x += blockDim.x) out[(int64_t)y * ld + x] = cur[y * nxp2 + x];
 }
 
 constexpr size_t kResidentMaxSmem = 200 * 1024;
@@ -165,7 +170,9 @@ st_status jacobi2d_resident(double* a, double* b, int64_t nx, int64_t ny, int64_
   const size_t smem = (size_t)(nx + 2) * (size_t)(ny + 2) * 2 * sizeof(double);
   ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi2d_resident_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResidentMaxSmem));
-  jacobi2d_resident_kernel<<<1, 1024, smem, s>>>(a, b, (int)(nx + 2), (int)(ny + 2), ld, iters);
+  const int bx = (int)std::min<int64_t>(1024, ((nx + 31) / 32) * 32);
+  const int by = std::max(1, std::min(1024 / bx, (int)ny));
+  jacobi2d_resident_kernel<<<1, dim3(bx, by), smem, s>>>(a, b, (int)(nx + 2), (int)(ny + 2), ld, iters);
   ST_LAUNCHED();
   return ST_OK;
 }
