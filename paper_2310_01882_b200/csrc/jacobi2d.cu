@@ -297,6 +297,150 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
   }
 }
 
+// ---- 4 columns per lane (two 16-byte pairs): 128-column strips, half the
+// shuffles per point and 2T/128 instead of 2T/64 redundant columns.
+struct Quad {
+  double2 a, b;  // columns x, x+1 | x+2, x+3
+};
+
+template <int T, bool kRows, bool kCols>
+__device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][2], const int k, Quad s, int64_t r, const bool (&ring)[4],
+                                           int64_t ring_lo, int64_t ring_hi) {
+#pragma unroll
+  for (int j = 0; j < T; ++j) {
+    const Quad n = st[j][k & 1];
+    const Quad c = st[j][(k + 1) & 1];
+    const double w = __shfl_up_sync(0xffffffffu, c.b.y, 1);
+    const double e = __shfl_down_sync(0xffffffffu, c.a.x, 1);
+    Quad o;
+    o.a.x = dmul(dadd(dadd(dadd(n.a.x, s.a.x), w), c.a.y), 0.25);
+    o.a.y = dmul(dadd(dadd(dadd(n.a.y, s.a.y), c.a.x), c.b.x), 0.25);
+    o.b.x = dmul(dadd(dadd(dadd(n.b.x, s.b.x), c.a.y), c.b.y), 0.25);
+    o.b.y = dmul(dadd(dadd(dadd(n.b.y, s.b.y), c.b.x), e), 0.25);
+    if (kCols) {
+      if (ring[0]) o.a.x = c.a.x;
+      if (ring[1]) o.a.y = c.a.y;
+      if (ring[2]) o.b.x = c.b.x;
+      if (ring[3]) o.b.y = c.b.y;
+    }
+    if (kRows) {
+      const int64_t row = r - j - 1;
+      if (row <= ring_lo || row >= ring_hi) o = c;
+    }
+    st[j][k & 1] = s;
+    s = o;
+  }
+  return s;
+}
+
+template <int T, int kMinBlocks>
+__global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
+    jacobi2d_tb4_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
+                        int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk, int64_t nstrips, int64_t ring_lo,
+                        int64_t ring_hi, int64_t nrows_buf) {
+  static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
+  constexpr int kCols = 128, kStride = kCols - 2 * T, G = 2;
+  const int lane = threadIdx.x & 31;
+  const int64_t strip = (int64_t)blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
+  if (strip >= nstrips) return;
+  const int64_t yc0 = y_lo + (int64_t)blockIdx.y * rows_per_chunk;
+  if (yc0 > y_hi) return;
+  const int64_t yc1 = min(y_hi, yc0 + rows_per_chunk - 1);
+
+  const int64_t x = strip * kStride - T + 4 * lane;
+  const int64_t x_first = strip * kStride - T;
+  const int64_t lo_c = x_first + T, hi_c = x_first + kCols - T;  // exact columns [lo_c, hi_c)
+  const bool has_a = x >= 0 && x < nxp2, has_b = x + 2 >= 0 && x + 2 < nxp2;
+  const bool sta0 = x >= lo_c && x < hi_c && x >= 0 && x < nxp2;
+  const bool sta1 = x + 1 >= lo_c && x + 1 < hi_c && x + 1 >= 0 && x + 1 < nxp2;
+  const bool stb0 = x + 2 >= lo_c && x + 2 < hi_c && x + 2 >= 0 && x + 2 < nxp2;
+  const bool stb1 = x + 3 >= lo_c && x + 3 < hi_c && x + 3 >= 0 && x + 3 < nxp2;
+  bool ring[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) ring[i] = (x + i == 0) || (x + i == nxp2 - 1);
+  const bool col_ring = x_first <= 0 || x_first + kCols >= nxp2 - 1;
+  const double* spa = src + (has_a ? x : 0);
+  const double* spb = src + (has_b ? x + 2 : 0);
+
+  const int64_t r_first = max(max(ring_lo, (int64_t)0), yc0 - T);
+  const int64_t r_load_last = min(min(ring_hi, nrows_buf - 1), yc1 + T);
+  const int64_t r_end = yc1 + T;
+
+  Quad st[T][2];
+#pragma unroll
+  for (int j = 0; j < T; ++j) {
+    st[j][0].a = st[j][0].b = st[j][1].a = st[j][1].b = make_double2(0.0, 0.0);
+  }
+  Quad buf[G];
+  const int64_t safe_off = r_first * ld;
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    const int64_t off = (r_first + k <= r_load_last) ? (r_first + k) * ld : safe_off;
+    buf[k].a = ldg2(spa + off);
+    buf[k].b = ldg2(spb + off);
+  }
+  int64_t loff = (r_first + G) * ld;
+  double* out = dst + x + (r_first - T) * ld;
+
+  for (int64_t r0 = r_first; r0 <= r_end; r0 += G) {
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const int64_t r = r0 + k;
+      if (r > r_end) break;
+      const Quad s0 = buf[k];
+      const int64_t off = (r + G <= r_load_last) ? loff : safe_off;
+      buf[k].a = ldg2(spa + off);
+      buf[k].b = ldg2(spb + off);
+      loff += ld;
+      const bool rows_chk = (r - T <= ring_lo) || (r - 1 >= ring_hi);
+      Quad o;
+      if (rows_chk) {
+        o = col_ring ? tb4_levels<T, true, true>(st, k, s0, r, ring, ring_lo, ring_hi)
+                     : tb4_levels<T, true, false>(st, k, s0, r, ring, ring_lo, ring_hi);
+      } else {
+        o = col_ring ? tb4_levels<T, false, true>(st, k, s0, r, ring, ring_lo, ring_hi)
+                     : tb4_levels<T, false, false>(st, k, s0, r, ring, ring_lo, ring_hi);
+      }
+      if (r - T >= yc0 && r - T <= yc1) {
+        if (sta0 && sta1) stg2(out, o.a);
+        else if (sta0) out[0] = o.a.x;
+        else if (sta1) out[1] = o.a.y;
+        if (stb0 && stb1) stg2(out + 2, o.b);
+        else if (stb0) out[2] = o.b.x;
+        else if (stb1) out[3] = o.b.y;
+      }
+      out += ld;
+    }
+  }
+}
+
+template <int T>
+st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
+                     int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s) {
+  const int64_t nxp2 = nx + 2;
+  constexpr int kStride = 128 - 2 * T;
+  const int64_t nstrips = (nxp2 + kStride - 1) / kStride;
+  const int64_t rows = y_hi - y_lo + 1;
+  const int64_t blocks_x = (nstrips + kStreamWarps - 1) / kStreamWarps;
+  static const int kOcc = env_int("ST_JACOBI_TB4_OCC", 1);
+  // short chunks balance the single-CTA-per-SM grid (measured: 192 rows best
+  // on C2); the 2T rows a chunk re-reads are mostly L2 hits because the chunks
+  // of a strip run at about the same time
+  static const int kRows = env_int("ST_JACOBI_TB4_ROWS", 192);
+  const int64_t rpc = std::max<int64_t>(1, std::min<int64_t>(kRows, rows));
+  const int64_t nchunks = (rows + rpc - 1) / rpc;
+  ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d tb: too many row chunks");
+  dim3 grid((unsigned)blocks_x, (unsigned)nchunks);
+  if (kOcc == 1)
+    jacobi2d_tb4_kernel<T, 1><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
+                                                              ring_hi, nrows_buf);
+  else
+    jacobi2d_tb4_kernel<T, 2><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
+                                                              ring_hi, nrows_buf);
+  ST_LAUNCHED();
+  return ST_OK;
+}
+
 template <int T>
 st_status launch_tb(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
                     int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s) {
@@ -343,12 +487,30 @@ st_status jacobi2d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 1>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 3>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2>));
   return ST_OK;
 }
 
 st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
                            int t, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s) {
   if (y_hi < y_lo) return ST_OK;
+  static const int kColsPerLane = env_int("ST_JACOBI_TB_COLS", 4);
+  if (kColsPerLane == 4) {
+    switch (t) {
+      case 2: return launch_tb4<2>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
+      case 4: return launch_tb4<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
+      case 6: return launch_tb4<6>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
+      case 8: return launch_tb4<8>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
+      default: break;
+    }
+  }
   switch (t) {
     case 2: return launch_tb<2>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
     case 4: return launch_tb<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);

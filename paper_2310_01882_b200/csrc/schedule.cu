@@ -17,7 +17,7 @@
 namespace st {
 
 namespace {
-constexpr int kAutoTblock = 6;           // tblock=0 (tuned on B200: 1271 Gpts/s on C2)
+constexpr int kAutoTblock = 8;  // tblock=0 (tuned on B200)
 constexpr int64_t kAutoMinExtent = 128;  // ... on grids at least this large in x and y
 
 void push(std::vector<st_op>& v, int32_t kind, int32_t buf, int32_t sweeps, int32_t flag, int64_t lo = 0,
