@@ -146,3 +146,27 @@ def test_launches_counted(cuda_lib):
     cuda_lib.st_jacobi2d_run(a, b, 7, tblock=1)
     torch.cuda.synchronize()
     assert cuda_lib.launch_count() - n0 == 7
+
+
+def test_pair_variant_of_tb_kernel_bitwise(cuda_lib):
+    # the 2-columns-per-lane temporal-blocking kernel (ST_JACOBI_TB_COLS=2) is kept as a
+    # lower-register variant; it must give the same bits as the oracle
+    import os
+    import pathlib
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle, stencil_inputs as si, paper_2310_01882_b200 as st
+ok = True
+for nx, ny, it, tb in ((250, 1100, 13, 2), (250, 1100, 17, 4), (301, 700, 25, 6), (130, 90, 19, 8)):
+    a = si.jacobi2d_grid(nx, ny)
+    ta = torch.from_numpy(a).cuda(); tb_ = torch.empty_like(ta)
+    r = st.st_jacobi2d_run(ta, tb_, it, tblock=tb, nx=nx).cpu().numpy()
+    ok &= bool(np.array_equal(r[:, :nx + 2], oracle.jacobi2d(a, it, nx=nx)[:, :nx + 2]))
+print("PAIR", ok)
+""" % str(pathlib.Path(__file__).resolve().parent.parent)
+    env = dict(os.environ, ST_JACOBI_TB_COLS="2")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert "PAIR True" in r.stdout, r.stdout + r.stderr[-2000:]
