@@ -98,59 +98,76 @@ st_status check_device_ptr(const void* p, const char* what) {
   return ST_OK;
 }
 
-// Executes the schedule of build_jacobi_schedule (schedule.cu) on the GPU.
-st_status run_schedule(const std::vector<st_op>& ops, st_comm* comm, double* a, double* b, int64_t nx,
-                       int64_t n, int64_t ld, int32_t h, cudaStream_t s) {
+// Executes a schedule of build_jacobi_schedule (schedule.cu) on the GPU.
+// `sweep(src, dst, op, remote)` runs one SWEEP op. With a LOCAL communicator the
+// pattern [boundary sweep lo, boundary sweep hi, async EXCHANGE of their
+// destination, (interior sweep), JOIN] is executed fused: the boundary sweeps
+// store their rows straight into the neighbours' ghost rows (NEXT #3) and the
+// exchange becomes device-side flag signalling; otherwise the exchange is the
+// transport's swap (NCCL p2p or copy engine).
+template <typename Sweep>
+st_status run_schedule_generic(const std::vector<st_op>& ops, st_comm* comm, double* a, double* b, int64_t n,
+                               int64_t pitch, cudaStream_t s, Sweep sweep) {
   double* buf[2] = {a, b};
-  const int64_t nrows = n + 2 * (int64_t)h;
-  for (const st_op& o : ops) {
+  const bool fuse = fused_halo_available(comm);
+  bool pending_fused = false;  // the exchange the next JOIN completes was fused
+  for (size_t i = 0; i < ops.size(); ++i) {
+    const st_op& o = ops[i];
+    if (fuse && o.kind == ST_OP_SWEEP && i + 2 < ops.size() && ops[i + 1].kind == ST_OP_SWEEP &&
+        ops[i + 2].kind == ST_OP_EXCHANGE && ops[i + 2].flag == 1 && ops[i + 2].buf == 1 - o.buf) {
+      Remote lo, hi;
+      ST_TRY(fused_halo_begin(comm, buf[1 - o.buf], n, s, &lo, &hi));
+      ST_TRY(sweep(buf[o.buf], buf[1 - o.buf], o, lo));               // first owned slabs -> rank-1
+      ST_TRY(sweep(buf[o.buf], buf[1 - o.buf], ops[i + 1], hi));      // last owned slabs  -> rank+1
+      ST_TRY(fused_halo_signal(comm, s));
+      pending_fused = true;
+      i += 2;  // the exchange op is replaced by the fused stores + flags
+      continue;
+    }
     switch (o.kind) {
       case ST_OP_SWEEP:
-        if (o.sweeps == 1)
-          ST_TRY(jacobi2d_sweep_rows(buf[o.buf], buf[1 - o.buf], nx, ld, o.y_lo, o.y_hi, s));
-        else
-          ST_TRY(jacobi2d_tb_rows(buf[o.buf], buf[1 - o.buf], nx, ld, o.y_lo, o.y_hi, o.sweeps, o.ring_lo,
-                                  o.ring_hi, nrows, s));
+        ST_TRY(sweep(buf[o.buf], buf[1 - o.buf], o, Remote()));
         break;
       case ST_OP_EXCHANGE:
-        ST_TRY(halo_exchange_async(comm, &buf[o.buf], 1, n, ld, o.sweeps, s, o.flag == 0));
+        ST_TRY(halo_exchange_async(comm, &buf[o.buf], 1, n, pitch, o.sweeps, s, o.flag == 0));
         break;
       case ST_OP_JOIN:
-        if (comm && comm->nranks > 1) ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
+        if (comm && comm->nranks > 1) {
+          if (pending_fused) ST_TRY(fused_halo_join(comm, s));
+          else ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
+        }
+        pending_fused = false;
         break;
       case ST_OP_SWAP:
         break;
       default:
-        ST_RETURN_IF(true, ST_EINTERNAL, "jacobi2d: bad schedule op %d", o.kind);
+        ST_RETURN_IF(true, ST_EINTERNAL, "jacobi: bad schedule op %d", o.kind);
     }
   }
   return ST_OK;
 }
 
-// Executes a dims=3 schedule: sweeps of planes, swaps of whole planes.
+st_status run_schedule(const std::vector<st_op>& ops, st_comm* comm, double* a, double* b, int64_t nx, int64_t n,
+                       int64_t ld, int32_t h, cudaStream_t s) {
+  const int64_t nrows = n + 2 * (int64_t)h;
+  return run_schedule_generic(ops, comm, a, b, n, ld, s,
+                              [&](const double* src, double* dst, const st_op& o, Remote rem) -> st_status {
+                                if (o.sweeps == 1)
+                                  return jacobi2d_sweep_rows(src, dst, nx, ld, o.y_lo, o.y_hi, s, rem);
+                                return jacobi2d_tb_rows(src, dst, nx, ld, o.y_lo, o.y_hi, o.sweeps, o.ring_lo,
+                                                        o.ring_hi, nrows, s, rem);
+                              });
+}
+
+// dims=3 schedule: sweeps of planes, swaps of whole planes.
 st_status run_schedule3d(const std::vector<st_op>& ops, st_comm* comm, double* a, double* b, int64_t nx,
                          int64_t ny, int64_t n, int64_t ldx, int32_t h, cudaStream_t s) {
-  double* buf[2] = {a, b};
-  const int64_t nplanes = n + 2 * (int64_t)h, plane = (ny + 2) * ldx;
-  for (const st_op& o : ops) {
-    switch (o.kind) {
-      case ST_OP_SWEEP:
-        ST_RETURN_IF(o.sweeps != 1, ST_EINTERNAL, "jacobi3d: pass of %d sweeps", o.sweeps);
-        ST_TRY(jacobi3d_sweep_planes(buf[o.buf], buf[1 - o.buf], nx, ny, nplanes, ldx, o.y_lo, o.y_hi, s));
-        break;
-      case ST_OP_EXCHANGE:
-        ST_TRY(halo_exchange_async(comm, &buf[o.buf], 1, n, plane, o.sweeps, s, o.flag == 0));
-        break;
-      case ST_OP_JOIN:
-        if (comm && comm->nranks > 1) ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
-        break;
-      case ST_OP_SWAP:
-        break;
-      default:
-        ST_RETURN_IF(true, ST_EINTERNAL, "jacobi3d: bad schedule op %d", o.kind);
-    }
-  }
-  return ST_OK;
+  const int64_t nplanes = n + 2 * (int64_t)h;
+  return run_schedule_generic(ops, comm, a, b, n, (ny + 2) * ldx, s,
+                              [&](const double* src, double* dst, const st_op& o, Remote rem) -> st_status {
+                                ST_RETURN_IF(o.sweeps != 1, ST_EINTERNAL, "jacobi3d: pass of %d sweeps", o.sweeps);
+                                return jacobi3d_sweep_planes(src, dst, nx, ny, nplanes, ldx, o.y_lo, o.y_hi, s, rem);
+                              });
 }
 
 }  // namespace

@@ -143,6 +143,55 @@ st_status local_exchange(st_comm* c, double* const* fields, int32_t nfields, int
 }
 }  // namespace
 
+bool fused_halo_available(const st_comm* comm) {
+  static const int kFused = env_int("ST_FUSED_HALO", 1);
+  return comm && comm->kind == st_comm::LOCAL && comm->nranks > 1 && kFused != 0;
+}
+
+st_status fused_halo_begin(st_comm* c, double* dst, int64_t n, cudaStream_t main, void* rem_lo_v, void* rem_hi_v) {
+  Remote* rem_lo = static_cast<Remote*>(rem_lo_v);
+  Remote* rem_hi = static_cast<Remote*>(rem_hi_v);
+  *rem_lo = Remote();
+  *rem_hi = Remote();
+  ST_RETURN_IF(c->bound.empty(), ST_EINVAL, "LOCAL comm: st_comm_bind the swapped buffers first");
+  ST_RETURN_IF(n != c->bound_n_slow, ST_EINVAL, "LOCAL comm: %lld owned slabs, bound with %lld", (long long)n,
+               (long long)c->bound_n_slow);
+  int idx = -1;
+  for (size_t i = 0; i < c->bound.size(); ++i)
+    if (c->bound[i] == dst) idx = (int)i;
+  ST_RETURN_IF(idx < 0, ST_EINVAL, "LOCAL comm: destination buffer was not bound");
+  const uint32_t k = ++c->seq;
+  ST_TRY(stream_write(main, c->flags + kFlagReady, k));  // my ghost slabs of dst are free
+  for (int side = 0; side < 2; ++side) {
+    const int32_t peer = side == 0 ? c->rank - 1 : c->rank + 1;
+    if (peer < 0 || peer >= c->nranks) continue;
+    st_comm* pc = c->group->ranks[(size_t)peer];
+    ST_RETURN_IF(!pc || pc->bound.size() != c->bound.size(), ST_EINVAL,
+                 "LOCAL comm: rank %d has not bound the same buffers", peer);
+    ST_TRY(stream_wait_geq(main, pc->flags + kFlagReady, k));
+    Remote& r = side == 0 ? *rem_lo : *rem_hi;
+    r.base = pc->bound[(size_t)idx];
+    // my first owned slabs -> rank-1's high ghosts (+n_{r-1}); my last owned -> rank+1's low ghosts (-n)
+    r.delta = side == 0 ? pc->bound_n_slow : -n;
+  }
+  return ST_OK;
+}
+
+st_status fused_halo_signal(st_comm* c, cudaStream_t main) {
+  const uint32_t k = c->seq;
+  if (c->rank > 0) ST_TRY(stream_write(main, c->group->ranks[(size_t)c->rank - 1]->flags + kFlagDoneFromHi, k));
+  if (c->rank < c->nranks - 1)
+    ST_TRY(stream_write(main, c->group->ranks[(size_t)c->rank + 1]->flags + kFlagDoneFromLo, k));
+  return ST_OK;
+}
+
+st_status fused_halo_join(st_comm* c, cudaStream_t main) {
+  const uint32_t k = c->seq;
+  if (c->rank > 0) ST_TRY(stream_wait_geq(main, c->flags + kFlagDoneFromLo, k));
+  if (c->rank < c->nranks - 1) ST_TRY(stream_wait_geq(main, c->flags + kFlagDoneFromHi, k));
+  return ST_OK;
+}
+
 st_status halo_exchange_async(st_comm* comm, double* const* fields, int32_t nfields,
                               int64_t n_slow_local, int64_t slab_pitch, int32_t width,
                               cudaStream_t main, bool join) {

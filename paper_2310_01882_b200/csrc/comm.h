@@ -54,6 +54,20 @@ st_status halo_exchange_async(st_comm* comm, double* const* fields, int32_t nfie
                               int64_t n_slow_local, int64_t slab_pitch, int32_t width,
                               cudaStream_t main, bool join);
 
+// Fused halo swap (LOCAL transport, NEXT #3): the boundary-row kernels of a
+// pass store their rows into the neighbours' ghost rows themselves.
+//   begin: main stream publishes "my ghost rows of `dst` are free" and waits
+//          until both neighbours published the same; returns the second
+//          destinations of the low/high boundary sweeps (base == nullptr if
+//          there is no neighbour on that side).
+//   signal: after the boundary sweeps, tell the neighbours their ghosts landed.
+//   join:  before the next pass, wait until the neighbours' rows landed here.
+// `n` = owned slabs; deltas are in slabs (rows for 2-D, planes for 3-D).
+bool fused_halo_available(const st_comm* comm);
+st_status fused_halo_begin(st_comm* comm, double* dst, int64_t n, cudaStream_t main, void* rem_lo, void* rem_hi);
+st_status fused_halo_signal(st_comm* comm, cudaStream_t main);
+st_status fused_halo_join(st_comm* comm, cudaStream_t main);
+
 st_status halo_plan(int32_t rank, int32_t nranks, int64_t n_slow_local, int64_t slab_pitch,
                     int32_t width, st_xfer sends[2], int32_t* nsend, st_xfer recvs[2],
                     int32_t* nrecv);

@@ -12,13 +12,23 @@
 
 namespace st {
 
+// Optional second destination of a sweep (fused halo swap, NEXT #3): every row
+// r the sweep writes to dst is also written to base[(r + delta) * ld ...] —
+// the neighbour rank's ghost rows — so boundary rows travel to the neighbour
+// in the same kernel that computes them (peer memory / NVLink when the
+// neighbour lives on another GPU). base == nullptr: no second destination.
+struct Remote {
+  double* base = nullptr;
+  int64_t delta = 0;
+};
+
 // ----------------------------------------------------------- Jacobi 2-D ---
 // One sweep dst = J(src) over buffer rows [y_lo, y_hi] (buffer row indices,
 // inclusive) and interior columns 1..nx; columns 0 and nx+1 are passed through
 // (dst = src) so the Dirichlet ring is preserved bit for bit. Rows outside the
 // range are neither read (except y_lo-1 and y_hi+1) nor written.
 st_status jacobi2d_sweep_rows(const double* src, double* dst, int64_t nx, int64_t ld,
-                              int64_t y_lo, int64_t y_hi, cudaStream_t s);
+                              int64_t y_lo, int64_t y_hi, cudaStream_t s, Remote rem = Remote());
 
 // `iters` sweeps entirely inside one CTA's shared memory (small grids: both
 // buffers fit in SMEM). Writes the final state (whole (ny+2) x (nx+2) window)
@@ -36,14 +46,14 @@ st_status jacobi2d_resident(double* a, double* b, int64_t nx, int64_t ny, int64_
 bool jacobi2d_tb_supported(int t);
 st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t ld,
                            int64_t y_lo, int64_t y_hi, int t, int64_t ring_lo,
-                           int64_t ring_hi, int64_t nrows_buf, cudaStream_t s);
+                           int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem = Remote());
 
 // ------------------------------------------------------------ Jacobi 3-D ---
 // One 7-point sweep dst = J(src) over planes [z_lo, z_hi] (buffer plane indices)
 // and the interior rows/columns; reads planes z_lo-1 .. z_hi+1. nplanes_buf =
 // planes in the buffer (TMA extent).
 st_status jacobi3d_sweep_planes(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
-                                int64_t ldx, int64_t z_lo, int64_t z_hi, cudaStream_t s);
+                                int64_t ldx, int64_t z_lo, int64_t z_hi, cudaStream_t s, Remote rem = Remote());
 // dst's side faces (x = 0, nx+1; y = 0, ny+1) of planes [z_lo, z_hi] <- src.
 st_status jacobi3d_copy_faces(const double* src, double* dst, int64_t nx, int64_t ny, int64_t ldx, int64_t z_lo,
                               int64_t z_hi, cudaStream_t s);

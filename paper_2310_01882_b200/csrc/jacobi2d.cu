@@ -38,7 +38,7 @@ template <int U>
 __global__ void __launch_bounds__(kStreamThreads)
     jacobi2d_stream_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2,
                            int64_t ld, int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk,
-                           int64_t nstrips) {
+                           int64_t nstrips, double* __restrict__ dst2, int64_t delta2) {
   const int lane = threadIdx.x & 31;
   const int64_t strip = (int64_t)blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
   if (strip >= nstrips) return;  // warp-uniform
@@ -89,6 +89,11 @@ __global__ void __launch_bounds__(kStreamThreads)
         double* dp = dst + (y + k) * ld + x;
         if (has_hi) stg2(dp, o);
         else if (has_pair) *dp = o.x;
+        if (dst2) {  // fused halo swap: the same row into the neighbour's ghost row
+          double* dq = dst2 + (y + k + delta2) * ld + x;
+          if (has_hi) stg2(dq, o);
+          else if (has_pair) *dq = o.x;
+        }
         qn = qc;
         qc = pf[k];
       }
@@ -145,7 +150,7 @@ constexpr size_t kResidentMaxSmem = 200 * 1024;
 }  // namespace
 
 st_status jacobi2d_sweep_rows(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo,
-                              int64_t y_hi, cudaStream_t s) {
+                              int64_t y_hi, cudaStream_t s, Remote rem) {
   if (y_hi < y_lo) return ST_OK;
   const int64_t nxp2 = nx + 2;
   const int64_t nstrips = (nxp2 + kStripCols - 1) / kStripCols;
@@ -155,7 +160,8 @@ st_status jacobi2d_sweep_rows(const double* src, double* dst, int64_t nx, int64_
   const int64_t nchunks = (rows + rpc - 1) / rpc;
   ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d: %lld row chunks exceed grid.y", (long long)nchunks);
   dim3 grid((unsigned)((nstrips + kStreamWarps - 1) / kStreamWarps), (unsigned)nchunks);
-  jacobi2d_stream_kernel<4><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips);
+  jacobi2d_stream_kernel<4><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, rem.base,
+                                                             rem.delta);
   ST_LAUNCHED();
   return ST_OK;
 }
@@ -232,7 +238,7 @@ template <int T, int kMinBlocks>
 __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
     jacobi2d_tb_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
                        int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk, int64_t nstrips, int64_t ring_lo,
-                       int64_t ring_hi, int64_t nrows_buf) {
+                       int64_t ring_hi, int64_t nrows_buf, double* __restrict__ dst2, int64_t delta2) {
   static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
   constexpr int kStride = kStripCols - 2 * T;
   const int lane = threadIdx.x & 31;
@@ -267,6 +273,7 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
   for (int k = 0; k < kTbGroup; ++k) buf[k] = ldg2(r_first + k <= r_load_last ? sp + (r_first + k) * ld : safe);
   const double* lp = sp + (r_first + kTbGroup) * ld;  // next row to load
   double* sp_out = dst + x + (r_first - T) * ld;      // row the next step stores
+  double* sp_out2 = dst2 ? dst2 + x + (r_first - T + delta2) * ld : nullptr;
 
   for (int64_t r0 = r_first; r0 <= r_end; r0 += kTbGroup) {
 #pragma unroll
@@ -291,8 +298,14 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
         if (st0 && st1) stg2(sp_out, o);
         else if (st0) sp_out[0] = o.x;
         else if (st1) sp_out[1] = o.y;
+        if (sp_out2) {  // fused halo swap
+          if (st0 && st1) stg2(sp_out2, o);
+          else if (st0) sp_out2[0] = o.x;
+          else if (st1) sp_out2[1] = o.y;
+        }
       }
       sp_out += ld;
+      if (sp_out2) sp_out2 += ld;
     }
   }
 }
@@ -337,7 +350,7 @@ template <int T, int kMinBlocks>
 __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
     jacobi2d_tb4_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
                         int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk, int64_t nstrips, int64_t ring_lo,
-                        int64_t ring_hi, int64_t nrows_buf) {
+                        int64_t ring_hi, int64_t nrows_buf, double* __restrict__ dst2, int64_t delta2) {
   static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
   constexpr int kCols = 128, kStride = kCols - 2 * T, G = 2;
   const int lane = threadIdx.x & 31;
@@ -381,6 +394,7 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
   }
   int64_t loff = (r_first + G) * ld;
   double* out = dst + x + (r_first - T) * ld;
+  double* out2 = dst2 ? dst2 + x + (r_first - T + delta2) * ld : nullptr;
 
   for (int64_t r0 = r_first; r0 <= r_end; r0 += G) {
 #pragma unroll
@@ -408,15 +422,24 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
         if (stb0 && stb1) stg2(out + 2, o.b);
         else if (stb0) out[2] = o.b.x;
         else if (stb1) out[3] = o.b.y;
+        if (out2) {  // fused halo swap: the same row into the neighbour's ghost row
+          if (sta0 && sta1) stg2(out2, o.a);
+          else if (sta0) out2[0] = o.a.x;
+          else if (sta1) out2[1] = o.a.y;
+          if (stb0 && stb1) stg2(out2 + 2, o.b);
+          else if (stb0) out2[2] = o.b.x;
+          else if (stb1) out2[3] = o.b.y;
+        }
       }
       out += ld;
+      if (out2) out2 += ld;
     }
   }
 }
 
 template <int T>
 st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
-                     int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s) {
+                     int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
   const int64_t nxp2 = nx + 2;
   constexpr int kStride = 128 - 2 * T;
   const int64_t nstrips = (nxp2 + kStride - 1) / kStride;
@@ -433,17 +456,17 @@ st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int
   dim3 grid((unsigned)blocks_x, (unsigned)nchunks);
   if (kOcc == 1)
     jacobi2d_tb4_kernel<T, 1><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
-                                                              ring_hi, nrows_buf);
+                                                              ring_hi, nrows_buf, rem.base, rem.delta);
   else
     jacobi2d_tb4_kernel<T, 2><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
-                                                              ring_hi, nrows_buf);
+                                                              ring_hi, nrows_buf, rem.base, rem.delta);
   ST_LAUNCHED();
   return ST_OK;
 }
 
 template <int T>
 st_status launch_tb(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
-                    int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s) {
+                    int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
   const int64_t nxp2 = nx + 2;
   constexpr int kStride = kStripCols - 2 * T;
   const int64_t nstrips = (nxp2 + kStride - 1) / kStride;
@@ -456,13 +479,13 @@ st_status launch_tb(const double* src, double* dst, int64_t nx, int64_t ld, int6
   static const int kOcc = env_int("ST_JACOBI_TB_OCC", 2);
   if (kOcc == 3)
     jacobi2d_tb_kernel<T, 3><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
-                                                             ring_hi, nrows_buf);
+                                                             ring_hi, nrows_buf, rem.base, rem.delta);
   else if (kOcc == 2)
     jacobi2d_tb_kernel<T, 2><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
-                                                             ring_hi, nrows_buf);
+                                                             ring_hi, nrows_buf, rem.base, rem.delta);
   else
     jacobi2d_tb_kernel<T, 1><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
-                                                             ring_hi, nrows_buf);
+                                                             ring_hi, nrows_buf, rem.base, rem.delta);
   ST_LAUNCHED();
   return ST_OK;
 }
@@ -499,23 +522,23 @@ st_status jacobi2d_preload() {
 }
 
 st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
-                           int t, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s) {
+                           int t, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
   if (y_hi < y_lo) return ST_OK;
   static const int kColsPerLane = env_int("ST_JACOBI_TB_COLS", 4);
   if (kColsPerLane == 4) {
     switch (t) {
-      case 2: return launch_tb4<2>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
-      case 4: return launch_tb4<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
-      case 6: return launch_tb4<6>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
-      case 8: return launch_tb4<8>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
+      case 2: return launch_tb4<2>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
+      case 4: return launch_tb4<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
+      case 6: return launch_tb4<6>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
+      case 8: return launch_tb4<8>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
       default: break;
     }
   }
   switch (t) {
-    case 2: return launch_tb<2>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
-    case 4: return launch_tb<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
-    case 6: return launch_tb<6>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
-    case 8: return launch_tb<8>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s);
+    case 2: return launch_tb<2>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
+    case 4: return launch_tb<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
+    case 6: return launch_tb<6>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
+    case 8: return launch_tb<8>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
     default: set_error("jacobi2d: tblock=%d not supported (2, 4, 6, 8)", t); return ST_ENOTSUP;
   }
 }

@@ -38,7 +38,8 @@ struct J3Tile {
 template <int BX, int BY, int S, int R>
 __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
     jacobi3d_kernel(const __grid_constant__ CUtensorMap tm, double* __restrict__ dst, int64_t nx, int64_t ny,
-                    int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t planes_per_chunk) {
+                    int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t planes_per_chunk, double* __restrict__ dst2,
+                    int64_t delta2) {
   using T = J3Tile<BX, BY>;
   constexpr int kSX = T::SX, WX = BX / 32;
   static_assert(S >= 4 && BY % R == 0 && BX % 32 == 0, "ring depth / rows per thread / tile width");
@@ -76,6 +77,7 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
   for (int i = 0; i < R; ++i) ok[i] = (yb + i <= ny) && (x <= nx);
   const int64_t plane_elems = (ny + 2) * ldx;
   double* out = dst + (za * (ny + 2) + yb) * ldx + x;
+  double* out2 = dst2 ? dst2 + ((za + delta2) * (ny + 2) + yb) * ldx + x : nullptr;  // fused halo swap
 
   int sm_ = 0, sc = 1, sp = 2;
   uint32_t par_p = 0;
@@ -102,9 +104,13 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
       const double xm = C[i * kSX - 1], xp = C[i * kSX + 1];
       const double sum = dadd(dadd(dadd(dadd(dadd(m[i], p[i]), ym), yp), xm), xp);
       const double v = __ddiv_rn(sum, 6.0);
-      if (ok[i]) out[i * ldx] = v;
+      if (ok[i]) {
+        out[i * ldx] = v;
+        if (out2) out2[i * ldx] = v;
+      }
     }
     out += plane_elems;
+    if (out2) out2 += plane_elems;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       m[i] = c[i];
@@ -141,7 +147,7 @@ __global__ void jacobi3d_copy_faces_kernel(const double* __restrict__ src, doubl
 
 template <int BX, int BY, int S, int R>
 st_status launch_j3(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf, int64_t ldx,
-                    int64_t z_lo, int64_t z_hi, cudaStream_t s) {
+                    int64_t z_lo, int64_t z_hi, cudaStream_t s, Remote rem) {
   using T = J3Tile<BX, BY>;
   CUtensorMap tm;
   const uint64_t dims[3] = {(uint64_t)(nx + 2), (uint64_t)(ny + 2), (uint64_t)nplanes_buf};
@@ -157,7 +163,7 @@ st_status launch_j3(const double* src, double* dst, int64_t nx, int64_t ny, int6
   ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "jacobi3d: grid too large");
   jacobi3d_kernel<BX, BY, S, R><<<dim3((unsigned)ntx, (unsigned)nty, (unsigned)nzc), (BX / 32) * (BY / R) * 32,
                                   smem, s>>>(
-      tm, dst, nx, ny, ldx, z_lo, z_hi, ppc);
+      tm, dst, nx, ny, ldx, z_lo, z_hi, ppc, rem.base, rem.delta);
   ST_LAUNCHED();
   return ST_OK;
 }
@@ -184,24 +190,24 @@ st_status jacobi3d_preload() {
 }
 
 st_status jacobi3d_sweep_planes(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
-                                int64_t ldx, int64_t z_lo, int64_t z_hi, cudaStream_t s) {
+                                int64_t ldx, int64_t z_lo, int64_t z_hi, cudaStream_t s, Remote rem) {
   if (z_hi < z_lo) return ST_OK;
   static const int kVariant = env_int("ST_J3_VARIANT", 0);
   switch (kVariant) {
-    case 1: return launch_j3<32, 32, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 2: return launch_j3<64, 16, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 3: return launch_j3<128, 16, 4, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 4: return launch_j3<64, 16, 8, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 5: return launch_j3<128, 16, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 6: return launch_j3<192, 8, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 7: return launch_j3<128, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 8: return launch_j3<128, 4, 8, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 9: return launch_j3<32, 16, 6, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 10: return launch_j3<128, 8, 12, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 11: return launch_j3<192, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 12: return launch_j3<128, 16, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    case 13: return launch_j3<128, 8, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);
-    default: return launch_j3<128, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s);  // tuned
+    case 1: return launch_j3<32, 32, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 2: return launch_j3<64, 16, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 3: return launch_j3<128, 16, 4, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 4: return launch_j3<64, 16, 8, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 5: return launch_j3<128, 16, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 6: return launch_j3<192, 8, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 7: return launch_j3<128, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 8: return launch_j3<128, 4, 8, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 9: return launch_j3<32, 16, 6, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 10: return launch_j3<128, 8, 12, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 11: return launch_j3<192, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 12: return launch_j3<128, 16, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    case 13: return launch_j3<128, 8, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
+    default: return launch_j3<128, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);  // tuned
   }
 }
 
