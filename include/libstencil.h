@@ -93,6 +93,24 @@ st_status st_comm_init(st_comm** out, int32_t nranks, int32_t rank,
  * Every rank must st_comm_bind the buffers it will swap. */
 st_status st_comm_init_local(st_comm** comms, int32_t nranks, const int32_t* devices);
 
+/* One rank of a multi-process group using the IPC transport: the LOCAL
+ * protocol (copy-engine or fused swaps ordered by device-side flags) on
+ * CUDA-IPC mappings of the neighbour processes' buffers and flags. Works across
+ * GPUs of one node (NVLink peer access) and for several ranks on one GPU.
+ * Follow with st_comm_export on every rank, an all-gather of the blobs by the
+ * caller (e.g. torch.distributed), and st_comm_import of the neighbours. */
+st_status st_comm_init_ipc(st_comm** out, int32_t nranks, int32_t rank, int32_t cuda_device);
+
+/* Binds `buffers` (as st_comm_bind) and writes this rank's IPC description
+ * (flags + buffers: handles, offsets, slab count) into blob[0..cap); *used =
+ * bytes written (call with cap = 0 to size it). IPC comms only. */
+st_status st_comm_export(st_comm* comm, double* const* buffers, int32_t nbuffers, int64_t n_slow_local,
+                         uint8_t* blob, int64_t cap, int64_t* used);
+
+/* Maps the blob exported by rank `peer` if it is a neighbour (rank -/+ 1);
+ * other ranks' blobs are ignored. IPC comms only. */
+st_status st_comm_import(st_comm* comm, int32_t peer, const uint8_t* blob, int64_t bytes);
+
 /* Registers the buffers this rank swaps (LOCAL transport; no-op for NCCL): all
  * ranks bind the same number of buffers in the same order (buffer i of rank r
  * exchanges with buffer i of its neighbours), each holding n_slow_local owned

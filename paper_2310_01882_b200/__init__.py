@@ -17,6 +17,7 @@ Entry points (same names as the C ABI, tensors instead of raw pointers):
     st_block_split(n, nranks, rank) -> (start, count)                                [host only]
     Comm.create(rank, nranks, unique_id, device) / Comm.from_process_group(pg, device)
     Comm.local_group(nranks, devices) -> [Comm]; comm.bind(buffers, n_slow_local)
+    Comm.create_ipc(rank, nranks, device); comm.bind_ipc(buffers, n_slow_local)      [multi-process]
 """
 from __future__ import annotations
 
@@ -62,6 +63,9 @@ _SIGS = {
     "st_comm_destroy": (ctypes.c_int, [_vp]),
     "st_comm_init_local": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, ctypes.POINTER(_i32)]),
     "st_comm_bind": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), _i32, _i64]),
+    "st_comm_init_ipc": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, _i32, _i32]),
+    "st_comm_export": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), _i32, _i64, _vp, _i64, ctypes.POINTER(_i64)]),
+    "st_comm_import": (ctypes.c_int, [_vp, _i32, _vp, _i64]),
     "st_comm_query": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "st_block_split": (ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "st_halo_plan": (ctypes.c_int, [_i32, _i32, _i64, _i64, _i32, ctypes.POINTER(Xfer),
@@ -162,6 +166,39 @@ class Comm:
         devs = (_i32 * nranks)(*devices)
         _check(lib().st_comm_init_local(hs, nranks, devs), "st_comm_init_local")
         return [cls(hs[r], r, nranks, devices[r]) for r in range(nranks)]
+
+    @classmethod
+    def create_ipc(cls, rank: int, nranks: int, device: int) -> "Comm":
+        """One rank of a multi-process IPC group (copy-engine / fused swaps on CUDA-IPC mappings)."""
+        h = _vp()
+        _check(lib().st_comm_init_ipc(ctypes.byref(h), nranks, rank, device), "st_comm_init_ipc")
+        c = cls(h.value, rank, nranks, device)
+        c.kind = "ipc"
+        return c
+
+    @classmethod
+    def ipc_from_process_group(cls, device: int, group=None) -> "Comm":
+        import torch.distributed as dist
+        return cls.create_ipc(dist.get_rank(group), dist.get_world_size(group), device)
+
+    def bind_ipc(self, buffers, n_slow_local: int, group=None) -> None:
+        """Collective (IPC comms): export this rank's buffers, all-gather the blobs over
+        torch.distributed, map the neighbours' buffers and flags."""
+        import torch.distributed as dist
+        for i, t in enumerate(buffers):
+            _f64_cuda(t, f"buffers[{i}]")
+        arr = (_vp * len(buffers))(*[t.data_ptr() for t in buffers])
+        need = _i64()
+        _check(lib().st_comm_export(self.handle, arr, len(buffers), n_slow_local, None, 0, ctypes.byref(need)),
+               "st_comm_export")
+        blob = (ctypes.c_uint8 * need.value)()
+        _check(lib().st_comm_export(self.handle, arr, len(buffers), n_slow_local, ctypes.cast(blob, _vp),
+                                    need.value, ctypes.byref(need)), "st_comm_export")
+        blobs = [None] * self.nranks
+        dist.all_gather_object(blobs, bytes(blob), group=group)
+        for peer, b in enumerate(blobs):
+            buf = (ctypes.c_uint8 * len(b)).from_buffer_copy(b)
+            _check(lib().st_comm_import(self.handle, peer, ctypes.cast(buf, _vp), len(b)), "st_comm_import")
 
     def bind(self, buffers, n_slow_local: int) -> None:
         """Registers the buffers this rank swaps (LOCAL transport; no-op for NCCL)."""

@@ -94,10 +94,35 @@ st_status stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t v) {
 
 constexpr int kFlagReady = 0, kFlagDoneFromLo = 1, kFlagDoneFromHi = 2;
 
+// Neighbour on `side` (0 = rank-1, 1 = rank+1) of a LOCAL/IPC comm; valid=false if none.
+st_status peer_view(st_comm* c, int side, st_peer* out) {
+  const int32_t peer = side == 0 ? c->rank - 1 : c->rank + 1;
+  out->valid = false;
+  if (peer < 0 || peer >= c->nranks) return ST_OK;
+  if (c->kind == st_comm::LOCAL) {
+    st_comm* pc = c->group->ranks[(size_t)peer];
+    ST_RETURN_IF(!pc, ST_EINVAL, "LOCAL comm: rank %d was destroyed", peer);
+    out->valid = true;
+    out->flags = pc->flags;
+    out->bound = pc->bound;
+    out->n_slow = pc->bound_n_slow;
+    out->device = pc->device;
+  } else {
+    const st_peer& p = c->ipc_peer[side];
+    ST_RETURN_IF(!p.valid, ST_EINVAL, "IPC comm: rank %d's blob was not imported", peer);
+    out->valid = true;
+    out->flags = p.flags;
+    out->bound = p.bound;
+    out->n_slow = p.n_slow;
+    out->device = p.device;
+  }
+  ST_RETURN_IF(out->bound.size() != c->bound.size(), ST_EINVAL, "rank %d has not bound the same buffers", peer);
+  return ST_OK;
+}
+
 // LOCAL transport: push my boundary slabs into the neighbours' ghost slabs.
 st_status local_exchange(st_comm* c, double* const* fields, int32_t nfields, int64_t n, int64_t pitch,
                          int32_t width, cudaStream_t main, bool join) {
-  st_local_group* g = c->group;
   ST_RETURN_IF(c->bound.empty(), ST_EINVAL, "LOCAL comm: st_comm_bind the swapped buffers first");
   ST_RETURN_IF(n != c->bound_n_slow, ST_EINVAL, "LOCAL comm: %lld owned slabs, bound with %lld",
                (long long)n, (long long)c->bound_n_slow);
@@ -116,24 +141,20 @@ st_status local_exchange(st_comm* c, double* const* fields, int32_t nfields, int
   ST_TRY(stream_write(cs, c->flags + kFlagReady, k));  // my ghost slabs may now be overwritten
   const size_t bytes = (size_t)width * (size_t)pitch * sizeof(double);
   for (int side = 0; side < 2; ++side) {
-    const int32_t peer = side == 0 ? c->rank - 1 : c->rank + 1;
-    if (peer < 0 || peer >= c->nranks) continue;
-    st_comm* pc = g->ranks[(size_t)peer];
-    ST_RETURN_IF(!pc || pc->bound.size() != c->bound.size(), ST_EINVAL,
-                 "LOCAL comm: rank %d has not bound the same buffers", peer);
-    ST_TRY(stream_wait_geq(cs, pc->flags + kFlagReady, k));
+    st_peer pc;
+    ST_TRY(peer_view(c, side, &pc));
+    if (!pc.valid) continue;
+    ST_TRY(stream_wait_geq(cs, pc.flags + kFlagReady, k));
     for (int f = 0; f < nfields; ++f) {
       double* src = fields[f];
-      double* dst = pc->bound[(size_t)idx[f]];
+      double* dst = pc.bound[(size_t)idx[f]];
       // to rank-1: my first owned slabs -> its high ghosts; to rank+1: my last owned -> its low ghosts
       const int64_t soff = side == 0 ? (int64_t)width * pitch : n * pitch;
-      const int64_t doff = side == 0 ? ((int64_t)width + pc->bound_n_slow) * pitch : 0;
-      if (pc->device == c->device)
-        ST_CHECK_CUDA(cudaMemcpyAsync(dst + doff, src + soff, bytes, cudaMemcpyDeviceToDevice, cs));
-      else
-        ST_CHECK_CUDA(cudaMemcpyPeerAsync(dst + doff, pc->device, src + soff, c->device, bytes, cs));
+      const int64_t doff = side == 0 ? ((int64_t)width + pc.n_slow) * pitch : 0;
+      // unified addressing: same-device, peer (NVLink) and IPC-mapped destinations alike
+      ST_CHECK_CUDA(cudaMemcpyAsync(dst + doff, src + soff, bytes, cudaMemcpyDefault, cs));
     }
-    ST_TRY(stream_write(cs, pc->flags + (side == 0 ? kFlagDoneFromHi : kFlagDoneFromLo), k));
+    ST_TRY(stream_write(cs, pc.flags + (side == 0 ? kFlagDoneFromHi : kFlagDoneFromLo), k));
   }
   if (c->rank > 0) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromLo, k));
   if (c->rank < c->nranks - 1) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromHi, k));
@@ -145,7 +166,7 @@ st_status local_exchange(st_comm* c, double* const* fields, int32_t nfields, int
 
 bool fused_halo_available(const st_comm* comm) {
   static const int kFused = env_int("ST_FUSED_HALO", 1);
-  return comm && comm->kind == st_comm::LOCAL && comm->nranks > 1 && kFused != 0;
+  return comm && comm->kind != st_comm::NCCL && comm->nranks > 1 && kFused != 0;
 }
 
 st_status fused_halo_begin(st_comm* c, double* dst, int64_t n, cudaStream_t main, void* rem_lo_v, void* rem_hi_v) {
@@ -163,25 +184,25 @@ st_status fused_halo_begin(st_comm* c, double* dst, int64_t n, cudaStream_t main
   const uint32_t k = ++c->seq;
   ST_TRY(stream_write(main, c->flags + kFlagReady, k));  // my ghost slabs of dst are free
   for (int side = 0; side < 2; ++side) {
-    const int32_t peer = side == 0 ? c->rank - 1 : c->rank + 1;
-    if (peer < 0 || peer >= c->nranks) continue;
-    st_comm* pc = c->group->ranks[(size_t)peer];
-    ST_RETURN_IF(!pc || pc->bound.size() != c->bound.size(), ST_EINVAL,
-                 "LOCAL comm: rank %d has not bound the same buffers", peer);
-    ST_TRY(stream_wait_geq(main, pc->flags + kFlagReady, k));
+    st_peer pc;
+    ST_TRY(peer_view(c, side, &pc));
+    if (!pc.valid) continue;
+    ST_TRY(stream_wait_geq(main, pc.flags + kFlagReady, k));
     Remote& r = side == 0 ? *rem_lo : *rem_hi;
-    r.base = pc->bound[(size_t)idx];
+    r.base = pc.bound[(size_t)idx];
     // my first owned slabs -> rank-1's high ghosts (+n_{r-1}); my last owned -> rank+1's low ghosts (-n)
-    r.delta = side == 0 ? pc->bound_n_slow : -n;
+    r.delta = side == 0 ? pc.n_slow : -n;
   }
   return ST_OK;
 }
 
 st_status fused_halo_signal(st_comm* c, cudaStream_t main) {
   const uint32_t k = c->seq;
-  if (c->rank > 0) ST_TRY(stream_write(main, c->group->ranks[(size_t)c->rank - 1]->flags + kFlagDoneFromHi, k));
-  if (c->rank < c->nranks - 1)
-    ST_TRY(stream_write(main, c->group->ranks[(size_t)c->rank + 1]->flags + kFlagDoneFromLo, k));
+  for (int side = 0; side < 2; ++side) {
+    st_peer pc;
+    ST_TRY(peer_view(c, side, &pc));
+    if (pc.valid) ST_TRY(stream_write(main, pc.flags + (side == 0 ? kFlagDoneFromHi : kFlagDoneFromLo), k));
+  }
   return ST_OK;
 }
 
@@ -199,7 +220,7 @@ st_status halo_exchange_async(st_comm* comm, double* const* fields, int32_t nfie
   int32_t ns = 0, nr = 0;
   ST_TRY(halo_plan(comm->rank, comm->nranks, n_slow_local, slab_pitch, width, sends, &ns, recvs, &nr));
   if (comm->nranks == 1) return ST_OK;
-  if (comm->kind == st_comm::LOCAL)
+  if (comm->kind != st_comm::NCCL)
     return local_exchange(comm, fields, nfields, n_slow_local, slab_pitch, width, main, join);
   ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier NCCL error");
   ST_CHECK_CUDA(cudaEventRecord(comm->ev_ready, main));
@@ -324,11 +345,132 @@ st_status st_comm_init_local(st_comm** comms, int32_t nranks, const int32_t* dev
   return ST_OK;
 }
 
+// ------------------------------------------------------------------ IPC ---
+namespace {
+constexpr uint32_t kBlobMagic = 0x53544950u;  // "STIP"
+struct BlobHeader {
+  uint32_t magic, version;
+  int32_t rank, device, nbuf, pad;
+  int64_t n_slow;
+};
+struct BlobEntry {
+  cudaIpcMemHandle_t handle;
+  int64_t offset;  // pointer - allocation base
+};
+using PFN_getRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+st_status ipc_entry(const void* ptr, BlobEntry* e) {
+  static PFN_getRange get_range = nullptr;
+  if (!get_range) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    ST_CHECK_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q));
+    ST_RETURN_IF(!p || q != cudaDriverEntryPointSuccess, ST_ECUDA, "cuMemGetAddressRange unavailable");
+    get_range = reinterpret_cast<PFN_getRange>(p);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  ST_RETURN_IF(get_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS, ST_EINVAL,
+               "IPC export: pointer is not device memory");
+  ST_CHECK_CUDA(cudaIpcGetMemHandle(&e->handle, reinterpret_cast<void*>(base)));
+  e->offset = (int64_t)(reinterpret_cast<uintptr_t>(ptr) - (uintptr_t)base);
+  return ST_OK;
+}
+}  // namespace
+
+st_status st_comm_init_ipc(st_comm** out, int32_t nranks, int32_t rank, int32_t cuda_device) {
+  clear_error();
+  ST_RETURN_IF(!out || nranks < 1 || rank < 0 || rank >= nranks, ST_EINVAL, "st_comm_init_ipc: bad arguments");
+  ST_TRY(load_stream_memops());
+  ST_CHECK_CUDA(cudaSetDevice(cuda_device));
+  ST_TRY(preload_kernels());
+  st_comm* c = new st_comm();
+  c->kind = st_comm::IPC;
+  c->rank = rank;
+  c->nranks = nranks;
+  c->device = cuda_device;
+  if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMalloc(&c->flags, 4 * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemset(c->flags, 0, 4 * sizeof(uint32_t)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    set_error("st_comm_init_ipc: stream/event/flag allocation failed");
+    st_comm_destroy(c);
+    return ST_ECUDA;
+  }
+  *out = c;
+  return ST_OK;
+}
+
+st_status st_comm_export(st_comm* c, double* const* buffers, int32_t nbuf, int64_t n_slow, uint8_t* blob, int64_t cap,
+                         int64_t* used) {
+  clear_error();
+  ST_RETURN_IF(!c || c->kind != st_comm::IPC, ST_EINVAL, "st_comm_export: needs an IPC comm");
+  ST_RETURN_IF(!used || nbuf < 0 || (nbuf > 0 && !buffers) || n_slow < 1, ST_EINVAL, "st_comm_export: bad arguments");
+  const int64_t need = (int64_t)sizeof(BlobHeader) + (int64_t)(nbuf + 1) * (int64_t)sizeof(BlobEntry);
+  *used = need;
+  if (cap == 0) return ST_OK;
+  ST_RETURN_IF(!blob || cap < need, ST_EINVAL, "st_comm_export: blob of %lld bytes < %lld", (long long)cap,
+               (long long)need);
+  c->bound.assign(buffers, buffers + nbuf);
+  c->bound_n_slow = n_slow;
+  BlobHeader h{kBlobMagic, 1u, c->rank, c->device, nbuf, 0, n_slow};
+  std::memcpy(blob, &h, sizeof(h));
+  BlobEntry* e = reinterpret_cast<BlobEntry*>(blob + sizeof(h));
+  ST_TRY(ipc_entry(c->flags, &e[0]));
+  for (int i = 0; i < nbuf; ++i) ST_TRY(ipc_entry(buffers[i], &e[i + 1]));
+  return ST_OK;
+}
+
+st_status st_comm_import(st_comm* c, int32_t peer, const uint8_t* blob, int64_t bytes) {
+  clear_error();
+  ST_RETURN_IF(!c || c->kind != st_comm::IPC || !blob, ST_EINVAL, "st_comm_import: needs an IPC comm and a blob");
+  if (peer != c->rank - 1 && peer != c->rank + 1) return ST_OK;  // only neighbours are mapped
+  ST_RETURN_IF(bytes < (int64_t)sizeof(BlobHeader), ST_EINVAL, "st_comm_import: short blob");
+  BlobHeader h;
+  std::memcpy(&h, blob, sizeof(h));
+  ST_RETURN_IF(h.magic != kBlobMagic || h.rank != peer || h.nbuf < 0 ||
+                   bytes < (int64_t)sizeof(h) + (int64_t)(h.nbuf + 1) * (int64_t)sizeof(BlobEntry),
+               ST_EINVAL, "st_comm_import: malformed blob for rank %d", peer);
+  st_peer& p = c->ipc_peer[peer == c->rank - 1 ? 0 : 1];
+  for (void* q : p.opened) cudaIpcCloseMemHandle(q);
+  p = st_peer();
+  const BlobEntry* e = reinterpret_cast<const BlobEntry*>(blob + sizeof(h));
+  std::vector<cudaIpcMemHandle_t> seen;
+  std::vector<char*> bases;
+  auto map = [&](const BlobEntry& en, void** outp) -> st_status {
+    for (size_t i = 0; i < seen.size(); ++i)  // one mapping per allocation
+      if (std::memcmp(&seen[i], &en.handle, sizeof(cudaIpcMemHandle_t)) == 0) {
+        *outp = bases[i] + en.offset;
+        return ST_OK;
+      }
+    void* base = nullptr;
+    ST_CHECK_CUDA(cudaIpcOpenMemHandle(&base, en.handle, cudaIpcMemLazyEnablePeerAccess));
+    seen.push_back(en.handle);
+    bases.push_back(static_cast<char*>(base));
+    p.opened.push_back(base);
+    *outp = static_cast<char*>(base) + en.offset;
+    return ST_OK;
+  };
+  void* fp = nullptr;
+  ST_TRY(map(e[0], &fp));
+  p.flags = static_cast<uint32_t*>(fp);
+  for (int i = 0; i < h.nbuf; ++i) {
+    void* bp = nullptr;
+    ST_TRY(map(e[i + 1], &bp));
+    p.bound.push_back(static_cast<double*>(bp));
+  }
+  p.n_slow = h.n_slow;
+  p.device = h.device;
+  p.valid = true;
+  return ST_OK;
+}
+
 st_status st_comm_bind(st_comm* comm, double* const* buffers, int32_t nbuffers, int64_t n_slow_local) {
   clear_error();
   ST_RETURN_IF(!comm || nbuffers < 0 || (nbuffers > 0 && !buffers) || n_slow_local < 1, ST_EINVAL,
                "st_comm_bind: bad arguments");
-  if (comm->kind != st_comm::LOCAL) return ST_OK;
+  if (comm->kind == st_comm::NCCL) return ST_OK;
   comm->bound.assign(buffers, buffers + nbuffers);
   comm->bound_n_slow = n_slow_local;
   return ST_OK;
@@ -344,6 +486,8 @@ st_status st_comm_destroy(st_comm* c) {
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  for (int side = 0; side < 2; ++side)
+    for (void* p : c->ipc_peer[side].opened) cudaIpcCloseMemHandle(p);
   if (c->flags) cudaFree(c->flags);
   if (c->group) {
     st_local_group* g = c->group;

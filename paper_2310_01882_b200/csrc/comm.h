@@ -3,6 +3,9 @@
 //
 // Two transports:
 //  * NCCL  — one process per GPU, ncclSend/ncclRecv on a comm stream.
+//  * IPC   — one process per rank (torchrun), same protocol as LOCAL on
+//            CUDA-IPC-mapped buffers and flags of the neighbour processes
+//            (so it also runs with several ranks on ONE GPU, which NCCL refuses).
 //  * LOCAL — a group of ranks inside one process (same or different GPUs):
 //            the swap is a copy-engine cudaMemcpyAsync into the neighbour's
 //            ghost slabs, ordered by device-side flags written/waited with
@@ -20,8 +23,19 @@
 
 struct st_local_group;
 
+// A neighbour rank's swap targets as seen from this process: its flags and its
+// bound buffers (direct pointers for LOCAL; IPC-mapped pointers for IPC).
+struct st_peer {
+  bool valid = false;
+  uint32_t* flags = nullptr;
+  std::vector<double*> bound;
+  int64_t n_slow = 0;
+  int32_t device = 0;
+  std::vector<void*> opened;  // IPC mappings to close
+};
+
 struct st_comm {
-  enum Kind { NCCL = 0, LOCAL = 1 };
+  enum Kind { NCCL = 0, LOCAL = 1, IPC = 2 };
   Kind kind = NCCL;
   ncclComm_t nccl = nullptr;
   int32_t rank = 0;
@@ -37,6 +51,8 @@ struct st_comm {
   uint32_t seq = 0;           // swaps issued so far (all ranks issue the same sequence)
   std::vector<double*> bound;  // buffers registered with st_comm_bind (same order on every rank)
   int64_t bound_n_slow = 0;    // owned slabs of this rank's bound buffers
+  // IPC transport: the two neighbours (0 = rank-1, 1 = rank+1), imported from their blobs
+  st_peer ipc_peer[2];
 };
 
 struct st_local_group {

@@ -1,0 +1,91 @@
+"""Multi-process IPC-transport cases (spawned by tests/test_gpu_ipc.py): every
+rank is its own process; all ranks may share one GPU (the IPC transport allows
+it, NCCL does not). Bitwise vs the oracle."""
+import os
+import pathlib
+import sys
+
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import oracle
+import paper_2310_01882_b200 as st
+import stencil_inputs as si
+
+
+def jacobi2d(rank, world, dev, h, iters, tblock):
+    nx, ny = 300, 260
+    g = si.jacobi2d_grid(nx, ny)
+    start, n = st.st_block_split(ny, world, rank)
+    loc = np.zeros((n + 2 * h, g.shape[1]))
+    for l in range(n + 2 * h):
+        gr = start + 1 + (l - h)
+        if 0 <= gr <= ny + 1:
+            loc[l] = g[gr]
+    a = torch.from_numpy(loc).to(dev)
+    if rank > 0:
+        a[:h] = float("nan")
+    if rank < world - 1:
+        a[h + n:] = float("nan")
+    b = torch.full_like(a, float("nan"))
+    comm = st.Comm.ipc_from_process_group(dev.index)
+    comm.bind_ipc([a, b], n)
+    r = st.st_jacobi2d_run(a, b, iters, tblock=tblock, halo=h, comm=comm, nx=nx)
+    torch.cuda.synchronize()
+    rows = [None] * world
+    dist.all_gather_object(rows, (start, r.cpu().numpy()[h:h + n, :nx + 2]))
+    comm.close()
+    if rank == 0:
+        want = oracle.jacobi2d(g, iters, nx=nx)
+        return all(np.array_equal(blk, want[s0 + 1:s0 + 1 + blk.shape[0], :nx + 2]) for s0, blk in rows)
+    return True
+
+
+def pw(rank, world, dev):
+    nx, ny, nz = 140, 20, 41
+    d = si.pw_inputs(nx, ny, nz)
+    z0, n = st.st_block_split(nz, world, rank)
+    dl = si.pw_inputs(nx, ny, nz, plane0=z0, planes=n + 2)
+    g = {k: (torch.from_numpy(v).to(dev) if isinstance(v, np.ndarray) else v) for k, v in dl.items()}
+    for k in "uvw":
+        if rank > 0:
+            g[k][0] = float("nan")
+        if rank < world - 1:
+            g[k][-1] = float("nan")
+    outs = [torch.zeros_like(g["u"]) for _ in range(3)]
+    comm = st.Comm.ipc_from_process_group(dev.index)
+    comm.bind_ipc([g["u"], g["v"], g["w"]], n)
+    st.st_pw_advect3d(g["u"], g["v"], g["w"], *outs, g["tcx"], g["tcy"], g["tzc1"], g["tzc2"], g["tzd1"], g["tzd2"],
+                      comm=comm)
+    torch.cuda.synchronize()
+    parts = [None] * world
+    dist.all_gather_object(parts, (z0, [o.cpu().numpy()[1:n + 1] for o in outs]))
+    comm.close()
+    if rank == 0:
+        want = oracle.pw_advect3d(d["u"], d["v"], d["w"], d)
+        return all(np.array_equal(blk, w[s0 + 1:s0 + 1 + blk.shape[0]]) for s0, blks in parts
+                   for blk, w in zip(blks, want))
+    return True
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    ngpu = torch.cuda.device_count()
+    dev = torch.device("cuda", rank % ngpu)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo")
+    case = sys.argv[1]
+    ok = {"j2_h1": lambda: jacobi2d(rank, world, dev, 1, 9, 1),
+          "j2_h4_t4": lambda: jacobi2d(rank, world, dev, 4, 13, 4),
+          "pw": lambda: pw(rank, world, dev)}[case]()
+    if rank == 0:
+        print("IPC CASE", case, "OK" if ok else "FAILED", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,43 @@
+"""GPU tests of the IPC transport: P processes (torchrun-style env, gloo for the
+out-of-band blob exchange) share the available GPU(s); the halo swap runs on
+CUDA-IPC mappings with device-side flags (fused and copy-engine). Bitwise vs the oracle."""
+import os
+import pathlib
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = pathlib.Path(__file__).resolve().parent
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", ["j2_h1", "j2_h4_t4", "pw"])
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_ipc_multiprocess_equals_oracle(cuda_lib, world, case, fused):
+    port = _port()
+    procs = []
+    for r in range(world):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), LOCAL_RANK=str(r), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), ST_FUSED_HALO=fused)
+        procs.append(subprocess.Popen([sys.executable, str(HERE / "ipc_cases.py"), case], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    outs = []
+    for p in procs:
+        try:
+            o, e = p.communicate(timeout=240)
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            pytest.fail("IPC case timed out")
+        outs.append((p.returncode, o, e))
+    assert all(rc == 0 for rc, _, _ in outs), [(rc, o[-500:], e[-1500:]) for rc, o, e in outs]
+    assert "OK" in outs[0][1]
