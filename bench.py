@@ -199,7 +199,10 @@ def main():
     ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
     ap.add_argument("--sweeps", type=int, default=1000, help="Jacobi sweeps per step (configs[1]: 1000)")
     ap.add_argument("--tblock", type=int, default=0)
-    ap.add_argument("--halo", type=int, default=6, help="ghost rows per side across ranks (N>1)")
+    ap.add_argument("--halo", type=int, default=8, help="ghost rows per side across ranks (N>1)")
+    ap.add_argument("--transport", choices=["ipc", "nccl"], default="ipc",
+                    help="N>1 halo transport: ipc = fused stores / copy engines over CUDA-IPC (default), nccl")
+    ap.add_argument("--same-gpu", action="store_true", help="all ranks on cuda:0 (functional check only)")
     ap.add_argument("--align", type=int, default=2, help="row pitch multiple in doubles (2 = 16-byte rows)")
     ap.add_argument("--pw-apps", type=int, default=20, help="PW applications timed")
     ap.add_argument("--no-pw", action="store_true")
@@ -221,20 +224,32 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_gpu:  # functional check of the N>1 path on a 1-GPU box (numbers meaningless)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     comm = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-        comm = st.Comm.from_process_group(local)
+        if args.transport == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+            comm = st.Comm.from_process_group(local)
+        else:  # IPC transport: gloo carries only the control plane (blobs, barriers, max)
+            dist.init_process_group("gloo")
+            comm = st.Comm.ipc_from_process_group(local)
     assert world == args.gpus or world == 1, "--gpus must match the torchrun world size"
+
+    def bind(buffers, n_slow):
+        """Register the buffers the next phase swaps (collective for the IPC transport)."""
+        if comm is not None and getattr(comm, "kind", "nccl") == "ipc":
+            comm.bind_ipc(buffers, n_slow)
 
     stream = torch.cuda.current_stream()
     hbm_peak, peak_src = peaks()
 
     def barrier():
+        torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
@@ -242,7 +257,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if args.transport == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -265,6 +280,7 @@ def main():
     sweeps = args.sweeps
 
     A.copy_(a0)
+    bind([A, B], ny_loc)
 
     def jacobi_step():
         # `sweeps` more sweeps of the resident grid; with an even count the state stays in A
@@ -344,6 +360,7 @@ def main():
         d = si.pw_inputs(nxy, nxy, nz_glob, ldx=pitch(nxy + 2, args.align), plane0=z0, planes=nz_loc + 2)
         g = {k: (torch.from_numpy(v).to(dev) if hasattr(v, "shape") else v) for k, v in d.items()}
         outs = [torch.empty_like(g["u"]) for _ in range(3)]
+        bind([g["u"], g["v"], g["w"]], nz_loc)
 
         def pw_app():
             st.st_pw_advect3d(g["u"], g["v"], g["w"], *outs, g["tcx"], g["tcy"], g["tzc1"], g["tzc2"],
@@ -383,6 +400,7 @@ def main():
         g3 = si.jacobi3d_grid(n3, n3, n3, ldx=ldx3, plane0=z0, planes=nz3 + 2)
         A3 = torch.from_numpy(g3).to(dev)
         B3 = torch.empty_like(A3)
+        bind([A3, B3], nz3)
         j3_sweeps = args.j3_sweeps
 
         def j3_step():
@@ -455,7 +473,8 @@ def main():
                                    + ("" if world == 1 else f"_rowslabs{world}"),
                        "sweeps_per_step": sweeps, "tblock": args.tblock, "ld": ld,
                        "l2": "no flush needed: each buffer is %.2f GB > 126 MB L2" % (rows * ld * 8 / 1e9),
-                       "step": "st_jacobi2d_run(iters=%d) continuing from the resident state" % sweeps},
+                       "step": "st_jacobi2d_run(iters=%d) continuing from the resident state" % sweeps,
+                       "transport": None if world == 1 else args.transport, "halo": halo},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved_gbs, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(achieved_gbs / hbm_peak, 4), "traffic": ncu_traffic(kname),
                          "bytes_per_pt_per_launch": JACOBI_BYTES_PER_PT, "sweeps_per_launch": pass_sweeps,
