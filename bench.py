@@ -237,7 +237,14 @@ def main():
             comm = st.Comm.from_process_group(local)
         else:  # IPC transport: gloo carries only the control plane (blobs, barriers, max)
             dist.init_process_group("gloo")
-            comm = st.Comm.ipc_from_process_group(local)
+            try:
+                comm = st.Comm.ipc_from_process_group(local)
+                probe = torch.zeros(8, 4, dtype=torch.float64, device=dev)
+                comm.bind_ipc([probe], 2)  # collective: fails on every rank if IPC mapping does not work
+            except Exception as e:  # the NCCL transport is the other GPU path, not a CPU fallback
+                print(f"[bench] IPC transport unavailable ({e}); using NCCL", file=sys.stderr)
+                comm = st.Comm.from_process_group(local)
+                args.transport = "nccl"
     assert world == args.gpus or world == 1, "--gpus must match the torchrun world size"
 
     def bind(buffers, n_slow):
@@ -257,7 +264,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev if args.transport == "nccl" else "cpu")
+        t = torch.tensor([x], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
