@@ -248,6 +248,11 @@ st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
                           int32_t halo, int64_t iters, int32_t tblock, st_comm* comm,
                           void* cuda_stream, int32_t* result_in_b);
 
+/* Diagnostic: counts into *mismatches (device, uint64, caller-zeroed) the x[i]
+ * (device, n doubles) for which the kernels' fast correctly rounded x/6 differs
+ * bitwise from the generic IEEE division. Used by the tests. */
+st_status st_selftest_div6(const double* x, int64_t n, unsigned long long* mismatches, void* cuda_stream);
+
 /* ------------------------------------------------------------------------ */
 /* 3-D Piacsek-Williams advection                              */
 /* ------------------------------------------------------------------------ */

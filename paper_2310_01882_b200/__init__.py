@@ -77,6 +77,7 @@ _SIGS = {
                                        ctypes.POINTER(_i32)]),
     "st_jacobi3d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i64, _i32, _vp, _vp,
                                        ctypes.POINTER(_i32)]),
+    "st_selftest_div6": (ctypes.c_int, [_vp, _i64, _vp, _vp]),
     "st_pw_advect3d": (ctypes.c_int, [_vp] * 6 + [_i64] * 4 + [_dbl, _dbl] + [_vp] * 4 + [_vp, _vp]),
 }
 EXPORTS = tuple(_SIGS)
@@ -319,6 +320,15 @@ def st_halo_exchange(comm: Comm, fields, n_slow_local: int, slab_pitch: int, wid
     arr = (_vp * len(fields))(*[t.data_ptr() for t in fields])
     _check(lib().st_halo_exchange(comm.handle, arr, len(fields), n_slow_local, slab_pitch, width,
                                   _stream_ptr(stream)), "st_halo_exchange")
+
+
+def st_selftest_div6(x) -> int:
+    """Number of x (float64 CUDA tensor) where the kernels' fast x/6 differs from IEEE division."""
+    import torch
+    _f64_cuda(x, "x")
+    cnt = torch.zeros(1, dtype=torch.int64, device=x.device)
+    _check(lib().st_selftest_div6(x.data_ptr(), x.numel(), cnt.data_ptr(), _stream_ptr()), "st_selftest_div6")
+    return int(cnt.item())
 
 
 # Friendlier aliases

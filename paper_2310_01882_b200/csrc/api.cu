@@ -220,6 +220,12 @@ st_status st_jacobi2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
   return run_schedule(ops, comm, a, b, nx, ny, ld, halo, s);
 }
 
+st_status st_selftest_div6(const double* x, int64_t n, unsigned long long* mismatches, void* cuda_stream) {
+  clear_error();
+  ST_RETURN_IF(!x || !mismatches || n < 0, ST_EINVAL, "st_selftest_div6: bad arguments");
+  return ddiv6_selftest(x, n, mismatches, static_cast<cudaStream_t>(cuda_stream));
+}
+
 st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t nz, int64_t ldx, int32_t halo,
                           int64_t iters, int32_t tblock, st_comm* comm, void* cuda_stream, int32_t* result_in_b) {
   clear_error();

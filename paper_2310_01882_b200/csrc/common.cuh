@@ -75,6 +75,25 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 
+// Correctly rounded x / 6.0 (== __ddiv_rn(x, 6.0), the oracle's `sum / 6.0`) in
+// 1 DMUL + 2 DFMA instead of the ~25-instruction generic division:
+//   q0 = RN(x * RN(1/6)); r = x - 6*q0 (exact: FMA residual of a faithful
+//   quotient); q = RN(q0 + r * RN(1/6)).
+// Why it is correctly rounded: x/6 = (x/2)/3 and a 53-bit significand divided
+// by 3 is never a rounding midpoint and stays >= ulp/6 away from every
+// midpoint, while q0 + r*RN(1/6) differs from x/6 by |r| * |RN(1/6) - 1/6| <=
+// 2^-52 ulp. Outside 2^-1000 < |x| < 2^1000 (subnormal results, overflow of
+// the residual) and for non-finite x the generic division is used.
+// tests/test_gpu_jacobi3d.py checks it bitwise against __ddiv_rn on random x.
+__device__ __forceinline__ double ddiv6(double x) {
+  const double ax = fabs(x);
+  if (!(ax > 0x1p-1000 && ax < 0x1p+1000)) return __ddiv_rn(x, 6.0);
+  constexpr double kInv6 = 0.16666666666666666;  // RN(1/6) = 0x3FC5555555555555
+  const double q0 = __dmul_rn(x, kInv6);
+  const double r = __fma_rn(-6.0, q0, x);
+  return __fma_rn(r, kInv6, q0);
+}
+
 // Streaming 16-byte load through the non-coherent path (inputs are read-only for
 // the duration of a kernel).
 __device__ __forceinline__ double2 ldg2(const double* p) {

@@ -54,6 +54,7 @@ st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t l
 // planes in the buffer (TMA extent).
 st_status jacobi3d_sweep_planes(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
                                 int64_t ldx, int64_t z_lo, int64_t z_hi, cudaStream_t s, Remote rem = Remote());
+st_status ddiv6_selftest(const double* x, int64_t n, unsigned long long* mismatches, cudaStream_t s);
 // dst's side faces (x = 0, nx+1; y = 0, ny+1) of planes [z_lo, z_hi] <- src.
 st_status jacobi3d_copy_faces(const double* src, double* dst, int64_t nx, int64_t ny, int64_t ldx, int64_t z_lo,
                               int64_t z_hi, cudaStream_t s);

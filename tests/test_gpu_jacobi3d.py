@@ -70,3 +70,21 @@ def test_single_rank_comm(cuda_lib, h):
         assert np.array_equal(got[h - 1:h + nz + 1], oracle.jacobi3d(g, iters))
     finally:
         comm.close()
+
+
+def test_fast_div6_is_correctly_rounded(cuda_lib):
+    # the 3-D kernel divides by 6 with 1 DMUL + 2 DFMA (common.cuh ddiv6); it must equal
+    # IEEE division bit for bit: random significands over all exponents, signs, and the
+    # special values, plus the values the stencil actually produces
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    n = 1 << 26
+    bits = torch.randint(0, 2 ** 62, (n,), device="cuda", generator=g, dtype=torch.int64)
+    sign = torch.randint(0, 2, (n,), device="cuda", generator=g, dtype=torch.int64) << 63
+    x = (bits | sign).view(torch.float64)
+    assert cuda_lib.st_selftest_div6(x) == 0
+    sums = torch.rand(n, device="cuda", generator=g, dtype=torch.float64) * 6 + 3  # six values in [0.5, 1.5)
+    assert cuda_lib.st_selftest_div6(sums) == 0
+    special = torch.tensor([0.0, -0.0, float("inf"), float("-inf"), float("nan"), 5e-324, 2.2250738585072014e-308,
+                            1.7976931348623157e308, 6.0, -6.0, 3.0, 1.0], dtype=torch.float64, device="cuda")
+    assert cuda_lib.st_selftest_div6(special) == 0
