@@ -51,6 +51,10 @@ def _load():
     lib.or_jacobi3d.argtypes = [_dp, _dp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
     lib.or_jacobi3d_slabs.restype = ctypes.c_int
     lib.or_jacobi3d_slabs.argtypes = [_dp, _dp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
+    lib.or_pencils_jacobi3d.restype = ctypes.c_int
+    lib.or_pencils_jacobi3d.argtypes = [_dp, _dp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int]
+    lib.or_pencils_pw.restype = ctypes.c_int
+    lib.or_pencils_pw.argtypes = pw + [ctypes.c_int, ctypes.c_int]
     lib.or_pw_points.restype = ctypes.c_int
     lib.or_pw_points.argtypes = [_dp] * 3 + [_i64] * 4 + [_dbl, _dbl] + [_dp] * 4 + [_dp, _i64, _dp]
     _lib = lib
@@ -175,4 +179,28 @@ def pw_slabs(u, v, w, co: dict, p: int, nx: int | None = None):
                              *[t.ctypes.data for t in tz], p)
     if rc < 0:
         raise ValueError("or_pw_slabs: bad arguments")
+    return su, sv, sw
+
+
+def pencils_jacobi3d(a0: np.ndarray, iters: int, py: int, pz: int, nx: int | None = None) -> np.ndarray:
+    """3-D Jacobi on a Py x Pz (y, z) process grid, 1-deep ghosts swapped every sweep."""
+    nz, ny, ldx = a0.shape[0] - 2, a0.shape[1] - 2, a0.shape[2]
+    nx = ldx - 2 if nx is None else nx
+    out = np.zeros_like(a0)
+    rc = _load().or_pencils_jacobi3d(np.ascontiguousarray(a0).ctypes.data, out.ctypes.data, nx, ny, nz, ldx, iters,
+                                     py, pz)
+    if rc < 0:
+        raise ValueError("or_pencils_jacobi3d: bad arguments")
+    return out
+
+
+def pencils_pw(u, v, w, co: dict, py: int, pz: int, nx: int | None = None):
+    """PW advection on a Py x Pz (y, z) process grid; ghosts (incl. y-z corners) come from the swap."""
+    nx, ny, nz, ldx, tz = _pw_args(u, v, w, co, nx)
+    su, sv, sw = (np.zeros_like(u) for _ in range(3))
+    rc = _load().or_pencils_pw(u.ctypes.data, v.ctypes.data, w.ctypes.data, su.ctypes.data, sv.ctypes.data,
+                               sw.ctypes.data, nx, ny, nz, ldx, co["tcx"], co["tcy"], *[t.ctypes.data for t in tz],
+                               py, pz)
+    if rc < 0:
+        raise ValueError("or_pencils_pw: bad arguments")
     return su, sv, sw

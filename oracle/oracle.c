@@ -35,6 +35,12 @@
  *                      (slowest index first, as Listing 1 orders i before j),
  *                      then / 6.0 (5 adds + 1 divide = 6 flops).
  *   or_jacobi3d_slabs  z-slab decomposition of or_jacobi3d (1 ghost plane).
+ *   or_pencils_jacobi3d / or_pencils_pw
+ *                      2-D (y, z) process grid ("decompose the 3D space into
+ *                      two dimensions"): Py x Pz blocks with one
+ *                      ghost layer in y and z, swapped before every sweep /
+ *                      application (y rows of all planes first, then whole z
+ *                      planes, so the (y, z) corner ghosts PW reads are filled).
  *
  * Pins (tests/test_oracle_*.py): J1-J10, P1-P9, D1 of SURVEY.md §8(c5).
  */
@@ -398,4 +404,155 @@ int or_jacobi3d_slabs(const double* a, double* out, int64_t nx, int64_t ny, int6
   for (int r = 0; r < p && A && B; ++r) { free(A[r]); free(B[r]); }
   free(A); free(B); free(st); free(nr);
   return ok ? 0 : -1;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Pencil (2-D y-z) decomposition of the 3-D stencils                          */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+  int64_t y0, ny, z0, nz; /* owned global interior rows y0+1..y0+ny, planes z0+1..z0+nz */
+  double* f[6];           /* local (nz+2) x (ny+2) x ldx buffers */
+} pencil;
+
+/* local (z, y) <-> global (z0+z, y0+y); copy whole local block from a global field */
+static void pencil_fill(pencil* b, int c, const double* g, int64_t gny, int64_t ldx) {
+  for (int64_t z = 0; z < b->nz + 2; ++z)
+    for (int64_t y = 0; y < b->ny + 2; ++y)
+      memcpy(b->f[c] + IDX3(z, y, 0, b->ny + 2, ldx), g + IDX3(b->z0 + z, b->y0 + y, 0, gny + 2, ldx),
+             sizeof(double) * (size_t)ldx);
+}
+
+/* halo swap of field c over the Py x Pz grid: y rows of every plane 0..nz+1
+ * first (the z-halo planes of the edge ranks carry global boundary values that
+ * the diagonal PW offsets read), then whole z planes (rows 0..ny+1, incl. the
+ * fresh y ghosts -> the (y, z) corner ghosts) */
+static void pencil_swap(pencil* B, int py, int pz, int c, int64_t ldx) {
+  for (int iz = 0; iz < pz; ++iz)
+    for (int iy = 0; iy < py; ++iy) {
+      pencil* b = &B[iz * py + iy];
+      const int64_t ny2 = b->ny + 2;
+      if (iy > 0) {
+        pencil* n = &B[iz * py + iy - 1];
+        for (int64_t z = 0; z <= b->nz + 1; ++z) /* my ghost row 0 <- lower neighbour's last owned row */
+          memcpy(b->f[c] + IDX3(z, 0, 0, ny2, ldx), n->f[c] + IDX3(z, n->ny, 0, n->ny + 2, ldx),
+                 sizeof(double) * (size_t)ldx);
+      }
+      if (iy < py - 1) {
+        pencil* n = &B[iz * py + iy + 1];
+        for (int64_t z = 0; z <= b->nz + 1; ++z)
+          memcpy(b->f[c] + IDX3(z, b->ny + 1, 0, ny2, ldx), n->f[c] + IDX3(z, 1, 0, n->ny + 2, ldx),
+                 sizeof(double) * (size_t)ldx);
+      }
+    }
+  for (int iz = 0; iz < pz; ++iz)
+    for (int iy = 0; iy < py; ++iy) {
+      pencil* b = &B[iz * py + iy];
+      const int64_t plane = (b->ny + 2) * ldx;
+      if (iz > 0) {
+        pencil* n = &B[(iz - 1) * py + iy];
+        memcpy(b->f[c], n->f[c] + n->nz * plane, sizeof(double) * (size_t)plane);
+      }
+      if (iz < pz - 1) {
+        pencil* n = &B[(iz + 1) * py + iy];
+        memcpy(b->f[c] + (b->nz + 1) * plane, n->f[c] + plane, sizeof(double) * (size_t)plane);
+      }
+    }
+}
+
+static pencil* pencils_make(int64_t ny, int64_t nz, int py, int pz, int64_t ldx, int nf) {
+  pencil* B = calloc((size_t)(py * pz), sizeof(pencil));
+  if (!B) return NULL;
+  for (int iz = 0; iz < pz; ++iz)
+    for (int iy = 0; iy < py; ++iy) {
+      pencil* b = &B[iz * py + iy];
+      block_split(ny, py, iy, &b->y0, &b->ny);
+      block_split(nz, pz, iz, &b->z0, &b->nz);
+      for (int c = 0; c < nf; ++c) {
+        b->f[c] = calloc((size_t)((b->nz + 2) * (b->ny + 2) * ldx), sizeof(double));
+        if (!b->f[c]) return NULL;
+      }
+    }
+  return B;
+}
+
+static void pencils_free(pencil* B, int n) {
+  for (int i = 0; B && i < n; ++i)
+    for (int c = 0; c < 6; ++c) free(B[i].f[c]);
+  free(B);
+}
+
+/* gather the owned interior of field c into the global field g */
+static void pencil_gather(pencil* B, int py, int pz, int c, double* g, int64_t gny, int64_t nx, int64_t ldx) {
+  for (int i = 0; i < py * pz; ++i) {
+    pencil* b = &B[i];
+    for (int64_t z = 1; z <= b->nz; ++z)
+      for (int64_t y = 1; y <= b->ny; ++y)
+        memcpy(g + IDX3(b->z0 + z, b->y0 + y, 1, gny + 2, ldx), b->f[c] + IDX3(z, y, 1, b->ny + 2, ldx),
+               sizeof(double) * (size_t)nx);
+  }
+}
+
+int or_pencils_jacobi3d(const double* a, double* out, int64_t nx, int64_t ny, int64_t nz, int64_t ldx,
+                        int64_t iters, int py, int pz) {
+  if (!a || !out || nx < 1 || ny < 1 || nz < 1 || ldx < nx + 2 || iters < 0 || py < 1 || pz < 1 || ny / py < 1 ||
+      nz / pz < 1)
+    return -1;
+  pencil* B = pencils_make(ny, nz, py, pz, ldx, 2);
+  if (!B) return -1;
+  for (int i = 0; i < py * pz; ++i) {
+    pencil_fill(&B[i], 0, a, ny, ldx);
+    pencil_fill(&B[i], 1, a, ny, ldx);
+  }
+  int cur = 0;
+  for (int64_t it = 0; it < iters; ++it) {
+    pencil_swap(B, py, pz, cur, ldx);
+    for (int i = 0; i < py * pz; ++i)
+      jacobi3d_sweep_planes(B[i].f[cur], B[i].f[1 - cur], nx, B[i].ny, ldx, 1, B[i].nz, 1);
+    cur = 1 - cur;
+  }
+  memcpy(out, a, sizeof(double) * (size_t)((nz + 2) * (ny + 2) * ldx));
+  pencil_gather(B, py, pz, cur, out, ny, nx, ldx);
+  pencils_free(B, py * pz);
+  return 0;
+}
+
+int or_pencils_pw(const double* u, const double* v, const double* w, double* su, double* sv, double* sw,
+                  int64_t nx, int64_t ny, int64_t nz, int64_t ldx, double tcx, double tcy, const double* tzc1,
+                  const double* tzc2, const double* tzd1, const double* tzd2, int py, int pz) {
+  if (!u || !v || !w || !su || !sv || !sw || nx < 1 || ny < 1 || nz < 1 || ldx < nx + 2 || py < 1 || pz < 1 ||
+      ny / py < 1 || nz / pz < 1)
+    return -1;
+  pencil* B = pencils_make(ny, nz, py, pz, ldx, 6);
+  if (!B) return -1;
+  const double* gin[3] = {u, v, w};
+  for (int i = 0; i < py * pz; ++i)
+    for (int c = 0; c < 3; ++c) pencil_fill(&B[i], c, gin[c], ny, ldx);
+  /* the ghosts of u, v, w come from the neighbours (poisoned first so a missed cell shows) */
+  for (int i = 0; i < py * pz; ++i) {
+    pencil* b = &B[i];
+    const int iy = i % py, iz = i / py;
+    for (int c = 0; c < 3; ++c)
+      for (int64_t z = 0; z < b->nz + 2; ++z)
+        for (int64_t y = 0; y < b->ny + 2; ++y) {
+          const int ghost_y = (y == 0 && iy > 0) || (y == b->ny + 1 && iy < py - 1);
+          const int ghost_z = (z == 0 && iz > 0) || (z == b->nz + 1 && iz < pz - 1);
+          if (ghost_y || ghost_z)
+            for (int64_t x = 0; x < nx + 2; ++x) b->f[c][IDX3(z, y, x, b->ny + 2, ldx)] = 1e300;
+        }
+  }
+  for (int c = 0; c < 3; ++c) pencil_swap(B, py, pz, c, ldx);
+  for (int i = 0; i < py * pz; ++i) {
+    pencil* b = &B[i];
+    const int64_t o = b->z0;
+    if (or_pw_advect3d(b->f[0], b->f[1], b->f[2], b->f[3], b->f[4], b->f[5], nx, b->ny, b->nz, ldx, tcx, tcy,
+                       tzc1 + o, tzc2 + o, tzd1 + o, tzd2 + o, 1) != 0) {
+      pencils_free(B, py * pz);
+      return -1;
+    }
+  }
+  double* gout[3] = {su, sv, sw};
+  for (int c = 0; c < 3; ++c) pencil_gather(B, py, pz, 3 + c, gout[c], ny, nx, ldx);
+  pencils_free(B, py * pz);
+  return 0;
 }

@@ -37,3 +37,21 @@ def test_D1_pw_slabs(p):
     got = oracle.pw_slabs(d["u"], d["v"], d["w"], d, p, nx=nx)
     for r, g in zip(ref, got):
         assert np.array_equal(r, g)
+
+
+@pytest.mark.parametrize("py,pz", [(1, 1), (2, 1), (1, 3), (2, 2), (3, 2), (4, 3)])
+def test_D1_pencils_jacobi3d(py, pz):
+    # 2-D (y, z) process grid, "decompose the 3D space into two dimensions"
+    a = si.jacobi3d_grid(11, 13, 14)
+    assert np.array_equal(oracle.pencils_jacobi3d(a, 7, py, pz), oracle.jacobi3d(a, 7))
+
+
+@pytest.mark.parametrize("py,pz", [(2, 1), (1, 2), (2, 2), (3, 3), (2, 4)])
+def test_D1_pencils_pw_needs_corner_ghosts(py, pz):
+    # PW reads (z+1, y-1) and (z-1, y+1): the y-then-z swap must fill the corner ghosts
+    nz, ny, nx = 13, 11, 9
+    d = si.pw_inputs(nx, ny, nz, ldx=12)
+    ref = oracle.pw_advect3d(d["u"], d["v"], d["w"], d, nx=nx)
+    got = oracle.pencils_pw(d["u"], d["v"], d["w"], d, py, pz, nx=nx)
+    for r, g in zip(ref, got):
+        assert np.array_equal(r, g)
