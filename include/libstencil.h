@@ -111,6 +111,17 @@ st_status st_comm_export(st_comm* comm, double* const* buffers, int32_t nbuffers
  * other ranks' blobs are ignored. IPC comms only. */
 st_status st_comm_import(st_comm* comm, int32_t peer, const uint8_t* blob, int64_t bytes);
 
+/* Pencils (2-D (y, z) process grid, "decompose the 3D space into two
+ * dimensions"; IPC/LOCAL transports): py ranks along y,
+ * nranks/py along z, rank = iz*py + iy; ny_local = this rank's owned rows.
+ * Call before st_comm_export / the pencil entry points. */
+st_status st_comm_set_grid(st_comm* comm, int32_t py, int64_t ny_local);
+
+/* Block of `rank` in a py x pz grid over ny rows and nz planes (remainder to
+ * the high ranks in each dimension). Host-only. */
+st_status st_pencil_split(int64_t ny, int64_t nz, int32_t py, int32_t pz, int32_t rank, int64_t* y0, int64_t* ny_local,
+                          int64_t* z0, int64_t* nz_local);
+
 /* Registers the buffers this rank swaps (LOCAL transport; no-op for NCCL): all
  * ranks bind the same number of buffers in the same order (buffer i of rank r
  * exchanges with buffer i of its neighbours), each holding n_slow_local owned
@@ -248,6 +259,14 @@ st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
                           int32_t halo, int64_t iters, int32_t tblock, st_comm* comm,
                           void* cuda_stream, int32_t* result_in_b);
 
+/* The 3-D 7-point Jacobi on a pencil block: a, b hold (nz_local+2) planes x
+ * (ny_local+2) rows x ldx (one ghost layer in y and z; on the grid's edges the
+ * ghost layer is the global Dirichlet face). Before every sweep the y ghost rows
+ * and then the z ghost planes are swapped with the 4 grid neighbours (comm set
+ * up with st_comm_set_grid; IPC or LOCAL transport). comm NULL: single block. */
+st_status st_jacobi3d_run_pencils(double* a, double* b, int64_t nx, int64_t ny_local, int64_t nz_local, int64_t ldx,
+                                  int64_t iters, st_comm* comm, void* cuda_stream, int32_t* result_in_b);
+
 /* Diagnostic: counts into *mismatches (device, uint64, caller-zeroed) the x[i]
  * (device, n doubles) for which the kernels' fast correctly rounded x/6 differs
  * bitwise from the generic IEEE division. Used by the tests. */
@@ -280,6 +299,14 @@ st_status st_pw_advect3d(double* u, double* v, double* w, double* su,
                          int64_t ldx, double tcx, double tcy, const double* tzc1,
                          const double* tzc2, const double* tzd1, const double* tzd2,
                          st_comm* comm, void* cuda_stream);
+
+/* PW advection on a pencil block (layout as st_jacobi3d_run_pencils; u, v, w
+ * ghosts — including the (y, z) corners the diagonal offsets read — are first
+ * swapped y-then-z with the grid neighbours). tz*: nz_local+2 doubles. */
+st_status st_pw_advect3d_pencils(double* u, double* v, double* w, double* su, double* sv, double* sw, int64_t nx,
+                                 int64_t ny_local, int64_t nz_local, int64_t ldx, double tcx, double tcy,
+                                 const double* tzc1, const double* tzc2, const double* tzd1, const double* tzd2,
+                                 st_comm* comm, void* cuda_stream);
 
 #ifdef __cplusplus
 }

@@ -78,6 +78,11 @@ _SIGS = {
     "st_jacobi3d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i64, _i32, _vp, _vp,
                                        ctypes.POINTER(_i32)]),
     "st_selftest_div6": (ctypes.c_int, [_vp, _i64, _vp, _vp]),
+    "st_comm_set_grid": (ctypes.c_int, [_vp, _i32, _i64]),
+    "st_pencil_split": (ctypes.c_int, [_i64, _i64, _i32, _i32, _i32] + [ctypes.POINTER(_i64)] * 4),
+    "st_jacobi3d_run_pencils": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp,
+                                               ctypes.POINTER(_i32)]),
+    "st_pw_advect3d_pencils": (ctypes.c_int, [_vp] * 6 + [_i64] * 4 + [_dbl, _dbl] + [_vp] * 4 + [_vp, _vp]),
     "st_pw_advect3d": (ctypes.c_int, [_vp] * 6 + [_i64] * 4 + [_dbl, _dbl] + [_vp] * 4 + [_vp, _vp]),
 }
 EXPORTS = tuple(_SIGS)
@@ -208,6 +213,10 @@ class Comm:
         arr = (_vp * len(buffers))(*[t.data_ptr() for t in buffers])
         _check(lib().st_comm_bind(self.handle, arr, len(buffers), n_slow_local), "st_comm_bind")
 
+    def set_grid(self, py: int, ny_local: int) -> None:
+        """Pencil decomposition: py ranks along y (rank = iz*py + iy); this rank owns ny_local rows."""
+        _check(lib().st_comm_set_grid(self.handle, py, ny_local), "st_comm_set_grid")
+
     def close(self) -> None:
         if self.handle:
             _check(lib().st_comm_destroy(self.handle), "st_comm_destroy")
@@ -229,6 +238,13 @@ def st_block_split(n: int, nranks: int, rank: int) -> tuple[int, int]:
     s, c = _i64(), _i64()
     _check(lib().st_block_split(n, nranks, rank, ctypes.byref(s), ctypes.byref(c)), "st_block_split")
     return s.value, c.value
+
+
+def st_pencil_split(ny: int, nz: int, py: int, pz: int, rank: int) -> tuple[int, int, int, int]:
+    """(y0, ny_local, z0, nz_local) of `rank` in a py x pz grid (host only)."""
+    o = [_i64() for _ in range(4)]
+    _check(lib().st_pencil_split(ny, nz, py, pz, rank, *[ctypes.byref(v) for v in o]), "st_pencil_split")
+    return tuple(v.value for v in o)
 
 
 def st_halo_plan(rank: int, nranks: int, n_slow_local: int, slab_pitch: int, width: int):
@@ -290,6 +306,38 @@ def st_jacobi3d_run(a, b, iters: int, tblock: int = 0, halo: int = 1, comm: Comm
     _check(lib().st_jacobi3d_run(a.data_ptr(), b.data_ptr(), nx, ny, nz, ldx, halo, iters, tblock,
                                  _comm_ptr(comm), _stream_ptr(stream), ctypes.byref(rib)), "st_jacobi3d_run")
     return b if rib.value else a
+
+
+def st_jacobi3d_run_pencils(a, b, iters: int, comm: Comm | None = None, nx: int | None = None, stream=None):
+    """3-D Jacobi on a pencil block (nz_local+2, ny_local+2, ldx); see include/libstencil.h."""
+    _f64_cuda(a, "a")
+    _f64_cuda(b, "b")
+    if a.dim() != 3 or a.shape != b.shape or not a.is_contiguous() or not b.is_contiguous():
+        raise ValueError("a, b: contiguous 3-D tensors of equal shape")
+    nzl, nyl, ldx = a.shape[0] - 2, a.shape[1] - 2, a.shape[2]
+    nx = ldx - 2 if nx is None else nx
+    rib = _i32()
+    _check(lib().st_jacobi3d_run_pencils(a.data_ptr(), b.data_ptr(), nx, nyl, nzl, ldx, iters, _comm_ptr(comm),
+                                         _stream_ptr(stream), ctypes.byref(rib)), "st_jacobi3d_run_pencils")
+    return b if rib.value else a
+
+
+def st_pw_advect3d_pencils(u, v, w, su, sv, sw, tcx: float, tcy: float, tzc1, tzc2, tzd1, tzd2,
+                           comm: Comm | None = None, nx: int | None = None, stream=None) -> None:
+    """PW advection on a pencil block; u, v, w ghosts (incl. corners) are swapped first."""
+    fields = (u, v, w, su, sv, sw)
+    for t, name in zip(fields, ("u", "v", "w", "su", "sv", "sw")):
+        _f64_cuda(t, name)
+        if t.dim() != 3 or t.shape != u.shape or not t.is_contiguous():
+            raise ValueError(f"{name}: contiguous 3-D tensor like u")
+    coefs = (tzc1, tzc2, tzd1, tzd2)
+    for t, name in zip(coefs, ("tzc1", "tzc2", "tzd1", "tzd2")):
+        _f64_cuda(t, name)
+    nzl, nyl, ldx = u.shape[0] - 2, u.shape[1] - 2, u.shape[2]
+    nx = ldx - 2 if nx is None else nx
+    _check(lib().st_pw_advect3d_pencils(*[t.data_ptr() for t in fields], nx, nyl, nzl, ldx, float(tcx), float(tcy),
+                                        *[t.data_ptr() for t in coefs], _comm_ptr(comm), _stream_ptr(stream)),
+           "st_pw_advect3d_pencils")
 
 
 def st_pw_advect3d(u, v, w, su, sv, sw, tcx: float, tcy: float, tzc1, tzc2, tzd1, tzd2,

@@ -263,6 +263,63 @@ st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
   return run_schedule3d(ops, comm, a, b, nx, ny, nz, ldx, halo, s);
 }
 
+st_status st_jacobi3d_run_pencils(double* a, double* b, int64_t nx, int64_t nyl, int64_t nzl, int64_t ldx,
+                                  int64_t iters, st_comm* comm, void* cuda_stream, int32_t* result_in_b) {
+  clear_error();
+  if (!comm || comm->nranks == 1) return st_jacobi3d_run(a, b, nx, nyl, nzl, ldx, 1, iters, 1, nullptr, cuda_stream,
+                                                         result_in_b);
+  ST_RETURN_IF(!a || !b || nx < 1 || nyl < 1 || nzl < 1 || iters < 0, ST_EINVAL,
+               "st_jacobi3d_run_pencils: bad arguments");
+  ST_RETURN_IF(ldx < nx + 2 || (ldx & 1) || !aligned16(a) || !aligned16(b), ST_EINVAL,
+               "st_jacobi3d_run_pencils: ldx even >= nx+2, 16-byte aligned fields");
+  const size_t bytes = (size_t)(nzl + 2) * (size_t)(nyl + 2) * (size_t)ldx * sizeof(double);
+  ST_RETURN_IF(overlaps(a, bytes, b, bytes), ST_EINVAL, "st_jacobi3d_run_pencils: a and b overlap");
+  ST_TRY(check_device_ptr(a, "a"));
+  ST_TRY(check_device_ptr(b, "b"));
+  ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier error");
+  if (result_in_b) *result_in_b = (int32_t)(iters & 1);
+  if (iters == 0) return ST_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  // ghost / Dirichlet shell a -> b: planes 0 and nzl+1, side faces (x and y) of the owned planes
+  const size_t pitch = (size_t)ldx * sizeof(double), width = (size_t)(nx + 2) * sizeof(double);
+  const int64_t plane = (nyl + 2) * ldx;
+  ST_CHECK_CUDA(cudaMemcpy2DAsync(b, pitch, a, pitch, width, (size_t)(nyl + 2), cudaMemcpyDeviceToDevice, s));
+  ST_CHECK_CUDA(cudaMemcpy2DAsync(b + (nzl + 1) * plane, pitch, a + (nzl + 1) * plane, pitch, width,
+                                  (size_t)(nyl + 2), cudaMemcpyDeviceToDevice, s));
+  ST_TRY(jacobi3d_copy_faces(a, b, nx, nyl, ldx, 1, nzl, s));
+  double* src = a;
+  double* dst = b;
+  for (int64_t it = 0; it < iters; ++it) {
+    ST_TRY(pencil_exchange_async(comm, &src, 1, nx, nyl, nzl, ldx, s, true));
+    ST_TRY(jacobi3d_sweep_planes(src, dst, nx, nyl, nzl + 2, ldx, 1, nzl, s));
+    double* t = src;
+    src = dst;
+    dst = t;
+  }
+  return ST_OK;
+}
+
+st_status st_pw_advect3d_pencils(double* u, double* v, double* w, double* su, double* sv, double* sw, int64_t nx,
+                                 int64_t nyl, int64_t nzl, int64_t ldx, double tcx, double tcy, const double* tzc1,
+                                 const double* tzc2, const double* tzd1, const double* tzd2, st_comm* comm,
+                                 void* cuda_stream) {
+  clear_error();
+  if (!comm || comm->nranks == 1)
+    return st_pw_advect3d(u, v, w, su, sv, sw, nx, nyl, nzl, ldx, tcx, tcy, tzc1, tzc2, tzd1, tzd2, nullptr,
+                          cuda_stream);
+  // validate as the single-block call, then swap ghosts (incl. corners) and advect
+  double* f[3] = {u, v, w};
+  const size_t bytes = (size_t)(nzl + 2) * (size_t)(nyl + 2) * (size_t)ldx * sizeof(double);
+  ST_RETURN_IF(!u || !v || !w || overlaps(u, bytes, v, bytes) || overlaps(u, bytes, w, bytes) ||
+                   overlaps(v, bytes, w, bytes),
+               ST_EINVAL, "st_pw_advect3d_pencils: u, v, w must be distinct");
+  ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier error");
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  ST_TRY(pencil_exchange_async(comm, f, 3, nx, nyl, nzl, ldx, s, true));
+  return st_pw_advect3d(u, v, w, su, sv, sw, nx, nyl, nzl, ldx, tcx, tcy, tzc1, tzc2, tzd1, tzd2, nullptr,
+                        cuda_stream);
+}
+
 st_status st_pw_advect3d(double* u, double* v, double* w, double* su, double* sv, double* sw,
                          int64_t nx, int64_t ny, int64_t nz, int64_t ldx, double tcx, double tcy,
                          const double* tzc1, const double* tzc2, const double* tzd1,

@@ -92,11 +92,10 @@ st_status stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t v) {
   return ST_OK;
 }
 
-constexpr int kFlagReady = 0, kFlagDoneFromLo = 1, kFlagDoneFromHi = 2;
+constexpr int kFlagReady = 0, kFlagDoneFromLo = 1, kFlagDoneFromHi = 2, kFlagDoneFromYLo = 3, kFlagDoneFromYHi = 4;
 
-// Neighbour on `side` (0 = rank-1, 1 = rank+1) of a LOCAL/IPC comm; valid=false if none.
-st_status peer_view(st_comm* c, int side, st_peer* out) {
-  const int32_t peer = side == 0 ? c->rank - 1 : c->rank + 1;
+// View of rank `peer` of a LOCAL/IPC comm (direct for LOCAL, IPC-mapped for IPC).
+st_status peer_of(st_comm* c, int32_t peer, st_peer* out) {
   out->valid = false;
   if (peer < 0 || peer >= c->nranks) return ST_OK;
   if (c->kind == st_comm::LOCAL) {
@@ -106,18 +105,23 @@ st_status peer_view(st_comm* c, int side, st_peer* out) {
     out->flags = pc->flags;
     out->bound = pc->bound;
     out->n_slow = pc->bound_n_slow;
+    out->n_mid = pc->n_mid;
     out->device = pc->device;
   } else {
-    const st_peer& p = c->ipc_peer[side];
-    ST_RETURN_IF(!p.valid, ST_EINVAL, "IPC comm: rank %d's blob was not imported", peer);
-    out->valid = true;
-    out->flags = p.flags;
-    out->bound = p.bound;
-    out->n_slow = p.n_slow;
-    out->device = p.device;
+    const st_peer* p = nullptr;
+    for (const auto& kv : c->ipc_peers)
+      if (kv.first == peer) p = &kv.second;
+    ST_RETURN_IF(!p || !p->valid, ST_EINVAL, "IPC comm: rank %d's blob was not imported", peer);
+    *out = *p;
+    out->opened.clear();
   }
   ST_RETURN_IF(out->bound.size() != c->bound.size(), ST_EINVAL, "rank %d has not bound the same buffers", peer);
   return ST_OK;
+}
+
+// Slab neighbour on `side` (0 = rank-1, 1 = rank+1); valid=false if none.
+st_status peer_view(st_comm* c, int side, st_peer* out) {
+  return peer_of(c, side == 0 ? c->rank - 1 : c->rank + 1, out);
 }
 
 // LOCAL transport: push my boundary slabs into the neighbours' ghost slabs.
@@ -163,6 +167,70 @@ st_status local_exchange(st_comm* c, double* const* fields, int32_t nfields, int
   return ST_OK;
 }
 }  // namespace
+
+st_status pencil_exchange_async(st_comm* c, double* const* fields, int32_t nfields, int64_t nx, int64_t nyl,
+                                int64_t nzl, int64_t ldx, cudaStream_t main, bool join) {
+  ST_RETURN_IF(c->kind == st_comm::NCCL, ST_ENOTSUP, "pencil decomposition needs the IPC or LOCAL transport");
+  ST_RETURN_IF(c->grid_py < 1 || c->nranks % c->grid_py != 0, ST_EINVAL, "pencils: st_comm_set_grid first");
+  ST_RETURN_IF(c->bound.empty(), ST_EINVAL, "pencils: st_comm_bind/st_comm_export the swapped buffers first");
+  ST_RETURN_IF(nyl != c->n_mid || nzl != c->bound_n_slow, ST_EINVAL, "pencils: block %lldx%lld, bound %lldx%lld",
+               (long long)nyl, (long long)nzl, (long long)c->n_mid, (long long)c->bound_n_slow);
+  ST_RETURN_IF(nfields > 8, ST_EINVAL, "pencils: at most 8 fields per swap");
+  int idx[8];
+  for (int f = 0; f < nfields; ++f) {
+    idx[f] = -1;
+    for (size_t i = 0; i < c->bound.size(); ++i)
+      if (c->bound[i] == fields[f]) idx[f] = (int)i;
+    ST_RETURN_IF(idx[f] < 0, ST_EINVAL, "pencils: field %d was not bound", f);
+  }
+  const int32_t py = c->grid_py, iy = c->rank % py, iz = c->rank / py, pz = c->nranks / py;
+  const uint32_t k = ++c->seq;
+  cudaStream_t cs = c->comm_stream;
+  const size_t row_bytes = (size_t)(nx + 2) * sizeof(double);
+  const int64_t my_plane = (nyl + 2) * ldx;
+  ST_CHECK_CUDA(cudaEventRecord(c->ev_ready, main));
+  ST_CHECK_CUDA(cudaStreamWaitEvent(cs, c->ev_ready, 0));
+  ST_TRY(stream_write(cs, c->flags + kFlagReady, k));
+  // phase y: one boundary row per plane into the y neighbours' ghost rows. The
+  // planes that are z ghosts (filled whole by phase z, possibly concurrently)
+  // are skipped; the z-halo planes of the grid's z edges are global boundary
+  // planes and are included (the diagonal PW offsets read their corners).
+  // y neighbours share this rank's z range, so they skip the same planes.
+  const int64_t zlo = iz > 0 ? 1 : 0, zhi = iz < pz - 1 ? nzl : nzl + 1;
+  for (int side = 0; side < 2; ++side) {
+    if ((side == 0 && iy == 0) || (side == 1 && iy == py - 1)) continue;
+    st_peer pc;
+    ST_TRY(peer_of(c, side == 0 ? c->rank - 1 : c->rank + 1, &pc));
+    ST_TRY(stream_wait_geq(cs, pc.flags + kFlagReady, k));
+    const int64_t peer_plane = (pc.n_mid + 2) * ldx;
+    const int64_t src_row = side == 0 ? 1 : nyl, dst_row = side == 0 ? pc.n_mid + 1 : 0;
+    for (int f = 0; f < nfields; ++f)
+      ST_CHECK_CUDA(cudaMemcpy2DAsync(pc.bound[(size_t)idx[f]] + zlo * peer_plane + dst_row * ldx,
+                                      (size_t)peer_plane * sizeof(double), fields[f] + zlo * my_plane + src_row * ldx,
+                                      (size_t)my_plane * sizeof(double), row_bytes, (size_t)(zhi - zlo + 1),
+                                      cudaMemcpyDefault, cs));
+    ST_TRY(stream_write(cs, pc.flags + (side == 0 ? kFlagDoneFromYHi : kFlagDoneFromYLo), k));
+  }
+  if (iy > 0) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromYLo, k));
+  if (iy < py - 1) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromYHi, k));
+  // phase z: whole boundary planes (rows 0..nyl+1, i.e. with the fresh y ghosts)
+  for (int side = 0; side < 2; ++side) {
+    if ((side == 0 && iz == 0) || (side == 1 && iz == pz - 1)) continue;
+    st_peer pc;
+    ST_TRY(peer_of(c, side == 0 ? c->rank - py : c->rank + py, &pc));
+    ST_TRY(stream_wait_geq(cs, pc.flags + kFlagReady, k));
+    const int64_t src_plane = side == 0 ? 1 : nzl, dst_plane = side == 0 ? pc.n_slow + 1 : 0;
+    for (int f = 0; f < nfields; ++f)
+      ST_CHECK_CUDA(cudaMemcpyAsync(pc.bound[(size_t)idx[f]] + dst_plane * my_plane, fields[f] + src_plane * my_plane,
+                                    (size_t)my_plane * sizeof(double), cudaMemcpyDefault, cs));
+    ST_TRY(stream_write(cs, pc.flags + (side == 0 ? kFlagDoneFromHi : kFlagDoneFromLo), k));
+  }
+  if (iz > 0) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromLo, k));
+  if (iz < pz - 1) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromHi, k));
+  ST_CHECK_CUDA(cudaEventRecord(c->ev_done, cs));
+  if (join) ST_CHECK_CUDA(cudaStreamWaitEvent(main, c->ev_done, 0));
+  return ST_OK;
+}
 
 bool fused_halo_available(const st_comm* comm) {
   static const int kFused = env_int("ST_FUSED_HALO", 1);
@@ -328,8 +396,8 @@ st_status st_comm_init_local(st_comm** comms, int32_t nranks, const int32_t* dev
     if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess ||
-        cudaMalloc(&c->flags, 4 * sizeof(uint32_t)) != cudaSuccess ||
-        cudaMemset(c->flags, 0, 4 * sizeof(uint32_t)) != cudaSuccess) {
+        cudaMalloc(&c->flags, 8 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemset(c->flags, 0, 8 * sizeof(uint32_t)) != cudaSuccess) {
       set_error("st_comm_init_local: stream/event/flag allocation failed");
       delete c;
       for (int q = 0; q < r; ++q) st_comm_destroy(comms[q]);
@@ -351,7 +419,7 @@ constexpr uint32_t kBlobMagic = 0x53544950u;  // "STIP"
 struct BlobHeader {
   uint32_t magic, version;
   int32_t rank, device, nbuf, pad;
-  int64_t n_slow;
+  int64_t n_slow, n_mid;
 };
 struct BlobEntry {
   cudaIpcMemHandle_t handle;
@@ -392,8 +460,8 @@ st_status st_comm_init_ipc(st_comm** out, int32_t nranks, int32_t rank, int32_t 
   if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess ||
-      cudaMalloc(&c->flags, 4 * sizeof(uint32_t)) != cudaSuccess ||
-      cudaMemset(c->flags, 0, 4 * sizeof(uint32_t)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+      cudaMalloc(&c->flags, 8 * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemset(c->flags, 0, 8 * sizeof(uint32_t)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
     set_error("st_comm_init_ipc: stream/event/flag allocation failed");
     st_comm_destroy(c);
     return ST_ECUDA;
@@ -414,7 +482,7 @@ st_status st_comm_export(st_comm* c, double* const* buffers, int32_t nbuf, int64
                (long long)need);
   c->bound.assign(buffers, buffers + nbuf);
   c->bound_n_slow = n_slow;
-  BlobHeader h{kBlobMagic, 1u, c->rank, c->device, nbuf, 0, n_slow};
+  BlobHeader h{kBlobMagic, 2u, c->rank, c->device, nbuf, 0, n_slow, c->n_mid};
   std::memcpy(blob, &h, sizeof(h));
   BlobEntry* e = reinterpret_cast<BlobEntry*>(blob + sizeof(h));
   ST_TRY(ipc_entry(c->flags, &e[0]));
@@ -425,14 +493,27 @@ st_status st_comm_export(st_comm* c, double* const* buffers, int32_t nbuf, int64
 st_status st_comm_import(st_comm* c, int32_t peer, const uint8_t* blob, int64_t bytes) {
   clear_error();
   ST_RETURN_IF(!c || c->kind != st_comm::IPC || !blob, ST_EINVAL, "st_comm_import: needs an IPC comm and a blob");
-  if (peer != c->rank - 1 && peer != c->rank + 1) return ST_OK;  // only neighbours are mapped
+  bool neighbour = peer == c->rank - 1 || peer == c->rank + 1;
+  if (c->grid_py > 0) {  // pencils: y neighbours in the same grid row, z neighbours +-py
+    const int32_t py = c->grid_py;
+    neighbour = (peer / py == c->rank / py && (peer == c->rank - 1 || peer == c->rank + 1)) ||
+                peer == c->rank - py || peer == c->rank + py;
+  }
+  if (!neighbour) return ST_OK;  // only neighbours are mapped
   ST_RETURN_IF(bytes < (int64_t)sizeof(BlobHeader), ST_EINVAL, "st_comm_import: short blob");
   BlobHeader h;
   std::memcpy(&h, blob, sizeof(h));
   ST_RETURN_IF(h.magic != kBlobMagic || h.rank != peer || h.nbuf < 0 ||
                    bytes < (int64_t)sizeof(h) + (int64_t)(h.nbuf + 1) * (int64_t)sizeof(BlobEntry),
                ST_EINVAL, "st_comm_import: malformed blob for rank %d", peer);
-  st_peer& p = c->ipc_peer[peer == c->rank - 1 ? 0 : 1];
+  st_peer* pp = nullptr;
+  for (auto& kv : c->ipc_peers)
+    if (kv.first == peer) pp = &kv.second;
+  if (!pp) {
+    c->ipc_peers.emplace_back(peer, st_peer());
+    pp = &c->ipc_peers.back().second;
+  }
+  st_peer& p = *pp;
   for (void* q : p.opened) cudaIpcCloseMemHandle(q);
   p = st_peer();
   const BlobEntry* e = reinterpret_cast<const BlobEntry*>(blob + sizeof(h));
@@ -461,9 +542,28 @@ st_status st_comm_import(st_comm* c, int32_t peer, const uint8_t* blob, int64_t 
     p.bound.push_back(static_cast<double*>(bp));
   }
   p.n_slow = h.n_slow;
+  p.n_mid = h.n_mid;
   p.device = h.device;
   p.valid = true;
   return ST_OK;
+}
+
+st_status st_comm_set_grid(st_comm* comm, int32_t py, int64_t ny_local) {
+  clear_error();
+  ST_RETURN_IF(!comm || py < 1 || comm->nranks % py != 0 || ny_local < 1, ST_EINVAL,
+               "st_comm_set_grid: py must divide nranks, ny_local >= 1");
+  comm->grid_py = py;
+  comm->n_mid = ny_local;
+  return ST_OK;
+}
+
+st_status st_pencil_split(int64_t ny, int64_t nz, int32_t py, int32_t pz, int32_t rank, int64_t* y0, int64_t* nyl,
+                          int64_t* z0, int64_t* nzl) {
+  clear_error();
+  ST_RETURN_IF(py < 1 || pz < 1 || rank < 0 || rank >= py * pz || !y0 || !nyl || !z0 || !nzl, ST_EINVAL,
+               "st_pencil_split: bad arguments");
+  ST_TRY(st_block_split(ny, py, rank % py, y0, nyl));
+  return st_block_split(nz, pz, rank / py, z0, nzl);
 }
 
 st_status st_comm_bind(st_comm* comm, double* const* buffers, int32_t nbuffers, int64_t n_slow_local) {
@@ -486,8 +586,8 @@ st_status st_comm_destroy(st_comm* c) {
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
-  for (int side = 0; side < 2; ++side)
-    for (void* p : c->ipc_peer[side].opened) cudaIpcCloseMemHandle(p);
+  for (auto& kv : c->ipc_peers)
+    for (void* p : kv.second.opened) cudaIpcCloseMemHandle(p);
   if (c->flags) cudaFree(c->flags);
   if (c->group) {
     st_local_group* g = c->group;

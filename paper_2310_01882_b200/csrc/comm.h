@@ -30,6 +30,7 @@ struct st_peer {
   uint32_t* flags = nullptr;
   std::vector<double*> bound;
   int64_t n_slow = 0;
+  int64_t n_mid = 0;  // pencils: owned rows (y) of the peer's blocks
   int32_t device = 0;
   std::vector<void*> opened;  // IPC mappings to close
 };
@@ -47,12 +48,17 @@ struct st_comm {
   bool broken = false;                 // set after an NCCL error
   // LOCAL transport
   st_local_group* group = nullptr;
-  uint32_t* flags = nullptr;  // device: [0] ready-to-receive, [1] done from rank-1, [2] done from rank+1
+  uint32_t* flags = nullptr;  // device: [0] ready, [1]/[2] done from the low/high slab (or z) neighbour,
+                              // [3]/[4] done from the low/high y neighbour (pencils)
   uint32_t seq = 0;           // swaps issued so far (all ranks issue the same sequence)
   std::vector<double*> bound;  // buffers registered with st_comm_bind (same order on every rank)
   int64_t bound_n_slow = 0;    // owned slabs of this rank's bound buffers
-  // IPC transport: the two neighbours (0 = rank-1, 1 = rank+1), imported from their blobs
-  st_peer ipc_peer[2];
+  // IPC transport: the neighbour ranks imported from their blobs (rank, view)
+  std::vector<std::pair<int32_t, st_peer>> ipc_peers;
+  // pencil grid (st_comm_set_grid): grid_py ranks along y, nranks/grid_py along z,
+  // rank = iz * grid_py + iy; n_mid = this rank's owned rows. grid_py == 0: slabs.
+  int32_t grid_py = 0;
+  int64_t n_mid = 0;
 };
 
 struct st_local_group {
@@ -83,6 +89,11 @@ bool fused_halo_available(const st_comm* comm);
 st_status fused_halo_begin(st_comm* comm, double* dst, int64_t n, cudaStream_t main, void* rem_lo, void* rem_hi);
 st_status fused_halo_signal(st_comm* comm, cudaStream_t main);
 st_status fused_halo_join(st_comm* comm, cudaStream_t main);
+
+// Pencil halo swap (LOCAL/IPC): y rows of every plane with the y neighbours,
+// then whole planes with the z neighbours (corner ghosts included).
+st_status pencil_exchange_async(st_comm* comm, double* const* fields, int32_t nfields, int64_t nx, int64_t nyl,
+                                int64_t nzl, int64_t ldx, cudaStream_t main, bool join);
 
 st_status halo_plan(int32_t rank, int32_t nranks, int64_t n_slow_local, int64_t slab_pitch,
                     int32_t width, st_xfer sends[2], int32_t* nsend, st_xfer recvs[2],

@@ -71,6 +71,56 @@ def pw(rank, world, dev):
     return True
 
 
+def pencils(rank, world, dev, which):
+    py = 2 if world % 2 == 0 else world
+    pz = world // py
+    nx, ny, nz = 70, 37, 29
+    y0, nyl, z0, nzl = st.st_pencil_split(ny, nz, py, pz, rank)
+    iy, iz = rank % py, rank // py
+    comm = st.Comm.ipc_from_process_group(dev.index)
+    comm.set_grid(py, nyl)
+
+    def block(f):
+        t = torch.from_numpy(np.ascontiguousarray(f[z0:z0 + nzl + 2, y0:y0 + nyl + 2])).to(dev)
+        if iy > 0:
+            t[:, 0] = float("nan")
+        if iy < py - 1:
+            t[:, -1] = float("nan")
+        if iz > 0:
+            t[0] = float("nan")
+        if iz < pz - 1:
+            t[-1] = float("nan")
+        return t
+
+    if which == "j3":
+        g = si.jacobi3d_grid(nx, ny, nz)
+        a = block(g)
+        b = torch.full_like(a, float("nan"))
+        comm.bind_ipc([a, b], nzl)
+        r = st.st_jacobi3d_run_pencils(a, b, 7, comm=comm, nx=nx)
+        torch.cuda.synchronize()
+        got = [r.cpu().numpy()[1:nzl + 1, 1:nyl + 1, :nx + 2]]
+        want_full = [oracle.jacobi3d(g, 7, nx=nx)]
+        sl = (slice(z0 + 1, z0 + 1 + nzl), slice(y0 + 1, y0 + 1 + nyl), slice(0, nx + 2))
+    else:
+        d = si.pw_inputs(nx, ny, nz)
+        u, v, w = block(d["u"]), block(d["v"]), block(d["w"])
+        tz = [torch.from_numpy(np.ascontiguousarray(d[k][z0:z0 + nzl + 2])).to(dev)
+              for k in ("tzc1", "tzc2", "tzd1", "tzd2")]
+        outs = [torch.zeros_like(u) for _ in range(3)]
+        comm.bind_ipc([u, v, w], nzl)
+        st.st_pw_advect3d_pencils(u, v, w, *outs, d["tcx"], d["tcy"], *tz, comm=comm, nx=nx)
+        torch.cuda.synchronize()
+        got = [o.cpu().numpy()[1:nzl + 1, 1:nyl + 1, 1:nx + 1] for o in outs]
+        want_full = list(oracle.pw_advect3d(d["u"], d["v"], d["w"], d, nx=nx))
+        sl = (slice(z0 + 1, z0 + 1 + nzl), slice(y0 + 1, y0 + 1 + nyl), slice(1, nx + 1))
+    ok = all(np.array_equal(gg, ww[sl]) for gg, ww in zip(got, want_full))
+    oks = [None] * world
+    dist.all_gather_object(oks, ok)
+    comm.close()
+    return all(oks)
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     ngpu = torch.cuda.device_count()
@@ -80,7 +130,9 @@ def main():
     case = sys.argv[1]
     ok = {"j2_h1": lambda: jacobi2d(rank, world, dev, 1, 9, 1),
           "j2_h4_t4": lambda: jacobi2d(rank, world, dev, 4, 13, 4),
-          "pw": lambda: pw(rank, world, dev)}[case]()
+          "pw": lambda: pw(rank, world, dev),
+          "pen_j3": lambda: pencils(rank, world, dev, "j3"),
+          "pen_pw": lambda: pencils(rank, world, dev, "pw")}[case]()
     if rank == 0:
         print("IPC CASE", case, "OK" if ok else "FAILED", flush=True)
     dist.destroy_process_group()

@@ -129,7 +129,104 @@ def pw_case(P, nx, ny, nz):
     return ok
 
 
+def pencil_block(g, ny, nz, py, pz, r):
+    y0, nyl, z0, nzl = st.st_pencil_split(ny, nz, py, pz, r)
+    return np.ascontiguousarray(g[z0:z0 + nzl + 2, y0:y0 + nyl + 2]), y0, nyl, z0, nzl
+
+
+def pencils_j3_case(py, pz, nx, ny, nz, iters):
+    P = py * pz
+    g = si.jacobi3d_grid(nx, ny, nz)
+    comms = st.Comm.local_group(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    ranks = []
+    for r in range(P):
+        loc, y0, nyl, z0, nzl = pencil_block(g, ny, nz, py, pz, r)
+        a = torch.from_numpy(loc).cuda()
+        iy, iz = r % py, r // py
+        if iy > 0:
+            a[:, 0] = float("nan")
+        if iy < py - 1:
+            a[:, -1] = float("nan")
+        if iz > 0:
+            a[0] = float("nan")
+        if iz < pz - 1:
+            a[-1] = float("nan")
+        b = torch.full_like(a, float("nan"))
+        comms[r].set_grid(py, nyl)
+        comms[r].bind([a, b], nzl)
+        ranks.append((a, b, y0, nyl, z0, nzl))
+    torch.cuda.synchronize()
+    outs = []
+    for r in range(P):
+        a, b = ranks[r][:2]
+        with torch.cuda.stream(streams[r]):
+            outs.append(st.st_jacobi3d_run_pencils(a, b, iters, comm=comms[r], nx=nx))
+    torch.cuda.synchronize()
+    want = oracle.jacobi3d(g, iters, nx=nx)
+    ok = True
+    for r in range(P):
+        _, _, y0, nyl, z0, nzl = ranks[r]
+        got = outs[r].cpu().numpy()[1:nzl + 1, 1:nyl + 1, :nx + 2]
+        ok &= bool(np.array_equal(got, want[z0 + 1:z0 + 1 + nzl, y0 + 1:y0 + 1 + nyl, :nx + 2]))
+    for c in comms:
+        c.close()
+    return ok
+
+
+def pencils_pw_case(py, pz, nx, ny, nz):
+    P = py * pz
+    d = si.pw_inputs(nx, ny, nz)
+    want = oracle.pw_advect3d(d["u"], d["v"], d["w"], d)
+    comms = st.Comm.local_group(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    parts = []
+    for r in range(P):
+        y0, nyl, z0, nzl = st.st_pencil_split(ny, nz, py, pz, r)
+        iy, iz = r % py, r // py
+        g = {}
+        for k in "uvw":
+            blk = torch.from_numpy(np.ascontiguousarray(d[k][z0:z0 + nzl + 2, y0:y0 + nyl + 2])).cuda()
+            if iy > 0:
+                blk[:, 0] = float("nan")
+            if iy < py - 1:
+                blk[:, -1] = float("nan")
+            if iz > 0:
+                blk[0] = float("nan")
+            if iz < pz - 1:
+                blk[-1] = float("nan")
+            g[k] = blk
+        for k in ("tzc1", "tzc2", "tzd1", "tzd2"):
+            g[k] = torch.from_numpy(np.ascontiguousarray(d[k][z0:z0 + nzl + 2])).cuda()
+        outs = [torch.zeros_like(g["u"]) for _ in range(3)]
+        comms[r].set_grid(py, nyl)
+        comms[r].bind([g["u"], g["v"], g["w"]], nzl)
+        parts.append((g, outs, y0, nyl, z0, nzl))
+    torch.cuda.synchronize()
+    for r in range(P):
+        g, outs = parts[r][:2]
+        with torch.cuda.stream(streams[r]):
+            st.st_pw_advect3d_pencils(g["u"], g["v"], g["w"], *outs, d["tcx"], d["tcy"], g["tzc1"], g["tzc2"],
+                                      g["tzd1"], g["tzd2"], comm=comms[r])
+    torch.cuda.synchronize()
+    ok = True
+    for g, outs, y0, nyl, z0, nzl in parts:
+        for o, w in zip(outs, want):
+            ok &= bool(np.array_equal(o.cpu().numpy()[1:nzl + 1, 1:nyl + 1, 1:nx + 1],
+                                      w[z0 + 1:z0 + 1 + nzl, y0 + 1:y0 + 1 + nyl, 1:nx + 1]))
+    for c in comms:
+        c.close()
+    return ok
+
+
 CASES = {
+    "pen_j3_2x1": lambda: pencils_j3_case(2, 1, 70, 40, 33, 6),
+    "pen_j3_1x2": lambda: pencils_j3_case(1, 2, 70, 40, 33, 6),
+    "pen_j3_2x2": lambda: pencils_j3_case(2, 2, 66, 37, 31, 7),
+    "pen_j3_3x2": lambda: pencils_j3_case(3, 2, 40, 50, 21, 5),
+    "pen_pw_2x2": lambda: pencils_pw_case(2, 2, 70, 30, 22),
+    "pen_pw_3x2": lambda: pencils_pw_case(3, 2, 40, 33, 17),
+    "pen_pw_1x3": lambda: pencils_pw_case(1, 3, 40, 20, 25),
     "j2_h1": lambda: jacobi2d_case(2, 130, 200, 1, 9, 1),
     "j2_p3_h1": lambda: jacobi2d_case(3, 70, 101, 1, 7, 1),
     "j2_h4_t4": lambda: jacobi2d_case(2, 300, 260, 4, 13, 4),

@@ -19,9 +19,11 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("case", ["j2_h1", "j2_h4_t4", "pw"])
-@pytest.mark.parametrize("fused", ["1", "0"])
+CASES = [(w, c, f) for w in (2, 3) for c in ("j2_h1", "j2_h4_t4", "pw") for f in ("1", "0")]
+CASES += [(w, c, "1") for w in (2, 3, 4) for c in ("pen_j3", "pen_pw")]  # pencils: y-z process grids
+
+
+@pytest.mark.parametrize("world,case,fused", CASES)
 def test_ipc_multiprocess_equals_oracle(cuda_lib, world, case, fused):
     port = _port()
     procs = []
