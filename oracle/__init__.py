@@ -55,6 +55,8 @@ def _load():
     lib.or_pencils_jacobi3d.argtypes = [_dp, _dp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int]
     lib.or_pencils_pw.restype = ctypes.c_int
     lib.or_pencils_pw.argtypes = pw + [ctypes.c_int, ctypes.c_int]
+    lib.or_gauss_seidel2d.restype = ctypes.c_int
+    lib.or_gauss_seidel2d.argtypes = [_dp, _i64, _i64, _i64, _i64]
     lib.or_pw_points.restype = ctypes.c_int
     lib.or_pw_points.argtypes = [_dp] * 3 + [_i64] * 4 + [_dbl, _dbl] + [_dp] * 4 + [_dp, _i64, _dp]
     _lib = lib
@@ -204,3 +206,14 @@ def pencils_pw(u, v, w, co: dict, py: int, pz: int, nx: int | None = None):
     if rc < 0:
         raise ValueError("or_pencils_pw: bad arguments")
     return su, sv, sw
+
+
+def gauss_seidel2d(a0: np.ndarray, iters: int, nx: int | None = None) -> np.ndarray:
+    """`iters` in-place lexicographic Gauss-Seidel sweeps (Listing 1 literally)."""
+    _check2d(a0)
+    ny, ld = a0.shape[0] - 2, a0.shape[1]
+    nx = ld - 2 if nx is None else nx
+    a = a0.copy()
+    if _load().or_gauss_seidel2d(a.ctypes.data, nx, ny, ld, iters) < 0:
+        raise ValueError("or_gauss_seidel2d: bad arguments")
+    return a

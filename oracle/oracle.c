@@ -35,6 +35,11 @@
  *                      (slowest index first, as Listing 1 orders i before j),
  *                      then / 6.0 (5 adds + 1 divide = 6 flops).
  *   or_jacobi3d_slabs  z-slab decomposition of or_jacobi3d (1 ghost plane).
+ *   or_gauss_seidel2d  PAPER.md:98-104 Listing 1 taken literally: the Fortran loop
+ *                      nest updates `data` IN PLACE, i (= y) outer, j (= x)
+ *                      inner, so (y-1, x) and (y, x-1) are this sweep's values
+ *                      and (y+1, x), (y, x+1) the previous sweep's
+ *                      (lexicographic Gauss-Seidel).
  *   or_pencils_jacobi3d / or_pencils_pw
  *                      2-D (y, z) process grid ("decompose the 3D space into
  *                      two dimensions"): Py x Pz blocks with one
@@ -554,5 +559,23 @@ int or_pencils_pw(const double* u, const double* v, const double* w, double* su,
   double* gout[3] = {su, sv, sw};
   for (int c = 0; c < 3; ++c) pencil_gather(B, py, pz, 3 + c, gout[c], ny, nx, ldx);
   pencils_free(B, py * pz);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Lexicographic in-place Gauss-Seidel (Listing 1 literally, NEXT #4)          */
+/* ------------------------------------------------------------------------- */
+
+/* `iters` in-place sweeps of a (rows 0..ny+1) x ld field; ring untouched. */
+int or_gauss_seidel2d(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters) {
+  if (!a || nx < 1 || ny < 1 || ld < nx + 2 || iters < 0) return -1;
+  for (int64_t it = 0; it < iters; ++it)
+    for (int64_t y = 1; y <= ny; ++y)     /* do i = 2, 255 */
+      for (int64_t x = 1; x <= nx; ++x) { /* do j = 2, 255 */
+        double sum = a[IDX2(y - 1, x, ld)] + a[IDX2(y + 1, x, ld)];
+        sum = sum + a[IDX2(y, x - 1, ld)];
+        sum = sum + a[IDX2(y, x + 1, ld)];
+        a[IDX2(y, x, ld)] = sum * 0.25;
+      }
   return 0;
 }

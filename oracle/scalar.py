@@ -71,6 +71,17 @@ def jacobi2d(a, iters, quarter):
     return cur
 
 
+def gauss_seidel2d(a, iters, quarter):
+    """Listing 1 executed literally (in place, i outer, j inner) on a list-of-lists grid."""
+    ny, nx = len(a) - 2, len(a[0]) - 2
+    cur = [row[:] for row in a]
+    for _ in range(iters):
+        for y in range(1, ny + 1):
+            for x in range(1, nx + 1):
+                cur[y][x] = jacobi_point(cur[y - 1][x], cur[y + 1][x], cur[y][x - 1], cur[y][x + 1], quarter)
+    return cur
+
+
 def pw_point(U, V, W, z, tcx, tcy, tzc1, tzc2, tzd1, tzd2):
     """PW advection at one point (R6). U(dz,dy,dx) etc. are accessors
     relative to the point; tz* are the values at plane z. Returns (su, sv, sw)."""
