@@ -232,6 +232,18 @@ st_status st_jacobi2d_run(double* a, double* b, int64_t nx, int64_t ny_local, in
                           int32_t halo, int64_t iters, int32_t tblock, st_comm* comm,
                           void* cuda_stream, int32_t* result_in_b);
 
+/* Listing 1 taken literally (R22; NEXT #4): `iters`
+ * IN-PLACE lexicographic Gauss-Seidel sweeps of `a` ((ny+2) rows x ld, ring =
+ * Dirichlet): rows in increasing y, columns in increasing x, each point
+ *     a[y][x] = (((a[y-1][x] + a[y+1][x]) + a[y][x-1]) + a[y][x+1]) * 0.25
+ * with the values the sequential loop sees (N, W already updated). Bitwise the
+ * sequential loop nest. `workspace` = st_gauss_seidel2d_workspace_bytes(ny)
+ * bytes of caller-owned device memory (progress words of the wavefront).
+ * ST_ENOTSUP if ceil(ny/32) warps cannot all be resident on the device. */
+int64_t st_gauss_seidel2d_workspace_bytes(int64_t ny);
+st_status st_gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters, void* workspace,
+                                int64_t workspace_bytes, void* cuda_stream);
+
 /* ------------------------------------------------------------------------ */
 /* 3-D 7-point Jacobi (the paper's benchmark 1)                 */
 /* ------------------------------------------------------------------------ */

@@ -78,6 +78,8 @@ _SIGS = {
     "st_jacobi3d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i64, _i32, _vp, _vp,
                                        ctypes.POINTER(_i32)]),
     "st_selftest_div6": (ctypes.c_int, [_vp, _i64, _vp, _vp]),
+    "st_gauss_seidel2d_workspace_bytes": (ctypes.c_int64, [_i64]),
+    "st_gauss_seidel2d_run": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp]),
     "st_comm_set_grid": (ctypes.c_int, [_vp, _i32, _i64]),
     "st_pencil_split": (ctypes.c_int, [_i64, _i64, _i32, _i32, _i32] + [ctypes.POINTER(_i64)] * 4),
     "st_jacobi3d_run_pencils": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp,
@@ -370,6 +372,24 @@ def st_halo_exchange(comm: Comm, fields, n_slow_local: int, slab_pitch: int, wid
                                   _stream_ptr(stream)), "st_halo_exchange")
 
 
+def st_gauss_seidel2d_run(a, iters: int, nx: int | None = None, workspace=None, stream=None):
+    """`iters` in-place lexicographic Gauss-Seidel sweeps of a (ny+2, ld) float64 CUDA tensor
+    (Listing 1 literally). Returns a."""
+    import torch
+    _f64_cuda(a, "a")
+    if a.dim() != 2 or a.stride(1) != 1:
+        raise ValueError("a: 2-D row-major tensor")
+    ny, ld = a.shape[0] - 2, a.stride(0)
+    nx = a.shape[1] - 2 if nx is None else nx
+    need = int(lib().st_gauss_seidel2d_workspace_bytes(ny))
+    if workspace is None:
+        workspace = torch.empty(max(1, need // 8), dtype=torch.int64, device=a.device)
+    _check(lib().st_gauss_seidel2d_run(a.data_ptr(), nx, ny, ld, iters, workspace.data_ptr(),
+                                       workspace.numel() * workspace.element_size(), _stream_ptr(stream)),
+           "st_gauss_seidel2d_run")
+    return a
+
+
 def st_selftest_div6(x) -> int:
     """Number of x (float64 CUDA tensor) where the kernels' fast x/6 differs from IEEE division."""
     import torch
@@ -382,5 +402,6 @@ def st_selftest_div6(x) -> int:
 # Friendlier aliases
 jacobi2d = st_jacobi2d_run
 jacobi3d = st_jacobi3d_run
+gauss_seidel2d = st_gauss_seidel2d_run
 pw_advect3d = st_pw_advect3d
 halo_exchange = st_halo_exchange

@@ -59,6 +59,14 @@ st_status ddiv6_selftest(const double* x, int64_t n, unsigned long long* mismatc
 st_status jacobi3d_copy_faces(const double* src, double* dst, int64_t nx, int64_t ny, int64_t ldx, int64_t z_lo,
                               int64_t z_hi, cudaStream_t s);
 
+// ------------------------------------------------------------ Gauss-Seidel 2-D ---
+// `iters` in-place lexicographic sweeps (Listing 1 literally); `progress` =
+// gauss_seidel2d_workspace_bytes(ny) of device scratch.
+st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters,
+                             unsigned long long* progress, cudaStream_t s);
+int64_t gauss_seidel2d_workspace_bytes(int64_t ny);
+st_status gauss_seidel2d_preload();
+
 // ------------------------------------------------------------ PW 3-D ---
 struct PwArgs {
   const double *u, *v, *w;
@@ -87,6 +95,7 @@ st_status jacobi3d_preload();
 st_status pw_advect3d_preload();
 inline st_status preload_kernels() {
   ST_TRY(jacobi2d_preload());
+  ST_TRY(gauss_seidel2d_preload());
   ST_TRY(jacobi3d_preload());
   return pw_advect3d_preload();
 }
