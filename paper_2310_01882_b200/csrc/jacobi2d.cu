@@ -346,7 +346,7 @@ __device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][2], const int k, Quad s
   return s;
 }
 
-template <int T, int kMinBlocks>
+template <int T, int kMinBlocks, bool kPairSteady>
 __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
     jacobi2d_tb4_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
                         int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk, int64_t nstrips, int64_t ring_lo,
@@ -396,7 +396,43 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
   double* out = dst + x + (r_first - T) * ld;
   double* out2 = dst2 ? dst2 + x + (r_first - T + delta2) * ld : nullptr;
 
+  auto store_row = [&](double* p, const Quad& o) {
+    if (sta0 && sta1) stg2(p, o.a);
+    else if (sta0) p[0] = o.a.x;
+    else if (sta1) p[1] = o.a.y;
+    if (stb0 && stb1) stg2(p + 2, o.b);
+    else if (stb0) p[2] = o.b.x;
+    else if (stb1) p[3] = o.b.y;
+  };
+
   for (int64_t r0 = r_first; r0 <= r_end; r0 += G) {
+    // Steady state: both steps of the group store, touch no ring row and no ring
+    // column. They form ONE basic block (no per-step dispatch), so the scheduler
+    // can run step 1's level j beside step 0's level j+1 — twice the independent
+    // dependency chains of a single step (the kernel is latency-bound at 8 warps/SM).
+    if (kPairSteady && !col_ring && r0 + 1 <= r_end && r0 - T >= yc0 && r0 + 1 - T <= yc1 &&
+        r0 - T > ring_lo && r0 < ring_hi) {
+      static_assert(G == 2, "pair path");
+      const Quad s0 = buf[0];
+      buf[0].a = ldg2(spa + ((r0 + G <= r_load_last) ? loff : safe_off));
+      buf[0].b = ldg2(spb + ((r0 + G <= r_load_last) ? loff : safe_off));
+      loff += ld;
+      const Quad s1 = buf[1];
+      buf[1].a = ldg2(spa + ((r0 + 1 + G <= r_load_last) ? loff : safe_off));
+      buf[1].b = ldg2(spb + ((r0 + 1 + G <= r_load_last) ? loff : safe_off));
+      loff += ld;
+      const Quad o0 = tb4_levels<T, false, false>(st, 0, s0, r0, ring, ring_lo, ring_hi);
+      const Quad o1 = tb4_levels<T, false, false>(st, 1, s1, r0 + 1, ring, ring_lo, ring_hi);
+      store_row(out, o0);
+      store_row(out + ld, o1);
+      if (out2) {
+        store_row(out2, o0);
+        store_row(out2 + ld, o1);
+        out2 += 2 * ld;
+      }
+      out += 2 * ld;
+      continue;
+    }
 #pragma unroll
     for (int k = 0; k < G; ++k) {
       const int64_t r = r0 + k;
@@ -416,20 +452,8 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
                      : tb4_levels<T, false, false>(st, k, s0, r, ring, ring_lo, ring_hi);
       }
       if (r - T >= yc0 && r - T <= yc1) {
-        if (sta0 && sta1) stg2(out, o.a);
-        else if (sta0) out[0] = o.a.x;
-        else if (sta1) out[1] = o.a.y;
-        if (stb0 && stb1) stg2(out + 2, o.b);
-        else if (stb0) out[2] = o.b.x;
-        else if (stb1) out[3] = o.b.y;
-        if (out2) {  // fused halo swap: the same row into the neighbour's ghost row
-          if (sta0 && sta1) stg2(out2, o.a);
-          else if (sta0) out2[0] = o.a.x;
-          else if (sta1) out2[1] = o.a.y;
-          if (stb0 && stb1) stg2(out2 + 2, o.b);
-          else if (stb0) out2[2] = o.b.x;
-          else if (stb1) out2[3] = o.b.y;
-        }
+        store_row(out, o);
+        if (out2) store_row(out2, o);  // fused halo swap: the same row into the neighbour's ghost row
       }
       out += ld;
       if (out2) out2 += ld;
@@ -454,12 +478,11 @@ st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int
   const int64_t nchunks = (rows + rpc - 1) / rpc;
   ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d tb: too many row chunks");
   dim3 grid((unsigned)blocks_x, (unsigned)nchunks);
-  if (kOcc == 1)
-    jacobi2d_tb4_kernel<T, 1><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
-                                                              ring_hi, nrows_buf, rem.base, rem.delta);
-  else
-    jacobi2d_tb4_kernel<T, 2><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
-                                                              ring_hi, nrows_buf, rem.base, rem.delta);
+  static const int kPair = env_int("ST_JACOBI_TB4_PAIR", 1);
+  auto* kern = kOcc == 1 ? (kPair ? jacobi2d_tb4_kernel<T, 1, true> : jacobi2d_tb4_kernel<T, 1, false>)
+                         : (kPair ? jacobi2d_tb4_kernel<T, 2, true> : jacobi2d_tb4_kernel<T, 2, false>);
+  kern<<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo, ring_hi, nrows_buf,
+                                       rem.base, rem.delta);
   ST_LAUNCHED();
   return ST_OK;
 }
@@ -510,14 +533,22 @@ st_status jacobi2d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 1>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 3>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, true>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2, true>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, true>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2, true>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, true>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2, true>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, true>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, true>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, false>));
   return ST_OK;
 }
 
