@@ -346,13 +346,14 @@ __device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][2], const int k, Quad s
   return s;
 }
 
-template <int T, int kMinBlocks, bool kPairSteady>
+template <int T, int kMinBlocks, int G>
 __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
     jacobi2d_tb4_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
                         int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk, int64_t nstrips, int64_t ring_lo,
                         int64_t ring_hi, int64_t nrows_buf, double* __restrict__ dst2, int64_t delta2) {
   static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
-  constexpr int kCols = 128, kStride = kCols - 2 * T, G = 2;
+  static_assert(G % 2 == 0, "row-slot renaming needs an even group");
+  constexpr int kCols = 128, kStride = kCols - 2 * T;
   const int lane = threadIdx.x & 31;
   const int64_t strip = (int64_t)blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
   if (strip >= nstrips) return;
@@ -406,31 +407,31 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
   };
 
   for (int64_t r0 = r_first; r0 <= r_end; r0 += G) {
-    // Steady state: both steps of the group store, touch no ring row and no ring
-    // column. They form ONE basic block (no per-step dispatch), so the scheduler
-    // can run step 1's level j beside step 0's level j+1 — twice the independent
-    // dependency chains of a single step (the kernel is latency-bound at 8 warps/SM).
-    if (kPairSteady && !col_ring && r0 + 1 <= r_end && r0 - T >= yc0 && r0 + 1 - T <= yc1 &&
-        r0 - T > ring_lo && r0 < ring_hi) {
-      static_assert(G == 2, "pair path");
-      const Quad s0 = buf[0];
-      buf[0].a = ldg2(spa + ((r0 + G <= r_load_last) ? loff : safe_off));
-      buf[0].b = ldg2(spb + ((r0 + G <= r_load_last) ? loff : safe_off));
-      loff += ld;
-      const Quad s1 = buf[1];
-      buf[1].a = ldg2(spa + ((r0 + 1 + G <= r_load_last) ? loff : safe_off));
-      buf[1].b = ldg2(spb + ((r0 + 1 + G <= r_load_last) ? loff : safe_off));
-      loff += ld;
-      const Quad o0 = tb4_levels<T, false, false>(st, 0, s0, r0, ring, ring_lo, ring_hi);
-      const Quad o1 = tb4_levels<T, false, false>(st, 1, s1, r0 + 1, ring, ring_lo, ring_hi);
-      store_row(out, o0);
-      store_row(out + ld, o1);
-      if (out2) {
-        store_row(out2, o0);
-        store_row(out2 + ld, o1);
-        out2 += 2 * ld;
+    // Steady state: every step of the group stores, touches no ring row and no
+    // ring column. The G steps form ONE basic block (no per-step dispatch), so the
+    // scheduler can run step k+1's level j beside step k's level j+1 — G times the
+    // independent dependency chains of one step (the kernel is latency-bound at
+    // 8 warps/SM). A shared-memory cp.async row ring (prefetch 8-16 rows ahead
+    // instead of G) measured 16-25 % slower and was dropped.
+    if (!col_ring && r0 + G - 1 <= r_end && r0 - T >= yc0 && r0 + G - 1 - T <= yc1 && r0 - T > ring_lo &&
+        r0 + G - 2 < ring_hi) {
+      Quad o[G];
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        const Quad s0 = buf[k];
+        const int64_t off = (r0 + k + G <= r_load_last) ? loff : safe_off;
+        buf[k].a = ldg2(spa + off);
+        buf[k].b = ldg2(spb + off);
+        loff += ld;
+        o[k] = tb4_levels<T, false, false>(st, k, s0, r0 + k, ring, ring_lo, ring_hi);
       }
-      out += 2 * ld;
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        store_row(out + k * ld, o[k]);
+        if (out2) store_row(out2 + k * ld, o[k]);
+      }
+      out += G * ld;
+      if (out2) out2 += G * ld;
       continue;
     }
 #pragma unroll
@@ -478,9 +479,10 @@ st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int
   const int64_t nchunks = (rows + rpc - 1) / rpc;
   ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d tb: too many row chunks");
   dim3 grid((unsigned)blocks_x, (unsigned)nchunks);
-  static const int kPair = env_int("ST_JACOBI_TB4_PAIR", 1);
-  auto* kern = kOcc == 1 ? (kPair ? jacobi2d_tb4_kernel<T, 1, true> : jacobi2d_tb4_kernel<T, 1, false>)
-                         : (kPair ? jacobi2d_tb4_kernel<T, 2, true> : jacobi2d_tb4_kernel<T, 2, false>);
+  // G = steps per group: 2 (measured best at T=8; 4 needs more than 255 registers)
+  static const int kG = env_int("ST_JACOBI_TB4_G", 2);
+  auto* kern = kOcc == 1 ? (kG == 4 ? jacobi2d_tb4_kernel<T, 1, 4> : jacobi2d_tb4_kernel<T, 1, 2>)
+                         : (kG == 4 ? jacobi2d_tb4_kernel<T, 2, 4> : jacobi2d_tb4_kernel<T, 2, 2>);
   kern<<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo, ring_hi, nrows_buf,
                                        rem.base, rem.delta);
   ST_LAUNCHED();
@@ -533,22 +535,22 @@ st_status jacobi2d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 1>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 3>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, true>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, false>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2, true>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2, false>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, true>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, false>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2, true>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2, false>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, true>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, false>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2, true>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2, false>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, true>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, false>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, true>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, 4>));
   return ST_OK;
 }
 
