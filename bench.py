@@ -208,6 +208,8 @@ def main():
     ap.add_argument("--no-pw", action="store_true")
     ap.add_argument("--no-j3", action="store_true")
     ap.add_argument("--j3-sweeps", type=int, default=100, help="3-D 7-point Jacobi sweeps timed (512^3)")
+    ap.add_argument("--no-gs", action="store_true")
+    ap.add_argument("--gs-sweeps", type=int, default=100, help="in-place Gauss-Seidel sweeps timed (16384^2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-sweeps", type=int, default=20)
@@ -444,6 +446,40 @@ def main():
                                   "kind": "oracle", "sample": f"2 sweeps of the 512^3 grid; {dt:.2f} s"}
         del A3, B3
 
+    # ------------------------------------------------------------------ in-place Gauss-Seidel (NEXT #4)
+    gs = None
+    if world == 1 and not args.no_gs:
+        ngs = 16384
+        ags = torch.from_numpy(si.jacobi2d_grid(ngs, ngs)).to(dev)
+        ws = torch.empty(int(st.lib().st_gauss_seidel2d_workspace_bytes(ngs)) // 8 + 1, dtype=torch.int64, device=dev)
+        st.st_gauss_seidel2d_run(ags, 1, workspace=ws)  # warm-up (module load)
+        torch.cuda.synchronize()
+        gl0 = st.launch_count()
+        ev0.record(stream)
+        st.st_gauss_seidel2d_run(ags, args.gs_sweeps, workspace=ws)
+        ev1.record(stream)
+        ev1.synchronize()
+        gs_launches = st.launch_count() - gl0
+        gs_ms = ev0.elapsed_time(ev1)
+        gs_gbs = JACOBI_BYTES_PER_PT * ngs * ngs * args.gs_sweeps / (gs_ms / 1e3) / 1e9
+        gs = {"workload": f"gauss_seidel2d_{ngs}x{ngs}_fp64_{args.gs_sweeps}sweeps_inplace_lexicographic",
+              "value": round(ngs * ngs * args.gs_sweeps / (gs_ms / 1e3) / 1e9, 3), "unit": UNIT,
+              "ms_per_step": round(gs_ms, 3), "sweeps_per_launch": args.gs_sweeps, "gpu_launches": gs_launches,
+              "roofline": {"bound": "hbm", "kernel": "gauss_seidel2d_kernel", "achieved": round(gs_gbs, 1),
+                           "peak": hbm_peak, "unit": "GB/s", "frac": round(gs_gbs / hbm_peak, 4),
+                           "traffic": ncu_traffic("gauss_seidel2d_kernel"), "bytes_per_pt_per_sweep":
+                           JACOBI_BYTES_PER_PT, "peak_source": peak_src}}
+        if not args.no_cpu:
+            import oracle
+            a_small = si.jacobi2d_grid(ngs, 2048)  # a 2048-row band of the same grid recipe
+            t0 = time.perf_counter()
+            oracle.gauss_seidel2d(a_small, 1)
+            dt = time.perf_counter() - t0
+            gs["cpu_baseline"] = {"value": round(ngs * 2048 / dt / 1e9, 4), "unit": UNIT, "cores": 1,
+                                  "kind": "oracle", "sample": f"1 sweep of a 16384x2048 grid (sequential by "
+                                  f"definition); {dt:.2f} s"}
+        del ags, ws
+
     # ------------------------------------------------------------------ C1: 64^2 + ring, 100 sweeps (latency-bound)
     c1 = None
     if world == 1:
@@ -494,6 +530,7 @@ def main():
             "cpu_baseline": cpu,
             "pw_advect3d": pw,
             "jacobi3d": j3,
+            "gauss_seidel2d": gs,
             "c1": c1,
         }
         print(json.dumps(out), flush=True)

@@ -20,8 +20,8 @@
 //    below's top row of the PREVIOUS sweep (wait until the strip below has
 //    published it for sweep s-1; the strip below cannot overwrite it for sweep
 //    s before this strip publishes the column, so no extra guard is needed).
-//    Waits and publications happen once per chunk of kChunk columns
-//    (ld.acquire / st.release at GPU scope; cross-strip data via L2).
+//    Waits and publications happen between groups of kPf columns
+//    (relaxed polling + ld.acquire / st.release at GPU scope; cross-strip data via L2).
 //  * All sweeps run in ONE launch; strips drift into a diagonal pipeline across
 //    sweeps. Every strip's warp must be resident (checked at launch), so the
 //    spin-waits cannot deadlock.
@@ -34,26 +34,39 @@ namespace st {
 
 namespace {
 
-constexpr int kGsWarps = 4;    // strips per CTA
-constexpr int kChunk = 64;     // columns per progress publication / wait
-constexpr int kPrefetch = 8;   // own-row E values loaded this many steps ahead
+constexpr int kGsWarps = 4;  // strips per CTA
+constexpr int kPf = 32;      // steps per group = prefetch distance (own row E; N for lane 0, S for lane 31)
+static_assert(kPf >= 32, "refill columns must stay >= 1 without a check");
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void spin_until(const unsigned long long* p, unsigned long long need) {
-  while (ld_acquire(p) < need) __nanosleep(64);
 }
 
 // prog[2*I] = columns of strip I's bottom row finished (sweep-major: s*nx + x);
 // prog[2*I+1] = the same for its top row. Zeroed before the launch.
+//
+// A step is one dependent chain (a shuffle and 4 fp64 ops), so everything else
+// is kept off it: every value a step reads is loaded kPf steps ahead into
+// registers (the lane's own row; the row above for lane 0, the row below for
+// lane 31 — one array, the two lanes are distinct), the steps of a group are
+// straight-line code (no per-step branches, so the shuffles stay plain SHFL),
+// and progress waits/publications happen between groups, every kPub groups.
+// A wait polls with relaxed loads under a warp vote, then takes one acquire
+// load: an ld.acquire.gpu invalidates the SM's whole L1 (CCTL.IVALL), which
+// measured ruinous as a polling loop.
+template <int kPub>
 __global__ void __launch_bounds__(32 * kGsWarps)
-    gauss_seidel2d_kernel(double* __restrict__ a, int64_t nx, int64_t ny, int64_t ld, int64_t iters,
+    gauss_seidel2d_kernel(double* __restrict__ a, int nx, int64_t ny, int64_t ld, int64_t iters,
                           unsigned long long* __restrict__ prog, int64_t nstrips) {
   const int lane = threadIdx.x & 31;
   const int64_t I = (int64_t)blockIdx.x * kGsWarps + (threadIdx.x >> 5);
@@ -63,66 +76,85 @@ __global__ void __launch_bounds__(32 * kGsWarps)
   const bool ring = y == ny + 1;    // the bottom Dirichlet row: supplies S, never changes
   const bool live = real || ring;   // lanes beyond ny+1 only take part in the shuffles
   const bool top_lane = lane == 0, bottom_lane = lane == 31;
-  const bool has_above = I > 0;                          // row 0 is the Dirichlet ring otherwise
-  const bool has_below = I + 1 < nstrips;                // lane 31's S comes from strip I+1
-  double* row = a + (live ? y : 0) * ld;
-  const double* above = a + (32 * I) * ld;               // row y-1 of lane 0
-  const double* below = a + (32 * I + 33) * ld;          // row y+1 of lane 31
-  unsigned long long* my_bot = prog + 2 * I;
-  unsigned long long* my_top = prog + 2 * I + 1;
-  const unsigned long long* up_bot = prog + 2 * (I - 1);   // strip above, bottom row
-  const unsigned long long* dn_top = prog + 2 * (I + 1) + 1;  // strip below, top row
-  const int64_t nsteps = nx + 31;
+  const bool has_above = I > 0;              // row 0 is the Dirichlet ring otherwise
+  const bool has_below = I + 1 < nstrips;    // lane 31's S row belongs to strip I+1
+  const bool need_below = bottom_lane && real;
+  const bool pub_bot = real && (bottom_lane || y == ny);  // the strip's last real row
+  double* const row = a + (live ? y : 0) * ld;
+  const double* const above = a + (32 * I) * ld;       // row y-1 of lane 0
+  const double* const below = a + (32 * I + 33) * ld;   // row y+1 of lane 31
+  unsigned long long* const my_bot = prog + 2 * I;
+  unsigned long long* const my_top = prog + 2 * I + 1;
+  const unsigned long long* const up_bot = prog + 2 * (I - 1);     // strip above, bottom row
+  const unsigned long long* const dn_top = prog + 2 * (I + 1) + 1;  // strip below, top row
+  const int nsteps = nx + 31;
+  const int ngroups = (nsteps + kPf - 1) / kPf;
+  const int x0 = 1 - lane;  // this lane's column at step 0 (x = k + x0)
+  // refill at step k: own row column k + x0 + 1 + kPf (valid while <= nx + 1);
+  // lane 0: row above, column k + 1 + kPf; lane 31: row below, column k - 30 + kPf (valid while <= nx)
+  const int k_pf_max = live ? nx - x0 - kPf : -1;
+  const double* const nbr = top_lane ? above + 1 + kPf : below + kPf - 30;
+  const int k_nb_max = top_lane ? nx - 1 - kPf : need_below ? nx + 30 - kPf : -1;
 
   for (int64_t s = 0; s < iters; ++s) {
+    const unsigned long long base = (unsigned long long)(s * nx);
+    // Before group g (g % kPub == 0): the steps of groups g .. g+kPub-1 load the
+    // row above up to column (g+kPub+1)*kPf (this sweep) and the row below up to
+    // (g+kPub+1)*kPf - 31 (previous sweep; sweep 0 reads the initial values).
+    auto wait = [&](int g) {
+      const int lim = (g + kPub + 1) * kPf;
+      const unsigned long long need_t = base + (unsigned long long)min(nx, lim);
+      const int cb = min(nx, lim - 31);
+      const bool wt = top_lane && has_above;
+      const bool wb = need_below && has_below && s > 0 && cb >= 1;
+      const unsigned long long need_b = base - (unsigned long long)nx + (unsigned long long)cb;
+      bool ok = (!wt || ld_relaxed(up_bot) >= need_t) && (!wb || ld_relaxed(dn_top) >= need_b);
+      while (!__all_sync(0xffffffffu, ok)) {
+        __nanosleep(32);
+        ok = (!wt || ld_relaxed(up_bot) >= need_t) && (!wb || ld_relaxed(dn_top) >= need_b);
+      }
+      if (wt) (void)ld_acquire(up_bot);  // synchronizes with the release that published it
+      if (wb) (void)ld_acquire(dn_top);
+    };
+    wait(0);
     double res = row[0];  // W of column 1 = the Dirichlet column
-    double pf[kPrefetch];  // E values: old row entries at columns x+1 .. x+kPrefetch
+    double e_prev = res;  // the lane's old value at column x-1 (the ring row's "result")
+    double pf[kPf], pn[kPf];  // slot d <-> steps k == d (mod kPf)
 #pragma unroll
-    for (int d = 0; d < kPrefetch; ++d) {
-      const int64_t c = 1 - lane + 1 + d;  // column x_r(step 0) + 1 + d
+    for (int d = 0; d < kPf; ++d) {
+      const int c = x0 + 1 + d;  // E of this lane at step d
       pf[d] = (live && c >= 1 && c <= nx + 1) ? row[c] : 0.0;
+      const int cn = top_lane ? 1 + d : d - 30;  // N of lane 0 / S of lane 31 at step d
+      pn[d] = ((top_lane || need_below) && cn >= 1 && cn <= nx) ? __ldcg((top_lane ? above : below) + cn) : 0.0;
     }
-    for (int64_t k0 = 0; k0 < nsteps; k0 += kPrefetch) {
+    for (int g = 0; g < ngroups; ++g) {
+      const int k0 = g * kPf;
+      if (g > 0 && g % kPub == 0) wait(g);
+      double* const rp = row + (k0 + x0);  // this lane's column at step k0 (dereferenced only in range)
 #pragma unroll
-      for (int d = 0; d < kPrefetch; ++d) {
-        const int64_t k = k0 + d;
-        if (k >= nsteps) break;  // warp-uniform
-        const int64_t x = k - lane + 1;
-        const bool act = x >= 1 && x <= nx;
-        // chunk boundaries: wait for the neighbours' progress (the whole warp waits)
-        if (((k) % kChunk) == 0) {
-          if (top_lane && has_above) {  // strip above's bottom row, this sweep, columns x .. x+kChunk-1
-            const int64_t need_x = min(nx, k + (int64_t)kChunk);
-            spin_until(up_bot, (unsigned long long)(s * nx + need_x));
-          }
-        }
-        if (((k - 31) % kChunk) == 0 && k >= 31) {
-          if (bottom_lane && has_below && real) {  // strip below's top row, previous sweep
-            const int64_t need_x = min(nx, k - 31 + (int64_t)kChunk);
-            if (s > 0) spin_until(dn_top, (unsigned long long)((s - 1) * nx + need_x));
-          }
-        }
-        __syncwarp();
+      for (int d = 0; d < kPf; ++d) {
+        const int k = k0 + d;
+        const int x = k + x0;
+        const bool act = (unsigned)(x - 1) < (unsigned)nx;
         const double e = pf[d];
         const double n_sh = __shfl_up_sync(0xffffffffu, res, 1);   // lane r-1's result of step k-1
         const double s_sh = __shfl_down_sync(0xffffffffu, e, 1);  // lane r+1's old value at this x
-        if (act && real) {
-          const double nn = top_lane ? (has_above ? __ldcg(above + x) : above[x]) : n_sh;
-          const double ss = bottom_lane ? __ldcg(below + x) : s_sh;
-          const double v = dmul(dadd(dadd(dadd(nn, ss), res), e), 0.25);
-          row[x] = v;
-          res = v;
-        } else if (act && ring) {
-          res = row[x];  // Dirichlet row: its "result" is its value
-        }
-        // refill the slot with the old value kPrefetch columns ahead
-        const int64_t c = x + 1 + kPrefetch;
-        pf[d] = (live && c >= 1 && c <= nx + 1) ? row[c] : 0.0;
-        // publish progress at chunk ends and at the end of the row
-        if (act && real && (x % kChunk == 0 || x == nx)) {
-          if (bottom_lane || y == ny) st_release(my_bot, (unsigned long long)(s * nx + x));
-          if (top_lane) st_release(my_top, (unsigned long long)(s * nx + x));
-        }
+        const double nn = top_lane ? pn[d] : n_sh;
+        const double ss = bottom_lane ? pn[d] : s_sh;
+        const double v = dmul(dadd(dadd(dadd(nn, ss), res), e), 0.25);
+        const bool upd = act && real;
+        if (upd) rp[d] = v;
+        res = upd ? v : ((act && ring) ? e_prev : res);  // Dirichlet row: its "result" is its value
+        e_prev = e;
+        // out-of-range slots keep stale values: only lanes past the grid edge read them
+        if (k <= k_pf_max) pf[d] = rp[d + 1 + kPf];
+        if (k <= k_nb_max) pn[d] = __ldcg(nbr + k);
+      }
+      if ((g + 1) % kPub == 0 || g + 1 == ngroups) {  // publish the finished columns
+        const int k_last = k0 + kPf - 1;
+        if (top_lane) st_release(my_top, base + (unsigned long long)min(nx, k_last + 1));
+        const int cb = min(nx, k_last + x0);
+        if (pub_bot && cb >= 1) st_release(my_bot, base + (unsigned long long)cb);
       }
     }
   }
@@ -132,16 +164,18 @@ __global__ void __launch_bounds__(32 * kGsWarps)
 
 st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters,
                              unsigned long long* progress, cudaStream_t s) {
+  ST_RETURN_IF(nx > (1 << 30), ST_ENOTSUP, "gauss_seidel2d: nx = %lld > 2^30", (long long)nx);
   const int64_t nstrips = (ny + 31) / 32;
+  static const int kPub = env_int("ST_GS_PUB", 1);  // groups of kPf columns per progress publication
+  auto* kern = kPub == 1 ? gauss_seidel2d_kernel<1> : kPub == 4 ? gauss_seidel2d_kernel<4> : gauss_seidel2d_kernel<2>;
   // every strip's warp must be resident at once (the strips spin on each other)
-  int per_sm = 0, dev = 0;
-  ST_CHECK_CUDA(cudaGetDevice(&dev));
-  ST_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gauss_seidel2d_kernel, 32 * kGsWarps, 0));
+  int per_sm = 0;
+  ST_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kGsWarps, 0));
   const int64_t blocks = (nstrips + kGsWarps - 1) / kGsWarps;
   ST_RETURN_IF(blocks > (int64_t)per_sm * num_sms(), ST_ENOTSUP,
                "gauss_seidel2d: %lld strips exceed the resident capacity (%d CTAs/SM)", (long long)nstrips, per_sm);
   ST_CHECK_CUDA(cudaMemsetAsync(progress, 0, (size_t)(2 * nstrips) * sizeof(unsigned long long), s));
-  gauss_seidel2d_kernel<<<(unsigned)blocks, 32 * kGsWarps, 0, s>>>(a, nx, ny, ld, iters, progress, nstrips);
+  kern<<<(unsigned)blocks, 32 * kGsWarps, 0, s>>>(a, (int)nx, ny, ld, iters, progress, nstrips);
   ST_LAUNCHED();
   return ST_OK;
 }
@@ -150,7 +184,9 @@ int64_t gauss_seidel2d_workspace_bytes(int64_t ny) { return 2 * ((ny + 31) / 32)
 
 st_status gauss_seidel2d_preload() {
   cudaFuncAttributes fa;
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_kernel));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_kernel<1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_kernel<2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_kernel<4>));
   return ST_OK;
 }
 

@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--sweeps", type=int, default=4)
 ap.add_argument("--apps", type=int, default=2)
 ap.add_argument("--tblock", type=int, default=1)
+ap.add_argument("--gs-sweeps", type=int, default=4)
 args = ap.parse_args()
 
 n = 16384
@@ -34,5 +35,9 @@ del g, outs
 a3 = torch.from_numpy(si.jacobi3d_grid(m, m, m)).cuda()
 b3 = torch.empty_like(a3)
 st.st_jacobi3d_run(a3, b3, args.apps)
+torch.cuda.synchronize()
+del a3, b3
+ag = torch.from_numpy(si.jacobi2d_grid(n, n)).cuda()
+st.st_gauss_seidel2d_run(ag, args.gs_sweeps)
 torch.cuda.synchronize()
 print("done")
