@@ -160,21 +160,216 @@ __global__ void __launch_bounds__(32 * kGsWarps)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tiled variant: the strip's rows are staged through shared memory in 32x32
+// tiles, so global traffic is whole 256-byte row segments (cp.async loads,
+// 16-byte stores) instead of one 8-byte access per lane and step to 32
+// different rows (which saturated the LSU / L2 request rate with 512 strips).
+// Lane r at step k still works on column x = k + 1 - r; it reads E (old value
+// at x+1) from the tile and writes its result at x into the tile — a diagonal
+// of the tile, conflict-free for a 32-double row pitch ((32r + c) mod 16 =
+// c mod 16 = (k - r) mod 16 distinct over 16 lanes).
+//
+// Tile m = columns [32m, 32m+32) of the strip's 32 rows (even start column:
+// 16-byte aligned for ld even). A warp keeps 4 tiles in flight: at the start of
+// group g (steps 32g..32g+31) tile g-2 is complete (lane 31 finished column
+// 32g-33 at step 32g-3): it is written back, its slot reloaded with tile g+2;
+// tiles g-1, g are being written, g+1 is read (E). Progress words count
+// columns written back to global memory (fence, then a relaxed flag store).
+constexpr int kTile = 32;
+constexpr int kRingTiles = 4;
+constexpr int kEpf = 8;  // steps of E prefetch from the tile (kTile % kEpf == 0)
+constexpr size_t kTiledSmem = (size_t)kRingTiles * kTile * kTile * sizeof(double);  // 32 KB per warp
+
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// One CTA = one warp = one strip (the strips spin on each other: all must be resident).
+// kPubT: tiles written back per progress publication (one GPU-scope fence each).
+template <int kPubT>
+__global__ void __launch_bounds__(32)
+    gauss_seidel2d_tiled_kernel(double* __restrict__ a, int nx, int64_t ny, int64_t ld, int64_t iters,
+                                unsigned long long* __restrict__ prog, int64_t nstrips) {
+  extern __shared__ __align__(16) double tiles[];  // [kRingTiles][32 rows][32 cols]
+  const int lane = threadIdx.x;
+  const int64_t I = blockIdx.x;
+  const int64_t y0 = 32 * I + 1;  // the strip's first row
+  const int64_t y = y0 + lane;
+  const bool real = y <= ny;
+  const bool ring = y == ny + 1;
+  const bool live = real || ring;
+  const bool top_lane = lane == 0, bottom_lane = lane == 31;
+  const bool has_above = I > 0;
+  const bool has_below = I + 1 < nstrips;
+  const bool need_below = bottom_lane && real;
+  const bool pub_bot = real && (bottom_lane || y == ny);
+  const double* const above = a + (y0 - 1) * ld;
+  const double* const below = a + (y0 + 32) * ld;
+  unsigned long long* const my_bot = prog + 2 * I;
+  unsigned long long* const my_top = prog + 2 * I + 1;
+  const unsigned long long* const up_bot = prog + 2 * (I - 1);
+  const unsigned long long* const dn_top = prog + 2 * (I + 1) + 1;
+  const int nsteps = nx + 31;
+  const int ngroups = (nsteps + kTile - 1) / kTile;
+  const int ntiles = (nx + 2 + kTile - 1) / kTile;
+  const int x0 = 1 - lane;
+  const int k_nb_max = top_lane ? nx - 1 - kPf : need_below ? nx + 30 - kPf : -1;
+  const double* const nbr = top_lane ? above + 1 + kPf : below + kPf - 30;
+  // tile copies: lane l moves the 16-byte chunk (l & 15) of tile rows 2i + (l >> 4), i = 0..15
+  const int cr = lane >> 4, cc = 2 * (lane & 15);
+  double* const my_tile_row = tiles + lane * kTile;  // this lane's row inside tile slot 0
+
+  auto tile_load = [&](int m) {  // tile m -> slot m % 4 (cp.async, one commit group)
+    double* slot = tiles + (m & (kRingTiles - 1)) * (kTile * kTile);
+    const int col = m * kTile + cc;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int r = 2 * i + cr;
+      if (col <= nx + 1 && y0 + r <= ny + 1) cp_async16_cg(slot + r * kTile + cc, a + (y0 + r) * ld + col);
+    }
+  };
+  auto tile_store = [&](int m) {  // rows 1..ny of tile m back to global (16-byte stores)
+    const double* slot = tiles + (m & (kRingTiles - 1)) * (kTile * kTile);
+    const int col = m * kTile + cc;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int r = 2 * i + cr;
+      if (col <= nx + 1 && y0 + r <= ny)
+        *reinterpret_cast<double2*>(a + (y0 + r) * ld + col) = *reinterpret_cast<const double2*>(slot + r * kTile + cc);
+    }
+  };
+  auto publish = [&](unsigned long long base, int col_done) {  // columns 1..col_done of both edge rows are in global
+    __threadfence();
+    __syncwarp();
+    if (col_done >= 1) {
+      if (top_lane) st_relaxed(my_top, base + (unsigned long long)min(nx, col_done));
+      if (pub_bot) st_relaxed(my_bot, base + (unsigned long long)min(nx, col_done));
+    }
+  };
+
+  for (int64_t s = 0; s < iters; ++s) {
+    const unsigned long long base = (unsigned long long)(s * nx);
+    // before group g (every kPubT groups): groups g .. g+kPubT-1 read the row above up
+    // to column (g+kPubT+1)*32 (this sweep) and the row below up to that - 31 (previous sweep)
+    auto wait = [&](int g) {
+      const int lim = (g + kPubT + 1) * kPf;
+      const unsigned long long need_t = base + (unsigned long long)min(nx, lim);
+      const int cb = min(nx, lim - 31);
+      const bool wt = top_lane && has_above;
+      const bool wb = need_below && has_below && s > 0 && cb >= 1;
+      const unsigned long long need_b = base - (unsigned long long)nx + (unsigned long long)cb;
+      bool ok = (!wt || ld_relaxed(up_bot) >= need_t) && (!wb || ld_relaxed(dn_top) >= need_b);
+      while (!__all_sync(0xffffffffu, ok)) {
+        __nanosleep(32);
+        ok = (!wt || ld_relaxed(up_bot) >= need_t) && (!wb || ld_relaxed(dn_top) >= need_b);
+      }
+      if (wt) (void)ld_acquire(up_bot);
+      if (wb) (void)ld_acquire(dn_top);
+    };
+    tile_load(0);
+    cp_async_commit_group();
+    if (ntiles > 1) tile_load(1);
+    cp_async_commit_group();
+    wait(0);
+    double pn[kPf];
+#pragma unroll
+    for (int d = 0; d < kPf; ++d) {
+      const int cn = top_lane ? 1 + d : d - 30;
+      pn[d] = ((top_lane || need_below) && cn >= 1 && cn <= nx) ? __ldcg((top_lane ? above : below) + cn) : 0.0;
+    }
+    cp_async_wait_group<1>();  // tile 0
+    __syncwarp();
+    double res = my_tile_row[0];  // W of column 1 = the Dirichlet column
+    double e_prev = res;
+    // E values are read kEpf steps ahead from the tile: the compiler cannot prove
+    // that the read of column x+1 does not alias the store to column x of the
+    // step before, so an in-step read would put LDS latency on the chain
+    auto toff = [&](int c) { return lane * kTile + ((c >> 5) & (kRingTiles - 1)) * (kTile * kTile) + (c & 31); };
+    double ep[kEpf];
+#pragma unroll
+    for (int d = 0; d < kEpf; ++d) ep[d] = tiles[toff(x0 + 1 + d)];
+    for (int g = 0; g < ngroups; ++g) {
+      if (g >= 2) {  // tile g-2 is complete: write it back (and publish every kPubT tiles)
+        __syncwarp();
+        tile_store(g - 2);
+        __syncwarp();
+        if ((g - 2) % kPubT == kPubT - 1) publish(base, (g - 2) * kTile + kTile - 1);
+      }
+      if (g + 2 < ntiles) tile_load(g + 2);
+      cp_async_commit_group();
+      cp_async_wait_group<1>();  // tiles <= g+1 have landed
+      __syncwarp();
+      if (g > 0 && g % kPubT == 0) wait(g);
+      const int k0 = g * kTile;
+#pragma unroll
+      for (int d = 0; d < kTile; ++d) {
+        const int k = k0 + d;
+        const int x = k + x0;
+        const bool act = (unsigned)(x - 1) < (unsigned)nx;
+        const double e = ep[d % kEpf];
+        ep[d % kEpf] = tiles[toff(x + 1 + kEpf)];
+        const double n_sh = __shfl_up_sync(0xffffffffu, res, 1);
+        const double s_sh = __shfl_down_sync(0xffffffffu, e, 1);
+        const double nn = top_lane ? pn[d] : n_sh;
+        const double ss = bottom_lane ? pn[d] : s_sh;
+        const double v = dmul(dadd(dadd(dadd(nn, ss), res), e), 0.25);
+        const bool upd = act && real;
+        if (upd) tiles[toff(x)] = v;
+        res = upd ? v : ((act && ring) ? e_prev : res);
+        e_prev = e;
+        if (k <= k_nb_max) pn[d] = __ldcg(nbr + k);
+      }
+    }
+    // flush the tiles not yet written back, then publish the whole row
+    __syncwarp();
+    for (int m = max(0, ngroups - 2); m < ntiles; ++m) tile_store(m);
+    __syncwarp();
+    publish(base, nx);
+    cp_async_wait_group<0>();
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters,
                              unsigned long long* progress, cudaStream_t s) {
   ST_RETURN_IF(nx > (1 << 30), ST_ENOTSUP, "gauss_seidel2d: nx = %lld > 2^30", (long long)nx);
   const int64_t nstrips = (ny + 31) / 32;
+  // the tiled kernel moves 16-byte row chunks: even pitch, 16-byte aligned base
+  static const int kVariant = env_int("ST_GS_TILED", 1);
+  const bool tiled = kVariant != 0 && (ld % 2) == 0 && aligned16(a);
+  ST_CHECK_CUDA(cudaMemsetAsync(progress, 0, (size_t)(2 * nstrips) * sizeof(unsigned long long), s));
+  int per_sm = 0;
+  if (tiled) {
+    static const int kPubT = env_int("ST_GS_PUBT", 4);
+    auto* tk = kPubT == 1   ? gauss_seidel2d_tiled_kernel<1>
+               : kPubT == 2 ? gauss_seidel2d_tiled_kernel<2>
+               : kPubT == 8 ? gauss_seidel2d_tiled_kernel<8>
+                            : gauss_seidel2d_tiled_kernel<4>;
+    ST_CHECK_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTiledSmem));
+    ST_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tk, 32, kTiledSmem));
+    // every strip's warp must be resident at once (the strips spin on each other)
+    ST_RETURN_IF(nstrips > (int64_t)per_sm * num_sms(), ST_ENOTSUP,
+                 "gauss_seidel2d: %lld strips exceed the resident capacity (%d CTAs/SM)", (long long)nstrips, per_sm);
+    tk<<<(unsigned)nstrips, 32, kTiledSmem, s>>>(a, (int)nx, ny, ld, iters, progress, nstrips);
+    ST_LAUNCHED();
+    return ST_OK;
+  }
   static const int kPub = env_int("ST_GS_PUB", 1);  // groups of kPf columns per progress publication
   auto* kern = kPub == 1 ? gauss_seidel2d_kernel<1> : kPub == 4 ? gauss_seidel2d_kernel<4> : gauss_seidel2d_kernel<2>;
-  // every strip's warp must be resident at once (the strips spin on each other)
-  int per_sm = 0;
   ST_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kGsWarps, 0));
   const int64_t blocks = (nstrips + kGsWarps - 1) / kGsWarps;
   ST_RETURN_IF(blocks > (int64_t)per_sm * num_sms(), ST_ENOTSUP,
                "gauss_seidel2d: %lld strips exceed the resident capacity (%d CTAs/SM)", (long long)nstrips, per_sm);
-  ST_CHECK_CUDA(cudaMemsetAsync(progress, 0, (size_t)(2 * nstrips) * sizeof(unsigned long long), s));
   kern<<<(unsigned)blocks, 32 * kGsWarps, 0, s>>>(a, (int)nx, ny, ld, iters, progress, nstrips);
   ST_LAUNCHED();
   return ST_OK;
@@ -187,6 +382,10 @@ st_status gauss_seidel2d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_kernel<1>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_kernel<2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_kernel<4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_tiled_kernel<1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_tiled_kernel<2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_tiled_kernel<4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_tiled_kernel<8>));
   return ST_OK;
 }
 
