@@ -20,6 +20,8 @@ def run_gs(st, a_np, iters, nx=None):
 SHAPES = [  # (nx, ny, ld, iters): strips of 32 rows, chunks of 64 columns, ragged tails
     (1, 1, 4, 3), (5, 3, 8, 4), (64, 32, 66, 2), (65, 33, 68, 3), (130, 64, 132, 5), (200, 95, 202, 7),
     (129, 200, 132, 11), (300, 257, 302, 4), (1000, 130, 1002, 3),
+    # odd pitches: the register (non-tiled) kernel
+    (65, 33, 67, 3), (200, 95, 203, 5),
 ]
 
 
