@@ -20,7 +20,6 @@
 
 #include "common.cuh"
 #include "internal.h"
-#include "tma.cuh"
 
 namespace st {
 
@@ -317,16 +316,13 @@ struct Quad {
   double2 a, b;  // columns x, x+1 | x+2, x+3
 };
 
-// Levels J0 .. J0+TW-1 of the T-level pipeline for one step: level j turns
-// rows (n, c) of level j-1 plus the new row s into row r-j-1 of level j.
-template <int TW, int J0, bool kRows, bool kCols>
-__device__ __forceinline__ Quad tb4_range(Quad (&st)[TW][2], const int k, Quad s, int64_t r, const bool (&ring)[4],
-                                          int64_t ring_lo, int64_t ring_hi) {
+template <int T, bool kRows, bool kCols>
+__device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][2], const int k, Quad s, int64_t r, const bool (&ring)[4],
+                                           int64_t ring_lo, int64_t ring_hi) {
 #pragma unroll
-  for (int jj = 0; jj < TW; ++jj) {
-    const int j = J0 + jj;
-    const Quad n = st[jj][k & 1];
-    const Quad c = st[jj][(k + 1) & 1];
+  for (int j = 0; j < T; ++j) {
+    const Quad n = st[j][k & 1];
+    const Quad c = st[j][(k + 1) & 1];
     const double w = __shfl_up_sync(0xffffffffu, c.b.y, 1);
     const double e = __shfl_down_sync(0xffffffffu, c.a.x, 1);
     Quad o;
@@ -344,16 +340,10 @@ __device__ __forceinline__ Quad tb4_range(Quad (&st)[TW][2], const int k, Quad s
       const int64_t row = r - j - 1;
       if (row <= ring_lo || row >= ring_hi) o = c;
     }
-    st[jj][k & 1] = s;
+    st[j][k & 1] = s;
     s = o;
   }
   return s;
-}
-
-template <int T, bool kRows, bool kCols>
-__device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][2], const int k, Quad s, int64_t r, const bool (&ring)[4],
-                                           int64_t ring_lo, int64_t ring_hi) {
-  return tb4_range<T, 0, kRows, kCols>(st, k, s, r, ring, ring_lo, ring_hi);
 }
 
 template <int T, int kMinBlocks, int G>
@@ -472,193 +462,6 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
   }
 }
 
-// ---- Split-level variant: one strip per CTA of two warps. Warp 0 loads the
-// input rows and runs levels 0 .. T/2-1; it hands its level-(T/2-1) rows to
-// warp 1 through a shared-memory ring (full/empty mbarriers per group of G
-// rows); warp 1 runs levels T/2 .. T-1 and stores. Same arithmetic, same step
-// order per level as jacobi2d_tb4_kernel, so bitwise the same result — but each
-// thread holds half the level state, so twice as many warps fit per SM to hide
-// the level chains' latency.
-constexpr int kSplitRing = 4;  // groups in flight between the two warps
-
-template <int T, int G>
-__global__ void __launch_bounds__(64)
-    jacobi2d_tb4s_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
-                         int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk, int64_t nstrips, int64_t ring_lo,
-                         int64_t ring_hi, int64_t nrows_buf, double* __restrict__ dst2, int64_t delta2) {
-  static_assert(T >= 4 && T % 4 == 0 && G % 2 == 0, "T/2 even levels per warp");
-  constexpr int TW = T / 2;
-  constexpr int kCols = 128, kStride = kCols - 2 * T;
-  __shared__ __align__(16) double hand[kSplitRing][G][kCols];
-  __shared__ __align__(8) uint64_t full[kSplitRing], empty[kSplitRing];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t strip = blockIdx.x;
-  const int64_t yc0 = y_lo + (int64_t)blockIdx.y * rows_per_chunk;
-  if (yc0 > y_hi) return;  // block-uniform
-  const int64_t yc1 = min(y_hi, yc0 + rows_per_chunk - 1);
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < kSplitRing; ++q) {
-      mbar_init(&full[q], 32);
-      mbar_init(&empty[q], 32);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  const int64_t x = strip * kStride - T + 4 * lane;
-  const int64_t x_first = strip * kStride - T;
-  const int64_t lo_c = x_first + T, hi_c = x_first + kCols - T;
-  const bool has_a = x >= 0 && x < nxp2, has_b = x + 2 >= 0 && x + 2 < nxp2;
-  bool ring[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) ring[i] = (x + i == 0) || (x + i == nxp2 - 1);
-  const bool col_ring = x_first <= 0 || x_first + kCols >= nxp2 - 1;
-  const int64_t r_first = max(max(ring_lo, (int64_t)0), yc0 - T);
-  const int64_t r_load_last = min(min(ring_hi, nrows_buf - 1), yc1 + T);
-  const int64_t r_end = yc1 + T;
-  // groups whose steps all skip the ring-row checks (and, for warp 1, all store)
-  auto steady = [&](int64_t r0) {
-    return !col_ring && r0 + G - 1 <= r_end && r0 - T >= yc0 && r0 + G - 1 - T <= yc1 && r0 - T > ring_lo &&
-           r0 + G - 2 < ring_hi;
-  };
-  Quad st[TW][2];
-#pragma unroll
-  for (int j = 0; j < TW; ++j) st[j][0].a = st[j][0].b = st[j][1].a = st[j][1].b = make_double2(0.0, 0.0);
-  double* const hl = &hand[0][0][0] + 2 * lane;  // lane pairs (x, x+1) at [0, 64), (x+2, x+3) at [64, 128)
-
-  if (warp == 0) {
-    const double* spa = src + (has_a ? x : 0);
-    const double* spb = src + (has_b ? x + 2 : 0);
-    Quad buf[G];
-    const int64_t safe_off = r_first * ld;
-#pragma unroll
-    for (int k = 0; k < G; ++k) {
-      const int64_t off = (r_first + k <= r_load_last) ? (r_first + k) * ld : safe_off;
-      buf[k].a = ldg2(spa + off);
-      buf[k].b = ldg2(spb + off);
-    }
-    int64_t loff = (r_first + G) * ld;
-    int grp = 0;
-    for (int64_t r0 = r_first; r0 <= r_end; r0 += G, ++grp) {
-      Quad o[G];
-      if (steady(r0)) {  // one basic block for the whole group (see jacobi2d_tb4_kernel)
-#pragma unroll
-        for (int k = 0; k < G; ++k) {
-          const Quad s0 = buf[k];
-          const int64_t off = (r0 + k + G <= r_load_last) ? loff : safe_off;
-          buf[k].a = ldg2(spa + off);
-          buf[k].b = ldg2(spb + off);
-          loff += ld;
-          o[k] = tb4_range<TW, 0, false, false>(st, k, s0, r0 + k, ring, ring_lo, ring_hi);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < G; ++k) {
-          const int64_t r = r0 + k;
-          const Quad s0 = buf[k];
-          const int64_t off = (r + G <= r_load_last) ? loff : safe_off;
-          buf[k].a = ldg2(spa + off);
-          buf[k].b = ldg2(spb + off);
-          loff += ld;
-          if (r > r_end) continue;
-          const bool rows_chk = (r - T <= ring_lo) || (r - 1 >= ring_hi);
-          if (rows_chk)
-            o[k] = col_ring ? tb4_range<TW, 0, true, true>(st, k, s0, r, ring, ring_lo, ring_hi)
-                            : tb4_range<TW, 0, true, false>(st, k, s0, r, ring, ring_lo, ring_hi);
-          else
-            o[k] = col_ring ? tb4_range<TW, 0, false, true>(st, k, s0, r, ring, ring_lo, ring_hi)
-                            : tb4_range<TW, 0, false, false>(st, k, s0, r, ring, ring_lo, ring_hi);
-        }
-      }
-      const int q = grp % kSplitRing;
-      if (grp >= kSplitRing) mbar_wait_parity(&empty[q], ((grp / kSplitRing) - 1) & 1);
-#pragma unroll
-      for (int k = 0; k < G; ++k) {
-        *reinterpret_cast<double2*>(hl + (q * G + k) * kCols) = o[k].a;
-        *reinterpret_cast<double2*>(hl + (q * G + k) * kCols + 64) = o[k].b;
-      }
-      mbar_arrive(&full[q]);
-    }
-  } else {
-    const bool sta0 = x >= lo_c && x < hi_c && x >= 0 && x < nxp2;
-    const bool sta1 = x + 1 >= lo_c && x + 1 < hi_c && x + 1 >= 0 && x + 1 < nxp2;
-    const bool stb0 = x + 2 >= lo_c && x + 2 < hi_c && x + 2 >= 0 && x + 2 < nxp2;
-    const bool stb1 = x + 3 >= lo_c && x + 3 < hi_c && x + 3 >= 0 && x + 3 < nxp2;
-    auto store_row = [&](double* p, const Quad& o) {
-      if (sta0 && sta1) stg2(p, o.a);
-      else if (sta0) p[0] = o.a.x;
-      else if (sta1) p[1] = o.a.y;
-      if (stb0 && stb1) stg2(p + 2, o.b);
-      else if (stb0) p[2] = o.b.x;
-      else if (stb1) p[3] = o.b.y;
-    };
-    double* out = dst + x + (r_first - T) * ld;
-    double* out2 = dst2 ? dst2 + x + (r_first - T + delta2) * ld : nullptr;
-    int grp = 0;
-    for (int64_t r0 = r_first; r0 <= r_end; r0 += G, ++grp) {
-      const int q = grp % kSplitRing;
-      mbar_wait_parity(&full[q], (grp / kSplitRing) & 1);
-      Quad sv[G];
-#pragma unroll
-      for (int k = 0; k < G; ++k) {
-        sv[k].a = *reinterpret_cast<const double2*>(hl + (q * G + k) * kCols);
-        sv[k].b = *reinterpret_cast<const double2*>(hl + (q * G + k) * kCols + 64);
-      }
-      mbar_arrive(&empty[q]);
-      if (steady(r0)) {
-        Quad o[G];
-#pragma unroll
-        for (int k = 0; k < G; ++k) o[k] = tb4_range<TW, TW, false, false>(st, k, sv[k], r0 + k, ring, ring_lo, ring_hi);
-#pragma unroll
-        for (int k = 0; k < G; ++k) {
-          store_row(out + k * ld, o[k]);
-          if (out2) store_row(out2 + k * ld, o[k]);
-        }
-        out += G * ld;
-        if (out2) out2 += G * ld;
-        continue;
-      }
-#pragma unroll
-      for (int k = 0; k < G; ++k) {
-        const int64_t r = r0 + k;
-        if (r > r_end) break;
-        const bool rows_chk = (r - T <= ring_lo) || (r - 1 >= ring_hi);
-        Quad o;
-        if (rows_chk)
-          o = col_ring ? tb4_range<TW, TW, true, true>(st, k, sv[k], r, ring, ring_lo, ring_hi)
-                       : tb4_range<TW, TW, true, false>(st, k, sv[k], r, ring, ring_lo, ring_hi);
-        else
-          o = col_ring ? tb4_range<TW, TW, false, true>(st, k, sv[k], r, ring, ring_lo, ring_hi)
-                       : tb4_range<TW, TW, false, false>(st, k, sv[k], r, ring, ring_lo, ring_hi);
-        if (r - T >= yc0 && r - T <= yc1) {
-          store_row(out, o);
-          if (out2) store_row(out2, o);
-        }
-        out += ld;
-        if (out2) out2 += ld;
-      }
-    }
-  }
-}
-
-template <int T>
-st_status launch_tb4s(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
-                      int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
-  const int64_t nxp2 = nx + 2;
-  constexpr int kStride = 128 - 2 * T;
-  const int64_t nstrips = (nxp2 + kStride - 1) / kStride;
-  const int64_t rows = y_hi - y_lo + 1;
-  static const int kRows = env_int("ST_JACOBI_TB4_ROWS", 192);
-  const int64_t rpc = std::max<int64_t>(1, std::min<int64_t>(kRows, rows));
-  const int64_t nchunks = (rows + rpc - 1) / rpc;
-  ST_RETURN_IF(nchunks > 65535 || nstrips > 0x7fffffff, ST_ENOTSUP, "jacobi2d tb: grid too large");
-  dim3 grid((unsigned)nstrips, (unsigned)nchunks);
-  jacobi2d_tb4s_kernel<T, 2><<<grid, 64, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo, ring_hi,
-                                                 nrows_buf, rem.base, rem.delta);
-  ST_LAUNCHED();
-  return ST_OK;
-}
-
 template <int T>
 st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
                      int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
@@ -748,8 +551,6 @@ st_status jacobi2d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, 4>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4s_kernel<4, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4s_kernel<8, 2>));
   return ST_OK;
 }
 
@@ -757,14 +558,6 @@ st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t l
                            int t, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
   if (y_hi < y_lo) return ST_OK;
   static const int kColsPerLane = env_int("ST_JACOBI_TB_COLS", 4);
-  static const int kSplit = env_int("ST_JACOBI_TB_SPLIT", 0);
-  if (kColsPerLane == 4 && kSplit) {
-    switch (t) {
-      case 4: return launch_tb4s<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
-      case 8: return launch_tb4s<8>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
-      default: break;
-    }
-  }
   if (kColsPerLane == 4) {
     switch (t) {
       case 2: return launch_tb4<2>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
