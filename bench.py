@@ -55,6 +55,12 @@ def ncu_traffic(kernel_key: str):
     return None if v is None else v.get("dram_bytes_per_launch")
 
 
+def gs_traffic_per_sweep():
+    """The GS launch runs all sweeps; tools/prof_kernels.py profiles a 4-sweep launch."""
+    v = ncu_traffic("gauss_seidel2d_tiled_kernel")
+    return None if v is None else v / 4
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
 
@@ -328,7 +334,7 @@ def main():
     # whatever its temporal-blocking depth (16 B per point per launch)
     achieved_gbs = JACOBI_BYTES_PER_PT * pts_rank / (launch_ms / 1e3) / 1e9
     effective_gbs = JACOBI_BYTES_PER_PT * pts_rank * sweeps / (step_ms / 1e3) / 1e9
-    kname = "jacobi2d_tb_kernel" if max(pass_sweeps) > 1 else "jacobi2d_stream_kernel"
+    kname = "jacobi2d_tb4_kernel" if max(pass_sweeps) > 1 else "jacobi2d_stream_kernel"
     clocks = clk.summary()
 
     # ------------------------------------------------------------------ e2e (host buffers)
@@ -465,10 +471,11 @@ def main():
         gs = {"workload": f"gauss_seidel2d_{ngs}x{ngs}_fp64_{args.gs_sweeps}sweeps_inplace_lexicographic",
               "value": round(ngs * ngs * args.gs_sweeps / (gs_ms / 1e3) / 1e9, 3), "unit": UNIT,
               "ms_per_step": round(gs_ms, 3), "sweeps_per_launch": args.gs_sweeps, "gpu_launches": gs_launches,
-              "roofline": {"bound": "hbm", "kernel": "gauss_seidel2d_kernel", "achieved": round(gs_gbs, 1),
+              "roofline": {"bound": "hbm", "kernel": "gauss_seidel2d_tiled_kernel", "achieved": round(gs_gbs, 1),
                            "peak": hbm_peak, "unit": "GB/s", "frac": round(gs_gbs / hbm_peak, 4),
-                           "traffic": ncu_traffic("gauss_seidel2d_kernel"), "bytes_per_pt_per_sweep":
-                           JACOBI_BYTES_PER_PT, "peak_source": peak_src}}
+                           "traffic": gs_traffic_per_sweep(), "traffic_unit": "DRAM bytes per sweep (ncu of a "
+                           "4-sweep launch / 4)", "bytes_per_pt_per_sweep": JACOBI_BYTES_PER_PT,
+                           "peak_source": peak_src}}
         if not args.no_cpu:
             import oracle
             a_small = si.jacobi2d_grid(ngs, 2048)  # a 2048-row band of the same grid recipe
