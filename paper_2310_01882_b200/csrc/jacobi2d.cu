@@ -145,6 +145,90 @@ __global__ void __launch_bounds__(1024)
     for (int x = threadIdx.x; x < nxp2; x += blockDim.x) out[(int64_t)y * ld + x] = cur[y * nxp2 + x];
 }
 
+// Register-resident variant for grids up to 64 columns (C1 = 64^2): the state
+// lives in registers for all sweeps. Lane l of warp w owns columns 1+2l, 2+2l
+// of rows 1+R*w .. R*(w+1); rows beyond ny+1 are idle, the ring row ny+1 (and
+// ring column nx+1 when it falls inside a lane) are held but never updated.
+// Per sweep: N/S inside a warp's rows come from its own registers, W/E from
+// warp shuffles, and the first/last row of every warp goes through shared
+// memory (double-buffered by sweep parity, so one barrier per sweep). Shared
+// traffic per sweep is 2 rows per warp instead of 4 reads + 1 write per point.
+constexpr int kRegResMaxWarps = 17;  // 68 rows: ny <= 67 with R = 4
+
+template <int R>
+__global__ void __launch_bounds__(32 * kRegResMaxWarps)
+    jacobi2d_regres_kernel(double* __restrict__ a, double* __restrict__ b, int nx, int ny, int64_t ld,
+                           int64_t iters) {
+  constexpr int kW = 64;  // columns per warp row (32 lanes x 2)
+  __shared__ __align__(16) double top_row[2][kRegResMaxWarps][kW];      // first row of each warp, per sweep parity
+  __shared__ __align__(16) double bot_row[2][kRegResMaxWarps + 1][kW];  // last row of each warp; [.][0] = ring row 0
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int x0 = 1 + 2 * lane;
+  double v[R][2];
+  double wr[R], er[R];  // ring column 0 (lane 0) and column 65 (lane 31, when nx == 64)
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int y = 1 + R * w + i;
+    const bool row_ok = y <= ny + 1;
+    const double* ar = a + (int64_t)(row_ok ? y : 0) * ld;
+    v[i][0] = (row_ok && x0 <= nx + 1) ? ar[x0] : 0.0;
+    v[i][1] = (row_ok && x0 + 1 <= nx + 1) ? ar[x0 + 1] : 0.0;
+    wr[i] = row_ok ? ar[0] : 0.0;
+    er[i] = (row_ok && nx + 1 == 2 * 32 + 1) ? ar[nx + 1] : 0.0;
+  }
+  // ring row 0 as the "last row of warp -1", in both parities
+  for (int c = threadIdx.x; c < kW; c += blockDim.x) {
+    const double r0 = (c + 1 <= nx + 1) ? a[c + 1] : 0.0;
+    bot_row[0][0][c] = r0;
+    bot_row[1][0][c] = r0;
+  }
+  const bool c0_upd = x0 <= nx, c1_upd = x0 + 1 <= nx;
+  for (int64_t it = 0; it < iters; ++it) {
+    const int p = (int)(it & 1);
+    *reinterpret_cast<double2*>(&top_row[p][w][2 * lane]) = make_double2(v[0][0], v[0][1]);
+    *reinterpret_cast<double2*>(&bot_row[p][w + 1][2 * lane]) = make_double2(v[R - 1][0], v[R - 1][1]);
+    __syncthreads();
+    const double2 nrow = *reinterpret_cast<const double2*>(&bot_row[p][w][2 * lane]);
+    const double2 srow = (w + 1 < nw) ? *reinterpret_cast<const double2*>(&top_row[p][w + 1][2 * lane])
+                                      : make_double2(0.0, 0.0);
+    double o[R][2];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int y = 1 + R * w + i;
+      const double n0 = i > 0 ? v[i - 1][0] : nrow.x, n1 = i > 0 ? v[i - 1][1] : nrow.y;
+      const double s0 = i + 1 < R ? v[i + 1][0] : srow.x, s1 = i + 1 < R ? v[i + 1][1] : srow.y;
+      double wv = __shfl_up_sync(0xffffffffu, v[i][1], 1);
+      double ev = __shfl_down_sync(0xffffffffu, v[i][0], 1);
+      if (lane == 0) wv = wr[i];
+      if (lane == 31) ev = er[i];
+      const bool row_upd = y <= ny;
+      o[i][0] = (row_upd && c0_upd) ? dmul(dadd(dadd(dadd(n0, s0), wv), v[i][1]), 0.25) : v[i][0];
+      o[i][1] = (row_upd && c1_upd) ? dmul(dadd(dadd(dadd(n1, s1), v[i][0]), ev), 0.25) : v[i][1];
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      v[i][0] = o[i][0];
+      v[i][1] = o[i][1];
+    }
+  }
+  double* out = (iters & 1) ? b : a;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int y = 1 + R * w + i;
+    if (y > ny + 1) continue;
+    double* orow = out + (int64_t)y * ld;
+    if (x0 <= nx + 1) orow[x0] = v[i][0];
+    if (x0 + 1 <= nx + 1) orow[x0 + 1] = v[i][1];
+    if (lane == 0) orow[0] = wr[i];
+    if (lane == 31 && nx + 1 == 2 * 32 + 1) orow[nx + 1] = er[i];
+  }
+  if (iters & 1) {  // the ring row 0 of b
+    for (int c = threadIdx.x; c < nx + 2; c += blockDim.x) b[c] = a[c];
+  }
+}
+
+constexpr int kRegResRows = 4;
+
 constexpr size_t kResidentMaxSmem = 200 * 1024;
 
 }  // namespace
@@ -173,6 +257,17 @@ bool jacobi2d_resident_fits(int64_t nx, int64_t ny) {
 
 st_status jacobi2d_resident(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t iters,
                             cudaStream_t s) {
+  static const int kRegRes = env_int("ST_JACOBI_REGRES", kRegResRows);  // rows per warp (0: shared-memory kernel)
+  if (kRegRes && nx <= 64) {
+    const int64_t rr = kRegRes == 8 ? 8 : kRegRes == 2 ? 2 : 4;
+    const int64_t warps = (ny + 1 + rr - 1) / rr;  // rows 1 .. ny+1 (incl. the ring row)
+    if (warps <= kRegResMaxWarps) {
+      auto* k = rr == 8 ? jacobi2d_regres_kernel<8> : rr == 2 ? jacobi2d_regres_kernel<2> : jacobi2d_regres_kernel<4>;
+      k<<<1, (unsigned)(32 * warps), 0, s>>>(a, b, (int)nx, (int)ny, ld, iters);
+      ST_LAUNCHED();
+      return ST_OK;
+    }
+  }
   const size_t smem = (size_t)(nx + 2) * (size_t)(ny + 2) * 2 * sizeof(double);
   ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi2d_resident_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResidentMaxSmem));
@@ -523,6 +618,9 @@ st_status jacobi2d_preload() {
   cudaFuncAttributes fa;
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_stream_kernel<4>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_resident_kernel));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<8>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<2, 1>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<2, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<2, 3>));
