@@ -193,6 +193,11 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // One CTA = one warp = one strip (the strips spin on each other: all must be resident).
+// The CTA is a single warp, so its barrier is a warp barrier; bar.sync (rather
+// than bar.warp.sync) is what compute-sanitizer's racecheck models as ordering
+// the cp.async tile writes (after cp.async.wait_group) against the tile reads.
+__device__ __forceinline__ void cta_sync() { __syncwarp(); }
+
 // kPubT: tiles written back per progress publication (one GPU-scope fence each).
 template <int kPubT>
 __global__ void __launch_bounds__(32)
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(32)
   };
   auto publish = [&](unsigned long long base, int col_done) {  // columns 1..col_done of both edge rows are in global
     __threadfence();
-    __syncwarp();
+    cta_sync();
     if (col_done >= 1) {
       if (top_lane) st_relaxed(my_top, base + (unsigned long long)min(nx, col_done));
       if (pub_bot) st_relaxed(my_bot, base + (unsigned long long)min(nx, col_done));
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(32)
       pn[d] = ((top_lane || need_below) && cn >= 1 && cn <= nx) ? __ldcg((top_lane ? above : below) + cn) : 0.0;
     }
     cp_async_wait_group<1>();  // tile 0
-    __syncwarp();
+    cta_sync();
     double res = my_tile_row[0];  // W of column 1 = the Dirichlet column
     double e_prev = res;
     // E values are read kEpf steps ahead from the tile: the compiler cannot prove
@@ -298,15 +303,18 @@ __global__ void __launch_bounds__(32)
     for (int d = 0; d < kEpf; ++d) ep[d] = tiles[toff(x0 + 1 + d)];
     for (int g = 0; g < ngroups; ++g) {
       if (g >= 2) {  // tile g-2 is complete: write it back (and publish every kPubT tiles)
-        __syncwarp();
+        cta_sync();
         tile_store(g - 2);
-        __syncwarp();
+        cta_sync();
         if ((g - 2) % kPubT == kPubT - 1) publish(base, (g - 2) * kTile + kTile - 1);
       }
+      // lanes that have not reached column 0 yet read stale slots (negative columns
+      // wrap to slot 3): order those reads before the slot's refill
+      if (g < 2) cta_sync();
       if (g + 2 < ntiles) tile_load(g + 2);
       cp_async_commit_group();
       cp_async_wait_group<1>();  // tiles <= g+1 have landed
-      __syncwarp();
+      cta_sync();
       if (g > 0 && g % kPubT == 0) wait(g);
       const int k0 = g * kTile;
 #pragma unroll
@@ -329,12 +337,12 @@ __global__ void __launch_bounds__(32)
       }
     }
     // flush the tiles not yet written back, then publish the whole row
-    __syncwarp();
+    cta_sync();
     for (int m = max(0, ngroups - 2); m < ntiles; ++m) tile_store(m);
-    __syncwarp();
+    cta_sync();
     publish(base, nx);
     cp_async_wait_group<0>();
-    __syncwarp();
+    cta_sync();
   }
 }
 

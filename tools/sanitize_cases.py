@@ -22,5 +22,11 @@ for nx, ny, nz in ((33, 31, 9), (70, 40, 66)):
     a = torch.from_numpy(si.jacobi3d_grid(nx, ny, nz)).cuda()
     b = torch.empty_like(a)
     st.st_jacobi3d_run(a, b, 3)
+for nx, ny, ld, iters in ((200, 95, 202, 3), (65, 33, 67, 2), (1000, 130, 1002, 2)):  # GS: tiled (even ld), register (odd)
+    a = torch.from_numpy(si.jacobi2d_grid(nx, ny, ld=ld)).cuda()
+    st.st_gauss_seidel2d_run(a, iters, nx=nx)
+for nx, ny in ((64, 64), (37, 21)):  # register-resident C1 kernel
+    a = torch.from_numpy(si.jacobi2d_grid(nx, ny)).cuda()
+    st.st_jacobi2d_run(a, torch.empty_like(a), 7)
 torch.cuda.synchronize()
 print("sanitize cases done")
