@@ -1,0 +1,112 @@
+"""Decomposition overhead on ONE GPU: the C2 Jacobi grid (16384^2) and the C3 PW
+grid (512^3) split into P = 1, 2, 4 slab ranks of a LOCAL group (all ranks in
+this process, all on cuda:0, each on its own stream, halo swaps by fused
+kernel stores + device-side flags). Total work is fixed, so Gpts/s(P) /
+Gpts/s(1) is the fraction of throughput the decomposition (ghost rows, swaps,
+flag waits, boundary/interior launch split) leaves — not multi-GPU scaling,
+which needs several GPUs. Device-timed: one event on the default stream before
+all ranks, one after all ranks joined."""
+import json
+import os
+import pathlib
+import sys
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent.parent))
+
+import numpy as np
+import torch
+
+import paper_2310_01882_b200 as st
+import stencil_inputs as si
+
+
+def timed(ranks_fn, streams, reps):
+    main = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ranks_fn()  # warm-up
+    torch.cuda.synchronize()
+    ev0.record(main)
+    for s in streams:
+        s.wait_event(ev0)
+    for _ in range(reps):
+        ranks_fn()
+    for s in streams:
+        main.wait_stream(s)
+    ev1.record(main)
+    ev1.synchronize()
+    return ev0.elapsed_time(ev1) / reps
+
+
+def jacobi(P, n=16384, sweeps=200, h=8):
+    comms = st.Comm.local_group(P) if P > 1 else [None]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    bufs = []
+    for r in range(P):
+        start, cnt = st.st_block_split(n, P, r)
+        hh = h if P > 1 else 1
+        lo = max(0, start + 1 - hh)
+        hi = min(n + 1, start + cnt + hh)
+        a_np = np.zeros((cnt + 2 * hh, n + 2))
+        a_np[lo - (start + 1 - hh): hi - (start + 1 - hh) + 1] = si.jacobi2d_grid(n, n, row0=lo, rows=hi - lo + 1)
+        a = torch.from_numpy(a_np).cuda()
+        b = torch.empty_like(a)
+        if comms[r] is not None:
+            comms[r].bind([a, b], cnt)
+        bufs.append((a, b, hh))
+    torch.cuda.synchronize()
+
+    def run():
+        for r in range(P):
+            a, b, hh = bufs[r]
+            with torch.cuda.stream(streams[r]):
+                st.st_jacobi2d_run(a, b, sweeps, tblock=0, halo=hh, comm=comms[r])
+
+    ms = timed(run, streams, 2)
+    for c in comms:
+        if c is not None:
+            c.close()
+    return n * n * sweeps / (ms / 1e3) / 1e9, ms
+
+
+def pw(P, n=512, apps=20):
+    comms = st.Comm.local_group(P) if P > 1 else [None]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    parts = []
+    for r in range(P):
+        z0, cnt = st.st_block_split(n, P, r)
+        d = si.pw_inputs(n, n, n, plane0=z0, planes=cnt + 2)
+        g = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in d.items()}
+        outs = [torch.empty_like(g["u"]) for _ in range(3)]
+        if comms[r] is not None:
+            comms[r].bind([g["u"], g["v"], g["w"]], cnt)
+        parts.append((g, outs))
+    torch.cuda.synchronize()
+
+    def run():
+        for r in range(P):
+            g, outs = parts[r]
+            with torch.cuda.stream(streams[r]):
+                st.st_pw_advect3d(g["u"], g["v"], g["w"], *outs, g["tcx"], g["tcy"], g["tzc1"], g["tzc2"],
+                                  g["tzd1"], g["tzd2"], comm=comms[r])
+
+    ms = timed(run, streams, apps)
+    for c in comms:
+        if c is not None:
+            c.close()
+    return n ** 3 / (ms / 1e3) / 1e9, ms
+
+
+if __name__ == "__main__":
+    out = {"what": "LOCAL rank group on one B200: throughput at fixed total work vs P=1", "jacobi2d_16384^2_200sw": {},
+           "pw_512^3": {}}
+    for P in (1, 2, 4):
+        v, ms = jacobi(P)
+        out["jacobi2d_16384^2_200sw"][P] = {"gpts": round(v, 1), "ms": round(ms, 2)}
+        v, ms = pw(P)
+        out["pw_512^3"][P] = {"gpts": round(v, 2), "ms_per_app": round(ms, 4)}
+    for k in ("jacobi2d_16384^2_200sw", "pw_512^3"):
+        base = out[k][1]["gpts"]
+        for P in out[k]:
+            out[k][P]["vs_P1"] = round(out[k][P]["gpts"] / base, 3)
+    print(json.dumps(out))
