@@ -217,6 +217,7 @@ def main():
     ap.add_argument("--no-gs", action="store_true")
     ap.add_argument("--gs-sweeps", type=int, default=100, help="in-place Gauss-Seidel sweeps timed (16384^2)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-e2e-pipeline", action="store_true", help="e2e: copies and compute strictly serial")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-sweeps", type=int, default=20)
     ap.add_argument("--cpu-sweeps", type=int, default=40)
@@ -362,7 +363,50 @@ def main():
         e_ms = max_over_ranks(sum(e_times) / len(e_times))
         e2e = {"value": round(pts_total / (e_ms / 1e3) / 1e9, 3), "unit": UNIT,
                "h2d_bytes_per_step": h_in.numel() * 8, "d2h_bytes_per_step": h_out.numel() * 8,
-               "ms_per_step": round(e_ms, 3)}
+               "ms_per_step": round(e_ms, 3), "pipelined": False}
+        if world == 1 and not args.no_e2e_pipeline:
+            # Pipelined over independent steps: step i's H2D, compute and D2H each run on their
+            # own stream; two device buffer sets let step i+1's H2D and step i-1's D2H overlap
+            # step i's compute. Every step still copies its whole input in and its result out.
+            sets = [(A, B), (torch.empty_like(A), torch.empty_like(B))]
+            s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+            in_done = [torch.cuda.Event() for _ in sets]
+            comp_done = [torch.cuda.Event() for _ in sets]
+            freed = [torch.cuda.Event() for _ in sets]
+
+            def pipelined(nsteps):
+                for i in range(nsteps):
+                    k = i % 2
+                    Ak, Bk = sets[k]
+                    if i >= 2:
+                        s_in.wait_event(freed[k])
+                    with torch.cuda.stream(s_in):
+                        Ak.copy_(h_in, non_blocking=True)
+                        in_done[k].record(s_in)
+                    stream.wait_event(in_done[k])
+                    r = st.st_jacobi2d_run(Ak, Bk, sweeps, tblock=args.tblock, halo=halo, comm=comm)
+                    comp_done[k].record(stream)
+                    s_out.wait_event(comp_done[k])
+                    with torch.cuda.stream(s_out):
+                        h_out.copy_(r, non_blocking=True)
+                        freed[k].record(s_out)
+
+            pipelined(2)
+            torch.cuda.synchronize()
+            kp = max(3, args.steps)
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record(s_in)
+            stream.wait_event(p0)
+            s_out.wait_event(p0)
+            pipelined(kp)
+            s_out.wait_stream(stream)
+            p1.record(s_out)
+            p1.synchronize()
+            pe_ms = p0.elapsed_time(p1) / kp
+            e2e.update({"value": round(pts_total / (pe_ms / 1e3) / 1e9, 3), "ms_per_step": round(pe_ms, 3),
+                        "pipelined": True, "steps_pipelined": kp, "ms_per_step_serial": round(e_ms, 3),
+                        "value_serial": round(pts_total / (e_ms / 1e3) / 1e9, 3)})
+            del sets
         del h_in, h_out
     del A, B, a0
 
