@@ -566,11 +566,23 @@ st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int
   const int64_t rows = y_hi - y_lo + 1;
   const int64_t blocks_x = (nstrips + kStreamWarps - 1) / kStreamWarps;
   static const int kOcc = env_int("ST_JACOBI_TB4_OCC", 1);
-  // short chunks balance the single-CTA-per-SM grid (measured: 192 rows best
-  // on C2); the 2T rows a chunk re-reads are mostly L2 hits because the chunks
-  // of a strip run at about the same time
-  static const int kRows = env_int("ST_JACOBI_TB4_ROWS", 192);
-  const int64_t rpc = std::max<int64_t>(1, std::min<int64_t>(kRows, rows));
+  // Row chunk: every chunk recomputes 2T warm-up rows, and with one CTA per SM
+  // a partly filled last wave idles SMs, so pick the chunk height R that
+  // minimises waves(R) x (R + 2T) (C2: R = 357 -> 6 waves of 874 CTAs, +2 %
+  // over the fixed 192-row chunks, measured). ST_JACOBI_TB4_ROWS overrides.
+  static const int kRows = env_int("ST_JACOBI_TB4_ROWS", 0);
+  int64_t rpc = kRows;
+  if (rpc <= 0) {
+    const int64_t slots = (int64_t)num_sms() * kOcc;
+    int64_t best = INT64_MAX;
+    rpc = rows;
+    for (int64_t r = 160; r <= 448; ++r) {
+      const int64_t ctas = blocks_x * ((rows + r - 1) / r);
+      const int64_t cost = ((ctas + slots - 1) / slots) * (std::min(r, rows) + 2 * T);
+      if (cost < best) { best = cost; rpc = r; }
+    }
+  }
+  rpc = std::max<int64_t>(1, std::min<int64_t>(rpc, rows));
   const int64_t nchunks = (rows + rpc - 1) / rpc;
   ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d tb: too many row chunks");
   dim3 grid((unsigned)blocks_x, (unsigned)nchunks);
