@@ -25,7 +25,7 @@ CFLAGS_ORACLE := -O2 -std=c11 -fPIC -ffp-contract=off -fno-fast-math -fopenmp -W
 # Product: sm_100a only. Kernels spell every rounding with __dadd_rn/__dmul_rn (no FMA
 # contraction) so results are bit-exact with the oracle; -fmad=false is belt and braces.
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false -Xcompiler -fPIC,-Wall \
+NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false $(EXTRA_NVFLAGS) -Xcompiler -fPIC,-Wall \
             -Xptxas -v -I$(INC) -I$(NCCL_DIR)/include -I$(CUDA_DIR)/include
 LDFLAGS  := -shared -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib \
             -lcudart_static -ldl -lrt -lpthread
