@@ -239,7 +239,8 @@ st_status st_jacobi2d_run(double* a, double* b, int64_t nx, int64_t ny_local, in
  * with the values the sequential loop sees (N, W already updated). Bitwise the
  * sequential loop nest. `workspace` = st_gauss_seidel2d_workspace_bytes(ny)
  * bytes of caller-owned device memory (progress words of the wavefront).
- * ST_ENOTSUP if ceil(ny/32) warps cannot all be resident on the device. */
+ * ST_ENOTSUP if ceil(ny/32) warps cannot all be resident on the device; the
+ * launch is cooperative (co-residency guaranteed by the driver, or ST_ECUDA). */
 int64_t st_gauss_seidel2d_workspace_bytes(int64_t ny);
 st_status st_gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters, void* workspace,
                                 int64_t workspace_bytes, void* cuda_stream);

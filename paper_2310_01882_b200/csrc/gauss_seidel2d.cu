@@ -368,7 +368,11 @@ st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int6
     // every strip's warp must be resident at once (the strips spin on each other)
     ST_RETURN_IF(nstrips > (int64_t)per_sm * num_sms(), ST_ENOTSUP,
                  "gauss_seidel2d: %lld strips exceed the resident capacity (%d CTAs/SM)", (long long)nstrips, per_sm);
-    tk<<<(unsigned)nstrips, 32, kTiledSmem, s>>>(a, (int)nx, ny, ld, iters, progress, nstrips);
+    // cooperative launch: the driver guarantees every strip's CTA is co-resident
+    // (or refuses the launch) — the strips spin on each other's progress words
+    int nx_i = (int)nx;
+    void* args[] = {&a, &nx_i, &ny, &ld, &iters, &progress, (void*)&nstrips};
+    ST_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)tk, dim3((unsigned)nstrips), dim3(32), args, kTiledSmem, s));
     ST_LAUNCHED();
     return ST_OK;
   }
@@ -378,7 +382,9 @@ st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int6
   const int64_t blocks = (nstrips + kGsWarps - 1) / kGsWarps;
   ST_RETURN_IF(blocks > (int64_t)per_sm * num_sms(), ST_ENOTSUP,
                "gauss_seidel2d: %lld strips exceed the resident capacity (%d CTAs/SM)", (long long)nstrips, per_sm);
-  kern<<<(unsigned)blocks, 32 * kGsWarps, 0, s>>>(a, (int)nx, ny, ld, iters, progress, nstrips);
+  int nx_i = (int)nx;
+  void* args[] = {&a, &nx_i, &ny, &ld, &iters, &progress, (void*)&nstrips};
+  ST_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)blocks), dim3(32 * kGsWarps), args, 0, s));
   ST_LAUNCHED();
   return ST_OK;
 }
