@@ -84,6 +84,16 @@ st_status st_comm_unique_id(uint8_t id[ST_UNIQUE_ID_BYTES]);
 st_status st_comm_init(st_comm** out, int32_t nranks, int32_t rank,
                        const uint8_t id[ST_UNIQUE_ID_BYTES], int32_t cuda_device);
 
+/* Borrow an existing NCCL communicator (e.g. torch's ProcessGroupNCCL
+ * `_comm_ptr()` for the group's device): `nccl_comm` is an ncclComm_t living on
+ * `cuda_device`; rank and size are taken from it. The library adds its own comm
+ * stream and events but never destroys the borrowed communicator — the owner
+ * keeps it alive until st_comm_destroy returns. ST_ENCCL if `nccl_comm` is not a
+ * valid communicator of the NCCL the library is linked against (one NCCL per
+ * process: the torch wheel's), ST_EINVAL if it lives on another device.
+ * SURVEY.md §8(b); NCCL p2p halo swaps over NVLink. */
+st_status st_comm_from_nccl(st_comm** out, void* nccl_comm, int32_t cuda_device);
+
 /* Single-process group of `nranks` ranks (LOCAL transport): comms[r] is rank r,
  * on CUDA device devices[r] (devices may repeat; distinct devices get peer
  * access enabled). The halo swap copies boundary slabs straight into the

@@ -61,6 +61,7 @@ _SIGS = {
     "st_comm_unique_id": (ctypes.c_int, [_vp]),
     "st_comm_init": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, _i32, _vp, _i32]),
     "st_comm_destroy": (ctypes.c_int, [_vp]),
+    "st_comm_from_nccl": (ctypes.c_int, [ctypes.POINTER(_vp), _vp, _i32]),
     "st_comm_init_local": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, ctypes.POINTER(_i32)]),
     "st_comm_bind": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), _i32, _i64]),
     "st_comm_init_ipc": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, _i32, _i32]),
@@ -164,6 +165,25 @@ class Comm:
         obj = [cls.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0, group=group)
         return cls.create(rank, nranks, obj[0], device)
+
+    @classmethod
+    def from_nccl(cls, nccl_comm_ptr: int, device: int) -> "Comm":
+        """Borrow an existing ncclComm_t (not destroyed by close(); its owner must outlive this Comm)."""
+        h = _vp()
+        _check(lib().st_comm_from_nccl(ctypes.byref(h), _vp(nccl_comm_ptr), device), "st_comm_from_nccl")
+        r, n, d = _i32(), _i32(), _i32()
+        _check(lib().st_comm_query(h, ctypes.byref(r), ctypes.byref(n), ctypes.byref(d)), "st_comm_query")
+        return cls(h.value, r.value, n.value, d.value)
+
+    @classmethod
+    def from_torch_nccl(cls, device: int, group=None) -> "Comm":
+        """Borrow torch's own NCCL communicator of `group` (ProcessGroupNCCL._comm_ptr(); the
+        group must have run a collective on `device` so that the communicator exists)."""
+        import torch
+        import torch.distributed as dist
+        pg = group if group is not None else dist.group.WORLD
+        backend = pg._get_backend(torch.device("cuda", device))
+        return cls.from_nccl(int(backend._comm_ptr()), device)
 
     @classmethod
     def local_group(cls, nranks: int, devices=None) -> list["Comm"]:

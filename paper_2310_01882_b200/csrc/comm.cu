@@ -356,6 +356,35 @@ st_status st_comm_init(st_comm** out, int32_t nranks, int32_t rank,
   return ST_OK;
 }
 
+st_status st_comm_from_nccl(st_comm** out, void* nccl_comm, int32_t cuda_device) {
+  clear_error();
+  ST_RETURN_IF(!out || !nccl_comm, ST_EINVAL, "st_comm_from_nccl: null argument");
+  ST_CHECK_CUDA(cudaSetDevice(cuda_device));
+  ncclComm_t nc = static_cast<ncclComm_t>(nccl_comm);
+  int nranks = 0, rank = 0, dev = -1;
+  ST_RETURN_IF(ncclCommCount(nc, &nranks) != ncclSuccess || ncclCommUserRank(nc, &rank) != ncclSuccess ||
+                   ncclCommCuDevice(nc, &dev) != ncclSuccess,
+               ST_ENCCL, "st_comm_from_nccl: not a valid NCCL communicator");
+  ST_RETURN_IF(dev != cuda_device, ST_EINVAL, "st_comm_from_nccl: communicator is on device %d, not %d", dev,
+               cuda_device);
+  ST_TRY(preload_kernels());
+  st_comm* c = new st_comm();
+  c->nccl = nc;
+  c->borrowed = true;
+  c->rank = rank;
+  c->nranks = nranks;
+  c->device = cuda_device;
+  if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess) {
+    set_error("st_comm_from_nccl: stream/event creation failed");
+    delete c;
+    return ST_ECUDA;
+  }
+  *out = c;
+  return ST_OK;
+}
+
 st_status st_comm_init_local(st_comm** comms, int32_t nranks, const int32_t* devices) {
   clear_error();
   ST_RETURN_IF(!comms || !devices || nranks < 1, ST_EINVAL, "st_comm_init_local: bad arguments");
@@ -582,7 +611,7 @@ st_status st_comm_destroy(st_comm* c) {
   cudaSetDevice(c->device);
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   st_status s = ST_OK;
-  if (c->nccl && ncclCommDestroy(c->nccl) != ncclSuccess) s = ST_ENCCL;
+  if (c->nccl && !c->borrowed && ncclCommDestroy(c->nccl) != ncclSuccess) s = ST_ENCCL;
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);

@@ -46,6 +46,7 @@ struct st_comm {
   cudaEvent_t ev_ready = nullptr;      // main -> comm: boundary rows are written
   cudaEvent_t ev_done = nullptr;       // comm -> main: ghost rows have arrived
   bool broken = false;                 // set after an NCCL error
+  bool borrowed = false;               // nccl came from st_comm_from_nccl: not destroyed here
   // LOCAL transport
   st_local_group* group = nullptr;
   uint32_t* flags = nullptr;  // device: [0] ready, [1]/[2] done from the low/high slab (or z) neighbour,

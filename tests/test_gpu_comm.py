@@ -151,3 +151,39 @@ def test_multi_gpu_decomposed_equals_oracle(cuda_lib, world):
         p.join(timeout=600)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert q.get(timeout=5) is True
+
+
+_BORROW_SCRIPT = r"""
+import os, sys
+sys.path.insert(0, os.environ["REPO"])
+import numpy as np, torch, torch.distributed as dist
+import oracle, stencil_inputs as si
+import paper_2310_01882_b200 as st
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+t = torch.ones(4, device="cuda")
+dist.all_reduce(t)  # materialise torch's communicator
+comm = st.Comm.from_torch_nccl(0)
+assert (comm.rank, comm.nranks, comm.device) == (0, 1, 0)
+nx, ny, h = 150, 90, 2
+a_glob = si.jacobi2d_grid(nx, ny)
+slab = np.zeros((ny + 2 * h, a_glob.shape[1])); slab[h - 1:h + ny + 1] = a_glob
+a = torch.from_numpy(slab).cuda(); b = torch.full_like(a, float("nan"))
+r = st.st_jacobi2d_run(a, b, 7, tblock=2, halo=h, comm=comm, nx=nx)
+ok = np.array_equal(r.cpu().numpy()[h - 1:h + ny + 1, :nx + 2], oracle.jacobi2d(a_glob, 7, nx=nx)[:, :nx + 2])
+comm.close()
+dist.all_reduce(t)  # torch's communicator is still alive (borrowed, not destroyed)
+dist.destroy_process_group()
+print("BORROW_OK" if ok else "BORROW_MISMATCH")
+"""
+
+
+def test_borrowed_torch_nccl_communicator(cuda_lib, tmp_path):
+    # st_comm_from_nccl (SURVEY.md §8(b)): torch's ProcessGroupNCCL communicator drives the slab path
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, REPO=repo, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    out = subprocess.run([sys.executable, "-c", _BORROW_SCRIPT], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert "BORROW_OK" in out.stdout, out.stdout + out.stderr
