@@ -193,9 +193,8 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // One CTA = one warp = one strip (the strips spin on each other: all must be resident).
-// The CTA is a single warp, so its barrier is a warp barrier; bar.sync (rather
-// than bar.warp.sync) is what compute-sanitizer's racecheck models as ordering
-// the cp.async tile writes (after cp.async.wait_group) against the tile reads.
+// The CTA is a single warp, so its barrier is a warp barrier (racecheck-clean:
+// cp.async.wait_group + bar.warp.sync order the tile writes against the reads).
 __device__ __forceinline__ void cta_sync() { __syncwarp(); }
 
 // kPubT: tiles written back per progress publication (one GPU-scope fence each).
