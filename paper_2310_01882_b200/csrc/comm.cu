@@ -92,7 +92,13 @@ st_status stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t v) {
   return ST_OK;
 }
 
-constexpr int kFlagReady = 0, kFlagDoneFromLo = 1, kFlagDoneFromHi = 2, kFlagDoneFromYLo = 3, kFlagDoneFromYHi = 4;
+// Flag words of a rank, all WRITTEN BY ITS NEIGHBOURS (remote stream writes) and
+// awaited only by the rank itself (local stream waits — no polling of peer
+// memory across NVLink): DoneFromX = the X neighbour has delivered my ghosts,
+// ReadyFromX = the X neighbour's ghosts facing me are free, so I may send.
+constexpr int kFlagDoneFromLo = 1, kFlagDoneFromHi = 2, kFlagDoneFromYLo = 3, kFlagDoneFromYHi = 4;
+constexpr int kFlagReadyFromLo = 5, kFlagReadyFromHi = 6, kFlagReadyFromYLo = 7, kFlagReadyFromYHi = 8;
+constexpr int kFlagWords = 16;
 
 // View of rank `peer` of a LOCAL/IPC comm (direct for LOCAL, IPC-mapped for IPC).
 st_status peer_of(st_comm* c, int32_t peer, st_peer* out) {
@@ -142,13 +148,18 @@ st_status local_exchange(st_comm* c, double* const* fields, int32_t nfields, int
   cudaStream_t cs = c->comm_stream;
   ST_CHECK_CUDA(cudaEventRecord(c->ev_ready, main));
   ST_CHECK_CUDA(cudaStreamWaitEvent(cs, c->ev_ready, 0));
-  ST_TRY(stream_write(cs, c->flags + kFlagReady, k));  // my ghost slabs may now be overwritten
+  // my ghost slabs may now be overwritten: tell both neighbours (I am rank-1's high, rank+1's low neighbour)
+  for (int side = 0; side < 2; ++side) {
+    st_peer pc;
+    ST_TRY(peer_view(c, side, &pc));
+    if (pc.valid) ST_TRY(stream_write(cs, pc.flags + (side == 0 ? kFlagReadyFromHi : kFlagReadyFromLo), k));
+  }
   const size_t bytes = (size_t)width * (size_t)pitch * sizeof(double);
   for (int side = 0; side < 2; ++side) {
     st_peer pc;
     ST_TRY(peer_view(c, side, &pc));
     if (!pc.valid) continue;
-    ST_TRY(stream_wait_geq(cs, pc.flags + kFlagReady, k));
+    ST_TRY(stream_wait_geq(cs, c->flags + (side == 0 ? kFlagReadyFromLo : kFlagReadyFromHi), k));
     for (int f = 0; f < nfields; ++f) {
       double* src = fields[f];
       double* dst = pc.bound[(size_t)idx[f]];
@@ -190,7 +201,19 @@ st_status pencil_exchange_async(st_comm* c, double* const* fields, int32_t nfiel
   const int64_t my_plane = (nyl + 2) * ldx;
   ST_CHECK_CUDA(cudaEventRecord(c->ev_ready, main));
   ST_CHECK_CUDA(cudaStreamWaitEvent(cs, c->ev_ready, 0));
-  ST_TRY(stream_write(cs, c->flags + kFlagReady, k));
+  // my ghosts may now be overwritten: tell the y and z neighbours
+  for (int side = 0; side < 2; ++side) {
+    if (!((side == 0 && iy == 0) || (side == 1 && iy == py - 1))) {
+      st_peer pc;
+      ST_TRY(peer_of(c, side == 0 ? c->rank - 1 : c->rank + 1, &pc));
+      ST_TRY(stream_write(cs, pc.flags + (side == 0 ? kFlagReadyFromYHi : kFlagReadyFromYLo), k));
+    }
+    if (!((side == 0 && iz == 0) || (side == 1 && iz == pz - 1))) {
+      st_peer pc;
+      ST_TRY(peer_of(c, side == 0 ? c->rank - py : c->rank + py, &pc));
+      ST_TRY(stream_write(cs, pc.flags + (side == 0 ? kFlagReadyFromHi : kFlagReadyFromLo), k));
+    }
+  }
   // phase y: one boundary row per plane into the y neighbours' ghost rows. The
   // planes that are z ghosts (filled whole by phase z, possibly concurrently)
   // are skipped; the z-halo planes of the grid's z edges are global boundary
@@ -201,7 +224,7 @@ st_status pencil_exchange_async(st_comm* c, double* const* fields, int32_t nfiel
     if ((side == 0 && iy == 0) || (side == 1 && iy == py - 1)) continue;
     st_peer pc;
     ST_TRY(peer_of(c, side == 0 ? c->rank - 1 : c->rank + 1, &pc));
-    ST_TRY(stream_wait_geq(cs, pc.flags + kFlagReady, k));
+    ST_TRY(stream_wait_geq(cs, c->flags + (side == 0 ? kFlagReadyFromYLo : kFlagReadyFromYHi), k));
     const int64_t peer_plane = (pc.n_mid + 2) * ldx;
     const int64_t src_row = side == 0 ? 1 : nyl, dst_row = side == 0 ? pc.n_mid + 1 : 0;
     for (int f = 0; f < nfields; ++f)
@@ -218,7 +241,7 @@ st_status pencil_exchange_async(st_comm* c, double* const* fields, int32_t nfiel
     if ((side == 0 && iz == 0) || (side == 1 && iz == pz - 1)) continue;
     st_peer pc;
     ST_TRY(peer_of(c, side == 0 ? c->rank - py : c->rank + py, &pc));
-    ST_TRY(stream_wait_geq(cs, pc.flags + kFlagReady, k));
+    ST_TRY(stream_wait_geq(cs, c->flags + (side == 0 ? kFlagReadyFromLo : kFlagReadyFromHi), k));
     const int64_t src_plane = side == 0 ? 1 : nzl, dst_plane = side == 0 ? pc.n_slow + 1 : 0;
     for (int f = 0; f < nfields; ++f)
       ST_CHECK_CUDA(cudaMemcpyAsync(pc.bound[(size_t)idx[f]] + dst_plane * my_plane, fields[f] + src_plane * my_plane,
@@ -250,12 +273,16 @@ st_status fused_halo_begin(st_comm* c, double* dst, int64_t n, cudaStream_t main
     if (c->bound[i] == dst) idx = (int)i;
   ST_RETURN_IF(idx < 0, ST_EINVAL, "LOCAL comm: destination buffer was not bound");
   const uint32_t k = ++c->seq;
-  ST_TRY(stream_write(main, c->flags + kFlagReady, k));  // my ghost slabs of dst are free
+  for (int side = 0; side < 2; ++side) {  // my ghost slabs of dst are free: tell the neighbours
+    st_peer pc;
+    ST_TRY(peer_view(c, side, &pc));
+    if (pc.valid) ST_TRY(stream_write(main, pc.flags + (side == 0 ? kFlagReadyFromHi : kFlagReadyFromLo), k));
+  }
   for (int side = 0; side < 2; ++side) {
     st_peer pc;
     ST_TRY(peer_view(c, side, &pc));
     if (!pc.valid) continue;
-    ST_TRY(stream_wait_geq(main, pc.flags + kFlagReady, k));
+    ST_TRY(stream_wait_geq(main, c->flags + (side == 0 ? kFlagReadyFromLo : kFlagReadyFromHi), k));
     Remote& r = side == 0 ? *rem_lo : *rem_hi;
     r.base = pc.bound[(size_t)idx];
     // my first owned slabs -> rank-1's high ghosts (+n_{r-1}); my last owned -> rank+1's low ghosts (-n)
@@ -425,8 +452,8 @@ st_status st_comm_init_local(st_comm** comms, int32_t nranks, const int32_t* dev
     if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess ||
-        cudaMalloc(&c->flags, 8 * sizeof(uint32_t)) != cudaSuccess ||
-        cudaMemset(c->flags, 0, 8 * sizeof(uint32_t)) != cudaSuccess) {
+        cudaMalloc(&c->flags, kFlagWords * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemset(c->flags, 0, kFlagWords * sizeof(uint32_t)) != cudaSuccess) {
       set_error("st_comm_init_local: stream/event/flag allocation failed");
       delete c;
       for (int q = 0; q < r; ++q) st_comm_destroy(comms[q]);
@@ -489,8 +516,8 @@ st_status st_comm_init_ipc(st_comm** out, int32_t nranks, int32_t rank, int32_t 
   if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess ||
-      cudaMalloc(&c->flags, 8 * sizeof(uint32_t)) != cudaSuccess ||
-      cudaMemset(c->flags, 0, 8 * sizeof(uint32_t)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+      cudaMalloc(&c->flags, kFlagWords * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemset(c->flags, 0, kFlagWords * sizeof(uint32_t)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
     set_error("st_comm_init_ipc: stream/event/flag allocation failed");
     st_comm_destroy(c);
     return ST_ECUDA;
