@@ -300,6 +300,11 @@ st_status pw_advect3d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<64, 16, 5, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<64, 16, 6, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<64, 8, 6, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 5, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<64, 16, 5, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 4, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 6, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 5, 8>));
   return ST_OK;
 }
 
@@ -318,7 +323,12 @@ st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaSt
     case 9: return launch_pw<192, 8, 4, 2>(a, z_lo, z_hi, s);
     case 10: return launch_pw<32, 32, 5, 2>(a, z_lo, z_hi, s);
     case 11: return launch_pw<128, 8, 5, 1>(a, z_lo, z_hi, s);
-    default: return launch_pw<128, 8, 5, 2>(a, z_lo, z_hi, s);  // tuned on B200
+    case 12: return launch_pw<128, 8, 5, 4>(a, z_lo, z_hi, s);
+    case 13: return launch_pw<64, 16, 5, 4>(a, z_lo, z_hi, s);
+    case 14: return launch_pw<128, 8, 4, 4>(a, z_lo, z_hi, s);
+    case 15: return launch_pw<128, 8, 6, 4>(a, z_lo, z_hi, s);
+    case 16: return launch_pw<128, 8, 5, 8>(a, z_lo, z_hi, s);
+    default: return launch_pw<128, 8, 5, 4>(a, z_lo, z_hi, s);  // tuned on B200
   }
 }
 
