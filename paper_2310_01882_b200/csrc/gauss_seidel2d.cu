@@ -291,8 +291,14 @@ __global__ void __launch_bounds__(32)
     }
     cp_async_wait_group<1>();  // tile 0
     cta_sync();
-    double res = my_tile_row[0];  // W of column 1 = the Dirichlet column
-    double e_prev = res;
+    // res = the lane's result of the previous step, taken unconditionally (no
+    // select on the chain): before a lane starts and after it ends it computes
+    // garbage that nobody reads — N of lane r+1 at column x is lane r's result
+    // at x, which is real whenever lane r+1 is active, the ring row's result is
+    // never used (only its old values, as S), and W of column 1 is the
+    // Dirichlet column w0, selected off the chain (W enters at the second add).
+    const double w0 = my_tile_row[0];
+    double res = w0;
     // E values are read kEpf steps ahead from the tile: the compiler cannot prove
     // that the read of column x+1 does not alias the store to column x of the
     // step before, so an in-step read would put LDS latency on the chain
@@ -327,11 +333,10 @@ __global__ void __launch_bounds__(32)
         const double s_sh = __shfl_down_sync(0xffffffffu, e, 1);
         const double nn = top_lane ? pn[d] : n_sh;
         const double ss = bottom_lane ? pn[d] : s_sh;
-        const double v = dmul(dadd(dadd(dadd(nn, ss), res), e), 0.25);
-        const bool upd = act && real;
-        if (upd) tiles[toff(x)] = v;
-        res = upd ? v : ((act && ring) ? e_prev : res);
-        e_prev = e;
+        const double ww = x == 1 ? w0 : res;
+        const double v = dmul(dadd(dadd(dadd(nn, ss), ww), e), 0.25);
+        if (act && real) tiles[toff(x)] = v;
+        res = v;
         if (k <= k_nb_max) pn[d] = __ldcg(nbr + k);
       }
     }
