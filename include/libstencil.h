@@ -50,7 +50,8 @@ typedef enum {
   ST_ECUDA = 2,     /* CUDA runtime/driver error */
   ST_ENCCL = 3,     /* NCCL error; the communicator is unusable */
   ST_ENOTSUP = 4,   /* valid request this build does not support */
-  ST_EINTERNAL = 5  /* library bug */
+  ST_EINTERNAL = 5, /* library bug */
+  ST_ETIMEDOUT = 6  /* st_comm_wait: queued work did not finish in time (e.g. a rank never joined a swap) */
 } st_status;
 
 #define ST_ABI_VERSION 1
@@ -93,6 +94,18 @@ st_status st_comm_init(st_comm** out, int32_t nranks, int32_t rank,
  * process: the torch wheel's), ST_EINVAL if it lives on another device.
  * SURVEY.md §8(b); NCCL p2p halo swaps over NVLink. */
 st_status st_comm_from_nccl(st_comm** out, void* nccl_comm, int32_t cuda_device);
+
+/* Failure detection: blocks until all work queued so far on
+ * `cuda_stream` (and the comm's own stream) has completed, polling every
+ * ~100 us instead of a blocking synchronize. NCCL communicators are also
+ * polled with ncclCommGetAsyncError. Returns ST_OK; ST_ENCCL on an asynchronous
+ * NCCL error (the communicator is aborted and unusable); ST_ECUDA on a device
+ * fault; ST_ETIMEDOUT if `timeout_ms` > 0 elapsed with work still pending —
+ * typically a neighbour that never joined a halo swap. On timeout an NCCL
+ * communicator is aborted (ncclCommAbort) so its kernels drain; a LOCAL/IPC
+ * flag wait cannot be cancelled: the work completes if the late rank joins,
+ * otherwise the caller must tear the process down. timeout_ms <= 0: no limit. */
+st_status st_comm_wait(st_comm* comm, void* cuda_stream, int32_t timeout_ms);
 
 /* Single-process group of `nranks` ranks (LOCAL transport): comms[r] is rank r,
  * on CUDA device devices[r] (devices may repeat; distinct devices get peer

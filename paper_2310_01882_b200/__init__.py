@@ -28,8 +28,8 @@ _HERE = pathlib.Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libstencil.so"
 UNIQUE_ID_BYTES = 128
 
-ST_OK, ST_EINVAL, ST_ECUDA, ST_ENCCL, ST_ENOTSUP, ST_EINTERNAL = range(6)
-_STATUS = {1: "EINVAL", 2: "ECUDA", 3: "ENCCL", 4: "ENOTSUP", 5: "EINTERNAL"}
+ST_OK, ST_EINVAL, ST_ECUDA, ST_ENCCL, ST_ENOTSUP, ST_EINTERNAL, ST_ETIMEDOUT = range(7)
+_STATUS = {1: "EINVAL", 2: "ECUDA", 3: "ENCCL", 4: "ENOTSUP", 5: "EINTERNAL", 6: "ETIMEDOUT"}
 
 _lib = None
 
@@ -62,6 +62,7 @@ _SIGS = {
     "st_comm_init": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, _i32, _vp, _i32]),
     "st_comm_destroy": (ctypes.c_int, [_vp]),
     "st_comm_from_nccl": (ctypes.c_int, [ctypes.POINTER(_vp), _vp, _i32]),
+    "st_comm_wait": (ctypes.c_int, [_vp, _vp, _i32]),
     "st_comm_init_local": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, ctypes.POINTER(_i32)]),
     "st_comm_bind": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), _i32, _i64]),
     "st_comm_init_ipc": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, _i32, _i32]),
@@ -184,6 +185,11 @@ class Comm:
         pg = group if group is not None else dist.group.WORLD
         backend = pg._get_backend(torch.device("cuda", device))
         return cls.from_nccl(int(backend._comm_ptr()), device)
+
+    def wait(self, stream=None, timeout_ms: int = 0) -> None:
+        """Failure detection: wait for the queued work (raises StencilError with code
+        ST_ETIMEDOUT if it is still pending after timeout_ms, ST_ENCCL on an async NCCL error)."""
+        _check(lib().st_comm_wait(self.handle, _stream_ptr(stream), int(timeout_ms)), "st_comm_wait")
 
     @classmethod
     def local_group(cls, nranks: int, devices=None) -> list["Comm"]:

@@ -9,8 +9,10 @@
 // sweep t overlaps the interior rows of sweep t.
 #include <cuda.h>
 
+#include <chrono>
 #include <cstring>
 #include <mutex>
+#include <thread>
 
 #include "comm.h"
 #include "common.cuh"
@@ -410,6 +412,45 @@ st_status st_comm_from_nccl(st_comm** out, void* nccl_comm, int32_t cuda_device)
   }
   *out = c;
   return ST_OK;
+}
+
+st_status st_comm_wait(st_comm* c, void* cuda_stream, int32_t timeout_ms) {
+  clear_error();
+  ST_RETURN_IF(!c, ST_EINVAL, "st_comm_wait: null comm");
+  ST_CHECK_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    bool pending = false;
+    for (cudaStream_t q : {s, c->comm_stream}) {
+      if (!q && q != s) continue;
+      const cudaError_t e = cudaStreamQuery(q);
+      if (e == cudaErrorNotReady) pending = true;
+      else ST_CHECK_CUDA(e);
+    }
+    if (c->nccl && !c->broken) {
+      ncclResult_t ar = ncclSuccess;
+      if (ncclCommGetAsyncError(c->nccl, &ar) != ncclSuccess || ar != ncclSuccess) {
+        c->broken = true;
+        if (!c->borrowed) ncclCommAbort(c->nccl), c->nccl = nullptr;
+        set_error("st_comm_wait: asynchronous NCCL error: %s", ncclGetErrorString(ar));
+        return ST_ENCCL;
+      }
+    }
+    if (!pending) return ST_OK;
+    const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0);
+    if (timeout_ms > 0 && ms.count() >= timeout_ms) {
+      if (c->nccl && !c->borrowed) {
+        ncclCommAbort(c->nccl);
+        c->nccl = nullptr;
+        c->broken = true;
+      }
+      set_error("st_comm_wait: rank %d: work still pending after %d ms (a neighbour did not join the swap?)",
+                c->rank, timeout_ms);
+      return ST_ETIMEDOUT;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(100));
+  }
 }
 
 st_status st_comm_init_local(st_comm** comms, int32_t nranks, const int32_t* devices) {

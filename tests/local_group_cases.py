@@ -219,7 +219,39 @@ def pencils_pw_case(py, pz, nx, ny, nz):
     return ok
 
 
+def late_rank_case():
+    """Failure detection: rank 1 does not join the swap; rank 0's
+    st_comm_wait reports ST_ETIMEDOUT instead of hanging or returning wrong data.
+    Then rank 1 joins late and the swap completes with the right ghost rows."""
+    P, nx, n, w = 2, 64, 16, 1
+    comms = st.Comm.local_group(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    bufs = []
+    for r in range(P):
+        t = torch.full((n + 2 * w, nx + 2), float(r + 1), dtype=torch.float64, device="cuda")
+        comms[r].bind([t], n)
+        bufs.append(t)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(streams[0]):
+        st.st_halo_exchange(comms[0], [bufs[0]], n, nx + 2, w)
+    timed_out = False
+    try:
+        comms[0].wait(streams[0], timeout_ms=300)
+    except st.StencilError as e:
+        timed_out = e.code == st.ST_ETIMEDOUT
+    with torch.cuda.stream(streams[1]):
+        st.st_halo_exchange(comms[1], [bufs[1]], n, nx + 2, w)
+    comms[0].wait(streams[0], timeout_ms=10000)
+    comms[1].wait(streams[1], timeout_ms=10000)
+    torch.cuda.synchronize()
+    ok = timed_out and bool((bufs[0][n + w:] == 2.0).all()) and bool((bufs[1][:w] == 1.0).all())
+    for c in comms:
+        c.close()
+    return ok
+
+
 CASES = {
+    "late_rank": late_rank_case,
     "pen_j3_2x1": lambda: pencils_j3_case(2, 1, 70, 40, 33, 6),
     "pen_j3_1x2": lambda: pencils_j3_case(1, 2, 70, 40, 33, 6),
     "pen_j3_2x2": lambda: pencils_j3_case(2, 2, 66, 37, 31, 7),

@@ -24,3 +24,11 @@ def test_local_group_equals_oracle(cuda_lib, case, fused):
     r = subprocess.run([sys.executable, str(HERE / "local_group_cases.py"), case], env=env, capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0 and "CASES OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+def test_late_rank_is_detected_not_hung(cuda_lib):
+    # st_comm_wait: a rank that never joins a swap surfaces as ST_ETIMEDOUT
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    r = subprocess.run([sys.executable, str(HERE / "local_group_cases.py"), "late_rank"], env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "CASES OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
