@@ -574,6 +574,7 @@ def main():
                          "bytes_per_pt_per_launch": JACOBI_BYTES_PER_PT, "sweeps_per_launch": pass_sweeps,
                          "launches_per_step": launches_per_step, "passes_per_step": passes_per_step,
                          "ms_per_pass": round(launch_ms, 5),
+                         "frac_of_nominal_8tbs": round(achieved_gbs / 8000.0, 4),
                          "effective_gbs_16B_per_update": round(effective_gbs, 1), "peak_source": peak_src},
             "e2e": e2e,
             "gpu_launches": launches,
