@@ -560,7 +560,8 @@ def main():
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
+            "ms_per_step_runs": [round(t, 3) for t in times], "higher_is_better": True,
             "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SplitMix64 seed 42, SURVEY.md §8(d) recipe)",
             "config": {"workload": f"jacobi2d_{n_glob}x{n_glob}_fp64_{sweeps}sweeps"
