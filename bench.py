@@ -246,12 +246,28 @@ def main():
             comm = st.Comm.from_process_group(local)
         else:  # IPC transport: gloo carries only the control plane (blobs, barriers, max)
             dist.init_process_group("gloo")
+            # probe: map the neighbours, run one real swap on a side stream and check the
+            # ghosts; every rank falls back together (the NCCL transport is the other GPU
+            # path, not a CPU fallback) if any rank failed
+            ok, err = 1, ""
             try:
                 comm = st.Comm.ipc_from_process_group(local)
-                probe = torch.zeros(8, 4, dtype=torch.float64, device=dev)
-                comm.bind_ipc([probe], 2)  # collective: fails on every rank if IPC mapping does not work
-            except Exception as e:  # the NCCL transport is the other GPU path, not a CPU fallback
-                print(f"[bench] IPC transport unavailable ({e}); using NCCL", file=sys.stderr)
+                probe = torch.full((8, 4), float(rank), dtype=torch.float64, device=dev)
+                comm.bind_ipc([probe], 2)
+                ps = torch.cuda.Stream()
+                st.st_halo_exchange(comm, [probe], 2, 4, 1, stream=ps)
+                comm.wait(ps, timeout_ms=30000)
+                if rank > 0:
+                    ok &= int(bool((probe[0] == rank - 1).all()))
+                if rank < world - 1:
+                    ok &= int(bool((probe[3] == rank + 1).all()))
+            except Exception as e:
+                ok, err = 0, str(e)
+            flag = torch.tensor([ok], dtype=torch.int32)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                print(f"[bench] IPC transport unavailable ({err or 'a rank failed the probe swap'}); using NCCL",
+                      file=sys.stderr)
                 comm = st.Comm.from_process_group(local)
                 args.transport = "nccl"
     assert world == args.gpus or world == 1, "--gpus must match the torchrun world size"
