@@ -59,6 +59,9 @@ def _load():
     lib.or_gauss_seidel2d.argtypes = [_dp, _i64, _i64, _i64, _i64]
     lib.or_pw_points.restype = ctypes.c_int
     lib.or_pw_points.argtypes = [_dp] * 3 + [_i64] * 4 + [_dbl, _dbl] + [_dp] * 4 + [_dp, _i64, _dp]
+    lib.or_stencil2d.restype = ctypes.c_int
+    lib.or_stencil2d.argtypes = [_dp, _dp, _i64, _i64, _i64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, _i64,
+                                 ctypes.c_int]
     _lib = lib
     return lib
 
@@ -217,3 +220,28 @@ def gauss_seidel2d(a0: np.ndarray, iters: int, nx: int | None = None) -> np.ndar
     if _load().or_gauss_seidel2d(a.ctypes.data, nx, ny, ld, iters) < 0:
         raise ValueError("or_gauss_seidel2d: bad arguments")
     return a
+
+
+def stencil_halo(offsets) -> int:
+    """R = max |offset| (input bounds = output bounds widened by the offsets)."""
+    return max(max(abs(int(dy)), abs(int(dx))) for dy, dx in offsets)
+
+
+def stencil2d(a0: np.ndarray, offsets, coeffs, iters: int, nx: int | None = None,
+              threads: int | None = None) -> np.ndarray:
+    """`iters` sweeps of the generic linear stencil sum_i c_i a(y+dy_i, x+dx_i), left to right
+    (reading R23). a0: (ny + 2R) x ld padded field, R = stencil_halo."""
+    assert a0.dtype == np.float64 and a0.ndim == 2 and a0.flags.c_contiguous
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.int32).reshape(-1, 2))
+    c = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float64))
+    assert len(off) == len(c) >= 1
+    R = stencil_halo(off)
+    ny, ld = a0.shape[0] - 2 * R, a0.shape[1]
+    nx = ld - 2 * R if nx is None else nx
+    a = a0.copy()
+    b = np.empty_like(a)
+    rc = _load().or_stencil2d(a.ctypes.data, b.ctypes.data, nx, ny, ld, off.ctypes.data, c.ctypes.data, len(c),
+                              iters, threads or default_threads())
+    if rc < 0:
+        raise ValueError("or_stencil2d: bad arguments")
+    return b if rc == 1 else a

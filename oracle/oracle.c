@@ -40,6 +40,11 @@
  *                      inner, so (y-1, x) and (y, x-1) are this sweep's values
  *                      and (y+1, x), (y, x+1) the previous sweep's
  *                      (lexicographic Gauss-Seidel).
+ *   or_stencil2d       generic linear stencil.apply (PAPER.md:107-126 apply/access,
+ *                      offsets from the discovery pass PAPER.md:149-191, 185):
+ *                      out = c_0*a(off_0) + c_1*a(off_1) + ... left to right;
+ *                      value semantics; R-wide Dirichlet ring (R = max |offset|,
+ *                      SPEC.md:197-205). Reading R23 of DESIGN.md.
  *   or_pencils_jacobi3d / or_pencils_pw
  *                      2-D (y, z) process grid ("decompose the 3D space into
  *                      two dimensions"): Py x Pz blocks with one
@@ -578,4 +583,48 @@ int or_gauss_seidel2d(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t ite
         a[IDX2(y, x, ld)] = sum * 0.25;
       }
   return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Generic linear 2-D stencil.apply (reading R23 of DESIGN.md)                 */
+/* ------------------------------------------------------------------------- */
+
+/* The stencil dialect's apply (stencil.access at constant
+ * offsets inside an apply region) for the loop nests the discovery pass
+ * extracts (Listing 3; RHS offsets PAPER.md:185), restricted
+ * to linear right-hand sides:
+ *   out(y,x) = c_0*a(y+dy_0, x+dx_0) + c_1*a(y+dy_1, x+dx_1) + ...
+ * evaluated left to right as written (Fortran order, one rounding per product
+ * and per sum, no contraction). Value semantics: Jacobi double
+ * buffering. Halo width R = max |offset| (input bounds = output bounds widened
+ * by the offsets); the R-wide ring is never written.
+ * a, b: (ny + 2R) rows x ld, interior rows R..R+ny-1, columns R..R+nx-1.
+ * off = [dy_0, dx_0, dy_1, dx_1, ...]. Returns 1 if the result is in b, 0 if in a. */
+int or_stencil2d(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, const int32_t* off,
+                 const double* c, int32_t n, int64_t iters, int nthreads) {
+  if (!a || !b || !off || !c || n < 1 || nx < 1 || ny < 1 || iters < 0) return -1;
+  int64_t R = 0;
+  for (int32_t i = 0; i < 2 * n; ++i) {
+    int64_t m = off[i] < 0 ? -off[i] : off[i];
+    if (m > R) R = m;
+  }
+  if (ld < nx + 2 * R) return -1;
+  if (nthreads < 1) nthreads = 1;
+  memcpy(b, a, sizeof(double) * (size_t)((ny + 2 * R) * ld));
+  double* src = a;
+  double* dst = b;
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+    for (int64_t y = R; y < R + ny; ++y)
+      for (int64_t x = R; x < R + nx; ++x) {
+        double acc = c[0] * src[IDX2(y + off[0], x + off[1], ld)];
+        for (int32_t i = 1; i < n; ++i) {
+          double t = c[i] * src[IDX2(y + off[2 * i], x + off[2 * i + 1], ld)];
+          acc = acc + t;
+        }
+        dst[IDX2(y, x, ld)] = acc;
+      }
+    double* t = src; src = dst; dst = t;
+  }
+  return (int)(iters & 1);
 }
