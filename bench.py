@@ -215,6 +215,7 @@ def main():
     ap.add_argument("--no-j3", action="store_true")
     ap.add_argument("--j3-sweeps", type=int, default=100, help="3-D 7-point Jacobi sweeps timed (512^3)")
     ap.add_argument("--no-gs", action="store_true")
+    ap.add_argument("--no-generic", action="store_true")
     ap.add_argument("--gs-sweeps", type=int, default=100, help="in-place Gauss-Seidel sweeps timed (16384^2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-e2e-pipeline", action="store_true", help="e2e: copies and compute strictly serial")
@@ -547,6 +548,40 @@ def main():
                                   f"definition); {dt:.2f} s"}
         del ags, ws
 
+    # ------------------------------------------------------------------ generic stencil.apply executor (R23)
+    gen = None
+    if world == 1 and not args.no_generic:
+        ng, gsw = 16384, 20
+        offs, coefs = [(-1, 0), (1, 0), (0, -1), (0, 1)], [0.25, 0.25, 0.25, 0.25]  # Listing 1, generic form
+        ag = torch.from_numpy(si.jacobi2d_grid(ng, ng)).to(dev)
+        bg = torch.empty_like(ag)
+        st.st_stencil2d_run(ag, bg, offs, coefs, 2)
+        torch.cuda.synchronize()
+        sl0 = st.launch_count()
+        ev0.record(stream)
+        st.st_stencil2d_run(ag, bg, offs, coefs, gsw)
+        ev1.record(stream)
+        ev1.synchronize()
+        g_ms = ev0.elapsed_time(ev1)
+        g_gbs = JACOBI_BYTES_PER_PT * ng * ng * gsw / (g_ms / 1e3) / 1e9
+        gen = {"workload": f"stencil2d_generic_5pt_{ng}x{ng}_fp64_{gsw}sweeps",
+               "value": round(ng * ng * gsw / (g_ms / 1e3) / 1e9, 3), "unit": UNIT, "ms_per_step": round(g_ms, 3),
+               "gpu_launches": st.launch_count() - sl0,
+               "roofline": {"bound": "hbm", "kernel": "stencil2d_kernel", "achieved": round(g_gbs, 1),
+                            "peak": hbm_peak, "unit": "GB/s", "frac": round(g_gbs / hbm_peak, 4),
+                            "traffic": ncu_traffic("stencil2d_kernel"), "bytes_per_pt": JACOBI_BYTES_PER_PT,
+                            "peak_source": peak_src}}
+        if not args.no_cpu:
+            import oracle
+            _, cores = host_info()
+            a_np = si.jacobi2d_grid(ng, ng)
+            t0 = time.perf_counter()
+            oracle.stencil2d(a_np, offs, coefs, 1, threads=cores)
+            dt = time.perf_counter() - t0
+            gen["cpu_baseline"] = {"value": round(ng * ng / dt / 1e9, 4), "unit": UNIT, "cores": cores,
+                                   "kind": "oracle", "sample": f"1 sweep of the 16384^2 grid; {dt:.2f} s"}
+        del ag, bg
+
     # ------------------------------------------------------------------ C1: 64^2 + ring, 100 sweeps (latency-bound)
     c1 = None
     if world == 1:
@@ -600,6 +635,7 @@ def main():
             "pw_advect3d": pw,
             "jacobi3d": j3,
             "gauss_seidel2d": gs,
+            "stencil2d_generic": gen,
             "c1": c1,
         }
         print(json.dumps(out), flush=True)

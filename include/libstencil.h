@@ -255,6 +255,23 @@ st_status st_jacobi2d_run(double* a, double* b, int64_t nx, int64_t ny_local, in
                           int32_t halo, int64_t iters, int32_t tblock, st_comm* comm,
                           void* cuda_stream, int32_t* result_in_b);
 
+/* Generic linear 2-D stencil.apply (reading R23 of DESIGN.md; NEXT #4): the
+ * stencil dialect's apply over constant-offset accesses of a
+ * loop nest the discovery pass extracts (RHS offsets
+ * PAPER.md:185), for linear right-hand sides:
+ *     out(y,x) = c_0*a(y+dy_0, x+dx_0) + c_1*a(y+dy_1, x+dx_1) + ...
+ * evaluated left to right, one rounding per product and per sum (no FMA).
+ * `offsets` (HOST, nterms x {dy, dx}, |offset| <= 8) and `coeffs` (HOST,
+ * nterms <= 32) are copied at the call. Halo R = max |offset|:
+ * a, b are (ny + 2R) rows x ld (ld >= nx + 2R), interior rows R..R+ny-1 and
+ * columns R..R+nx-1; the R-wide ring is a fixed Dirichlet boundary. Value
+ * semantics (Jacobi ping-pong): the library copies a -> b first; after `iters`
+ * sweeps the result is in b iff (*result_in_b = iters & 1). Errors as
+ * st_jacobi2d_run (ST_EINVAL before anything is enqueued). */
+st_status st_stencil2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, const int32_t* offsets,
+                           const double* coeffs, int32_t nterms, int64_t iters, void* cuda_stream,
+                           int32_t* result_in_b);
+
 /* Listing 1 taken literally (R22; NEXT #4): `iters`
  * IN-PLACE lexicographic Gauss-Seidel sweeps of `a` ((ny+2) rows x ld, ring =
  * Dirichlet): rows in increasing y, columns in increasing x, each point

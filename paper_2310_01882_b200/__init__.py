@@ -63,6 +63,8 @@ _SIGS = {
     "st_comm_destroy": (ctypes.c_int, [_vp]),
     "st_comm_from_nccl": (ctypes.c_int, [ctypes.POINTER(_vp), _vp, _i32]),
     "st_comm_wait": (ctypes.c_int, [_vp, _vp, _i32]),
+    "st_stencil2d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp,
+                                        ctypes.POINTER(_i32)]),
     "st_comm_init_local": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, ctypes.POINTER(_i32)]),
     "st_comm_bind": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), _i32, _i64]),
     "st_comm_init_ipc": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, _i32, _i32]),
@@ -416,6 +418,30 @@ def st_gauss_seidel2d_run(a, iters: int, nx: int | None = None, workspace=None, 
     return a
 
 
+def st_stencil2d_run(a, b, offsets, coeffs, iters: int, nx: int | None = None, stream=None):
+    """Generic linear stencil.apply (reading R23): `iters` sweeps of
+    sum_i coeffs[i] * a(y + dy_i, x + dx_i), left to right, on (ny + 2R, ld) float64 CUDA
+    tensors (R = max |offset|). Returns whichever of a, b holds the result."""
+    _f64_cuda(a, "a")
+    _f64_cuda(b, "b")
+    if a.dim() != 2 or a.shape != b.shape or a.stride() != b.stride() or a.stride(1) != 1:
+        raise ValueError("a, b: same-shape 2-D row-major tensors")
+    offs = [int(v) for dy_dx in offsets for v in dy_dx]
+    n = len(offs) // 2
+    if n < 1 or len(coeffs) != n:
+        raise ValueError("one coefficient per (dy, dx) offset")
+    R = max(abs(v) for v in offs)
+    ld = a.stride(0)
+    ny = a.shape[0] - 2 * R
+    nx = a.shape[1] - 2 * R if nx is None else nx
+    o = (_i32 * (2 * n))(*offs)
+    c = (_dbl * n)(*[float(v) for v in coeffs])
+    in_b = _i32(0)
+    _check(lib().st_stencil2d_run(a.data_ptr(), b.data_ptr(), nx, ny, ld, ctypes.cast(o, _vp), ctypes.cast(c, _vp),
+                                  n, iters, _stream_ptr(stream), ctypes.byref(in_b)), "st_stencil2d_run")
+    return b if in_b.value else a
+
+
 def st_selftest_div6(x) -> int:
     """Number of x (float64 CUDA tensor) where the kernels' fast x/6 differs from IEEE division."""
     import torch
@@ -429,5 +455,6 @@ def st_selftest_div6(x) -> int:
 jacobi2d = st_jacobi2d_run
 jacobi3d = st_jacobi3d_run
 gauss_seidel2d = st_gauss_seidel2d_run
+stencil2d = st_stencil2d_run
 pw_advect3d = st_pw_advect3d
 halo_exchange = st_halo_exchange

@@ -220,6 +220,32 @@ st_status st_jacobi2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
   return run_schedule(ops, comm, a, b, nx, ny, ld, halo, s);
 }
 
+st_status st_stencil2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, const int32_t* offsets,
+                           const double* coeffs, int32_t nterms, int64_t iters, void* cuda_stream,
+                           int32_t* result_in_b) {
+  clear_error();
+  ST_RETURN_IF(!a || !b || !offsets || !coeffs, ST_EINVAL, "st_stencil2d_run: null pointer");
+  ST_RETURN_IF(nterms < 1 || nterms > kStencilMaxTerms, ST_EINVAL, "st_stencil2d_run: %d terms (1..%d)", nterms,
+               kStencilMaxTerms);
+  int64_t R = 0;
+  for (int i = 0; i < 2 * nterms; ++i) {
+    const int64_t m = offsets[i] < 0 ? -(int64_t)offsets[i] : offsets[i];
+    ST_RETURN_IF(m > kStencilMaxOffset, ST_EINVAL, "st_stencil2d_run: |offset| %lld > %d", (long long)m,
+                 kStencilMaxOffset);
+    R = std::max(R, m);
+  }
+  ST_RETURN_IF(nx < 1 || ny < 1 || ld < nx + 2 * R || iters < 0, ST_EINVAL,
+               "st_stencil2d_run: bad extents (nx %lld, ny %lld, ld %lld, halo %lld)", (long long)nx, (long long)ny,
+               (long long)ld, (long long)R);
+  const size_t bytes = (size_t)(ny + 2 * R) * (size_t)ld * sizeof(double);
+  ST_RETURN_IF(overlaps(a, bytes, b, bytes), ST_EINVAL, "st_stencil2d_run: a and b overlap");
+  ST_TRY(check_device_ptr(a, "a"));
+  ST_TRY(check_device_ptr(b, "b"));
+  if (result_in_b) *result_in_b = (int32_t)(iters & 1);
+  if (iters == 0) return ST_OK;
+  return stencil2d_run(a, b, nx, ny, ld, R, offsets, coeffs, nterms, iters, static_cast<cudaStream_t>(cuda_stream));
+}
+
 int64_t st_gauss_seidel2d_workspace_bytes(int64_t ny) { return ny < 1 ? 0 : gauss_seidel2d_workspace_bytes(ny); }
 
 st_status st_gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters, void* workspace,

@@ -22,6 +22,12 @@ struct Remote {
   int64_t delta = 0;
 };
 
+// ------------------------------------------------ generic 2-D stencil ---
+constexpr int kStencilMaxTerms = 32;
+constexpr int kStencilMaxOffset = 8;
+st_status stencil2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t R, const int32_t* off,
+                        const double* coeffs, int32_t n, int64_t iters, cudaStream_t s);
+
 // ----------------------------------------------------------- Jacobi 2-D ---
 // One sweep dst = J(src) over buffer rows [y_lo, y_hi] (buffer row indices,
 // inclusive) and interior columns 1..nx; columns 0 and nx+1 are passed through
@@ -92,11 +98,13 @@ st_status build_jacobi_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_
 // preload all kernels at creation.
 st_status jacobi2d_preload();
 st_status jacobi3d_preload();
+st_status stencil2d_preload();
 st_status pw_advect3d_preload();
 inline st_status preload_kernels() {
   ST_TRY(jacobi2d_preload());
   ST_TRY(gauss_seidel2d_preload());
   ST_TRY(jacobi3d_preload());
+  ST_TRY(stencil2d_preload());
   return pw_advect3d_preload();
 }
 

@@ -1,0 +1,66 @@
+"""GPU parity of the generic linear stencil.apply executor (reading R23;
+st_stencil2d_run) against the CPU oracle — bitwise: both evaluate the terms
+left to right with one rounding per product and per sum."""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+rng = np.random.default_rng(185)
+
+STENCILS = {
+    "listing1_generic": ([(-1, 0), (1, 0), (0, -1), (0, 1)], [0.25, 0.25, 0.25, 0.25]),
+    "nine_point_R2": ([(0, 0), (-2, 0), (2, 0), (0, -2), (0, 2), (-1, -1), (1, 1), (-1, 1), (1, -1)],
+                      [0.2, 0.1, 0.1, 0.1, 0.1, 0.1, 0.1, 0.1, 0.1]),
+    "asymmetric_R3": ([(3, -2), (-1, 3), (0, 0), (0, -1)], [0.7, -0.3, 0.45, 0.15]),
+    "identity": ([(0, 0)], [1.0]),
+    "shift": ([(0, 1)], [1.0]),
+    "max_offset_8": ([(8, 0), (-8, 0), (0, 8), (0, -8), (0, 0)], [0.1, 0.2, 0.3, 0.15, 0.25]),
+}
+
+
+def run(st, a_np, offs, coefs, iters, nx=None):
+    import torch
+    a = torch.from_numpy(a_np).cuda()
+    b = torch.full_like(a, float("nan"))
+    r = st.st_stencil2d_run(a, b, offs, coefs, iters, nx=nx)
+    torch.cuda.synchronize()
+    assert (r is b) == bool(iters & 1)
+    return r.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", list(STENCILS))
+@pytest.mark.parametrize("ny,nx,pad,iters", [(1, 1, 0, 3), (7, 33, 3, 2), (40, 65, 0, 5), (97, 130, 2, 4),
+                                             (257, 300, 4, 3)])
+def test_stencil_bitwise(cuda_lib, name, ny, nx, pad, iters):
+    offs, coefs = STENCILS[name]
+    R = oracle.stencil_halo(offs)
+    a = rng.standard_normal((ny + 2 * R, nx + 2 * R + pad))
+    want = oracle.stencil2d(a, offs, coefs, iters, nx=nx)
+    got = run(cuda_lib, a, offs, coefs, iters, nx=nx)
+    assert np.array_equal(got[:, :nx + 2 * R], want[:, :nx + 2 * R])
+
+
+def test_random_stencils_bitwise(cuda_lib):
+    for _ in range(10):
+        n = int(rng.integers(1, 33))
+        R = int(rng.integers(1, 5))
+        offs = [(int(rng.integers(-R, R + 1)), int(rng.integers(-R, R + 1))) for _ in range(n)]
+        coefs = list(rng.standard_normal(n))
+        Rr = oracle.stencil_halo(offs)
+        ny, nx = int(rng.integers(1, 120)), int(rng.integers(1, 150))
+        a = rng.standard_normal((ny + 2 * Rr, nx + 2 * Rr))
+        assert np.array_equal(run(cuda_lib, a, offs, coefs, 3), oracle.stencil2d(a, offs, coefs, 3))
+
+
+def test_rejects_bad_arguments(cuda_lib):
+    import torch
+    a = torch.zeros(10, 10, dtype=torch.float64, device="cuda")
+    b = torch.zeros_like(a)
+    with pytest.raises(cuda_lib.StencilError):
+        cuda_lib.st_stencil2d_run(a, b, [(0, 9)], [1.0], 1)  # |offset| > 8
+    with pytest.raises(cuda_lib.StencilError):
+        cuda_lib.st_stencil2d_run(a, b, [(0, 5)], [1.0], 1)  # halo 5 leaves no interior
+    with pytest.raises(cuda_lib.StencilError):
+        cuda_lib.st_stencil2d_run(a, a, [(0, 1)], [1.0], 1)  # a and b overlap

@@ -40,4 +40,8 @@ del a3, b3
 ag = torch.from_numpy(si.jacobi2d_grid(n, n)).cuda()
 st.st_gauss_seidel2d_run(ag, args.gs_sweeps)
 torch.cuda.synchronize()
+del ag
+ag = torch.rand(n + 2, n + 2, dtype=torch.float64, device="cuda")
+st.st_stencil2d_run(ag, torch.empty_like(ag), [(-1, 0), (1, 0), (0, -1), (0, 1)], [0.25] * 4, 2)
+torch.cuda.synchronize()
 print("done")

@@ -28,5 +28,9 @@ for nx, ny, ld, iters in ((200, 95, 202, 3), (65, 33, 67, 2), (1000, 130, 1002, 
 for nx, ny in ((64, 64), (37, 21)):  # register-resident C1 kernel
     a = torch.from_numpy(si.jacobi2d_grid(nx, ny)).cuda()
     st.st_jacobi2d_run(a, torch.empty_like(a), 7)
+for offs in ([(-1, 0), (1, 0), (0, -1), (0, 1)], [(3, -2), (-1, 3), (0, 0), (8, 0)]):  # generic stencil
+    R = max(max(abs(dy), abs(dx)) for dy, dx in offs)
+    a = torch.rand(37 + 2 * R, 45 + 2 * R, dtype=torch.float64, device="cuda")
+    st.st_stencil2d_run(a, torch.empty_like(a), offs, [0.5] * len(offs), 3)
 torch.cuda.synchronize()
 print("sanitize cases done")
