@@ -1,0 +1,101 @@
+"""Expression stencil oracle (NEXT #4: "offset list + expression", SURVEY.md §8(f);
+reading R24 of DESIGN.md).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py); shares nothing with the CUDA path.
+
+A Fortran loop body the discovery pass turns into a stencil.apply region
+(Listing 3; RHS accesses) is an
+arithmetic expression over accesses at constant offsets. Here it is written with
+a(dy, dx) for the access at row offset dy, column offset dx, numeric literals
+(binary64), + - * /, unary minus and parentheses, with C/Fortran/Python
+precedence and left associativity. Each sweep evaluates the expression with NumPy
+float64 arrays (elementwise, one IEEE rounding per operation, in parse order,
+never contracted) on the shifted views of the previous iterate (value semantics,
+PAPER.md:126). Halo R = max |offset|: the R-wide ring is fixed.
+"""
+from __future__ import annotations
+
+import ast
+import re
+
+import numpy as np
+
+_ACCESS = re.compile(r"a\(\s*(-?\d+)\s*,\s*(-?\d+)\s*\)")
+_ALLOWED = re.compile(r"^[\sa0-9.eE+\-*/(),]*$")
+
+
+def offsets(expr: str) -> list[tuple[int, int]]:
+    """The (dy, dx) accesses of the expression, in order of appearance."""
+    return [(int(dy), int(dx)) for dy, dx in _ACCESS.findall(expr)]
+
+
+def halo(expr: str) -> int:
+    offs = offsets(expr)
+    if not offs:
+        raise ValueError("expression has no a(dy, dx) access")
+    return max(max(abs(dy), abs(dx)) for dy, dx in offs)
+
+
+def check(expr: str) -> None:
+    """Accept only accesses, literals, + - * /, unary minus and parentheses."""
+    if not _ALLOWED.match(expr):
+        raise ValueError(f"expression has characters outside a(), digits, . e E + - * / ( ) ,: {expr!r}")
+    tree = ast.parse(expr, mode="eval")
+    for node in ast.walk(tree):
+        if isinstance(node, ast.Call):
+            if not (isinstance(node.func, ast.Name) and node.func.id == "a" and len(node.args) == 2):
+                raise ValueError("only a(dy, dx) calls are allowed")
+        elif isinstance(node, ast.BinOp):
+            if not isinstance(node.op, (ast.Add, ast.Sub, ast.Mult, ast.Div)):
+                raise ValueError("only + - * / are allowed")
+        elif isinstance(node, ast.UnaryOp):
+            if not isinstance(node.op, (ast.USub, ast.UAdd)):
+                raise ValueError("only unary +/- are allowed")
+        elif isinstance(node, ast.Constant):
+            if not isinstance(node.value, (int, float)) or isinstance(node.value, bool):
+                raise ValueError("only numeric literals are allowed")
+        elif not isinstance(node, (ast.Expression, ast.Name, ast.Load, ast.Add, ast.Sub, ast.Mult, ast.Div,
+                                   ast.USub, ast.UAdd)):
+            raise ValueError(f"unsupported syntax: {type(node).__name__}")
+
+
+class _FloatLiterals(ast.NodeTransformer):
+    """Every numeric literal outside an access is a binary64 value (as in the CUDA path,
+    where the generated source spells it as a double literal)."""
+
+    def visit_Call(self, node):
+        return node  # a(dy, dx): the offsets stay integers
+
+    def visit_Constant(self, node):
+        return ast.copy_location(ast.Constant(float(node.value)), node)
+
+
+def _compile(expr: str):
+    tree = ast.fix_missing_locations(_FloatLiterals().visit(ast.parse(expr, mode="eval")))
+    return compile(tree, "<stencil>", "eval")
+
+
+def stencil2d_expr(a0: np.ndarray, expr: str, iters: int, nx: int | None = None) -> np.ndarray:
+    """`iters` sweeps of the expression stencil on the padded field a0 ((ny + 2R) x ld)."""
+    check(expr)
+    R = halo(expr)
+    ny = a0.shape[0] - 2 * R
+    nx = a0.shape[1] - 2 * R if nx is None else nx
+    if ny < 1 or nx < 1:
+        raise ValueError("no interior")
+    code = _compile(expr)
+    cur = a0.copy()
+    for _ in range(iters):
+        def a(dy, dx, _c=cur):
+            return _c[R + dy:R + dy + ny, R + dx:R + dx + nx]
+        out = eval(code, {"__builtins__": {}}, {"a": a})
+        nxt = cur.copy()
+        nxt[R:R + ny, R:R + nx] = out
+        cur = nxt
+    return cur
+
+
+def eval_exact(expr: str, a_of):
+    """Evaluate the expression with a user access function (e.g. returning Fractions)."""
+    check(expr)
+    return eval(compile(ast.parse(expr, mode="eval"), "<stencil>", "eval"), {"__builtins__": {}}, {"a": a_of})

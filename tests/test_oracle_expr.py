@@ -1,0 +1,70 @@
+"""Pins of the expression-stencil oracle (reading R24): Listing 1 written as an
+expression equals the pinned C Jacobi oracle bitwise; linear expressions equal
+the C generic-stencil oracle bitwise; nonlinear expressions on integer data equal
+exact rational evaluation; the parser rejects anything but accesses, literals,
++ - * / and parentheses."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import expr as ox
+
+rng = np.random.default_rng(149)
+
+
+def test_listing1_expression_equals_jacobi_oracle():
+    # Listing 1: data(j,i-1)+data(j,i+1)+data(j-1,i)+data(j+1,i) with j = x, i = y
+    e = "(a(-1,0) + a(1,0) + a(0,-1) + a(0,1)) * 0.25"
+    a = rng.standard_normal((35, 41))
+    assert np.array_equal(ox.stencil2d_expr(a, e, 7), oracle.jacobi2d(a, 7))
+
+
+def test_linear_expression_equals_generic_oracle():
+    offs = [(2, -1), (0, 0), (-1, 2), (1, 1)]
+    coefs = [0.3, -0.7, 0.125, 1.5]
+    e = " + ".join(f"{c!r}*a({dy},{dx})" for (dy, dx), c in zip(offs, coefs))
+    a = rng.standard_normal((30, 33))
+    assert np.array_equal(ox.stencil2d_expr(a, e, 4), oracle.stencil2d(a, offs, coefs, 4))
+
+
+@pytest.mark.parametrize("e", [
+    "a(0,1)*a(0,-1) - a(1,0)",
+    "-(a(1,1) - 2*a(0,0)) * (a(-1,-1) + 3)",
+    "(a(0,0) + a(2,0))*(a(0,0) - a(-2,0)) - a(0,2)*4",
+])
+def test_nonlinear_exact_rationals(e):
+    # integer data, one sweep: every intermediate is an exact small integer in binary64
+    R = ox.halo(e)
+    a = rng.integers(-9, 10, size=(6 + 2 * R, 7 + 2 * R)).astype(np.float64)
+    got = ox.stencil2d_expr(a, e, 1)
+    want = a.copy()
+    for y in range(R, R + 6):
+        for x in range(R, R + 7):
+            want[y, x] = float(ox.eval_exact(e, lambda dy, dx: Fraction(a[y + dy, x + dx])))
+    assert np.array_equal(got, want)
+
+
+def test_division_and_literals_are_binary64():
+    # 1/3 is float division (not C integer division) and literals are binary64 nearest
+    a = np.full((3, 3), 3.0)
+    got = ox.stencil2d_expr(a, "a(0,0) * (1/3) + 0.1", 1)
+    assert got[1, 1] == 3.0 * (1.0 / 3.0) + 0.1
+
+
+@pytest.mark.parametrize("bad", ["a(0,0) ** 2", "a(0,0) if 1 else 0", "b(0,0)", "a(0,0); import os",
+                                 "abs(a(0,0))", "a(0,0) % 2", "a(0)"])
+def test_rejects_unsupported_syntax(bad):
+    with pytest.raises((ValueError, SyntaxError)):
+        ox.stencil2d_expr(np.zeros((5, 5)), bad, 1)
+
+
+def test_ring_fixed_and_offsets_parsed():
+    e = "a(-3,1) + 0.5*a(2,-2)"
+    assert ox.offsets(e) == [(-3, 1), (2, -2)] and ox.halo(e) == 3
+    a = rng.standard_normal((20, 18))
+    got = ox.stencil2d_expr(a, e, 3)
+    mask = np.ones_like(a, dtype=bool)
+    mask[3:-3, 3:-3] = False
+    assert np.array_equal(got[mask], a[mask])
