@@ -272,6 +272,23 @@ st_status st_stencil2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t
                            const double* coeffs, int32_t nterms, int64_t iters, void* cuda_stream,
                            int32_t* result_in_b);
 
+/* Expression stencil (reading R24 of DESIGN.md; NEXT #4 "offset list +
+ * expression -> NVRTC-compiled kernel"): `expr` is the loop body's right-hand
+ * side over accesses a(dy, dx) (|offset| <= 8), numeric literals, + - * /,
+ * unary signs and parentheses, e.g. Listing 1:
+ *     "(a(-1,0) + a(1,0) + a(0,-1) + a(0,1)) * 0.25"
+ * C/Fortran precedence, left associative; literals are binary64 (never integer
+ * arithmetic); every operation rounds once, none is contracted. The text is
+ * validated and translated token by token, compiled once per (expression,
+ * device) with NVRTC for sm_100a (--fmad=false; loaded with dlopen:
+ * ST_ENOTSUP without libnvrtc) and cached for the process. Layout, halo
+ * R = max |offset|, ring, value semantics and result_in_b as st_stencil2d_run.
+ * st_stencil2d_expr_halo validates `expr` on the host only and returns R
+ * (ST_EINVAL with the reason in st_last_error for anything outside the grammar). */
+st_status st_stencil2d_expr_halo(const char* expr, int32_t* halo);
+st_status st_stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, const char* expr,
+                                int64_t iters, void* cuda_stream, int32_t* result_in_b);
+
 /* Listing 1 taken literally (R22; NEXT #4): `iters`
  * IN-PLACE lexicographic Gauss-Seidel sweeps of `a` ((ny+2) rows x ld, ring =
  * Dirichlet): rows in increasing y, columns in increasing x, each point

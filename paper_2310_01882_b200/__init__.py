@@ -65,6 +65,9 @@ _SIGS = {
     "st_comm_wait": (ctypes.c_int, [_vp, _vp, _i32]),
     "st_stencil2d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp,
                                         ctypes.POINTER(_i32)]),
+    "st_stencil2d_expr_halo": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_i32)]),
+    "st_stencil2d_expr_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, ctypes.c_char_p, _i64, _vp,
+                                             ctypes.POINTER(_i32)]),
     "st_comm_init_local": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, ctypes.POINTER(_i32)]),
     "st_comm_bind": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), _i32, _i64]),
     "st_comm_init_ipc": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, _i32, _i32]),
@@ -442,6 +445,30 @@ def st_stencil2d_run(a, b, offsets, coeffs, iters: int, nx: int | None = None, s
     return b if in_b.value else a
 
 
+def st_stencil2d_expr_halo(expr: str) -> int:
+    """Validates an expression stencil on the host and returns its halo R = max |offset|."""
+    r = _i32(0)
+    _check(lib().st_stencil2d_expr_halo(expr.encode(), ctypes.byref(r)), "st_stencil2d_expr_halo")
+    return r.value
+
+
+def st_stencil2d_expr_run(a, b, expr: str, iters: int, nx: int | None = None, stream=None):
+    """`iters` sweeps of the expression stencil (reading R24; NVRTC-compiled, cached) on
+    (ny + 2R, ld) float64 CUDA tensors. Returns whichever of a, b holds the result."""
+    _f64_cuda(a, "a")
+    _f64_cuda(b, "b")
+    if a.dim() != 2 or a.shape != b.shape or a.stride() != b.stride() or a.stride(1) != 1:
+        raise ValueError("a, b: same-shape 2-D row-major tensors")
+    R = st_stencil2d_expr_halo(expr)
+    ld = a.stride(0)
+    ny = a.shape[0] - 2 * R
+    nx = a.shape[1] - 2 * R if nx is None else nx
+    in_b = _i32(0)
+    _check(lib().st_stencil2d_expr_run(a.data_ptr(), b.data_ptr(), nx, ny, ld, expr.encode(), iters,
+                                       _stream_ptr(stream), ctypes.byref(in_b)), "st_stencil2d_expr_run")
+    return b if in_b.value else a
+
+
 def st_selftest_div6(x) -> int:
     """Number of x (float64 CUDA tensor) where the kernels' fast x/6 differs from IEEE division."""
     import torch
@@ -456,5 +483,6 @@ jacobi2d = st_jacobi2d_run
 jacobi3d = st_jacobi3d_run
 gauss_seidel2d = st_gauss_seidel2d_run
 stencil2d = st_stencil2d_run
+stencil2d_expr = st_stencil2d_expr_run
 pw_advect3d = st_pw_advect3d
 halo_exchange = st_halo_exchange

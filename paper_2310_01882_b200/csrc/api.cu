@@ -246,6 +246,35 @@ st_status st_stencil2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t
   return stencil2d_run(a, b, nx, ny, ld, R, offsets, coeffs, nterms, iters, static_cast<cudaStream_t>(cuda_stream));
 }
 
+st_status st_stencil2d_expr_halo(const char* expr, int32_t* halo) {
+  clear_error();
+  ST_RETURN_IF(!expr || !halo, ST_EINVAL, "st_stencil2d_expr_halo: null pointer");
+  std::string cexpr;
+  int64_t R = 0;
+  ST_TRY(stencil_expr_translate(expr, &cexpr, &R));
+  *halo = (int32_t)R;
+  return ST_OK;
+}
+
+st_status st_stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, const char* expr,
+                                int64_t iters, void* cuda_stream, int32_t* result_in_b) {
+  clear_error();
+  ST_RETURN_IF(!a || !b || !expr, ST_EINVAL, "st_stencil2d_expr_run: null pointer");
+  std::string cexpr;
+  int64_t R = 0;
+  ST_TRY(stencil_expr_translate(expr, &cexpr, &R));
+  ST_RETURN_IF(nx < 1 || ny < 1 || ld < nx + 2 * R || iters < 0, ST_EINVAL,
+               "st_stencil2d_expr_run: bad extents (nx %lld, ny %lld, ld %lld, halo %lld)", (long long)nx,
+               (long long)ny, (long long)ld, (long long)R);
+  const size_t bytes = (size_t)(ny + 2 * R) * (size_t)ld * sizeof(double);
+  ST_RETURN_IF(overlaps(a, bytes, b, bytes), ST_EINVAL, "st_stencil2d_expr_run: a and b overlap");
+  ST_TRY(check_device_ptr(a, "a"));
+  ST_TRY(check_device_ptr(b, "b"));
+  if (result_in_b) *result_in_b = (int32_t)(iters & 1);
+  if (iters == 0) return ST_OK;
+  return stencil2d_expr_run(a, b, nx, ny, ld, R, cexpr, iters, static_cast<cudaStream_t>(cuda_stream));
+}
+
 int64_t st_gauss_seidel2d_workspace_bytes(int64_t ny) { return ny < 1 ? 0 : gauss_seidel2d_workspace_bytes(ny); }
 
 st_status st_gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters, void* workspace,

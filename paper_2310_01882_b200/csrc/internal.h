@@ -2,6 +2,8 @@
 // the kernel translation units. Not part of the public ABI.
 #pragma once
 
+#include <string>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -27,6 +29,10 @@ constexpr int kStencilMaxTerms = 32;
 constexpr int kStencilMaxOffset = 8;
 st_status stencil2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t R, const int32_t* off,
                         const double* coeffs, int32_t n, int64_t iters, cudaStream_t s);
+
+st_status stencil_expr_translate(const char* expr, std::string* cexpr, int64_t* R);
+st_status stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t R,
+                             const std::string& cexpr, int64_t iters, cudaStream_t s);
 
 // ----------------------------------------------------------- Jacobi 2-D ---
 // One sweep dst = J(src) over buffer rows [y_lo, y_hi] (buffer row indices,

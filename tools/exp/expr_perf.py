@@ -1,0 +1,17 @@
+"""Throughput of NVRTC-compiled expression stencils on 16384^2 (and first-call compile time)."""
+import sys, pathlib, time
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent.parent))
+import torch
+import paper_2310_01882_b200 as st
+n = 16384
+for e in ("(a(-1,0)+a(1,0)+a(0,-1)+a(0,1))*0.25", "(a(0,0) + a(2,0))*(a(0,0) - a(-2,0)) / (1 + a(0,2)*a(0,2))"):
+    R = st.st_stencil2d_expr_halo(e)
+    a = torch.rand(n + 2 * R, n + 2 * R, dtype=torch.float64, device="cuda")
+    b = torch.empty_like(a)
+    t0 = time.perf_counter(); st.st_stencil2d_expr_run(a, b, e, 2); torch.cuda.synchronize(); tc = time.perf_counter() - t0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    it = 20
+    e0.record(); st.st_stencil2d_expr_run(a, b, e, it); e1.record(); e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    print(f"{e}: first call (compile) {tc:.2f} s; {n * n * it / (ms / 1e3) / 1e9:.1f} Gpts/s, "
+          f"{16 * n * n * it / (ms / 1e3) / 1e9:.0f} GB/s (16 B/pt)")

@@ -32,5 +32,7 @@ for offs in ([(-1, 0), (1, 0), (0, -1), (0, 1)], [(3, -2), (-1, 3), (0, 0), (8, 
     R = max(max(abs(dy), abs(dx)) for dy, dx in offs)
     a = torch.rand(37 + 2 * R, 45 + 2 * R, dtype=torch.float64, device="cuda")
     st.st_stencil2d_run(a, torch.empty_like(a), offs, [0.5] * len(offs), 3)
+a = torch.rand(41, 53, dtype=torch.float64, device="cuda")  # NVRTC expression stencil
+st.st_stencil2d_expr_run(a, torch.empty_like(a), "-(a(3,0) - 2*a(0,0)) / 3 + 0.1*a(-2,2)", 3)
 torch.cuda.synchronize()
 print("sanitize cases done")
