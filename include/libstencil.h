@@ -286,6 +286,14 @@ st_status st_stencil2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t
  * st_stencil2d_expr_halo validates `expr` on the host only and returns R
  * (ST_EINVAL with the reason in st_last_error for anything outside the grammar). */
 st_status st_stencil2d_expr_halo(const char* expr, int32_t* halo);
+/* The same for 3-D fields (x fastest, z slowest; R5): accesses
+ * a(dz, dy, dx); arrays (nz + 2R) planes x (ny + 2R) rows x ldx, interior
+ * planes/rows/columns R .. R+n-1. The paper's benchmark 1 is
+ * "(a(-1,0,0)+a(1,0,0)+a(0,-1,0)+a(0,1,0)+a(0,0,-1)+a(0,0,1))/6" (R20/R21).
+ * st_stencil_expr_info returns the halo and the access arity (2 or 3). */
+st_status st_stencil_expr_info(const char* expr, int32_t* halo, int32_t* dims);
+st_status st_stencil3d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t nz, int64_t ldx,
+                                const char* expr, int64_t iters, void* cuda_stream, int32_t* result_in_b);
 st_status st_stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, const char* expr,
                                 int64_t iters, void* cuda_stream, int32_t* result_in_b);
 

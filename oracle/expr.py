@@ -21,12 +21,25 @@ import re
 import numpy as np
 
 _ACCESS = re.compile(r"a\(\s*(-?\d+)\s*,\s*(-?\d+)\s*\)")
+_ACCESS3 = re.compile(r"a\(\s*(-?\d+)\s*,\s*(-?\d+)\s*,\s*(-?\d+)\s*\)")
 _ALLOWED = re.compile(r"^[\sa0-9.eE+\-*/(),]*$")
 
 
 def offsets(expr: str) -> list[tuple[int, int]]:
     """The (dy, dx) accesses of the expression, in order of appearance."""
     return [(int(dy), int(dx)) for dy, dx in _ACCESS.findall(expr)]
+
+
+def offsets3(expr: str) -> list[tuple[int, int, int]]:
+    """The (dz, dy, dx) accesses of a 3-D expression, in order of appearance."""
+    return [(int(dz), int(dy), int(dx)) for dz, dy, dx in _ACCESS3.findall(expr)]
+
+
+def halo3(expr: str) -> int:
+    offs = offsets3(expr)
+    if not offs:
+        raise ValueError("expression has no a(dz, dy, dx) access")
+    return max(max(abs(v) for v in o) for o in offs)
 
 
 def halo(expr: str) -> int:
@@ -43,8 +56,8 @@ def check(expr: str) -> None:
     tree = ast.parse(expr, mode="eval")
     for node in ast.walk(tree):
         if isinstance(node, ast.Call):
-            if not (isinstance(node.func, ast.Name) and node.func.id == "a" and len(node.args) == 2):
-                raise ValueError("only a(dy, dx) calls are allowed")
+            if not (isinstance(node.func, ast.Name) and node.func.id == "a" and len(node.args) in (2, 3)):
+                raise ValueError("only a(dy, dx) / a(dz, dy, dx) calls are allowed")
         elif isinstance(node, ast.BinOp):
             if not isinstance(node.op, (ast.Add, ast.Sub, ast.Mult, ast.Div)):
                 raise ValueError("only + - * / are allowed")
@@ -91,6 +104,27 @@ def stencil2d_expr(a0: np.ndarray, expr: str, iters: int, nx: int | None = None)
         out = eval(code, {"__builtins__": {}}, {"a": a})
         nxt = cur.copy()
         nxt[R:R + ny, R:R + nx] = out
+        cur = nxt
+    return cur
+
+
+def stencil3d_expr(a0: np.ndarray, expr: str, iters: int, nx: int | None = None) -> np.ndarray:
+    """`iters` sweeps of a 3-D expression stencil over a(dz, dy, dx) on the padded field
+    a0 ((nz + 2R) x (ny + 2R) x ldx, x fastest)."""
+    check(expr)
+    R = halo3(expr)
+    nz, ny = a0.shape[0] - 2 * R, a0.shape[1] - 2 * R
+    nx = a0.shape[2] - 2 * R if nx is None else nx
+    if min(nx, ny, nz) < 1:
+        raise ValueError("no interior")
+    code = _compile(expr)
+    cur = a0.copy()
+    for _ in range(iters):
+        def a(dz, dy, dx, _c=cur):
+            return _c[R + dz:R + dz + nz, R + dy:R + dy + ny, R + dx:R + dx + nx]
+        out = eval(code, {"__builtins__": {}}, {"a": a})
+        nxt = cur.copy()
+        nxt[R:R + nz, R:R + ny, R:R + nx] = out
         cur = nxt
     return cur
 

@@ -66,6 +66,9 @@ _SIGS = {
     "st_stencil2d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp,
                                         ctypes.POINTER(_i32)]),
     "st_stencil2d_expr_halo": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_i32)]),
+    "st_stencil_expr_info": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
+    "st_stencil3d_expr_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_char_p, _i64, _vp,
+                                             ctypes.POINTER(_i32)]),
     "st_stencil2d_expr_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, ctypes.c_char_p, _i64, _vp,
                                              ctypes.POINTER(_i32)]),
     "st_comm_init_local": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, ctypes.POINTER(_i32)]),
@@ -466,6 +469,34 @@ def st_stencil2d_expr_run(a, b, expr: str, iters: int, nx: int | None = None, st
     in_b = _i32(0)
     _check(lib().st_stencil2d_expr_run(a.data_ptr(), b.data_ptr(), nx, ny, ld, expr.encode(), iters,
                                        _stream_ptr(stream), ctypes.byref(in_b)), "st_stencil2d_expr_run")
+    return b if in_b.value else a
+
+
+def st_stencil_expr_info(expr: str) -> tuple[int, int]:
+    """(halo R, access arity 2 or 3) of a validated expression stencil."""
+    r, d = _i32(0), _i32(0)
+    _check(lib().st_stencil_expr_info(expr.encode(), ctypes.byref(r), ctypes.byref(d)), "st_stencil_expr_info")
+    return r.value, d.value
+
+
+def st_stencil3d_expr_run(a, b, expr: str, iters: int, nx: int | None = None, stream=None):
+    """3-D expression stencil over a(dz, dy, dx) on (nz + 2R, ny + 2R, ldx) float64 CUDA tensors
+    (x fastest). Returns whichever of a, b holds the result."""
+    _f64_cuda(a, "a")
+    _f64_cuda(b, "b")
+    if a.dim() != 3 or a.shape != b.shape or a.stride() != b.stride() or a.stride(2) != 1:
+        raise ValueError("a, b: same-shape 3-D tensors, x contiguous")
+    R, dims = st_stencil_expr_info(expr)
+    if dims != 3:
+        raise ValueError("3-D accesses a(dz, dy, dx) expected")
+    ldx = a.stride(1)
+    if a.stride(0) != (a.shape[1]) * ldx:
+        raise ValueError("planes must be contiguous (stride(0) == rows * ldx)")
+    nz, ny = a.shape[0] - 2 * R, a.shape[1] - 2 * R
+    nx = a.shape[2] - 2 * R if nx is None else nx
+    in_b = _i32(0)
+    _check(lib().st_stencil3d_expr_run(a.data_ptr(), b.data_ptr(), nx, ny, nz, ldx, expr.encode(), iters,
+                                       _stream_ptr(stream), ctypes.byref(in_b)), "st_stencil3d_expr_run")
     return b if in_b.value else a
 
 

@@ -246,14 +246,44 @@ st_status st_stencil2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t
   return stencil2d_run(a, b, nx, ny, ld, R, offsets, coeffs, nterms, iters, static_cast<cudaStream_t>(cuda_stream));
 }
 
-st_status st_stencil2d_expr_halo(const char* expr, int32_t* halo) {
+st_status st_stencil_expr_info(const char* expr, int32_t* halo, int32_t* dims) {
   clear_error();
-  ST_RETURN_IF(!expr || !halo, ST_EINVAL, "st_stencil2d_expr_halo: null pointer");
+  ST_RETURN_IF(!expr || !halo || !dims, ST_EINVAL, "st_stencil_expr_info: null pointer");
   std::string cexpr;
   int64_t R = 0;
-  ST_TRY(stencil_expr_translate(expr, &cexpr, &R));
+  int d = 0;
+  ST_TRY(stencil_expr_translate(expr, &cexpr, &R, &d));
   *halo = (int32_t)R;
+  *dims = d;
   return ST_OK;
+}
+
+st_status st_stencil2d_expr_halo(const char* expr, int32_t* halo) {
+  int32_t dims = 0;
+  ST_TRY(st_stencil_expr_info(expr, halo, &dims));
+  ST_RETURN_IF(dims != 2, ST_EINVAL, "expression: 2-D accesses a(dy, dx) expected");
+  return ST_OK;
+}
+
+st_status st_stencil3d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t nz, int64_t ldx,
+                                const char* expr, int64_t iters, void* cuda_stream, int32_t* result_in_b) {
+  clear_error();
+  ST_RETURN_IF(!a || !b || !expr, ST_EINVAL, "st_stencil3d_expr_run: null pointer");
+  std::string cexpr;
+  int64_t R = 0;
+  int dims = 0;
+  ST_TRY(stencil_expr_translate(expr, &cexpr, &R, &dims));
+  ST_RETURN_IF(dims != 3, ST_EINVAL, "st_stencil3d_expr_run: 3-D accesses a(dz, dy, dx) expected");
+  ST_RETURN_IF(nx < 1 || ny < 1 || nz < 1 || ldx < nx + 2 * R || iters < 0, ST_EINVAL,
+               "st_stencil3d_expr_run: bad extents (nx %lld, ny %lld, nz %lld, ldx %lld, halo %lld)", (long long)nx,
+               (long long)ny, (long long)nz, (long long)ldx, (long long)R);
+  const size_t bytes = (size_t)(nz + 2 * R) * (size_t)(ny + 2 * R) * (size_t)ldx * sizeof(double);
+  ST_RETURN_IF(overlaps(a, bytes, b, bytes), ST_EINVAL, "st_stencil3d_expr_run: a and b overlap");
+  ST_TRY(check_device_ptr(a, "a"));
+  ST_TRY(check_device_ptr(b, "b"));
+  if (result_in_b) *result_in_b = (int32_t)(iters & 1);
+  if (iters == 0) return ST_OK;
+  return stencil3d_expr_run(a, b, nx, ny, nz, ldx, R, cexpr, iters, static_cast<cudaStream_t>(cuda_stream));
 }
 
 st_status st_stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, const char* expr,
@@ -262,7 +292,9 @@ st_status st_stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, in
   ST_RETURN_IF(!a || !b || !expr, ST_EINVAL, "st_stencil2d_expr_run: null pointer");
   std::string cexpr;
   int64_t R = 0;
-  ST_TRY(stencil_expr_translate(expr, &cexpr, &R));
+  int dims = 0;
+  ST_TRY(stencil_expr_translate(expr, &cexpr, &R, &dims));
+  ST_RETURN_IF(dims != 2, ST_EINVAL, "st_stencil2d_expr_run: 2-D accesses a(dy, dx) expected");
   ST_RETURN_IF(nx < 1 || ny < 1 || ld < nx + 2 * R || iters < 0, ST_EINVAL,
                "st_stencil2d_expr_run: bad extents (nx %lld, ny %lld, ld %lld, halo %lld)", (long long)nx,
                (long long)ny, (long long)ld, (long long)R);

@@ -30,8 +30,10 @@ constexpr int kStencilMaxOffset = 8;
 st_status stencil2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t R, const int32_t* off,
                         const double* coeffs, int32_t n, int64_t iters, cudaStream_t s);
 
-st_status stencil_expr_translate(const char* expr, std::string* cexpr, int64_t* R);
+st_status stencil_expr_translate(const char* expr, std::string* cexpr, int64_t* R, int* dims);
 st_status stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t R,
+                             const std::string& cexpr, int64_t iters, cudaStream_t s);
+st_status stencil3d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t nz, int64_t ldx, int64_t R,
                              const std::string& cexpr, int64_t iters, cudaStream_t s);
 
 // ----------------------------------------------------------- Jacobi 2-D ---

@@ -35,9 +35,10 @@ namespace {
 // ------------------------------------------------------------- translation ---
 // Returns the C expression (accesses -> A(dy,dx), literals -> double literals)
 // and the halo R, or an error message.
-bool translate(const char* expr, std::string* out, int64_t* R, std::string* err) {
+bool translate(const char* expr, std::string* out, int64_t* R, int* dims, std::string* err) {
   out->clear();
   *R = -1;
+  *dims = 0;
   const size_t n = std::strlen(expr);
   int depth = 0;
   size_t i = 0;
@@ -58,24 +59,30 @@ bool translate(const char* expr, std::string* out, int64_t* R, std::string* err)
         j = k;
         return true;
       };
-      long dy = 0, dx = 0;
       skip();
-      if (!expect_operand || j >= n || expr[j] != '(') { *err = "bad access (expected a(dy, dx))"; return false; }
+      if (!expect_operand || j >= n || expr[j] != '(') { *err = "bad access (expected a(dy, dx) or a(dz, dy, dx))"; return false; }
       ++j;
-      if (!integer(&dy)) { *err = "bad access offset"; return false; }
-      skip();
-      if (j >= n || expr[j] != ',') { *err = "bad access (expected ',')"; return false; }
-      ++j;
-      if (!integer(&dx)) { *err = "bad access offset"; return false; }
-      skip();
-      if (j >= n || expr[j] != ')') { *err = "bad access (expected ')')"; return false; }
-      ++j;
-      if (std::labs(dy) > kStencilMaxOffset || std::labs(dx) > kStencilMaxOffset) {
-        *err = "access offset beyond the supported halo";
+      std::vector<long> idx;
+      for (;;) {
+        long v = 0;
+        if (!integer(&v)) { *err = "bad access offset"; return false; }
+        idx.push_back(v);
+        skip();
+        if (j < n && expr[j] == ',') { ++j; continue; }
+        if (j < n && expr[j] == ')') { ++j; break; }
+        *err = "bad access (expected ',' or ')')";
         return false;
       }
-      *R = std::max<int64_t>(*R, std::max(std::labs(dy), std::labs(dx)));
-      *out += "A(" + std::to_string(dy) + "," + std::to_string(dx) + ")";
+      if (idx.size() != 2 && idx.size() != 3) { *err = "an access has 2 (dy, dx) or 3 (dz, dy, dx) offsets"; return false; }
+      if (*dims == 0) *dims = (int)idx.size();
+      if ((int)idx.size() != *dims) { *err = "all accesses must have the same number of offsets"; return false; }
+      std::string m = "A(";
+      for (size_t q = 0; q < idx.size(); ++q) {
+        if (std::labs(idx[q]) > kStencilMaxOffset) { *err = "access offset beyond the supported halo"; return false; }
+        *R = std::max<int64_t>(*R, std::labs(idx[q]));
+        m += (q ? "," : "") + std::to_string(idx[q]);
+      }
+      *out += m + ")";
       i = j;
       expect_operand = false;
       continue;
@@ -154,6 +161,28 @@ st_expr_kernel(const double* __restrict__ src, double* __restrict__ dst, long lo
 }
 )";
 
+// 3-D: x fastest, z slowest (R5); a thread owns one (x, y) column of a
+// chunk of 8 planes.
+const char* kKernelTemplate3 = R"(
+#define A(dz, dy, dx) __ldg(p + (long long)(dz) * plane + (long long)(dy) * ldx + (dx))
+extern "C" __global__ void __launch_bounds__(128)
+st_expr_kernel(const double* __restrict__ src, double* __restrict__ dst, long long nx, long long ny,
+               long long nz, long long ldx, long long R) {
+  const long long x = R + (long long)blockIdx.x * 32 + threadIdx.x;
+  const long long y = R + (long long)blockIdx.y * 4 + threadIdx.y;
+  if (x >= R + nx || y >= R + ny) return;
+  const long long plane = (ny + 2 * R) * ldx;
+  const long long zb = R + (long long)blockIdx.z * 8;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const long long z = zb + k;
+    if (z >= R + nz) return;
+    const double* p = src + z * plane + y * ldx + x;
+    dst[z * plane + y * ldx + x] = (@EXPR@);
+  }
+}
+)";
+
 // ------------------------------------------------------------------- NVRTC ---
 struct Nvrtc {
   decltype(&nvrtcCreateProgram) create = nullptr;
@@ -219,8 +248,8 @@ st_status driver(Driver* d) {
 std::mutex g_cache_mu;
 std::map<std::string, CUfunction> g_cache;  // (device, translated expression) -> kernel
 
-st_status compiled_kernel(const std::string& cexpr, int dev, CUfunction* fn) {
-  const std::string key = std::to_string(dev) + "|" + cexpr;
+st_status compiled_kernel(const std::string& cexpr, int dims, int dev, CUfunction* fn) {
+  const std::string key = std::to_string(dev) + "|" + std::to_string(dims) + "|" + cexpr;
   std::lock_guard<std::mutex> lock(g_cache_mu);
   auto it = g_cache.find(key);
   if (it != g_cache.end()) {
@@ -229,7 +258,7 @@ st_status compiled_kernel(const std::string& cexpr, int dev, CUfunction* fn) {
   }
   const Nvrtc& f = nvrtc();
   ST_RETURN_IF(!f.ok, ST_ENOTSUP, "NVRTC (libnvrtc.so.12) is not available");
-  std::string src = kKernelTemplate;
+  std::string src = dims == 3 ? kKernelTemplate3 : kKernelTemplate;
   src.replace(src.find("@EXPR@"), 6, cexpr);
   nvrtcProgram prog;
   ST_RETURN_IF(f.create(&prog, src.c_str(), "st_expr.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS, ST_EINTERNAL,
@@ -264,9 +293,9 @@ st_status compiled_kernel(const std::string& cexpr, int dev, CUfunction* fn) {
 
 }  // namespace
 
-st_status stencil_expr_translate(const char* expr, std::string* cexpr, int64_t* R) {
+st_status stencil_expr_translate(const char* expr, std::string* cexpr, int64_t* R, int* dims) {
   std::string err;
-  ST_RETURN_IF(!translate(expr, cexpr, R, &err), ST_EINVAL, "expression: %s", err.c_str());
+  ST_RETURN_IF(!translate(expr, cexpr, R, dims, &err), ST_EINVAL, "expression: %s", err.c_str());
   return ST_OK;
 }
 
@@ -275,7 +304,7 @@ st_status stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64
   int dev = 0;
   ST_CHECK_CUDA(cudaGetDevice(&dev));
   CUfunction k;
-  ST_TRY(compiled_kernel(cexpr, dev, &k));
+  ST_TRY(compiled_kernel(cexpr, 2, dev, &k));
   Driver d;
   ST_TRY(driver(&d));
   ST_CHECK_CUDA(cudaMemcpyAsync(b, a, (size_t)(ny + 2 * R) * (size_t)ld * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -290,6 +319,35 @@ st_status stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64
     ST_RETURN_IF(d.launch(k, gx, (unsigned)gy, 1, 32, 4, 1, 0, reinterpret_cast<CUstream>(s), args, nullptr) !=
                      CUDA_SUCCESS,
                  ST_ECUDA, "cuLaunchKernel(st_expr_kernel) failed");
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+    const double* nsrc = dst;
+    dst = const_cast<double*>(src);
+    src = nsrc;
+  }
+  return ST_OK;
+}
+
+st_status stencil3d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t nz, int64_t ldx, int64_t R,
+                             const std::string& cexpr, int64_t iters, cudaStream_t s) {
+  int dev = 0;
+  ST_CHECK_CUDA(cudaGetDevice(&dev));
+  CUfunction k;
+  ST_TRY(compiled_kernel(cexpr, 3, dev, &k));
+  Driver d;
+  ST_TRY(driver(&d));
+  ST_CHECK_CUDA(cudaMemcpyAsync(b, a, (size_t)(nz + 2 * R) * (size_t)(ny + 2 * R) * (size_t)ldx * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+  const int64_t gy = (ny + 3) / 4, gz = (nz + 7) / 8;
+  ST_RETURN_IF(gy > 65535 || gz > 65535, ST_ENOTSUP, "stencil3d_expr: grid too large");
+  const unsigned gx = (unsigned)((nx + 31) / 32);
+  const double* src = a;
+  double* dst = b;
+  long long nxl = nx, nyl = ny, nzl = nz, ldl = ldx, Rl = R;
+  for (int64_t it = 0; it < iters; ++it) {
+    void* args[] = {&src, &dst, &nxl, &nyl, &nzl, &ldl, &Rl};
+    ST_RETURN_IF(d.launch(k, gx, (unsigned)gy, (unsigned)gz, 32, 4, 1, 0, reinterpret_cast<CUstream>(s), args,
+                          nullptr) != CUDA_SUCCESS,
+                 ST_ECUDA, "cuLaunchKernel(st_expr_kernel 3-D) failed");
     launch_counter().fetch_add(1, std::memory_order_relaxed);
     const double* nsrc = dst;
     dst = const_cast<double*>(src);

@@ -32,3 +32,15 @@ def test_accepts_and_reports_halo(lib, e):
 def test_rejects(lib, e):
     with pytest.raises(lib.StencilError):
         lib.st_stencil2d_expr_halo(e)
+
+
+@pytest.mark.parametrize("e,want", [("(a(-1,0,0)+a(1,0,0)+a(0,-1,0)+a(0,1,0)+a(0,0,-1)+a(0,0,1))/6", (1, 3)),
+                                    ("a(0,2)", (2, 2)), ("a(3,-1,0)*a(0,0,0)", (3, 3))])
+def test_info_reports_halo_and_arity(lib, e, want):
+    assert lib.st_stencil_expr_info(e) == want
+
+
+@pytest.mark.parametrize("e", ["a(0,0) + a(0,0,0)", "a(1,2,3,4)"])
+def test_rejects_mixed_or_wrong_arity(lib, e):
+    with pytest.raises(lib.StencilError):
+        lib.st_stencil_expr_info(e)

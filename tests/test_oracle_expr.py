@@ -68,3 +68,23 @@ def test_ring_fixed_and_offsets_parsed():
     mask = np.ones_like(a, dtype=bool)
     mask[3:-3, 3:-3] = False
     assert np.array_equal(got[mask], a[mask])
+
+
+def test_benchmark1_expression_equals_jacobi3d_oracle():
+    # the paper's benchmark 1 as an expression: readings R20/R21 exactly
+    e = "(a(-1,0,0) + a(1,0,0) + a(0,-1,0) + a(0,1,0) + a(0,0,-1) + a(0,0,1)) / 6"
+    a = rng.standard_normal((9, 11, 14))
+    assert np.array_equal(ox.stencil3d_expr(a, e, 4), oracle.jacobi3d(a, 4))
+
+
+def test_3d_nonlinear_exact_rationals():
+    e = "a(1,0,-1)*a(0,2,0) - 3*a(-1,-1,1)"
+    R = ox.halo3(e)
+    a = rng.integers(-5, 6, size=(3 + 2 * R, 4 + 2 * R, 5 + 2 * R)).astype(np.float64)
+    got = ox.stencil3d_expr(a, e, 1)
+    want = a.copy()
+    for z in range(R, R + 3):
+        for y in range(R, R + 4):
+            for x in range(R, R + 5):
+                want[z, y, x] = float(ox.eval_exact(e, lambda dz, dy, dx: Fraction(a[z + dz, y + dy, x + dx])))
+    assert np.array_equal(got, want)

@@ -15,3 +15,14 @@ for e in ("(a(-1,0)+a(1,0)+a(0,-1)+a(0,1))*0.25", "(a(0,0) + a(2,0))*(a(0,0) - a
     ms = e0.elapsed_time(e1)
     print(f"{e}: first call (compile) {tc:.2f} s; {n * n * it / (ms / 1e3) / 1e9:.1f} Gpts/s, "
           f"{16 * n * n * it / (ms / 1e3) / 1e9:.0f} GB/s (16 B/pt)")
+m = 512
+e = "(a(-1,0,0)+a(1,0,0)+a(0,-1,0)+a(0,1,0)+a(0,0,-1)+a(0,0,1))/6"
+a = torch.rand(m + 2, m + 2, m + 2, dtype=torch.float64, device="cuda")
+b = torch.empty_like(a)
+st.st_stencil3d_expr_run(a, b, e, 2)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); st.st_stencil3d_expr_run(a, b, e, 20); e1.record(); e1.synchronize()
+ms = e0.elapsed_time(e1)
+print(f"3-D benchmark 1 expression 512^3: {m ** 3 * 20 / (ms / 1e3) / 1e9:.1f} Gpts/s, "
+      f"{16 * m ** 3 * 20 / (ms / 1e3) / 1e9:.0f} GB/s (16 B/pt)")
