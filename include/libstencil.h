@@ -294,6 +294,21 @@ st_status st_stencil2d_expr_halo(const char* expr, int32_t* halo);
 st_status st_stencil_expr_info(const char* expr, int32_t* halo, int32_t* dims);
 st_status st_stencil3d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t nz, int64_t ldx,
                                 const char* expr, int64_t iters, void* cuda_stream, int32_t* result_in_b);
+
+/* Fused region ("three separate stencil computations across three
+ * fields which are then fused ... into a single stencil region"): one pass over
+ * the interior computes nout (<= 8) outputs from nin (<= 8) input fields. Each
+ * exprs[j] (HOST string) uses f<i>(dz, dy, dx) for input field i, k<c> for the
+ * value of per-plane coefficient array c (device, nz + 2R doubles) at the output
+ * point's plane, literals, + - * /, unary signs and parentheses (grammar and
+ * rounding as st_stencil2d_expr_run; compiled once per region with NVRTC). All
+ * fields are (nz + 2R) x (ny + 2R) x ldx, x fastest, R = max |offset|; only
+ * interior points of the outputs are written. Inputs may alias each other,
+ * outputs may not overlap anything. One application per call (not iterated).
+ * The Piacsek-Williams advection is pw_fused_expressions() of the binding. */
+st_status st_stencil3d_fused_run(const double* const* inputs, int32_t nin, double* const* outputs, int32_t nout,
+                                 const char* const* exprs, const double* const* plane_coefs, int32_t ncoef,
+                                 int64_t nx, int64_t ny, int64_t nz, int64_t ldx, void* cuda_stream);
 st_status st_stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, const char* expr,
                                 int64_t iters, void* cuda_stream, int32_t* result_in_b);
 

@@ -77,7 +77,7 @@ class _FloatLiterals(ast.NodeTransformer):
     where the generated source spells it as a double literal)."""
 
     def visit_Call(self, node):
-        return node  # a(dy, dx): the offsets stay integers
+        return node  # a(dy, dx) / f<i>(dz, dy, dx): the offsets stay integers
 
     def visit_Constant(self, node):
         return ast.copy_location(ast.Constant(float(node.value)), node)
@@ -133,3 +133,67 @@ def eval_exact(expr: str, a_of):
     """Evaluate the expression with a user access function (e.g. returning Fractions)."""
     check(expr)
     return eval(compile(ast.parse(expr, mode="eval"), "<stencil>", "eval"), {"__builtins__": {}}, {"a": a_of})
+
+
+# ----------------------------------------------------------------- fused multi-field regions
+_FIELD = re.compile(r"^f([0-7])$")
+_COEF = re.compile(r"^k([0-7])$")
+_ALLOWED_FUSED = re.compile(r"^[\sfk0-9.eE+\-*/(),]*$")
+
+
+def check_fused(expr: str) -> None:
+    """Fused-region grammar: field accesses f0..f7(dz, dy, dx), per-plane coefficients k0..k7
+    (their value at the output point's plane), literals, + - * /, unary signs, parentheses."""
+    if not _ALLOWED_FUSED.match(expr):
+        raise ValueError(f"expression has characters outside f(), k, digits, . e E + - * / ( ) ,: {expr!r}")
+    tree = ast.parse(expr, mode="eval")
+    for node in ast.walk(tree):
+        if isinstance(node, ast.Call):
+            if not (isinstance(node.func, ast.Name) and _FIELD.match(node.func.id) and len(node.args) == 3):
+                raise ValueError("only f<i>(dz, dy, dx) calls are allowed")
+        elif isinstance(node, ast.Name):
+            if not (_FIELD.match(node.id) or _COEF.match(node.id)):
+                raise ValueError(f"unknown name {node.id}")
+        elif isinstance(node, ast.BinOp):
+            if not isinstance(node.op, (ast.Add, ast.Sub, ast.Mult, ast.Div)):
+                raise ValueError("only + - * / are allowed")
+        elif isinstance(node, ast.UnaryOp):
+            if not isinstance(node.op, (ast.USub, ast.UAdd)):
+                raise ValueError("only unary +/- are allowed")
+        elif isinstance(node, ast.Constant):
+            if not isinstance(node.value, (int, float)) or isinstance(node.value, bool):
+                raise ValueError("only numeric literals are allowed")
+        elif not isinstance(node, (ast.Expression, ast.Load, ast.Add, ast.Sub, ast.Mult, ast.Div, ast.USub,
+                                   ast.UAdd)):
+            raise ValueError(f"unsupported syntax: {type(node).__name__}")
+
+
+def fused_halo(exprs) -> int:
+    offs = [tuple(int(v) for v in m) for e in exprs
+            for m in re.findall(r"f[0-7]\(\s*(-?\d+)\s*,\s*(-?\d+)\s*,\s*(-?\d+)\s*\)", e)]
+    if not offs:
+        raise ValueError("no field access")
+    return max(max(abs(v) for v in o) for o in offs)
+
+
+def fused3d_expr(inputs, exprs, plane_coefs=(), nx: int | None = None, out=None):
+    """One application of a fused region (several stencils over several fields
+    computed in one pass): output j = exprs[j] evaluated at every interior point of the
+    (nz + 2R) x (ny + 2R) x ldx fields, R = max |offset|; k<j> is plane_coefs[j][z]. Output
+    halos are left as they are (zeros unless `out` is given)."""
+    for e in exprs:
+        check_fused(e)
+    R = fused_halo(exprs)
+    a0 = inputs[0]
+    nz, ny = a0.shape[0] - 2 * R, a0.shape[1] - 2 * R
+    nx = a0.shape[2] - 2 * R if nx is None else nx
+    env = {}
+    for i, f in enumerate(inputs):
+        env[f"f{i}"] = (lambda _f: lambda dz, dy, dx: _f[R + dz:R + dz + nz, R + dy:R + dy + ny,
+                                                           R + dx:R + dx + nx])(f)
+    for j, c in enumerate(plane_coefs):
+        env[f"k{j}"] = np.asarray(c, dtype=np.float64)[R:R + nz, None, None]
+    outs = out if out is not None else [np.zeros_like(a0) for _ in exprs]
+    for o, e in zip(outs, exprs):
+        o[R:R + nz, R:R + ny, R:R + nx] = eval(_compile(e), {"__builtins__": {}}, env)
+    return outs

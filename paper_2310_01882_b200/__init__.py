@@ -67,6 +67,9 @@ _SIGS = {
                                         ctypes.POINTER(_i32)]),
     "st_stencil2d_expr_halo": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_i32)]),
     "st_stencil_expr_info": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
+    "st_stencil3d_fused_run": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, ctypes.POINTER(_vp), _i32,
+                                              ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_vp), _i32, _i64, _i64,
+                                              _i64, _i64, _vp]),
     "st_stencil3d_expr_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_char_p, _i64, _vp,
                                              ctypes.POINTER(_i32)]),
     "st_stencil2d_expr_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, ctypes.c_char_p, _i64, _vp,
@@ -498,6 +501,44 @@ def st_stencil3d_expr_run(a, b, expr: str, iters: int, nx: int | None = None, st
     _check(lib().st_stencil3d_expr_run(a.data_ptr(), b.data_ptr(), nx, ny, nz, ldx, expr.encode(), iters,
                                        _stream_ptr(stream), ctypes.byref(in_b)), "st_stencil3d_expr_run")
     return b if in_b.value else a
+
+
+def st_stencil3d_fused_run(inputs, outputs, exprs, plane_coefs=(), nx: int | None = None, stream=None) -> None:
+    """One application of a fused region: outputs[j] = exprs[j] over f<i> = inputs[i] and
+    k<c> = plane_coefs[c][z]. Fields: (nz + 2R, ny + 2R, ldx) float64 CUDA tensors."""
+    import re
+    for i, t in enumerate(list(inputs) + list(outputs) + list(plane_coefs)):
+        _f64_cuda(t, f"tensor {i}")
+    a0 = inputs[0]
+    offs = [int(v) for e in exprs for m in re.findall(r"f[0-7]\(\s*(-?\d+)\s*,\s*(-?\d+)\s*,\s*(-?\d+)\s*\)", e)
+            for v in m]
+    R = max(abs(v) for v in offs) if offs else 0
+    ldx = a0.stride(1)
+    nz, ny = a0.shape[0] - 2 * R, a0.shape[1] - 2 * R
+    nx = a0.shape[2] - 2 * R if nx is None else nx
+    ins = (_vp * len(inputs))(*[t.data_ptr() for t in inputs])
+    outs = (_vp * len(outputs))(*[t.data_ptr() for t in outputs])
+    ex = (ctypes.c_char_p * len(exprs))(*[e.encode() for e in exprs])
+    ks = (_vp * max(1, len(plane_coefs)))(*[t.data_ptr() for t in plane_coefs])
+    _check(lib().st_stencil3d_fused_run(ins, len(inputs), outs, len(outputs), ex, ks, len(plane_coefs), nx, ny, nz,
+                                        ldx, _stream_ptr(stream)), "st_stencil3d_fused_run")
+
+
+def pw_fused_expressions(tcx: float, tcy: float) -> list[str]:
+    """The Piacsek-Williams advection (reading R6's association trees) as the three
+    expressions of one fused region over f0 = u, f1 = v, f2 = w with per-plane coefficients
+    k0 = tzc1, k1 = tzc2, k2 = tzd1, k3 = tzd2 (tcx, tcy inlined at full binary64 precision)."""
+    X, Y = repr(float(tcx)), repr(float(tcy))
+    su = (f"(({X} * (f0(0,0,-1)*(f0(0,0,0)+f0(0,0,-1)) - f0(0,0,1)*(f0(0,0,0)+f0(0,0,1))))"
+          f" + ({Y} * (f0(0,-1,0)*(f1(0,-1,0)+f1(0,-1,1)) - f0(0,1,0)*(f1(0,0,0)+f1(0,0,1)))))"
+          " + ((k0*f0(-1,0,0))*(f2(-1,0,0)+f2(-1,0,1)) - (k1*f0(1,0,0))*(f2(0,0,0)+f2(0,0,1)))")
+    sv = (f"(({X} * (f1(0,0,-1)*(f0(0,0,-1)+f0(0,1,-1)) - f1(0,0,1)*(f0(0,0,0)+f0(0,1,0))))"
+          f" + ({Y} * (f1(0,-1,0)*(f1(0,0,0)+f1(0,-1,0)) - f1(0,1,0)*(f1(0,0,0)+f1(0,1,0)))))"
+          " + ((k0*f1(-1,0,0))*(f2(-1,0,0)+f2(-1,1,0)) - (k1*f1(1,0,0))*(f2(0,0,0)+f2(0,1,0)))")
+    sw = (f"(({X} * (f2(0,0,-1)*(f0(0,0,-1)+f0(1,0,-1)) - f2(0,0,1)*(f0(0,0,0)+f0(1,0,0))))"
+          f" + ({Y} * (f2(0,-1,0)*(f1(0,-1,0)+f1(1,-1,0)) - f2(0,1,0)*(f1(0,0,0)+f1(1,0,0)))))"
+          " + ((k2*f2(-1,0,0))*(f2(0,0,0)+f2(-1,0,0)) - (k3*f2(1,0,0))*(f2(0,0,0)+f2(1,0,0)))")
+    return [su, sv, sw]
 
 
 def st_selftest_div6(x) -> int:

@@ -307,6 +307,39 @@ st_status st_stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, in
   return stencil2d_expr_run(a, b, nx, ny, ld, R, cexpr, iters, static_cast<cudaStream_t>(cuda_stream));
 }
 
+st_status st_stencil3d_fused_run(const double* const* inputs, int32_t nin, double* const* outputs, int32_t nout,
+                                 const char* const* exprs, const double* const* plane_coefs, int32_t ncoef,
+                                 int64_t nx, int64_t ny, int64_t nz, int64_t ldx, void* cuda_stream) {
+  clear_error();
+  ST_RETURN_IF(!inputs || !outputs || !exprs || (ncoef > 0 && !plane_coefs), ST_EINVAL,
+               "st_stencil3d_fused_run: null pointer");
+  int64_t R = 0;
+  ST_TRY(stencil3d_fused_run(inputs, nin, outputs, nout, exprs, plane_coefs, ncoef, nx, ny, nz, ldx, &R, true,
+                             nullptr));
+  ST_RETURN_IF(nx < 1 || ny < 1 || nz < 1 || ldx < nx + 2 * R, ST_EINVAL,
+               "st_stencil3d_fused_run: bad extents (nx %lld, ny %lld, nz %lld, ldx %lld, halo %lld)", (long long)nx,
+               (long long)ny, (long long)nz, (long long)ldx, (long long)R);
+  const size_t bytes = (size_t)(nz + 2 * R) * (size_t)(ny + 2 * R) * (size_t)ldx * sizeof(double);
+  for (int i = 0; i < nin; ++i) {
+    ST_RETURN_IF(!inputs[i], ST_EINVAL, "st_stencil3d_fused_run: null input %d", i);
+    ST_TRY(check_device_ptr(inputs[i], "input"));
+  }
+  for (int j = 0; j < nout; ++j) {
+    ST_RETURN_IF(!outputs[j], ST_EINVAL, "st_stencil3d_fused_run: null output %d", j);
+    ST_TRY(check_device_ptr(outputs[j], "output"));
+    for (int i = 0; i < nin; ++i)  // outputs never overlap inputs or each other (inputs may alias)
+      ST_RETURN_IF(overlaps(outputs[j], bytes, inputs[i], bytes), ST_EINVAL, "output %d overlaps input %d", j, i);
+    for (int q = 0; q < j; ++q)
+      ST_RETURN_IF(overlaps(outputs[j], bytes, outputs[q], bytes), ST_EINVAL, "outputs %d and %d overlap", q, j);
+  }
+  for (int j = 0; j < ncoef; ++j) {
+    ST_RETURN_IF(!plane_coefs[j], ST_EINVAL, "st_stencil3d_fused_run: null coefficient array %d", j);
+    ST_TRY(check_device_ptr(plane_coefs[j], "plane coefficients"));
+  }
+  return stencil3d_fused_run(inputs, nin, outputs, nout, exprs, plane_coefs, ncoef, nx, ny, nz, ldx, &R, false,
+                             static_cast<cudaStream_t>(cuda_stream));
+}
+
 int64_t st_gauss_seidel2d_workspace_bytes(int64_t ny) { return ny < 1 ? 0 : gauss_seidel2d_workspace_bytes(ny); }
 
 st_status st_gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters, void* workspace,

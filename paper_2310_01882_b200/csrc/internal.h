@@ -35,6 +35,10 @@ st_status stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64
                              const std::string& cexpr, int64_t iters, cudaStream_t s);
 st_status stencil3d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t nz, int64_t ldx, int64_t R,
                              const std::string& cexpr, int64_t iters, cudaStream_t s);
+st_status stencil3d_fused_run(const double* const* in, int32_t nin, double* const* out, int32_t nout,
+                              const char* const* exprs, const double* const* coefs, int32_t ncoef, int64_t nx,
+                              int64_t ny, int64_t nz, int64_t ldx, int64_t* R_out, bool validate_only,
+                              cudaStream_t s);
 
 // ----------------------------------------------------------- Jacobi 2-D ---
 // One sweep dst = J(src) over buffer rows [y_lo, y_hi] (buffer row indices,

@@ -35,10 +35,15 @@ namespace {
 // ------------------------------------------------------------- translation ---
 // Returns the C expression (accesses -> A(dy,dx), literals -> double literals)
 // and the halo R, or an error message.
-bool translate(const char* expr, std::string* out, int64_t* R, int* dims, std::string* err) {
+// fused: accesses are f<i>(dz, dy, dx) (input field i) and k<j> names the
+// per-plane coefficient j; max_field / max_coef report the highest indices used.
+bool translate(const char* expr, std::string* out, int64_t* R, int* dims, std::string* err, bool fused = false,
+               int* max_field = nullptr, int* max_coef = nullptr) {
   out->clear();
   *R = -1;
   *dims = 0;
+  if (max_field) *max_field = -1;
+  if (max_coef) *max_coef = -1;
   const size_t n = std::strlen(expr);
   int depth = 0;
   size_t i = 0;
@@ -46,8 +51,28 @@ bool translate(const char* expr, std::string* out, int64_t* R, int* dims, std::s
   while (i < n) {
     const char ch = expr[i];
     if (std::isspace((unsigned char)ch)) { ++i; continue; }
-    if (ch == 'a') {  // a ( int , int )
+    if (fused && ch == 'k') {  // k<j>: per-plane coefficient
+      if (!expect_operand || i + 1 >= n || expr[i + 1] < '0' || expr[i + 1] > '7' ||
+          (i + 2 < n && (std::isalnum((unsigned char)expr[i + 2]) || expr[i + 2] == '.'))) {
+        *err = "bad coefficient name (k0..k7)";
+        return false;
+      }
+      const int jk = expr[i + 1] - '0';
+      if (max_coef) *max_coef = std::max(*max_coef, jk);
+      *out += "K" + std::to_string(jk);
+      i += 2;
+      expect_operand = false;
+      continue;
+    }
+    if ((!fused && ch == 'a') || (fused && ch == 'f')) {  // a(dy, dx) / a(dz, dy, dx) / f<i>(dz, dy, dx)
       size_t j = i + 1;
+      int field = -1;
+      if (fused) {
+        if (j >= n || expr[j] < '0' || expr[j] > '7') { *err = "bad field name (f0..f7)"; return false; }
+        field = expr[j] - '0';
+        ++j;
+        if (max_field) *max_field = std::max(*max_field, field);
+      }
       auto skip = [&] { while (j < n && std::isspace((unsigned char)expr[j])) ++j; };
       auto integer = [&](long* v) -> bool {
         skip();
@@ -74,9 +99,10 @@ bool translate(const char* expr, std::string* out, int64_t* R, int* dims, std::s
         return false;
       }
       if (idx.size() != 2 && idx.size() != 3) { *err = "an access has 2 (dy, dx) or 3 (dz, dy, dx) offsets"; return false; }
+      if (fused && idx.size() != 3) { *err = "field accesses are f<i>(dz, dy, dx)"; return false; }
       if (*dims == 0) *dims = (int)idx.size();
       if ((int)idx.size() != *dims) { *err = "all accesses must have the same number of offsets"; return false; }
-      std::string m = "A(";
+      std::string m = fused ? "F" + std::to_string(field) + "(" : std::string("A(");
       for (size_t q = 0; q < idx.size(); ++q) {
         if (std::labs(idx[q]) > kStencilMaxOffset) { *err = "access offset beyond the supported halo"; return false; }
         *R = std::max<int64_t>(*R, std::labs(idx[q]));
@@ -139,7 +165,7 @@ bool translate(const char* expr, std::string* out, int64_t* R, int* dims, std::s
     ++i;
   }
   if (expect_operand || depth != 0) { *err = "incomplete expression"; return false; }
-  if (*R < 0) { *err = "the expression has no a(dy, dx) access"; return false; }
+  if (*R < 0) { *err = "the expression has no field access"; return false; }
   return true;
 }
 
@@ -179,6 +205,29 @@ st_expr_kernel(const double* __restrict__ src, double* __restrict__ dst, long lo
     if (z >= R + nz) return;
     const double* p = src + z * plane + y * ldx + x;
     dst[z * plane + y * ldx + x] = (@EXPR@);
+  }
+}
+)";
+
+// Fused region: several outputs from several fields in one pass.
+// @DEFS@ = F<i>/K<j> macros, @BODY@ = one store per output.
+const char* kKernelTemplateFused = R"(
+struct Ptrs { const double* in[8]; double* out[8]; const double* k[8]; };
+extern "C" __global__ void __launch_bounds__(128)
+st_expr_kernel(const __grid_constant__ Ptrs P, long long nx, long long ny, long long nz, long long ldx,
+               long long R) {
+  const long long x = R + (long long)blockIdx.x * 32 + threadIdx.x;
+  const long long y = R + (long long)blockIdx.y * 4 + threadIdx.y;
+  if (x >= R + nx || y >= R + ny) return;
+  const long long plane = (ny + 2 * R) * ldx;
+  const long long zb = R + (long long)blockIdx.z * 8;
+#pragma unroll 1
+  for (int kz = 0; kz < 8; ++kz) {
+    const long long z = zb + kz;
+    if (z >= R + nz) return;
+    const long long o = z * plane + y * ldx + x;
+@DEFS@
+@BODY@
   }
 }
 )";
@@ -258,8 +307,16 @@ st_status compiled_kernel(const std::string& cexpr, int dims, int dev, CUfunctio
   }
   const Nvrtc& f = nvrtc();
   ST_RETURN_IF(!f.ok, ST_ENOTSUP, "NVRTC (libnvrtc.so.12) is not available");
-  std::string src = dims == 3 ? kKernelTemplate3 : kKernelTemplate;
-  src.replace(src.find("@EXPR@"), 6, cexpr);
+  std::string src;
+  if (dims == 4) {  // fused region: cexpr = "<defs>\x1f<body>"
+    const size_t cut = cexpr.find('\x1f');
+    src = kKernelTemplateFused;
+    src.replace(src.find("@DEFS@"), 6, cexpr.substr(0, cut));
+    src.replace(src.find("@BODY@"), 6, cexpr.substr(cut + 1));
+  } else {
+    src = dims == 3 ? kKernelTemplate3 : kKernelTemplate;
+    src.replace(src.find("@EXPR@"), 6, cexpr);
+  }
   nvrtcProgram prog;
   ST_RETURN_IF(f.create(&prog, src.c_str(), "st_expr.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS, ST_EINTERNAL,
                "nvrtcCreateProgram failed");
@@ -353,6 +410,58 @@ st_status stencil3d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64
     dst = const_cast<double*>(src);
     src = nsrc;
   }
+  return ST_OK;
+}
+
+st_status stencil3d_fused_run(const double* const* in, int32_t nin, double* const* out, int32_t nout,
+                              const char* const* exprs, const double* const* coefs, int32_t ncoef, int64_t nx,
+                              int64_t ny, int64_t nz, int64_t ldx, int64_t* R_out, bool validate_only,
+                              cudaStream_t s) {
+  ST_RETURN_IF(nin < 1 || nin > 8 || nout < 1 || nout > 8 || ncoef < 0 || ncoef > 8, ST_EINVAL,
+               "fused region: 1..8 inputs, 1..8 outputs, 0..8 coefficient arrays");
+  std::string defs, body;
+  int64_t R = -1;
+  for (int j = 0; j < nout; ++j) {
+    ST_RETURN_IF(!exprs[j], ST_EINVAL, "fused region: null expression %d", j);
+    std::string c, err;
+    int64_t r = 0;
+    int dims = 0, mf = -1, mk = -1;
+    ST_RETURN_IF(!translate(exprs[j], &c, &r, &dims, &err, true, &mf, &mk), ST_EINVAL, "expression %d: %s", j,
+                 err.c_str());
+    ST_RETURN_IF(mf >= nin, ST_EINVAL, "expression %d reads field f%d of %d inputs", j, mf, nin);
+    ST_RETURN_IF(mk >= ncoef, ST_EINVAL, "expression %d reads coefficient k%d of %d arrays", j, mk, ncoef);
+    R = std::max(R, r);
+    body += "    P.out[" + std::to_string(j) + "][o] = (" + c + ");\n";
+  }
+  *R_out = R;
+  if (validate_only) return ST_OK;
+  for (int i = 0; i < nin; ++i)
+    defs += "#define F" + std::to_string(i) + "(dz, dy, dx) __ldg(P.in[" + std::to_string(i) +
+            "] + o + (long long)(dz) * plane + (long long)(dy) * ldx + (dx))\n";
+  for (int j = 0; j < ncoef; ++j)
+    defs += "    const double K" + std::to_string(j) + " = __ldg(P.k[" + std::to_string(j) + "] + z);\n";
+  int dev = 0;
+  ST_CHECK_CUDA(cudaGetDevice(&dev));
+  CUfunction k;
+  ST_TRY(compiled_kernel(defs + '\x1f' + body, 4, dev, &k));
+  Driver d;
+  ST_TRY(driver(&d));
+  struct Ptrs {
+    const double* in[8];
+    double* out[8];
+    const double* k[8];
+  } P{};
+  for (int i = 0; i < nin; ++i) P.in[i] = in[i];
+  for (int j = 0; j < nout; ++j) P.out[j] = out[j];
+  for (int j = 0; j < ncoef; ++j) P.k[j] = coefs[j];
+  const int64_t gy = (ny + 3) / 4, gz = (nz + 7) / 8;
+  ST_RETURN_IF(gy > 65535 || gz > 65535, ST_ENOTSUP, "fused region: grid too large");
+  long long nxl = nx, nyl = ny, nzl = nz, ldl = ldx, Rl = R;
+  void* args[] = {&P, &nxl, &nyl, &nzl, &ldl, &Rl};
+  ST_RETURN_IF(d.launch(k, (unsigned)((nx + 31) / 32), (unsigned)gy, (unsigned)gz, 32, 4, 1, 0,
+                        reinterpret_cast<CUstream>(s), args, nullptr) != CUDA_SUCCESS,
+               ST_ECUDA, "cuLaunchKernel(fused region) failed");
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
   return ST_OK;
 }
 

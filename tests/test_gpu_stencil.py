@@ -133,3 +133,44 @@ def test_benchmark1_expression_equals_jacobi3d_kernel(cuda_lib):
     r1 = cuda_lib.st_stencil3d_expr_run(a, torch.empty_like(a), e, 5, nx=70)
     r2 = cuda_lib.st_jacobi3d_run(a2, torch.empty_like(a2), 5, nx=70)
     assert torch.equal(r1[:, :, :72], r2[:, :, :72])
+
+
+# ---------------------------------------------------------------- fused regions
+@pytest.mark.parametrize("nx,ny,nz", [(1, 1, 1), (23, 17, 11), (130, 33, 20)])
+def test_fused_pw_region_equals_pw_kernel_and_oracle(cuda_lib, nx, ny, nz):
+    # benchmark 2 written as one fused region of three NVRTC-compiled expressions is bitwise
+    # the hand-written TMA PW kernel and the C oracle
+    import torch
+    import stencil_inputs as si
+    d = si.pw_inputs(nx, ny, nz)
+    g = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in d.items()}
+    exprs = cuda_lib.pw_fused_expressions(d["tcx"], d["tcy"])
+    outs = [torch.zeros_like(g["u"]) for _ in range(3)]
+    cuda_lib.st_stencil3d_fused_run([g["u"], g["v"], g["w"]], outs, exprs, [g["tzc1"], g["tzc2"], g["tzd1"], g["tzd2"]],
+                                    nx=nx)
+    ref = [torch.zeros_like(g["u"]) for _ in range(3)]
+    cuda_lib.st_pw_advect3d(g["u"], g["v"], g["w"], *ref, g["tcx"], g["tcy"], g["tzc1"], g["tzc2"], g["tzd1"],
+                            g["tzd2"], nx=nx)
+    torch.cuda.synchronize()
+    want = oracle.pw_advect3d(d["u"], d["v"], d["w"], d, nx=nx)
+    for o, r, w in zip(outs, ref, want):
+        o, r = o.cpu().numpy()[:, :, :nx + 2], r.cpu().numpy()[:, :, :nx + 2]
+        assert np.array_equal(o[1:-1, 1:-1, 1:-1], w[1:-1, 1:-1, 1:nx + 1])
+        assert np.array_equal(o, r)
+
+
+def test_fused_random_region_bitwise(cuda_lib):
+    import torch
+    from oracle import expr as ox
+    exprs = ["f0(1,0,-1)*k0 - f1(0,-2,1)/(1 + f0(0,0,0)*f0(0,0,0))", "2*f1(0,0,0) + f0(-1,1,-1)*k1 - 0.5*f2(0,0,2)"]
+    R = ox.fused_halo(exprs)
+    nz, ny, nx = 12, 19, 45
+    ins = [rng.uniform(0.5, 1.5, size=(nz + 2 * R, ny + 2 * R, nx + 2 * R)) for _ in range(3)]
+    ks = [rng.uniform(0.5, 1.5, size=nz + 2 * R) for _ in range(2)]
+    want = ox.fused3d_expr(ins, exprs, ks)
+    gi = [torch.from_numpy(a).cuda() for a in ins]
+    go = [torch.zeros_like(gi[0]) for _ in exprs]
+    cuda_lib.st_stencil3d_fused_run(gi, go, exprs, [torch.from_numpy(k).cuda() for k in ks])
+    torch.cuda.synchronize()
+    for o, w in zip(go, want):
+        assert np.array_equal(o.cpu().numpy(), w)

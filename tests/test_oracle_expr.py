@@ -88,3 +88,37 @@ def test_3d_nonlinear_exact_rationals():
             for x in range(R, R + 5):
                 want[z, y, x] = float(ox.eval_exact(e, lambda dz, dy, dx: Fraction(a[z + dz, y + dy, x + dx])))
     assert np.array_equal(got, want)
+
+
+def test_fused_pw_region_equals_pw_oracle():
+    # benchmark 2 written as one fused region of three expressions evaluates
+    # bitwise like the hand-written C PW oracle (the expressions come from the product's helper;
+    # the reference is or_pw_advect3d, so the two sides share nothing)
+    import paper_2310_01882_b200 as st
+    import stencil_inputs as si
+    d = si.pw_inputs(23, 17, 11)
+    exprs = st.pw_fused_expressions(d["tcx"], d["tcy"])
+    got = ox.fused3d_expr([d["u"], d["v"], d["w"]], exprs, [d["tzc1"], d["tzc2"], d["tzd1"], d["tzd2"]], nx=23)
+    want = oracle.pw_advect3d(d["u"], d["v"], d["w"], d)
+    for g, w in zip(got, want):
+        assert np.array_equal(g[1:-1, 1:-1, 1:24], w[1:-1, 1:-1, 1:24])
+
+
+def test_fused_integer_exact_and_grammar():
+    e = ["f0(1,0,0)*k1 - f1(0,-1,1)", "2*f1(0,0,0) + f0(-1,1,-1)*f0(0,0,0)*k0"]
+    a = [rng.integers(-6, 7, size=(5, 6, 7)).astype(np.float64) for _ in range(2)]
+    k = [rng.integers(-3, 4, size=5).astype(np.float64) for _ in range(2)]
+    got = ox.fused3d_expr(a, e, k)
+    for j, ej in enumerate(e):
+        want = np.zeros_like(a[0])
+        for z in range(1, 4):
+            for y in range(1, 5):
+                for x in range(1, 6):
+                    env = {"f0": lambda dz, dy, dx: Fraction(a[0][z + dz, y + dy, x + dx]),
+                           "f1": lambda dz, dy, dx: Fraction(a[1][z + dz, y + dy, x + dx]),
+                           "k0": Fraction(k[0][z]), "k1": Fraction(k[1][z])}
+                    want[z, y, x] = float(eval(ej, {"__builtins__": {}}, env))
+        assert np.array_equal(got[j], want)
+    for bad in ["a(0,0,0)", "f8(0,0,0)", "k9", "f0(0,0)", "f0(0,0,0)**2"]:
+        with pytest.raises((ValueError, SyntaxError)):
+            ox.fused3d_expr(a, [bad], k)

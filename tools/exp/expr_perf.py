@@ -26,3 +26,19 @@ e0.record(); st.st_stencil3d_expr_run(a, b, e, 20); e1.record(); e1.synchronize(
 ms = e0.elapsed_time(e1)
 print(f"3-D benchmark 1 expression 512^3: {m ** 3 * 20 / (ms / 1e3) / 1e9:.1f} Gpts/s, "
       f"{16 * m ** 3 * 20 / (ms / 1e3) / 1e9:.0f} GB/s (16 B/pt)")
+import stencil_inputs as si
+m = 512
+d = si.pw_inputs(m, m, m)
+g = {k: (torch.from_numpy(v).cuda() if hasattr(v, "shape") else v) for k, v in d.items()}
+outs = [torch.empty_like(g["u"]) for _ in range(3)]
+ex = st.pw_fused_expressions(d["tcx"], d["tcy"])
+args = ([g["u"], g["v"], g["w"]], outs, ex, [g["tzc1"], g["tzc2"], g["tzd1"], g["tzd2"]])
+st.st_stencil3d_fused_run(*args)
+torch.cuda.synchronize()
+e0.record()
+for _ in range(10):
+    st.st_stencil3d_fused_run(*args)
+e1.record(); e1.synchronize()
+ms = e0.elapsed_time(e1) / 10
+print(f"PW as a fused expression region 512^3: {m ** 3 / (ms / 1e3) / 1e9:.1f} Gpts/s, "
+      f"{48 * m ** 3 / (ms / 1e3) / 1e9:.0f} GB/s (48 B/pt)")
