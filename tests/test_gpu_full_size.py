@@ -11,6 +11,8 @@ on samples the oracle can compute independently:
   discrete sine eigenmode (pin J6) must decay as lambda^1000 within the
   accumulated rounding bound; an integer linear field must stay an exact fixed
   point (pin J3).
+* The in-place Gauss-Seidel grid of the bench (16384^2, one launch): every point
+  vs the sequential oracle after 2 sweeps; a linear field stays fixed for 100.
 
 Inputs are generated band by band straight into device memory (the generator
 indexes the global grid, so a band has exactly the full grid's values)."""
@@ -108,4 +110,26 @@ def test_C2_1000_sweeps_eigenmode_and_fixed_point(cuda_lib):
     a = (3 * x - 2 * y + 7).contiguous()
     out = cuda_lib.st_jacobi2d_run(a.clone(), torch.empty_like(a), iters, tblock=0)
     assert torch.equal(out, a)
+    torch.cuda.empty_cache()
+
+
+def test_gauss_seidel_16384_full_grid_2_sweeps_and_fixed_point(cuda_lib):
+    # the bench's GS grid (16384^2, tiled wavefront kernel, one launch): every point vs the
+    # sequential oracle after 2 sweeps, and an integer linear field stays fixed for 100 sweeps
+    import torch
+    n = 16384
+    a_np = si.jacobi2d_grid(n, n)
+    want = oracle.gauss_seidel2d(a_np, 2)
+    a = torch.from_numpy(a_np).cuda()
+    cuda_lib.st_gauss_seidel2d_run(a, 2)
+    got = a.cpu().numpy()
+    bad = np.argwhere(got.view(np.uint64) != want.view(np.uint64))
+    assert bad.size == 0, f"{len(bad)} mismatches, first {bad[:3].tolist()}"
+    del a, a_np, want, got
+    y = torch.arange(n + 2, dtype=torch.float64, device="cuda")[:, None]
+    x = torch.arange(n + 2, dtype=torch.float64, device="cuda")[None, :]
+    lin = (5 * x - 3 * y + 2).contiguous()
+    g = lin.clone()
+    cuda_lib.st_gauss_seidel2d_run(g, 100)
+    assert torch.equal(g, lin)
     torch.cuda.empty_cache()
