@@ -35,6 +35,7 @@ UNIT = "Gpts/s"
 JACOBI_BYTES_PER_PT = 16  # one 8-byte read + one 8-byte write per point per sweep
 PW_BYTES_PER_PT = 48      # u,v,w read + su,sv,sw written
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+FP64_PEAK_TFLOPS = 18.5    # measured non-FMA fp64 rate (tools/exp/fp64_pipe.cu)
 
 
 def peaks():
@@ -628,6 +629,12 @@ def main():
                          "ms_per_pass": round(launch_ms, 5),
                          "frac_of_nominal_8tbs": round(achieved_gbs / 8000.0, 4),
                          "effective_gbs_16B_per_update": round(effective_gbs, 1), "peak_source": peak_src},
+            # the same kernel against the fp64 pipe (temporal blocking lifts it off the HBM roof):
+            # 4 flops per update (3 DADD + 1 DMUL, never contracted), peak = the measured DADD rate
+            "roofline_fp64": {"bound": "alu", "achieved": round(4 * value / 1e3, 3), "peak": FP64_PEAK_TFLOPS,
+                              "unit": "TFLOP/s", "frac": round(4 * value / 1e3 / FP64_PEAK_TFLOPS, 4),
+                              "peak_source": "tools/exp/fp64_pipe.cu: 63.6 DADD/clk/SM x 148 SMs (18.5 T/s); "
+                                             "no FMA (DESIGN.md R11)"},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
