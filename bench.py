@@ -631,8 +631,8 @@ def main():
                          "effective_gbs_16B_per_update": round(effective_gbs, 1), "peak_source": peak_src},
             # the same kernel against the fp64 pipe (temporal blocking lifts it off the HBM roof):
             # 4 flops per update (3 DADD + 1 DMUL, never contracted), peak = the measured DADD rate
-            "roofline_fp64": {"bound": "alu", "achieved": round(4 * value / 1e3, 3), "peak": FP64_PEAK_TFLOPS,
-                              "unit": "TFLOP/s", "frac": round(4 * value / 1e3 / FP64_PEAK_TFLOPS, 4),
+            "roofline_fp64": {"bound": "alu", "achieved": round(4 * value / world / 1e3, 3), "peak": FP64_PEAK_TFLOPS,
+                              "unit": "TFLOP/s (per GPU)", "frac": round(4 * value / world / 1e3 / FP64_PEAK_TFLOPS, 4),
                               "peak_source": "tools/exp/fp64_pipe.cu: 63.6 DADD/clk/SM x 148 SMs (18.5 T/s); "
                                              "no FMA (DESIGN.md R11)"},
             "e2e": e2e,
