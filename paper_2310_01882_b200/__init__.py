@@ -557,4 +557,13 @@ gauss_seidel2d = st_gauss_seidel2d_run
 stencil2d = st_stencil2d_run
 stencil2d_expr = st_stencil2d_expr_run
 pw_advect3d = st_pw_advect3d
-halo_exchange = st_halo_exchange
+
+
+def halo_exchange(comm: Comm, tensors, width: int = 1, stream=None) -> None:
+    """SURVEY.md §8(b) convention: swap the `width` first/last owned slabs of every tensor
+    (slabs = the slowest axis: rows of a 2-D field, planes of a 3-D one) with the neighbour
+    ranks; each tensor holds n_slow_local + 2*width slabs."""
+    t0 = tensors[0]
+    if any(t.shape != t0.shape or t.stride() != t0.stride() for t in tensors):
+        raise ValueError("all tensors must have the same shape and strides")
+    st_halo_exchange(comm, list(tensors), t0.shape[0] - 2 * width, t0.stride(0), width, stream=stream)

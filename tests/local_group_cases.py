@@ -240,7 +240,7 @@ def late_rank_case():
     except st.StencilError as e:
         timed_out = e.code == st.ST_ETIMEDOUT
     with torch.cuda.stream(streams[1]):
-        st.st_halo_exchange(comms[1], [bufs[1]], n, nx + 2, w)
+        st.halo_exchange(comms[1], [bufs[1]], w)  # SURVEY §8(b) convention (shape-derived slabs)
     comms[0].wait(streams[0], timeout_ms=10000)
     comms[1].wait(streams[1], timeout_ms=10000)
     torch.cuda.synchronize()
