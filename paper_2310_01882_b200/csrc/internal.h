@@ -110,6 +110,8 @@ st_status build_jacobi_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_
 // preload all kernels at creation.
 st_status jacobi2d_preload();
 st_status jacobi3d_preload();
+st_status jacobi3d_two_sweeps(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nz, int64_t ldx,
+                              cudaStream_t s);
 st_status stencil2d_preload();
 st_status pw_advect3d_preload();
 inline st_status preload_kernels() {

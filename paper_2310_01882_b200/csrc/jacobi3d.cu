@@ -176,6 +176,189 @@ st_status launch_j3(const double* src, double* dst, int64_t nx, int64_t ny, int6
   return ST_OK;
 }
 
+
+// ---- Two sweeps per pass (temporal blocking T = 2, single domain). A CTA owns
+// a BX x BY interior column and a chunk of output planes. Input planes (tile +
+// 2-cell apron; the box starts at x0-3 so TMA's 16-byte start rule holds) stream
+// through an S-slot TMA ring; for every plane L the CTA first computes the
+// first-sweep values of the (BX+2) x (BY+2) region around its tile into a 3-plane
+// shared-memory ring (Dirichlet points copy their input value), then the second
+// sweep of plane L-1 from that ring. Per point and sweep the arithmetic is the
+// single-sweep kernel's (sum order z-, z+, y-, y+, x-, x+, then / 6), so two
+// passes of this kernel are bitwise two single sweeps.
+template <int BX, int BY>
+struct J3T2Tile {
+  static constexpr int SX = BX + 6, SY = BY + 4;            // input tile: x0-3 .. x0+BX+2, y0-2 .. y0+BY+1
+  static constexpr int kPlaneBytes = SX * SY * 8;
+  static constexpr int kPlaneStride = ((kPlaneBytes + 127) / 128) * 128 / 8;
+  static constexpr uint32_t kTxBytes = kPlaneBytes;
+  static constexpr int LX = BX + 2, LY = BY + 2;             // first-sweep region: x0-1 .. x0+BX, y0-1 .. y0+BY
+  static constexpr int kL0 = LX * LY;
+};
+
+template <int BX, int BY, int S, int R>
+__global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
+    jacobi3d_t2_kernel(const __grid_constant__ CUtensorMap tm, double* __restrict__ dst, int64_t nx, int64_t ny,
+                       int64_t nz, int64_t ldx, int64_t planes_per_chunk) {
+  using T = J3T2Tile<BX, BY>;
+  constexpr int NT = (BX / 32) * (BY / R) * 32, WX = BX / 32;
+  constexpr int kHalo = 2 * T::LX + 2 * BY;  // first-sweep points outside the BX x BY tile
+  static_assert(S >= 4 && BY % R == 0 && BX % 32 == 0 && kHalo <= NT, "ring depth / tile shape");
+  extern __shared__ __align__(1024) double ring[];  // [S input planes][3 first-sweep planes][S mbarriers]
+  double* l0 = ring + S * T::kPlaneStride;
+  uint64_t* full = reinterpret_cast<uint64_t*>(l0 + 3 * T::kL0);
+
+  const int lane = threadIdx.x & 31;
+  const int wx = (threadIdx.x >> 5) % WX;
+  const int wy = (threadIdx.x >> 5) / WX;
+  const int64_t x0 = 1 + (int64_t)blockIdx.x * BX;
+  const int64_t y0 = 1 + (int64_t)blockIdx.y * BY;
+  const int64_t za = 1 + (int64_t)blockIdx.z * planes_per_chunk;
+  const int64_t zb = min(nz, za + planes_per_chunk - 1);
+  const int np = (int)(zb - za + 5);  // input planes za-2 .. zb+2
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm);
+    for (int q = 0; q < S; ++q) mbar_init(&full[q], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int32_t cx = (int32_t)(x0 - 3), cy = (int32_t)(y0 - 2);
+  auto issue = [&](int p, int slot) {
+    mbar_arrive_expect_tx(&full[slot], T::kTxBytes);
+    tma_load_3d(ring + slot * T::kPlaneStride, &tm, cx, cy, (int32_t)(za - 2 + p), &full[slot]);
+  };
+  if (threadIdx.x == 0)
+    for (int p = 0; p < S && p < np; ++p) issue(p, p);
+
+  // Own points: column lx = 1 + wx*32 + lane, rows ly0 .. ly0+R-1 of the first-sweep region
+  // (= the thread's output points). Their input and first-sweep z columns ride in registers.
+  const int lxo = 1 + wx * 32 + lane, ly0 = 1 + wy * R;
+  const int qo = ly0 * T::LX + lxo;                 // first-sweep index of row 0
+  const int co = (ly0 + 1) * T::SX + lxo + 2;       // input-tile offset of row 0
+  const int64_t x = x0 + wx * 32 + lane, yb = y0 + (int64_t)wy * R;
+  bool ok[R], oring[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    ok[i] = (yb + i <= ny) && (x <= nx);
+    oring[i] = (x == nx + 1) || (yb + i == ny + 1);
+  }
+  // Halo point (threads < kHalo): rows 0 and LY-1 of the region, then columns 0 and LX-1
+  const bool has_h = threadIdx.x < kHalo;
+  int hq = 0;
+  {
+    const int t = threadIdx.x;
+    int ly, lx;
+    if (t < T::LX) { ly = 0; lx = t; }
+    else if (t < 2 * T::LX) { ly = T::LY - 1; lx = t - T::LX; }
+    else { const int u = t - 2 * T::LX; ly = 1 + (u >> 1); lx = (u & 1) ? T::LX - 1 : 0; }
+    hq = has_h ? ly * T::LX + lx : 0;
+  }
+  const int hly = hq / T::LX, hlx = hq - hly * T::LX;
+  const int hc = (hly + 1) * T::SX + hlx + 2;
+  const int64_t hgx = x0 - 1 + hlx, hgy = y0 - 1 + hly;
+  const bool hring = hgx == 0 || hgx == nx + 1 || hgy == 0 || hgy == ny + 1;
+
+  const int64_t plane_elems = (ny + 2) * ldx;
+  double* out = dst + (za * (ny + 2) + yb) * ldx + x;
+
+  mbar_wait_parity(&full[0], 0);
+  mbar_wait_parity(&full[1], 0);
+  double im[R], ic[R], ip[R];  // input, own column: planes L-1, L, L+1
+  double am[R], ac[R], ap[R];  // first sweep, own column: planes O-1, O, O+1 (O = L-1)
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    im[i] = ring[co + i * T::SX];
+    ic[i] = ring[T::kPlaneStride + co + i * T::SX];
+    am[i] = ac[i] = 0.0;
+  }
+  double him = ring[hc], hic = ring[T::kPlaneStride + hc];
+
+  int slot_m = 0;  // ring slot of input plane L-1 (index j)
+  for (int j = 0; j < np - 2; ++j) {  // first-sweep planes za-1 .. zb+1
+    const int s1 = (slot_m + 1) % S, s2 = (slot_m + 2) % S;
+    mbar_wait_parity(&full[s2], ((j + 2) / S) & 1);
+    const int64_t L = za - 1 + j;
+    const double* Ic = ring + s1 * T::kPlaneStride;
+    const double* Ip = ring + s2 * T::kPlaneStride;
+    double* Lout = l0 + (int)(L % 3) * T::kL0;
+    const bool zring = (L == 0) || (L == nz + 1);
+    // ---- first sweep of plane L: own points (z and own-row y neighbours from registers)
+#pragma unroll
+    for (int i = 0; i < R; ++i) ip[i] = Ip[co + i * T::SX];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int c = co + i * T::SX;
+      const double ym = i > 0 ? ic[i - 1] : Ic[c - T::SX];
+      const double yp = i + 1 < R ? ic[i + 1] : Ic[c + T::SX];
+      const double sum = dadd(dadd(dadd(dadd(dadd(im[i], ip[i]), ym), yp), Ic[c - 1]), Ic[c + 1]);
+      const double v = (zring || oring[i]) ? ic[i] : ddiv6(sum);  // Dirichlet: unchanged by the sweep
+      ap[i] = v;
+      Lout[qo + i * T::LX] = v;
+    }
+    // ---- first sweep of plane L: the halo point
+    if (has_h) {
+      const double hip = Ip[hc];
+      const double sum = dadd(dadd(dadd(dadd(dadd(him, hip), Ic[hc - T::SX]), Ic[hc + T::SX]), Ic[hc - 1]), Ic[hc + 1]);
+      Lout[hq] = (zring || hring) ? hic : ddiv6(sum);
+      him = hic;
+      hic = hip;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      im[i] = ic[i];
+      ic[i] = ip[i];
+    }
+    __syncthreads();
+    // ---- second sweep of plane O = L-1: z neighbours from registers, in-plane from the ring
+    if (j >= 2) {
+      const double* Zc = l0 + (int)((L - 1) % 3) * T::kL0;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int q = qo + i * T::LX;
+        const double ym = i > 0 ? ac[i - 1] : Zc[q - T::LX];
+        const double yp = i + 1 < R ? ac[i + 1] : Zc[q + T::LX];
+        const double sum = dadd(dadd(dadd(dadd(dadd(am[i], ap[i]), ym), yp), Zc[q - 1]), Zc[q + 1]);
+        if (ok[i]) out[i * ldx] = ddiv6(sum);
+      }
+      out += plane_elems;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      am[i] = ac[i];
+      ac[i] = ap[i];
+    }
+    __syncthreads();  // every read of input plane index j and of first-sweep plane O-1 is done
+    if (threadIdx.x == 0 && j + S < np) {
+      fence_proxy_async_smem();
+      issue(j + S, slot_m);
+    }
+    slot_m = s1;
+  }
+}
+
+template <int BX, int BY, int S, int R>
+st_status launch_j3t2(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nz, int64_t ldx,
+                      cudaStream_t s) {
+  using T = J3T2Tile<BX, BY>;
+  CUtensorMap tm;
+  const uint64_t dims[3] = {(uint64_t)(nx + 2), (uint64_t)(ny + 2), (uint64_t)(nz + 2)};
+  const uint32_t box[3] = {(uint32_t)T::SX, (uint32_t)T::SY, 1u};
+  ST_TRY(make_tmap_3d_f64(&tm, src, dims, (uint64_t)ldx * 8, (uint64_t)ldx * 8 * (uint64_t)(ny + 2), box));
+  const size_t smem = (size_t)S * T::kPlaneStride * sizeof(double) + 3 * T::kL0 * sizeof(double) +
+                      S * sizeof(uint64_t);
+  ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi3d_t2_kernel<BX, BY, S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  const int64_t ntx = (nx + BX - 1) / BX, nty = (ny + BY - 1) / BY;
+  static const int kPpc = env_int("ST_J3T2_PLANES", 64);
+  const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(kPpc, nz));
+  const int64_t nzc = (nz + ppc - 1) / ppc;
+  ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "jacobi3d: grid too large");
+  jacobi3d_t2_kernel<BX, BY, S, R><<<dim3((unsigned)ntx, (unsigned)nty, (unsigned)nzc), (BX / 32) * (BY / R) * 32,
+                                     smem, s>>>(tm, dst, nx, ny, nz, ldx, ppc);
+  ST_LAUNCHED();
+  return ST_OK;
+}
 }  // namespace
 
 st_status jacobi3d_preload() {
@@ -194,7 +377,24 @@ st_status jacobi3d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<64, 16, 6, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<64, 16, 8, 1>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_copy_faces_kernel));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 6, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 4, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 5, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 5, 2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 4, 4>));
   return ST_OK;
+}
+
+st_status jacobi3d_two_sweeps(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nz, int64_t ldx,
+                              cudaStream_t s) {
+  static const int kV = env_int("ST_J3T2_VARIANT", 0);
+  switch (kV) {
+    case 1: return launch_j3t2<128, 16, 4, 2>(src, dst, nx, ny, nz, ldx, s);
+    case 2: return launch_j3t2<128, 16, 5, 2>(src, dst, nx, ny, nz, ldx, s);
+    case 3: return launch_j3t2<128, 8, 5, 2>(src, dst, nx, ny, nz, ldx, s);
+    case 4: return launch_j3t2<128, 16, 4, 4>(src, dst, nx, ny, nz, ldx, s);
+    default: return launch_j3t2<128, 8, 6, 2>(src, dst, nx, ny, nz, ldx, s);
+  }
 }
 
 st_status jacobi3d_sweep_planes(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,

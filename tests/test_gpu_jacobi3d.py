@@ -52,8 +52,24 @@ def test_tblock_rejected(cuda_lib):
     import torch
     a = torch.zeros(6, 6, 6, dtype=torch.float64, device="cuda")
     with pytest.raises(cuda_lib.StencilError) as e:
-        cuda_lib.st_jacobi3d_run(a, a.clone(), 3, tblock=2)
+        cuda_lib.st_jacobi3d_run(a, a.clone(), 3, tblock=3)
     assert e.value.code == cuda_lib.ST_ENOTSUP
+
+
+@pytest.mark.parametrize("iters", [2, 3, 4, 5, 6, 9])
+@pytest.mark.parametrize("shape", [(45, 37, 21), (130, 17, 70), (1, 1, 1), (300, 9, 3)])
+def test_two_sweep_passes_equal_single_sweeps(cuda_lib, iters, shape):
+    # temporal blocking T = 2 (tblock 0 = auto, 2 = forced) is bitwise T = 1 and the oracle,
+    # for every parity of the pass count
+    import torch
+    nx, ny, nz = shape
+    g = si.jacobi3d_grid(nx, ny, nz)
+    want = oracle.jacobi3d(g, iters)
+    for tb in (1, 2, 0):
+        a = torch.from_numpy(g).cuda()
+        r = cuda_lib.st_jacobi3d_run(a, torch.full_like(a, float("nan")), iters, tblock=tb)
+        torch.cuda.synchronize()
+        assert np.array_equal(r.cpu().numpy(), want), f"tblock={tb}"
 
 
 @pytest.mark.parametrize("h", [1, 3])
