@@ -495,14 +495,21 @@ def main():
         ev1.synchronize()
         j3_launches = st.launch_count() - jl0
         j3_ms = max_over_ranks(ev0.elapsed_time(ev1))
-        j3_launch_ms = j3_ms / max(1, j3_launches - 1)  # minus the one-off face copy
+        # one launch per pass (plus the one-off face copy); a single domain runs two sweeps per
+        # pass (jacobi3d_t2_kernel), slabs one: a pass reads and writes the grid once (16 B/pt)
+        t2 = world == 1 and j3_sweeps >= 2
+        j3_kernel = "jacobi3d_t2_kernel" if t2 else "jacobi3d_kernel"
+        j3_launch_ms = j3_ms / max(1, j3_launches - 1)
         j3_gbs = JACOBI_BYTES_PER_PT * n3 * n3 * nz3 / (j3_launch_ms / 1e3) / 1e9
         j3 = {"workload": f"jacobi3d_{n3}^3_fp64_{j3_sweeps}sweeps" + ("" if world == 1 else f"_zslabs{world}"),
               "value": round(n3 ** 3 * j3_sweeps / (j3_ms / 1e3) / 1e9, 3), "unit": UNIT,
               "ms_per_step": round(j3_ms, 3), "gpu_launches": j3_launches,
-              "roofline": {"bound": "hbm", "kernel": "jacobi3d_kernel", "achieved": round(j3_gbs, 1),
+              "roofline": {"bound": "hbm", "kernel": j3_kernel, "achieved": round(j3_gbs, 1),
                            "peak": hbm_peak, "unit": "GB/s", "frac": round(j3_gbs / hbm_peak, 4),
-                           "traffic": ncu_traffic("jacobi3d_kernel"), "bytes_per_pt": JACOBI_BYTES_PER_PT,
+                           "traffic": ncu_traffic(j3_kernel), "bytes_per_pt_per_launch": JACOBI_BYTES_PER_PT,
+                           "sweeps_per_launch": 2 if t2 else 1,
+                           "effective_gbs_16B_per_update": round(
+                               JACOBI_BYTES_PER_PT * n3 * n3 * nz3 * j3_sweeps / (j3_ms / 1e3) / 1e9, 1),
                            "peak_source": peak_src}}
         if world == 1 and not args.no_cpu:
             import oracle

@@ -350,7 +350,7 @@ st_status launch_j3t2(const double* src, double* dst, int64_t nx, int64_t ny, in
   ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi3d_t2_kernel<BX, BY, S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
   const int64_t ntx = (nx + BX - 1) / BX, nty = (ny + BY - 1) / BY;
-  static const int kPpc = env_int("ST_J3T2_PLANES", 64);
+  static const int kPpc = env_int("ST_J3T2_PLANES", 96);
   const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(kPpc, nz));
   const int64_t nzc = (nz + ppc - 1) / ppc;
   ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "jacobi3d: grid too large");
