@@ -204,9 +204,9 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
   constexpr int NT = (BX / 32) * (BY / R) * 32, WX = BX / 32;
   constexpr int kHalo = 2 * T::LX + 2 * BY;  // first-sweep points outside the BX x BY tile
   static_assert(S >= 4 && BY % R == 0 && BX % 32 == 0 && kHalo <= NT, "ring depth / tile shape");
-  extern __shared__ __align__(1024) double ring[];  // [S input planes][3 first-sweep planes][S mbarriers]
+  extern __shared__ __align__(1024) double ring[];  // [S input planes][4 first-sweep planes][S mbarriers]
   double* l0 = ring + S * T::kPlaneStride;
-  uint64_t* full = reinterpret_cast<uint64_t*>(l0 + 3 * T::kL0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(l0 + 4 * T::kL0);
 
   const int lane = threadIdx.x & 31;
   const int wx = (threadIdx.x >> 5) % WX;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
     const int64_t L = za - 1 + j;
     const double* Ic = ring + s1 * T::kPlaneStride;
     const double* Ip = ring + s2 * T::kPlaneStride;
-    double* Lout = l0 + (int)(L % 3) * T::kL0;
+    double* Lout = l0 + (int)(L & 3) * T::kL0;  // 4 slots: a mask, not a 64-bit modulo
     const bool zring = (L == 0) || (L == nz + 1);
     // ---- first sweep of plane L: own points (z and own-row y neighbours from registers)
 #pragma unroll
@@ -310,9 +310,17 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
       ic[i] = ip[i];
     }
     __syncthreads();
+    // One barrier per plane: input plane index j (slot slot_m) was last read from shared
+    // memory in step j-1, and the first-sweep slot step j+1 writes, (L+1) & 3 = plane L-3,
+    // was last read by step j-2's second sweep — both before this barrier; the only
+    // shared-memory reads of the first-sweep ring (plane L-1 below) follow step j-1's barrier.
+    if (threadIdx.x == 0 && j + S < np) {
+      fence_proxy_async_smem();
+      issue(j + S, slot_m);
+    }
     // ---- second sweep of plane O = L-1: z neighbours from registers, in-plane from the ring
     if (j >= 2) {
-      const double* Zc = l0 + (int)((L - 1) % 3) * T::kL0;
+      const double* Zc = l0 + (int)((L - 1) & 3) * T::kL0;
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         const int q = qo + i * T::LX;
@@ -328,11 +336,6 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
       am[i] = ac[i];
       ac[i] = ap[i];
     }
-    __syncthreads();  // every read of input plane index j and of first-sweep plane O-1 is done
-    if (threadIdx.x == 0 && j + S < np) {
-      fence_proxy_async_smem();
-      issue(j + S, slot_m);
-    }
     slot_m = s1;
   }
 }
@@ -345,7 +348,7 @@ st_status launch_j3t2(const double* src, double* dst, int64_t nx, int64_t ny, in
   const uint64_t dims[3] = {(uint64_t)(nx + 2), (uint64_t)(ny + 2), (uint64_t)(nz + 2)};
   const uint32_t box[3] = {(uint32_t)T::SX, (uint32_t)T::SY, 1u};
   ST_TRY(make_tmap_3d_f64(&tm, src, dims, (uint64_t)ldx * 8, (uint64_t)ldx * 8 * (uint64_t)(ny + 2), box));
-  const size_t smem = (size_t)S * T::kPlaneStride * sizeof(double) + 3 * T::kL0 * sizeof(double) +
+  const size_t smem = (size_t)S * T::kPlaneStride * sizeof(double) + 4 * T::kL0 * sizeof(double) +
                       S * sizeof(uint64_t);
   ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi3d_t2_kernel<BX, BY, S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
@@ -391,9 +394,9 @@ st_status jacobi3d_two_sweeps(const double* src, double* dst, int64_t nx, int64_
   switch (kV) {
     case 1: return launch_j3t2<128, 16, 4, 2>(src, dst, nx, ny, nz, ldx, s);
     case 2: return launch_j3t2<128, 16, 5, 2>(src, dst, nx, ny, nz, ldx, s);
-    case 3: return launch_j3t2<128, 8, 5, 2>(src, dst, nx, ny, nz, ldx, s);
+    case 3: return launch_j3t2<128, 8, 6, 2>(src, dst, nx, ny, nz, ldx, s);
     case 4: return launch_j3t2<128, 16, 4, 4>(src, dst, nx, ny, nz, ldx, s);
-    default: return launch_j3t2<128, 8, 6, 2>(src, dst, nx, ny, nz, ldx, s);
+    default: return launch_j3t2<128, 8, 5, 2>(src, dst, nx, ny, nz, ldx, s);
   }
 }
 

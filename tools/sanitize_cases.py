@@ -21,7 +21,8 @@ for nx, ny, nz in ((70, 13, 9), (129, 17, 70)):
 for nx, ny, nz in ((33, 31, 9), (70, 40, 66)):
     a = torch.from_numpy(si.jacobi3d_grid(nx, ny, nz)).cuda()
     b = torch.empty_like(a)
-    st.st_jacobi3d_run(a, b, 3)
+    st.st_jacobi3d_run(a, b, 3)  # T=1 sweeps (odd pass count)
+    st.st_jacobi3d_run(a, b, 4)  # two T=2 passes (jacobi3d_t2_kernel)
 for nx, ny, ld, iters in ((200, 95, 202, 3), (65, 33, 67, 2), (1000, 130, 1002, 2)):  # GS: tiled (even ld), register (odd)
     a = torch.from_numpy(si.jacobi2d_grid(nx, ny, ld=ld)).cuda()
     st.st_gauss_seidel2d_run(a, iters, nx=nx)
