@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(1024)
 // warp shuffles, and the first/last row of every warp goes through shared
 // memory (double-buffered by sweep parity, so one barrier per sweep). Shared
 // traffic per sweep is 2 rows per warp instead of 4 reads + 1 write per point.
-constexpr int kRegResMaxWarps = 17;  // 68 rows: ny <= 67 with R = 4
+constexpr int kRegResMaxWarps = 22;  // 88 rows with R = 4 (ny <= 87), 66 with R = 3
 
 template <int R>
 __global__ void __launch_bounds__(32 * kRegResMaxWarps)
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(32 * kRegResMaxWarps)
   }
 }
 
-constexpr int kRegResRows = 4;
+constexpr int kRegResRows = 3;
 
 constexpr size_t kResidentMaxSmem = 200 * 1024;
 
@@ -259,10 +259,13 @@ st_status jacobi2d_resident(double* a, double* b, int64_t nx, int64_t ny, int64_
                             cudaStream_t s) {
   static const int kRegRes = env_int("ST_JACOBI_REGRES", kRegResRows);  // rows per warp (0: shared-memory kernel)
   if (kRegRes && nx <= 64) {
-    const int64_t rr = kRegRes == 8 ? 8 : kRegRes == 2 ? 2 : 4;
+    const int64_t rr = kRegRes == 8 ? 8 : kRegRes == 2 ? 2 : kRegRes == 3 ? 3 : 4;
     const int64_t warps = (ny + 1 + rr - 1) / rr;  // rows 1 .. ny+1 (incl. the ring row)
     if (warps <= kRegResMaxWarps) {
-      auto* k = rr == 8 ? jacobi2d_regres_kernel<8> : rr == 2 ? jacobi2d_regres_kernel<2> : jacobi2d_regres_kernel<4>;
+      auto* k = rr == 8   ? jacobi2d_regres_kernel<8>
+                : rr == 2 ? jacobi2d_regres_kernel<2>
+                : rr == 3 ? jacobi2d_regres_kernel<3>
+                          : jacobi2d_regres_kernel<4>;
       k<<<1, (unsigned)(32 * warps), 0, s>>>(a, b, (int)nx, (int)ny, ld, iters);
       ST_LAUNCHED();
       return ST_OK;
@@ -631,6 +634,7 @@ st_status jacobi2d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_stream_kernel<4>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_resident_kernel));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<3>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<4>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<8>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<2, 1>));
