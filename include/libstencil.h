@@ -225,6 +225,14 @@ st_status st_jacobi2d_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_t
                                int32_t halo, int64_t iters, int32_t tblock, st_op* ops,
                                int64_t cap, int64_t* nops);
 
+/* The schedule of st_jacobi3d_run for one rank, as st_jacobi2d_schedule with
+ * planes for rows: nz_local owned planes, `halo` ghost planes per side,
+ * tblock 0 (auto), 1 or 2 (sweeps per pass; y_lo/y_hi/ring_lo/ring_hi are
+ * plane indices of the slab buffer). Host-only; no device needed. */
+st_status st_jacobi3d_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_t nz_local,
+                               int32_t halo, int64_t iters, int32_t tblock, st_op* ops,
+                               int64_t cap, int64_t* nops);
+
 /* `iters` sweeps of
  *     B[y][x] = (((A[y-1][x] + A[y+1][x]) + A[y][x-1]) + A[y][x+1]) * 0.25
  * over the interior 1 <= y <= ny_local, 1 <= x <= nx, with value semantics
@@ -345,8 +353,13 @@ st_status st_gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, i
  *             depth; planes are swapped with rank -/+ 1 every `halo` sweeps
  *             (boundary planes first, swap overlapped with the interior
  *             planes); edge ranks keep the global Dirichlet plane next to their
- *             owned planes. Requires nz_local >= halo.
- *   tblock    0 or 1 (one sweep per pass over HBM); others -> ST_ENOTSUP.
+ *             owned planes. Requires nz_local >= halo. The exact step
+ *             sequence is st_jacobi3d_schedule's.
+ *   tblock    1 = one sweep per pass over HBM; 2 = two sweeps per pass
+ *             (temporal blocking; across ranks it needs halo >= 2, else
+ *             ST_EINVAL); 0 = auto: 2 on a single domain and on slabs with
+ *             halo >= 2, else 1; others -> ST_ENOTSUP. Any choice gives
+ *             bitwise the same result.
  *   *result_in_b (may be NULL) = iters & 1. */
 st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t nz_local, int64_t ldx,
                           int32_t halo, int64_t iters, int32_t tblock, st_comm* comm,

@@ -14,6 +14,7 @@ Entry points (same names as the C ABI, tensors instead of raw pointers):
     st_halo_exchange(comm, fields, n_slow_local, slab_pitch, width)
     st_halo_plan(rank, nranks, n_slow_local, slab_pitch, width) -> (sends, recvs)   [host only]
     st_jacobi2d_schedule(rank, nranks, nx, ny_local, halo, iters, tblock) -> [ops]   [host only]
+    st_jacobi3d_schedule(rank, nranks, nx, nz_local, halo, iters, tblock) -> [ops]   [host only]
     st_block_split(n, nranks, rank) -> (start, count)                                [host only]
     Comm.create(rank, nranks, unique_id, device) / Comm.from_process_group(pg, device)
     Comm.local_group(nranks, devices) -> [Comm]; comm.bind(buffers, n_slow_local)
@@ -85,6 +86,8 @@ _SIGS = {
                                     ctypes.POINTER(_i32), ctypes.POINTER(Xfer), ctypes.POINTER(_i32)]),
     "st_halo_exchange": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), _i32, _i64, _i64, _i32, _vp]),
     "st_jacobi2d_schedule": (ctypes.c_int, [_i32, _i32, _i64, _i64, _i32, _i64, _i32, ctypes.POINTER(Op), _i64,
+                                            ctypes.POINTER(_i64)]),
+    "st_jacobi3d_schedule": (ctypes.c_int, [_i32, _i32, _i64, _i64, _i32, _i64, _i32, ctypes.POINTER(Op), _i64,
                                             ctypes.POINTER(_i64)]),
     "st_jacobi2d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i32, _i64, _i32, _vp, _vp,
                                        ctypes.POINTER(_i32)]),
@@ -295,16 +298,25 @@ def st_halo_plan(rank: int, nranks: int, n_slow_local: int, slab_pitch: int, wid
     return [conv(sends[i]) for i in range(ns.value)], [conv(recvs[i]) for i in range(nr.value)]
 
 
+def _schedule(name, rank, nranks, nx, n_local, halo, iters, tblock):
+    fn = getattr(lib(), name)
+    n = _i64()
+    _check(fn(rank, nranks, nx, n_local, halo, iters, tblock, None, 0, ctypes.byref(n)), name)
+    arr = (Op * max(1, n.value))()
+    _check(fn(rank, nranks, nx, n_local, halo, iters, tblock, arr, n.value, ctypes.byref(n)), name)
+    return [{f: getattr(arr[i], f) for f, _ in Op._fields_} for i in range(n.value)]
+
+
 def st_jacobi2d_schedule(rank: int, nranks: int, nx: int, ny_local: int, halo: int, iters: int,
                          tblock: int = 0) -> list[dict]:
     """The step schedule st_jacobi2d_run executes for one rank (host only)."""
-    n = _i64()
-    _check(lib().st_jacobi2d_schedule(rank, nranks, nx, ny_local, halo, iters, tblock, None, 0, ctypes.byref(n)),
-           "st_jacobi2d_schedule")
-    arr = (Op * max(1, n.value))()
-    _check(lib().st_jacobi2d_schedule(rank, nranks, nx, ny_local, halo, iters, tblock, arr, n.value,
-                                      ctypes.byref(n)), "st_jacobi2d_schedule")
-    return [{f: getattr(arr[i], f) for f, _ in Op._fields_} for i in range(n.value)]
+    return _schedule("st_jacobi2d_schedule", rank, nranks, nx, ny_local, halo, iters, tblock)
+
+
+def st_jacobi3d_schedule(rank: int, nranks: int, nx: int, nz_local: int, halo: int, iters: int,
+                         tblock: int = 0) -> list[dict]:
+    """The step schedule st_jacobi3d_run executes for one rank (host only; rows = planes)."""
+    return _schedule("st_jacobi3d_schedule", rank, nranks, nx, nz_local, halo, iters, tblock)
 
 
 # ------------------------------------------------------------- compute ---

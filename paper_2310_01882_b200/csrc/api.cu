@@ -165,7 +165,11 @@ st_status run_schedule3d(const std::vector<st_op>& ops, st_comm* comm, double* a
   const int64_t nplanes = n + 2 * (int64_t)h;
   return run_schedule_generic(ops, comm, a, b, n, (ny + 2) * ldx, s,
                               [&](const double* src, double* dst, const st_op& o, Remote rem) -> st_status {
-                                ST_RETURN_IF(o.sweeps != 1, ST_EINTERNAL, "jacobi3d: pass of %d sweeps", o.sweeps);
+                                ST_RETURN_IF(o.sweeps != 1 && o.sweeps != 2, ST_EINTERNAL,
+                                             "jacobi3d: pass of %d sweeps", o.sweeps);
+                                if (o.sweeps == 2)
+                                  return jacobi3d_two_sweeps(src, dst, nx, ny, nplanes, ldx, o.y_lo, o.y_hi,
+                                                             o.ring_lo, o.ring_hi, s, rem);
                                 return jacobi3d_sweep_planes(src, dst, nx, ny, nplanes, ldx, o.y_lo, o.y_hi, s, rem);
                               });
 }
@@ -375,8 +379,9 @@ st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
   ST_RETURN_IF(!aligned16(a) || !aligned16(b), ST_EINVAL, "st_jacobi3d_run: fields must be 16-byte aligned");
   ST_RETURN_IF(iters < 0 || tblock < 0 || halo < 1, ST_EINVAL, "st_jacobi3d_run: iters=%lld tblock=%d halo=%d",
                (long long)iters, tblock, halo);
-  ST_RETURN_IF(tblock > 2 || (tblock == 2 && comm && comm->nranks > 1), ST_ENOTSUP,
-               "st_jacobi3d_run: tblock=%d not supported (0, 1; 2 on a single domain)", tblock);
+  ST_RETURN_IF(tblock > 2, ST_ENOTSUP, "st_jacobi3d_run: tblock=%d not supported (0, 1, 2)", tblock);
+  ST_RETURN_IF(tblock == 2 && comm && comm->nranks > 1 && halo < 2, ST_EINVAL,
+               "st_jacobi3d_run: tblock=2 across ranks needs halo >= 2");
   ST_RETURN_IF(!comm && halo != 1, ST_EINVAL, "st_jacobi3d_run: halo must be 1 without a comm");
   ST_RETURN_IF(comm && nz < halo, ST_EINVAL, "st_jacobi3d_run: slab of %lld planes < halo %d", (long long)nz, halo);
   ST_RETURN_IF(nx + 2 > (int64_t)INT32_MAX || ny + 2 > (int64_t)INT32_MAX || nz + 2 * halo > (int64_t)INT32_MAX,
@@ -391,7 +396,7 @@ st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
   const int32_t nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
   if (comm) ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier NCCL error");
   std::vector<st_op> ops;
-  ST_TRY(build_jacobi_schedule(rank, nranks, nx, nz, halo, iters, 1, ops, 3));
+  ST_TRY(build_jacobi_schedule(rank, nranks, nx, nz, halo, iters, tblock, ops, 3));
   // ghost / Dirichlet planes and the side faces of the owned planes a -> b (pitch padding untouched)
   const size_t pitch = (size_t)ldx * sizeof(double), width = (size_t)(nx + 2) * sizeof(double);
   const int64_t plane = (ny + 2) * ldx;
@@ -400,23 +405,9 @@ st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
   ST_CHECK_CUDA(cudaMemcpy2DAsync(b + (halo + nz) * plane, pitch, a + (halo + nz) * plane, pitch, width,
                                   (size_t)halo * (size_t)(ny + 2), cudaMemcpyDeviceToDevice, s));
   ST_TRY(jacobi3d_copy_faces(a, b, nx, ny, ldx, halo, halo + nz - 1, s));
-  // single domain: two sweeps per pass (temporal blocking T = 2, auto unless tblock = 1);
-  // the pass count keeps the parity of iters so the result lands in b iff iters is odd
-  static const int kT2 = env_int("ST_J3_T2", 1);
-  if (nranks == 1 && halo == 1 && iters >= 2 && (tblock == 2 || (tblock == 0 && kT2))) {
-    int64_t two = iters / 2, one = iters % 2;
-    if (two & 1) { two -= 1; one += 2; }
-    const double* src = a;
-    double* dst = b;
-    for (int64_t p = 0; p < two + one; ++p) {
-      if (p < two) ST_TRY(jacobi3d_two_sweeps(src, dst, nx, ny, nz, ldx, s));
-      else ST_TRY(jacobi3d_sweep_planes(src, dst, nx, ny, nz + 2, ldx, 1, nz, s, Remote()));
-      double* t = const_cast<double*>(src);
-      src = dst;
-      dst = t;
-    }
-    return ST_OK;
-  }
+  // two sweeps per pass (temporal blocking T = 2) where the ghosts allow it: the single domain
+  // and slabs with halo >= 2 (schedule.cu choose_tblock3d); the schedule keeps the parity so
+  // the result lands in b iff iters is odd
   return run_schedule3d(ops, comm, a, b, nx, ny, nz, ldx, halo, s);
 }
 

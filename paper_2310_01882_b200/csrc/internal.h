@@ -110,8 +110,10 @@ st_status build_jacobi_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_
 // preload all kernels at creation.
 st_status jacobi2d_preload();
 st_status jacobi3d_preload();
-st_status jacobi3d_two_sweeps(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nz, int64_t ldx,
-                              cudaStream_t s);
+// two sweeps per launch (T = 2) of output planes [z_lo, z_hi]; planes <= ring_lo / >= ring_hi are Dirichlet
+st_status jacobi3d_two_sweeps(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
+                              int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi,
+                              cudaStream_t s, Remote rem = Remote());
 st_status stencil2d_preload();
 st_status pw_advect3d_preload();
 inline st_status preload_kernels() {

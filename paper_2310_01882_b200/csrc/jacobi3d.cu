@@ -177,8 +177,12 @@ st_status launch_j3(const double* src, double* dst, int64_t nx, int64_t ny, int6
 }
 
 
-// ---- Two sweeps per pass (temporal blocking T = 2, single domain). A CTA owns
-// a BX x BY interior column and a chunk of output planes. Input planes (tile +
+// ---- Two sweeps per pass (temporal blocking T = 2). A CTA owns a BX x BY
+// interior column and a chunk of the output planes [z_lo, z_hi] of a buffer of
+// nplanes_buf planes; planes <= ring_lo / >= ring_hi are Dirichlet planes (the
+// single domain: 0 and nz+1; a slab: its global boundary plane, or none — then
+// the first sweep also runs on the ghost planes z_lo-1 and z_hi+1, which the
+// caller's ghost depth >= 2 provides). Input planes (tile +
 // 2-cell apron; the box starts at x0-3 so TMA's 16-byte start rule holds) stream
 // through an S-slot TMA ring; for every plane L the CTA first computes the
 // first-sweep values of the (BX+2) x (BY+2) region around its tile into a 3-plane
@@ -196,10 +200,11 @@ struct J3T2Tile {
   static constexpr int kL0 = LX * LY;
 };
 
-template <int BX, int BY, int S, int R>
+template <int BX, int BY, int S, int R, bool kRem>
 __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
     jacobi3d_t2_kernel(const __grid_constant__ CUtensorMap tm, double* __restrict__ dst, int64_t nx, int64_t ny,
-                       int64_t nz, int64_t ldx, int64_t planes_per_chunk) {
+                       int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi,
+                       int64_t planes_per_chunk, double* __restrict__ dst2, int64_t delta2) {
   using T = J3T2Tile<BX, BY>;
   constexpr int NT = (BX / 32) * (BY / R) * 32, WX = BX / 32;
   constexpr int kHalo = 2 * T::LX + 2 * BY;  // first-sweep points outside the BX x BY tile
@@ -213,8 +218,8 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
   const int wy = (threadIdx.x >> 5) / WX;
   const int64_t x0 = 1 + (int64_t)blockIdx.x * BX;
   const int64_t y0 = 1 + (int64_t)blockIdx.y * BY;
-  const int64_t za = 1 + (int64_t)blockIdx.z * planes_per_chunk;
-  const int64_t zb = min(nz, za + planes_per_chunk - 1);
+  const int64_t za = z_lo + (int64_t)blockIdx.z * planes_per_chunk;
+  const int64_t zb = min(z_hi, za + planes_per_chunk - 1);
   const int np = (int)(zb - za + 5);  // input planes za-2 .. zb+2
 
   if (threadIdx.x == 0) {
@@ -261,6 +266,8 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
 
   const int64_t plane_elems = (ny + 2) * ldx;
   double* out = dst + (za * (ny + 2) + yb) * ldx + x;
+  // fused halo swap (kRem: a separate instantiation, the plain one keeps its registers)
+  double* out2 = kRem ? dst2 + ((za + delta2) * (ny + 2) + yb) * ldx + x : nullptr;
 
   mbar_wait_parity(&full[0], 0);
   mbar_wait_parity(&full[1], 0);
@@ -282,7 +289,7 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
     const double* Ic = ring + s1 * T::kPlaneStride;
     const double* Ip = ring + s2 * T::kPlaneStride;
     double* Lout = l0 + (int)(L & 3) * T::kL0;  // 4 slots: a mask, not a 64-bit modulo
-    const bool zring = (L == 0) || (L == nz + 1);
+    const bool zring = (L <= ring_lo) || (L >= ring_hi);
     // ---- first sweep of plane L: own points (z and own-row y neighbours from registers)
 #pragma unroll
     for (int i = 0; i < R; ++i) ip[i] = Ip[co + i * T::SX];
@@ -327,9 +334,14 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
         const double ym = i > 0 ? ac[i - 1] : Zc[q - T::LX];
         const double yp = i + 1 < R ? ac[i + 1] : Zc[q + T::LX];
         const double sum = dadd(dadd(dadd(dadd(dadd(am[i], ap[i]), ym), yp), Zc[q - 1]), Zc[q + 1]);
-        if (ok[i]) out[i * ldx] = ddiv6(sum);
+        if (ok[i]) {
+          const double v = ddiv6(sum);
+          out[i * ldx] = v;
+          if (kRem) out2[i * ldx] = v;
+        }
       }
       out += plane_elems;
+      if (kRem) out2 += plane_elems;
     }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -341,24 +353,24 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
 }
 
 template <int BX, int BY, int S, int R>
-st_status launch_j3t2(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nz, int64_t ldx,
-                      cudaStream_t s) {
+st_status launch_j3t2(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf, int64_t ldx,
+                      int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi, cudaStream_t s, Remote rem) {
   using T = J3T2Tile<BX, BY>;
   CUtensorMap tm;
-  const uint64_t dims[3] = {(uint64_t)(nx + 2), (uint64_t)(ny + 2), (uint64_t)(nz + 2)};
+  const uint64_t dims[3] = {(uint64_t)(nx + 2), (uint64_t)(ny + 2), (uint64_t)nplanes_buf};
   const uint32_t box[3] = {(uint32_t)T::SX, (uint32_t)T::SY, 1u};
   ST_TRY(make_tmap_3d_f64(&tm, src, dims, (uint64_t)ldx * 8, (uint64_t)ldx * 8 * (uint64_t)(ny + 2), box));
   const size_t smem = (size_t)S * T::kPlaneStride * sizeof(double) + 4 * T::kL0 * sizeof(double) +
                       S * sizeof(uint64_t);
-  ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi3d_t2_kernel<BX, BY, S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-  const int64_t ntx = (nx + BX - 1) / BX, nty = (ny + BY - 1) / BY;
+  auto kern = rem.base ? jacobi3d_t2_kernel<BX, BY, S, R, true> : jacobi3d_t2_kernel<BX, BY, S, R, false>;
+  ST_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t ntx = (nx + BX - 1) / BX, nty = (ny + BY - 1) / BY, nz = z_hi - z_lo + 1;
   static const int kPpc = env_int("ST_J3T2_PLANES", 96);
   const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(kPpc, nz));
   const int64_t nzc = (nz + ppc - 1) / ppc;
   ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "jacobi3d: grid too large");
-  jacobi3d_t2_kernel<BX, BY, S, R><<<dim3((unsigned)ntx, (unsigned)nty, (unsigned)nzc), (BX / 32) * (BY / R) * 32,
-                                     smem, s>>>(tm, dst, nx, ny, nz, ldx, ppc);
+  kern<<<dim3((unsigned)ntx, (unsigned)nty, (unsigned)nzc), (BX / 32) * (BY / R) * 32, smem, s>>>(tm, dst, nx, ny, ldx, z_lo, z_hi, ring_lo, ring_hi, ppc,
+                                                rem.base, rem.delta);
   ST_LAUNCHED();
   return ST_OK;
 }
@@ -380,23 +392,26 @@ st_status jacobi3d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<64, 16, 6, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<64, 16, 8, 1>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_copy_faces_kernel));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 6, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 4, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 5, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 5, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 4, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 6, 2, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 4, 2, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 5, 2, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 5, 2, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 4, 4, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 5, 2, true>));
   return ST_OK;
 }
 
-st_status jacobi3d_two_sweeps(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nz, int64_t ldx,
-                              cudaStream_t s) {
+st_status jacobi3d_two_sweeps(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
+                              int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi,
+                              cudaStream_t s, Remote rem) {
+  if (z_hi < z_lo) return ST_OK;
   static const int kV = env_int("ST_J3T2_VARIANT", 0);
   switch (kV) {
-    case 1: return launch_j3t2<128, 16, 4, 2>(src, dst, nx, ny, nz, ldx, s);
-    case 2: return launch_j3t2<128, 16, 5, 2>(src, dst, nx, ny, nz, ldx, s);
-    case 3: return launch_j3t2<128, 8, 6, 2>(src, dst, nx, ny, nz, ldx, s);
-    case 4: return launch_j3t2<128, 16, 4, 4>(src, dst, nx, ny, nz, ldx, s);
-    default: return launch_j3t2<128, 8, 5, 2>(src, dst, nx, ny, nz, ldx, s);
+    case 1: return launch_j3t2<128, 16, 4, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);
+    case 2: return launch_j3t2<128, 16, 5, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);
+    case 3: return launch_j3t2<128, 8, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);
+    case 4: return launch_j3t2<128, 16, 4, 4>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);
+    default: return launch_j3t2<128, 8, 5, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);
   }
 }
 

@@ -46,16 +46,23 @@ int choose_tblock(int32_t nranks, int64_t nx, int64_t n, int32_t h, int32_t tblo
   return t >= 2 ? t : 1;
 }
 
+// dims=3: two sweeps per pass (jacobi3d_t2_kernel) whenever the ghosts cover them
+int choose_tblock3d(int32_t nranks, int32_t h, int32_t tblock) {
+  if (tblock > 0) return tblock;
+  static const int kT2 = env_int("ST_J3_T2", 1);
+  return kT2 && (nranks == 1 || h >= 2) ? 2 : 1;
+}
+
 st_status build_jacobi_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_t n, int32_t h,
                                 int64_t iters, int32_t tblock, std::vector<st_op>& ops, int dims) {
   ST_RETURN_IF(nranks < 1 || rank < 0 || rank >= nranks, ST_EINVAL, "schedule: rank %d of %d", rank, nranks);
   ST_RETURN_IF(nx < 1 || n < 1 || h < 1 || iters < 0 || tblock < 0, ST_EINVAL, "schedule: bad extents/counts");
   ST_RETURN_IF(nranks > 1 && n < h, ST_EINVAL, "schedule: slab of %lld rows < halo %d", (long long)n, h);
-  ST_RETURN_IF(dims == 3 && tblock > 1, ST_ENOTSUP, "jacobi3d: tblock=%d not supported (0, 1)", tblock);
-  const int T = dims == 3 ? 1 : choose_tblock(nranks, nx, n, h, tblock);
-  ST_RETURN_IF(T > 1 && !jacobi2d_tb_supported(T), ST_ENOTSUP,
+  ST_RETURN_IF(dims == 3 && tblock > 2, ST_ENOTSUP, "jacobi3d: tblock=%d not supported (0, 1, 2)", tblock);
+  const int T = dims == 3 ? choose_tblock3d(nranks, h, tblock) : choose_tblock(nranks, nx, n, h, tblock);
+  ST_RETURN_IF(dims == 2 && T > 1 && !jacobi2d_tb_supported(T), ST_ENOTSUP,
                "jacobi2d: tblock=%d not supported (1, 2, 4, 6, 8)", T);
-  ST_RETURN_IF(nranks > 1 && T > h, ST_EINVAL, "jacobi2d: tblock=%d needs halo >= %d", T, T);
+  ST_RETURN_IF(nranks > 1 && T > h, ST_EINVAL, "jacobi%dd: tblock=%d needs halo >= %d", dims, T, T);
 
   // passes: T-sweep (temporally blocked) passes, a remainder, and the parity
   // fix-up of plan_passes so the result lands in b iff iters is odd
@@ -123,6 +130,18 @@ st_status build_jacobi_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_
 }
 
 }  // namespace st
+
+extern "C" st_status st_jacobi3d_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_t nz_local,
+                                          int32_t halo, int64_t iters, int32_t tblock, st_op* ops, int64_t cap,
+                                          int64_t* nops) {
+  st::clear_error();
+  ST_RETURN_IF(!nops || (cap > 0 && !ops), ST_EINVAL, "st_jacobi3d_schedule: null output");
+  std::vector<st_op> v;
+  ST_TRY(st::build_jacobi_schedule(rank, nranks, nx, nz_local, halo, iters, tblock, v, 3));
+  *nops = (int64_t)v.size();
+  for (int64_t i = 0; i < cap && i < (int64_t)v.size(); ++i) ops[i] = v[(size_t)i];
+  return ST_OK;
+}
 
 extern "C" st_status st_jacobi2d_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_t ny_local,
                                           int32_t halo, int64_t iters, int32_t tblock, st_op* ops, int64_t cap,

@@ -44,6 +44,35 @@ def jacobi2d(rank, world, dev, h, iters, tblock):
     return True
 
 
+def jacobi3d(rank, world, dev, h, iters, tblock):
+    # z slabs; h >= 2 runs two sweeps per pass (jacobi3d_t2_kernel) across ranks
+    nx, ny, nz = 70, 33, 29
+    g = si.jacobi3d_grid(nx, ny, nz)
+    start, n = st.st_block_split(nz, world, rank)
+    loc = np.zeros((n + 2 * h, ny + 2, g.shape[2]))
+    for l in range(n + 2 * h):
+        gz = start + 1 + (l - h)
+        if 0 <= gz <= nz + 1:
+            loc[l] = g[gz]
+    a = torch.from_numpy(loc).to(dev)
+    if rank > 0:
+        a[:h] = float("nan")
+    if rank < world - 1:
+        a[h + n:] = float("nan")
+    b = torch.full_like(a, float("nan"))
+    comm = st.Comm.ipc_from_process_group(dev.index)
+    comm.bind_ipc([a, b], n)
+    r = st.st_jacobi3d_run(a, b, iters, tblock=tblock, halo=h, comm=comm, nx=nx)
+    torch.cuda.synchronize()
+    blocks = [None] * world
+    dist.all_gather_object(blocks, (start, r.cpu().numpy()[h:h + n, :, :nx + 2]))
+    comm.close()
+    if rank == 0:
+        want = oracle.jacobi3d(g, iters, nx=nx)
+        return all(np.array_equal(blk, want[s0 + 1:s0 + 1 + blk.shape[0], :, :nx + 2]) for s0, blk in blocks)
+    return True
+
+
 def pw(rank, world, dev):
     nx, ny, nz = 140, 20, 41
     d = si.pw_inputs(nx, ny, nz)
@@ -131,6 +160,8 @@ def main():
     ok = {"j2_h1": lambda: jacobi2d(rank, world, dev, 1, 9, 1),
           "j2_h4_t4": lambda: jacobi2d(rank, world, dev, 4, 13, 4),
           "pw": lambda: pw(rank, world, dev),
+          "j3_h2_t2": lambda: jacobi3d(rank, world, dev, 2, 9, 0),
+          "j3_h3_t2": lambda: jacobi3d(rank, world, dev, 3, 8, 2),
           "pen_j3": lambda: pencils(rank, world, dev, "j3"),
           "pen_pw": lambda: pencils(rank, world, dev, "pw")}[case]()
     if rank == 0:

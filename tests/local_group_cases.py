@@ -62,7 +62,7 @@ def jacobi2d_case(P, nx, ny, h, iters, tblock, poison=True):
     return ok
 
 
-def jacobi3d_case(P, nx, ny, nz, h, iters):
+def jacobi3d_case(P, nx, ny, nz, h, iters, tblock=0):
     g = si.jacobi3d_grid(nx, ny, nz)
     comms = st.Comm.local_group(P)
     streams = [torch.cuda.Stream() for _ in range(P)]
@@ -83,7 +83,7 @@ def jacobi3d_case(P, nx, ny, nz, h, iters):
     for r in range(P):
         a, b, start, n = ranks[r]
         with torch.cuda.stream(streams[r]):
-            outs.append(st.st_jacobi3d_run(a, b, iters, halo=h, comm=comms[r], nx=nx))
+            outs.append(st.st_jacobi3d_run(a, b, iters, tblock=tblock, halo=h, comm=comms[r], nx=nx))
     torch.cuda.synchronize()
     want = oracle.jacobi3d(g, iters, nx=nx)
     ok = True
@@ -265,7 +265,11 @@ CASES = {
     "j2_p4_h6_t6": lambda: jacobi2d_case(4, 260, 520, 6, 25, 6),
     "j2_p3_h3_t1": lambda: jacobi2d_case(3, 90, 99, 3, 10, 1),
     "j3_h1": lambda: jacobi3d_case(2, 70, 40, 33, 1, 7),
-    "j3_p3_h2": lambda: jacobi3d_case(3, 40, 30, 31, 2, 6),
+    "j3_p3_h2": lambda: jacobi3d_case(3, 40, 30, 31, 2, 6),          # auto: two sweeps per pass
+    "j3_p3_h2_t1": lambda: jacobi3d_case(3, 40, 30, 31, 2, 6, 1),
+    "j3_p2_h2_t2": lambda: jacobi3d_case(2, 140, 37, 40, 2, 9, 2),   # odd iters: a 1-sweep pass
+    "j3_p4_h3_t2": lambda: jacobi3d_case(4, 70, 20, 23, 3, 11, 2),   # slabs of 5-6 planes < 2*halo
+    "j3_p2_h4_t2": lambda: jacobi3d_case(2, 33, 17, 300, 4, 12, 2),  # several T=2 chunks per slab
     "pw_p2": lambda: pw_case(2, 140, 20, 41),
     "pw_p4": lambda: pw_case(4, 70, 17, 40),
 }

@@ -1,4 +1,5 @@
-"""Test-side executor of libstencil's Jacobi schedule (st_jacobi2d_schedule).
+"""Test-side executor of libstencil's Jacobi schedules (st_jacobi2d_schedule,
+st_jacobi3d_schedule: the same logic with z planes for rows).
 
 Runs the exact op sequence the CUDA path runs, with a plain NumPy definition
 of each op, so the host logic of the decomposition (slab split, ghost depth,
@@ -32,11 +33,29 @@ def sweep_pass(src: np.ndarray, dst: np.ndarray, nx: int, y_lo: int, y_hi: int, 
     dst[y_lo:y_hi + 1, :nx + 2] = cur[y_lo:y_hi + 1, :nx + 2]
 
 
+def sweep_pass3d(src: np.ndarray, dst: np.ndarray, nx: int, z_lo: int, z_hi: int, b: int,
+                 ring_lo: int, ring_hi: int) -> None:
+    """3-D ST_OP_SWEEP: dst planes [z_lo, z_hi] := b 7-point sweeps after src (sum order z-, z+,
+    y-, y+, x-, x+, then / 6; R20/R21); planes <= ring_lo / >= ring_hi are Dirichlet."""
+    nplanes, ny = src.shape[0], src.shape[1] - 2
+    cur = src.copy()
+    for lvl in range(1, b + 1):
+        lo = max(z_lo - (b - lvl), ring_lo + 1, 1)
+        hi = min(z_hi + (b - lvl), ring_hi - 1, nplanes - 2)
+        nxt = cur.copy()
+        if hi >= lo:
+            c = lambda dz, dy, dx: cur[lo + dz:hi + 1 + dz, 1 + dy:ny + 1 + dy, 1 + dx:nx + 1 + dx]
+            nxt[lo:hi + 1, 1:ny + 1, 1:nx + 1] = (((((c(-1, 0, 0) + c(1, 0, 0)) + c(0, -1, 0)) + c(0, 1, 0))
+                                                    + c(0, 0, -1)) + c(0, 0, 1)) / 6.0
+        cur = nxt
+    dst[z_lo:z_hi + 1, :, :nx + 2] = cur[z_lo:z_hi + 1, :, :nx + 2]
+
+
 def slab_arrays(a_glob: np.ndarray, nranks: int, rank: int, h: int):
     """Rank slab of the global padded grid with h ghost rows per side (zeros where no row exists)."""
     ny = a_glob.shape[0] - 2
     start, n = st.st_block_split(ny, nranks, rank)
-    buf = np.zeros((n + 2 * h, a_glob.shape[1]))
+    buf = np.zeros((n + 2 * h,) + a_glob.shape[1:])
     for l in range(n + 2 * h):
         g = start + 1 + (l - h)
         if 0 <= g <= ny + 1:
@@ -45,38 +64,49 @@ def slab_arrays(a_glob: np.ndarray, nranks: int, rank: int, h: int):
 
 
 def run_simulated(a_glob: np.ndarray, nx: int, nranks: int, h: int, iters: int, tblock: int) -> np.ndarray:
-    """All ranks in one process; returns the gathered global result."""
+    """All ranks in one process; returns the gathered global result. A 3-D a_glob
+    (planes, ny+2, ldx) runs st_jacobi3d_schedule with 3-D sweeps."""
     ny = a_glob.shape[0] - 2
+    dims = a_glob.ndim
+    schedule = st.st_jacobi3d_schedule if dims == 3 else st.st_jacobi2d_schedule
+    sweep = sweep_pass3d if dims == 3 else sweep_pass
     ranks = []
     for r in range(nranks):
         a, start, n = slab_arrays(a_glob, nranks, r, h)
         b = a.copy()  # the library copies ghost/Dirichlet rows a -> b
-        ops = st.st_jacobi2d_schedule(r, nranks, nx, n, h, iters, tblock)
+        ops = schedule(r, nranks, nx, n, h, iters, tblock)
         ranks.append({"buf": [a, b], "start": start, "n": n, "ops": ops})
-    nops = {len(x["ops"]) for x in ranks}
-    assert len(nops) == 1, "every rank runs the same op sequence"
-    for i in range(nops.pop()):
-        kinds = {x["ops"][i]["kind"] for x in ranks}
-        assert len(kinds) == 1
-        kind = kinds.pop()
-        if kind == st.OP_SWEEP:
-            for x in ranks:
-                o = x["ops"][i]
-                sweep_pass(x["buf"][o["buf"]], x["buf"][1 - o["buf"]], nx, o["y_lo"], o["y_hi"], o["sweeps"],
-                           o["ring_lo"], o["ring_hi"])
-        elif kind == st.OP_EXCHANGE:
-            pitch = a_glob.shape[1]
-            flat = [x["buf"][x["ops"][i]["buf"]].reshape(-1) for x in ranks]
-            snap = [f.copy() for f in flat]
-            for r, x in enumerate(ranks):
-                w = x["ops"][i]["sweeps"]
-                sends, recvs = st.st_halo_plan(r, nranks, x["n"], pitch, w)
-                for peer, off, cnt in recvs:
-                    # what peer sends to r
-                    ps, _ = st.st_halo_plan(peer, nranks, ranks[peer]["n"], pitch, w)
-                    src = [s for s in ps if s[0] == r][0]
-                    assert src[2] == cnt
-                    flat[r][off:off + cnt] = snap[peer][src[1]:src[1] + cnt]
+    # ranks run independently between swaps (a slab thinner than 2*halo has no boundary/interior
+    # split, so op lists may differ); every rank has the same number of swaps, executed together
+    nex = {sum(o["kind"] == st.OP_EXCHANGE for o in x["ops"]) for x in ranks}
+    assert len(nex) == 1, "every rank takes part in every swap"
+    pos = [0] * nranks
+    pitch = int(np.prod(a_glob.shape[1:]))
+    for _ in range(nex.pop() + 1):
+        ex = []
+        for r, x in enumerate(ranks):
+            while pos[r] < len(x["ops"]) and x["ops"][pos[r]]["kind"] != st.OP_EXCHANGE:
+                o = x["ops"][pos[r]]
+                if o["kind"] == st.OP_SWEEP:
+                    sweep(x["buf"][o["buf"]], x["buf"][1 - o["buf"]], nx, o["y_lo"], o["y_hi"], o["sweeps"],
+                          o["ring_lo"], o["ring_hi"])
+                pos[r] += 1
+            ex.append(x["ops"][pos[r]] if pos[r] < len(x["ops"]) else None)
+            pos[r] += 1
+        if ex[0] is None:
+            break
+        assert len({o["sweeps"] for o in ex}) == 1
+        flat = [x["buf"][o["buf"]].reshape(-1) for x, o in zip(ranks, ex)]
+        snap = [f.copy() for f in flat]
+        for r, x in enumerate(ranks):
+            w = ex[r]["sweeps"]
+            sends, recvs = st.st_halo_plan(r, nranks, x["n"], pitch, w)
+            for peer, off, cnt in recvs:
+                # what peer sends to r
+                ps, _ = st.st_halo_plan(peer, nranks, ranks[peer]["n"], pitch, w)
+                src = [s for s in ps if s[0] == r][0]
+                assert src[2] == cnt
+                flat[r][off:off + cnt] = snap[peer][src[1]:src[1] + cnt]
     out = np.zeros_like(a_glob)
     for r, x in enumerate(ranks):
         fin = x["buf"][iters & 1]
@@ -97,11 +127,13 @@ def run_gloo_rank(a_glob: np.ndarray, nx: int, h: int, iters: int, tblock: int) 
     ny = a_glob.shape[0] - 2
     a, start, n = slab_arrays(a_glob, nranks, rank, h)
     buf = [a, a.copy()]
-    pitch = a_glob.shape[1]
-    for o in st.st_jacobi2d_schedule(rank, nranks, nx, n, h, iters, tblock):
+    pitch = int(np.prod(a_glob.shape[1:]))
+    schedule = st.st_jacobi3d_schedule if a_glob.ndim == 3 else st.st_jacobi2d_schedule
+    sweep = sweep_pass3d if a_glob.ndim == 3 else sweep_pass
+    for o in schedule(rank, nranks, nx, n, h, iters, tblock):
         if o["kind"] == st.OP_SWEEP:
-            sweep_pass(buf[o["buf"]], buf[1 - o["buf"]], nx, o["y_lo"], o["y_hi"], o["sweeps"], o["ring_lo"],
-                       o["ring_hi"])
+            sweep(buf[o["buf"]], buf[1 - o["buf"]], nx, o["y_lo"], o["y_hi"], o["sweeps"], o["ring_lo"],
+                  o["ring_hi"])
         elif o["kind"] == st.OP_EXCHANGE:
             flat = torch.from_numpy(buf[o["buf"]].reshape(-1))  # shares memory with the slab
             sends, recvs = st.st_halo_plan(rank, nranks, n, pitch, o["sweeps"])

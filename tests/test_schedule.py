@@ -1,4 +1,4 @@
-"""CPU tests of the host-side decomposition logic (st_jacobi2d_schedule,
+"""CPU tests of the host-side decomposition logic (st_jacobi2d/3d_schedule,
 st_halo_plan, st_block_split): the schedule the CUDA path runs, executed with
 NumPy ops for simulated ranks, is bitwise the oracle (SURVEY.md §8(c5) D1/D2,
 SPEC.md:465 ranks-sim == serial)."""
@@ -67,3 +67,38 @@ def test_schedule_rejects():
         st.st_jacobi2d_schedule(0, 2, 64, 64, 2, 5, 4)  # T deeper than the ghosts
     with pytest.raises(st.StencilError):
         st.st_jacobi2d_schedule(0, 1, 64, 64, 1, 5, 3)  # odd T
+
+
+@pytest.mark.parametrize("nranks,h,iters,tblock", [
+    (1, 1, 7, 0), (1, 1, 6, 2), (1, 1, 5, 1),
+    (2, 1, 5, 0), (3, 1, 4, 1),               # halo 1: one sweep per pass
+    (2, 2, 7, 0), (3, 2, 6, 2), (4, 3, 9, 2),  # T = 2 across ranks (auto with halo >= 2)
+    (2, 2, 1, 2), (3, 4, 11, 0), (2, 3, 8, 1),
+])
+def test_schedule3d_simulated_equals_oracle(nranks, h, iters, tblock):
+    nx, ny, nz = 9, 7, 23
+    a = si.jacobi3d_grid(nx, ny, nz)
+    got = run_simulated(a, nx, nranks, h, iters, tblock)
+    assert np.array_equal(got, oracle.jacobi3d(a, iters, nx=nx))
+
+
+def test_schedule3d_tblock_choice():
+    def sweeps(ops):  # sweeps per pass (a pass = the sweep ops before a SWAP)
+        out, last = [], None
+        for o in ops:
+            if o["kind"] == st.OP_SWEEP:
+                last = o["sweeps"]
+            elif o["kind"] == st.OP_SWAP:
+                out.append(last)
+        return out
+    assert set(sweeps(st.st_jacobi3d_schedule(0, 1, 512, 512, 1, 100, 0))) == {2}
+    assert set(sweeps(st.st_jacobi3d_schedule(1, 4, 512, 128, 1, 100, 0))) == {1}   # halo 1 -> one sweep
+    multi = st.st_jacobi3d_schedule(1, 4, 512, 128, 2, 100, 0)
+    assert set(sweeps(multi)) == {2} and sum(sweeps(multi)) == 100
+    for it in range(12):
+        sw = sweeps(st.st_jacobi3d_schedule(0, 2, 64, 64, 2, it, 2))
+        assert sum(sw) == it and len(sw) % 2 == it % 2
+    with pytest.raises(st.StencilError):
+        st.st_jacobi3d_schedule(0, 2, 64, 64, 1, 5, 2)  # T = 2 needs two ghost planes
+    with pytest.raises(st.StencilError):
+        st.st_jacobi3d_schedule(0, 1, 64, 64, 1, 5, 4)  # only 1 and 2 in 3-D
