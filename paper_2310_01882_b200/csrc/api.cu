@@ -405,6 +405,16 @@ st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
   ST_CHECK_CUDA(cudaMemcpy2DAsync(b + (halo + nz) * plane, pitch, a + (halo + nz) * plane, pitch, width,
                                   (size_t)halo * (size_t)(ny + 2), cudaMemcpyDeviceToDevice, s));
   ST_TRY(jacobi3d_copy_faces(a, b, nx, ny, ldx, halo, halo + nz - 1, s));
+  // Two-sweep passes across ranks also sweep the ghost planes once, which reads their side
+  // faces; the fused swap stores only the interior of a plane, so b's ghost planes get their
+  // (constant) side faces from a after one whole-plane swap into a.
+  bool t2_ranks = false;
+  for (const st_op& o : ops) t2_ranks |= nranks > 1 && o.kind == ST_OP_SWEEP && o.sweeps == 2;
+  if (t2_ranks) {
+    ST_TRY(halo_exchange_async(comm, &a, 1, nz, plane, halo, s, true));
+    ST_TRY(jacobi3d_copy_faces(a, b, nx, ny, ldx, 0, halo - 1, s));
+    ST_TRY(jacobi3d_copy_faces(a, b, nx, ny, ldx, halo + nz, nz + 2 * halo - 1, s));
+  }
   // two sweeps per pass (temporal blocking T = 2) where the ghosts allow it: the single domain
   // and slabs with halo >= 2 (schedule.cu choose_tblock3d); the schedule keeps the parity so
   // the result lands in b iff iters is odd

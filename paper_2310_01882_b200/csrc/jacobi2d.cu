@@ -414,13 +414,17 @@ struct Quad {
   double2 a, b;  // columns x, x+1 | x+2, x+3
 };
 
-template <int T, bool kRows, bool kCols>
-__device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][2], const int k, Quad s, int64_t r, const bool (&ring)[4],
+// State of level j: rows n, c of level j-1's output in slots k % NS, (k+1) % NS; the new
+// row s goes to slot (k+2) % NS. NS = 2 overwrites n's slot; NS = 3 writes the free third
+// slot, so s and n never need the same registers and a group of G = 3 steps returns every
+// value to its register with no copies at the loop edge.
+template <int T, int NS, bool kRows, bool kCols>
+__device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][NS], const int k, Quad s, int64_t r, const bool (&ring)[4],
                                            int64_t ring_lo, int64_t ring_hi) {
 #pragma unroll
   for (int j = 0; j < T; ++j) {
-    const Quad n = st[j][k & 1];
-    const Quad c = st[j][(k + 1) & 1];
+    const Quad n = st[j][k % NS];
+    const Quad c = st[j][(k + 1) % NS];
     const double w = __shfl_up_sync(0xffffffffu, c.b.y, 1);
     const double e = __shfl_down_sync(0xffffffffu, c.a.x, 1);
     Quad o;
@@ -438,7 +442,7 @@ __device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][2], const int k, Quad s
       const int64_t row = r - j - 1;
       if (row <= ring_lo || row >= ring_hi) o = c;
     }
-    st[j][k & 1] = s;
+    st[j][(k + 2) % NS] = s;
     s = o;
   }
   return s;
@@ -450,7 +454,8 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
                         int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk, int64_t nstrips, int64_t ring_lo,
                         int64_t ring_hi, int64_t nrows_buf, double* __restrict__ dst2, int64_t delta2) {
   static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
-  static_assert(G % 2 == 0, "row-slot renaming needs an even group");
+  constexpr int NS = G % 3 == 0 ? 3 : 2;  // row slots per level (tb4_levels)
+  static_assert(G % NS == 0, "row-slot renaming needs a group of whole slot cycles");
   constexpr int kCols = 128, kStride = kCols - 2 * T;
   const int lane = threadIdx.x & 31;
   const int64_t strip = (int64_t)blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
@@ -478,10 +483,11 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
   const int64_t r_load_last = min(min(ring_hi, nrows_buf - 1), yc1 + T);
   const int64_t r_end = yc1 + T;
 
-  Quad st[T][2];
+  Quad st[T][NS];
 #pragma unroll
   for (int j = 0; j < T; ++j) {
-    st[j][0].a = st[j][0].b = st[j][1].a = st[j][1].b = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) st[j][q].a = st[j][q].b = make_double2(0.0, 0.0);
   }
   Quad buf[G];
   const int64_t safe_off = r_first * ld;
@@ -521,7 +527,7 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
         buf[k].a = ldg2(spa + off);
         buf[k].b = ldg2(spb + off);
         loff += ld;
-        o[k] = tb4_levels<T, false, false>(st, k, s0, r0 + k, ring, ring_lo, ring_hi);
+        o[k] = tb4_levels<T, NS, false, false>(st, k, s0, r0 + k, ring, ring_lo, ring_hi);
       }
 #pragma unroll
       for (int k = 0; k < G; ++k) {
@@ -544,11 +550,11 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
       const bool rows_chk = (r - T <= ring_lo) || (r - 1 >= ring_hi);
       Quad o;
       if (rows_chk) {
-        o = col_ring ? tb4_levels<T, true, true>(st, k, s0, r, ring, ring_lo, ring_hi)
-                     : tb4_levels<T, true, false>(st, k, s0, r, ring, ring_lo, ring_hi);
+        o = col_ring ? tb4_levels<T, NS, true, true>(st, k, s0, r, ring, ring_lo, ring_hi)
+                     : tb4_levels<T, NS, true, false>(st, k, s0, r, ring, ring_lo, ring_hi);
       } else {
-        o = col_ring ? tb4_levels<T, false, true>(st, k, s0, r, ring, ring_lo, ring_hi)
-                     : tb4_levels<T, false, false>(st, k, s0, r, ring, ring_lo, ring_hi);
+        o = col_ring ? tb4_levels<T, NS, false, true>(st, k, s0, r, ring, ring_lo, ring_hi)
+                     : tb4_levels<T, NS, false, false>(st, k, s0, r, ring, ring_lo, ring_hi);
       }
       if (r - T >= yc0 && r - T <= yc1) {
         store_row(out, o);
@@ -589,10 +595,12 @@ st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int
   const int64_t nchunks = (rows + rpc - 1) / rpc;
   ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d tb: too many row chunks");
   dim3 grid((unsigned)blocks_x, (unsigned)nchunks);
-  // G = steps per group: 2 (measured best at T=8; 4 needs more than 255 registers)
+  // G = steps per group: 2 (measured best at T=8; 4 needs more than 255 registers);
+  // 3 = three row slots per level (no register copies at the loop edge; T <= 6 fits)
   static const int kG = env_int("ST_JACOBI_TB4_G", 2);
-  auto* kern = kOcc == 1 ? (kG == 4 ? jacobi2d_tb4_kernel<T, 1, 4> : jacobi2d_tb4_kernel<T, 1, 2>)
-                         : (kG == 4 ? jacobi2d_tb4_kernel<T, 2, 4> : jacobi2d_tb4_kernel<T, 2, 2>);
+  auto* kern = kG == 3 ? jacobi2d_tb4_kernel<T, 1, 3>
+               : kOcc == 1 ? (kG == 4 ? jacobi2d_tb4_kernel<T, 1, 4> : jacobi2d_tb4_kernel<T, 1, 2>)
+                           : (kG == 4 ? jacobi2d_tb4_kernel<T, 2, 4> : jacobi2d_tb4_kernel<T, 2, 2>);
   kern<<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo, ring_hi, nrows_buf,
                                        rem.base, rem.delta);
   ST_LAUNCHED();
@@ -651,18 +659,22 @@ st_status jacobi2d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 3>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, 3>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2, 4>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, 3>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2, 4>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, 3>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2, 4>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, 3>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, 4>));
   return ST_OK;

@@ -44,9 +44,8 @@ def jacobi2d(rank, world, dev, h, iters, tblock):
     return True
 
 
-def jacobi3d(rank, world, dev, h, iters, tblock):
+def jacobi3d(rank, world, dev, h, iters, tblock, nx=70, ny=33, nz=29):
     # z slabs; h >= 2 runs two sweeps per pass (jacobi3d_t2_kernel) across ranks
-    nx, ny, nz = 70, 33, 29
     g = si.jacobi3d_grid(nx, ny, nz)
     start, n = st.st_block_split(nz, world, rank)
     loc = np.zeros((n + 2 * h, ny + 2, g.shape[2]))
@@ -69,7 +68,15 @@ def jacobi3d(rank, world, dev, h, iters, tblock):
     comm.close()
     if rank == 0:
         want = oracle.jacobi3d(g, iters, nx=nx)
-        return all(np.array_equal(blk, want[s0 + 1:s0 + 1 + blk.shape[0], :, :nx + 2]) for s0, blk in blocks)
+        ok = True
+        for r, (s0, blk) in enumerate(blocks):
+            w = want[s0 + 1:s0 + 1 + blk.shape[0], :, :nx + 2]
+            if not np.array_equal(blk, w):
+                bad = np.argwhere(blk.view(np.uint64) != w.view(np.uint64))
+                print(f"rank {r}: {len(bad)} mismatches, planes {sorted(set(bad[:, 0].tolist()))[:10]}, "
+                      f"first {bad[:3].tolist()}", flush=True)
+                ok = False
+        return ok
     return True
 
 
@@ -161,6 +168,10 @@ def main():
           "j2_h4_t4": lambda: jacobi2d(rank, world, dev, 4, 13, 4),
           "pw": lambda: pw(rank, world, dev),
           "j3_h2_t2": lambda: jacobi3d(rank, world, dev, 2, 9, 0),
+          "j3_h2_t1": lambda: jacobi3d(rank, world, dev, 2, 9, 1),
+          "j3_h1": lambda: jacobi3d(rank, world, dev, 1, 5, 1),
+          "j3_dbg": lambda: jacobi3d(rank, world, dev, int(os.environ["J3_H"]), int(os.environ["J3_IT"]),
+                                     int(os.environ["J3_TB"]), *[int(v) for v in os.environ["J3_DIMS"].split(",")]),
           "j3_h3_t2": lambda: jacobi3d(rank, world, dev, 3, 8, 2),
           "pen_j3": lambda: pencils(rank, world, dev, "j3"),
           "pen_pw": lambda: pencils(rank, world, dev, "pw")}[case]()

@@ -74,6 +74,10 @@ def jacobi3d_case(P, nx, ny, nz, h, iters, tblock=0):
             gz = start + 1 + (l - h)
             if 0 <= gz <= nz + 1:
                 loc[l] = g[gz]
+        if r > 0:
+            loc[:h] = np.nan  # ghost planes must come from the swap (incl. their side faces)
+        if r < P - 1:
+            loc[h + n:] = np.nan
         a = torch.from_numpy(loc).cuda()
         b = torch.full_like(a, float("nan"))
         comms[r].bind([a, b], n)
@@ -270,6 +274,7 @@ CASES = {
     "j3_p2_h2_t2": lambda: jacobi3d_case(2, 140, 37, 40, 2, 9, 2),   # odd iters: a 1-sweep pass
     "j3_p4_h3_t2": lambda: jacobi3d_case(4, 70, 20, 23, 3, 11, 2),   # slabs of 5-6 planes < 2*halo
     "j3_p2_h4_t2": lambda: jacobi3d_case(2, 33, 17, 300, 4, 12, 2),  # several T=2 chunks per slab
+    "j3_p2_h2_t2_b": lambda: jacobi3d_case(2, 70, 33, 29, 2, 9, 0),
     "pw_p2": lambda: pw_case(2, 140, 20, 41),
     "pw_p4": lambda: pw_case(4, 70, 17, 40),
 }
