@@ -82,12 +82,13 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 // Why it is correctly rounded: x/6 = (x/2)/3 and a 53-bit significand divided
 // by 3 is never a rounding midpoint and stays >= ulp/6 away from every
 // midpoint, while q0 + r*RN(1/6) differs from x/6 by |r| * |RN(1/6) - 1/6| <=
-// 2^-52 ulp. Outside 2^-1000 < |x| < 2^1000 (subnormal results, overflow of
-// the residual) and for non-finite x the generic division is used.
+// 2^-52 ulp. Outside 2^-999 <= |x| < 2^1000 (subnormal results, overflow of
+// the residual) and for zero and non-finite x the generic division is used;
+// the range test reads the biased exponent (integer ops, not two fp64 compares).
 // tests/test_gpu_jacobi3d.py checks it bitwise against __ddiv_rn on random x.
 __device__ __forceinline__ double ddiv6(double x) {
-  const double ax = fabs(x);
-  if (!(ax > 0x1p-1000 && ax < 0x1p+1000)) return __ddiv_rn(x, 6.0);
+  const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;  // 2^-999: 24, 2^1000: 2023
+  if (e - 24u > 1998u) return __ddiv_rn(x, 6.0);
   constexpr double kInv6 = 0.16666666666666666;  // RN(1/6) = 0x3FC5555555555555
   const double q0 = __dmul_rn(x, kInv6);
   const double r = __fma_rn(-6.0, q0, x);

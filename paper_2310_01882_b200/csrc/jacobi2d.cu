@@ -456,6 +456,11 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
   static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
   constexpr int NS = G % 3 == 0 ? 3 : 2;  // row slots per level (tb4_levels)
   static_assert(G % NS == 0, "row-slot renaming needs a group of whole slot cycles");
+#ifndef ST_TB4_PREFETCH3
+#define ST_TB4_PREFETCH3 3
+#endif
+  constexpr int P = G == 3 ? ST_TB4_PREFETCH3 : G;  // rows loaded ahead (register buffer depth)
+  static_assert(G % P == 0, "prefetch slots renamed within a group");
   constexpr int kCols = 128, kStride = kCols - 2 * T;
   const int lane = threadIdx.x & 31;
   const int64_t strip = (int64_t)blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
@@ -489,15 +494,15 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
 #pragma unroll
     for (int q = 0; q < NS; ++q) st[j][q].a = st[j][q].b = make_double2(0.0, 0.0);
   }
-  Quad buf[G];
+  Quad buf[P];
   const int64_t safe_off = r_first * ld;
 #pragma unroll
-  for (int k = 0; k < G; ++k) {
+  for (int k = 0; k < P; ++k) {
     const int64_t off = (r_first + k <= r_load_last) ? (r_first + k) * ld : safe_off;
     buf[k].a = ldg2(spa + off);
     buf[k].b = ldg2(spb + off);
   }
-  int64_t loff = (r_first + G) * ld;
+  int64_t loff = (r_first + P) * ld;
   double* out = dst + x + (r_first - T) * ld;
   double* out2 = dst2 ? dst2 + x + (r_first - T + delta2) * ld : nullptr;
 
@@ -522,10 +527,10 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
       Quad o[G];
 #pragma unroll
       for (int k = 0; k < G; ++k) {
-        const Quad s0 = buf[k];
-        const int64_t off = (r0 + k + G <= r_load_last) ? loff : safe_off;
-        buf[k].a = ldg2(spa + off);
-        buf[k].b = ldg2(spb + off);
+        const Quad s0 = buf[k % P];
+        const int64_t off = (r0 + k + P <= r_load_last) ? loff : safe_off;
+        buf[k % P].a = ldg2(spa + off);
+        buf[k % P].b = ldg2(spb + off);
         loff += ld;
         o[k] = tb4_levels<T, NS, false, false>(st, k, s0, r0 + k, ring, ring_lo, ring_hi);
       }
@@ -542,10 +547,10 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
     for (int k = 0; k < G; ++k) {
       const int64_t r = r0 + k;
       if (r > r_end) break;
-      const Quad s0 = buf[k];
-      const int64_t off = (r + G <= r_load_last) ? loff : safe_off;
-      buf[k].a = ldg2(spa + off);
-      buf[k].b = ldg2(spb + off);
+      const Quad s0 = buf[k % P];
+      const int64_t off = (r + P <= r_load_last) ? loff : safe_off;
+      buf[k % P].a = ldg2(spa + off);
+      buf[k % P].b = ldg2(spb + off);
       loff += ld;
       const bool rows_chk = (r - T <= ring_lo) || (r - 1 >= ring_hi);
       Quad o;

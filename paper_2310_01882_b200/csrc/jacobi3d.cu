@@ -190,6 +190,11 @@ st_status launch_j3(const double* src, double* dst, int64_t nx, int64_t ny, int6
 // sweep of plane L-1 from that ring. Per point and sweep the arithmetic is the
 // single-sweep kernel's (sum order z-, z+, y-, y+, x-, x+, then / 6), so two
 // passes of this kernel are bitwise two single sweeps.
+#ifndef ST_J3T2_UNROLL
+#define ST_J3T2_UNROLL 3
+#endif
+constexpr int kJ3T2Unroll = ST_J3T2_UNROLL;  // plane-loop unroll (3: the z queues rename instead of copying)
+
 template <int BX, int BY>
 struct J3T2Tile {
   static constexpr int SX = BX + 6, SY = BY + 4;            // input tile: x0-3 .. x0+BX+2, y0-2 .. y0+BY+1
@@ -281,10 +286,13 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
   }
   double him = ring[hc], hic = ring[T::kPlaneStride + hc];
 
-  int slot_m = 0;  // ring slot of input plane L-1 (index j)
+  // ring slots of input planes j, j+1, j+2 and the fill parity of plane j+2's slot
+  // (counters, not j % S and j / S: S = 5 is no power of two)
+  int slot_m = 0, s1 = 1, s2 = 2;
+  uint32_t par2 = 0;
+#pragma unroll kJ3T2Unroll
   for (int j = 0; j < np - 2; ++j) {  // first-sweep planes za-1 .. zb+1
-    const int s1 = (slot_m + 1) % S, s2 = (slot_m + 2) % S;
-    mbar_wait_parity(&full[s2], ((j + 2) / S) & 1);
+    mbar_wait_parity(&full[s2], par2);
     const int64_t L = za - 1 + j;
     const double* Ic = ring + s1 * T::kPlaneStride;
     const double* Ip = ring + s2 * T::kPlaneStride;
@@ -349,6 +357,9 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
       ac[i] = ap[i];
     }
     slot_m = s1;
+    s1 = s2;
+    s2 = s2 + 1 == S ? 0 : s2 + 1;
+    par2 ^= s2 == 0 ? 1u : 0u;
   }
 }
 

@@ -97,15 +97,62 @@ def pw(P, n=512, apps=20):
     return n ** 3 / (ms / 1e3) / 1e9, ms
 
 
+_G3 = {}
+
+
+def jacobi3d(P, n=512, sweeps=100, h=2):
+    # z slabs; h = 2 ghost planes run two sweeps per pass across ranks (T = 2), h = 1 one
+    if n not in _G3:
+        _G3[n] = torch.from_numpy(si.jacobi3d_grid(n, n, n)).cuda()  # generated once, sliced per rank
+    g = _G3[n]
+    comms = st.Comm.local_group(P) if P > 1 else [None]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    bufs = []
+    for r in range(P):
+        z0, cnt = st.st_block_split(n, P, r)
+        hh = h if P > 1 else 1
+        a = torch.zeros((cnt + 2 * hh, n + 2, n + 2), dtype=torch.float64, device="cuda")
+        lo = max(0, z0 + 1 - hh)
+        hi = min(n + 1, z0 + cnt + hh)
+        a[lo - (z0 + 1 - hh): hi - (z0 + 1 - hh) + 1] = g[lo:hi + 1]
+        b = torch.empty_like(a)
+        if comms[r] is not None:
+            comms[r].bind([a, b], cnt)
+        bufs.append((a, b, hh))
+    torch.cuda.synchronize()
+
+    def run():
+        for r in range(P):
+            a, b, hh = bufs[r]
+            with torch.cuda.stream(streams[r]):
+                st.st_jacobi3d_run(a, b, sweeps, halo=hh, comm=comms[r])
+
+    ms = timed(run, streams, 2)
+    for c in comms:
+        if c is not None:
+            c.close()
+    return n ** 3 * sweeps / (ms / 1e3) / 1e9, ms
+
+
 if __name__ == "__main__":
+    only3d = sys.argv[1:] == ["3d"]  # just the 3-D Jacobi legs
     out = {"what": "LOCAL rank group on one B200: throughput at fixed total work vs P=1", "jacobi2d_16384^2_200sw": {},
-           "pw_512^3": {}}
+           "pw_512^3": {}, "jacobi3d_512^3_100sw_h2": {}, "jacobi3d_512^3_100sw_h1": {}}
     for P in (1, 2, 4):
+        for h in (2, 1):
+            v, ms = jacobi3d(P, h=h)
+            out[f"jacobi3d_512^3_100sw_h{h}"][P] = {"gpts": round(v, 1), "ms": round(ms, 2)}
+            print(f"jacobi3d P={P} h={h}: {v:.1f} Gpts/s", file=sys.stderr, flush=True)
+        if only3d:
+            continue
         v, ms = jacobi(P)
         out["jacobi2d_16384^2_200sw"][P] = {"gpts": round(v, 1), "ms": round(ms, 2)}
         v, ms = pw(P)
         out["pw_512^3"][P] = {"gpts": round(v, 2), "ms_per_app": round(ms, 4)}
-    for k in ("jacobi2d_16384^2_200sw", "pw_512^3"):
+    for k in ("jacobi2d_16384^2_200sw", "pw_512^3", "jacobi3d_512^3_100sw_h2", "jacobi3d_512^3_100sw_h1"):
+        if not out[k]:
+            del out[k]
+            continue
         base = out[k][1]["gpts"]
         for P in out[k]:
             out[k][P]["vs_P1"] = round(out[k][P]["gpts"] / base, 3)
