@@ -31,6 +31,11 @@ namespace {
 
 constexpr int kMaxPlanesPerChunk = 256;
 
+#ifndef ST_PW_UNROLL
+#define ST_PW_UNROLL 1
+#endif
+constexpr int kPwUnroll = ST_PW_UNROLL;  // plane-loop unroll of pw_advect3d_kernel
+
 template <int BX, int BY>
 struct PwTile {
   static constexpr int SX = BX + 2;  // smem row: 1-column apron each side
@@ -174,6 +179,7 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
     uc[i] = ring[T::kSlotStride + o]; vc[i] = ring[T::kSlotStride + PS + o]; wc[i] = ring[T::kSlotStride + 2 * PS + o];
   }
 
+#pragma unroll kPwUnroll
   for (int j = 0; j + 2 < np; ++j) {  // output plane za+j from input planes j, j+1, j+2
     mbar_wait_parity(&full[sp], par_p);
     const double* U0 = ring + sc * T::kSlotStride + oc;
