@@ -96,11 +96,20 @@ def test_fast_div6_is_correctly_rounded(cuda_lib):
     g = torch.Generator(device="cuda").manual_seed(1234)
     n = 1 << 26
     bits = torch.randint(0, 2 ** 62, (n,), device="cuda", generator=g, dtype=torch.int64)
+    top = torch.randint(0, 2, (n,), device="cuda", generator=g, dtype=torch.int64) << 62  # exponents >= 1024 too
     sign = torch.randint(0, 2, (n,), device="cuda", generator=g, dtype=torch.int64) << 63
-    x = (bits | sign).view(torch.float64)
+    x = (bits | top | sign).view(torch.float64)
     assert cuda_lib.st_selftest_div6(x) == 0
     sums = torch.rand(n, device="cuda", generator=g, dtype=torch.float64) * 6 + 3  # six values in [0.5, 1.5)
     assert cuda_lib.st_selftest_div6(sums) == 0
     special = torch.tensor([0.0, -0.0, float("inf"), float("-inf"), float("nan"), 5e-324, 2.2250738585072014e-308,
                             1.7976931348623157e308, 6.0, -6.0, 3.0, 1.0], dtype=torch.float64, device="cuda")
     assert cuda_lib.st_selftest_div6(special) == 0
+    # both ends of ddiv6's fast range (biased exponents 24 .. 2022) and their neighbours
+    import numpy as np
+    edge = []
+    for e in (22, 23, 24, 25, 2021, 2022, 2023, 2024):
+        for m in (0, 1, 2 ** 51, 2 ** 52 - 1):
+            edge += [(e << 52) | m, (1 << 63) | (e << 52) | m]
+    ev = torch.from_numpy(np.array(edge, dtype=np.uint64).view(np.float64)).cuda()
+    assert cuda_lib.st_selftest_div6(ev) == 0
