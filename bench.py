@@ -474,7 +474,12 @@ def main():
         z0, nz3 = st.st_block_split(n3, world, rank)
         h3 = 1 if world == 1 else 2  # two ghost planes: slabs also run two sweeps per pass
         ldx3 = pitch(n3 + 2, args.align)
-        g3 = si.jacobi3d_grid(n3, n3, n3, ldx=ldx3, plane0=z0, planes=nz3 + 2)
+        # slab buffer: nz3 + 2*h3 planes, buffer plane l = global padded plane z0 + 1 + l - h3
+        # (planes beyond the grid stay zero; they are never read)
+        g3 = np.zeros((nz3 + 2 * h3, n3 + 2, ldx3))
+        zlo, zhi = max(0, z0 + 1 - h3), min(n3 + 1, z0 + nz3 + h3)
+        g3[zlo - (z0 + 1 - h3): zhi - (z0 + 1 - h3) + 1] = si.jacobi3d_grid(n3, n3, n3, ldx=ldx3, plane0=zlo,
+                                                                        planes=zhi - zlo + 1)
         A3 = torch.from_numpy(g3).to(dev)
         B3 = torch.empty_like(A3)
         bind([A3, B3], nz3)
