@@ -27,10 +27,10 @@
 #define ST_STENCIL_TU 4
 #endif
 #ifndef ST_STENCIL_SX
-#define ST_STENCIL_SX 32
+#define ST_STENCIL_SX 64
 #endif
 #ifndef ST_STENCIL_SY
-#define ST_STENCIL_SY 4
+#define ST_STENCIL_SY 2
 #endif
 
 namespace st {
