@@ -414,6 +414,24 @@ struct Quad {
   double2 a, b;  // columns x, x+1 | x+2, x+3
 };
 
+// G = 3 variant: input rows staged in a per-warp shared-memory ring of kTbRing
+// rows by cp.async (each lane copies and later reads only its own 32 bytes, so
+// no barrier is needed), read back one step ahead so the LDS latency is off the
+// chain; frees the register prefetch for the three-slot level state.
+constexpr int kTbRing = 8;
+__device__ __forceinline__ void tb_cp16(uint32_t smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void tb_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tb_wait_ring() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(kTbRing - 1) : "memory");
+}
+__device__ __forceinline__ double2 tb_lds2(uint32_t smem) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem) : "memory");
+  return v;
+}
+
 // State of level j: rows n, c of level j-1's output in slots k % NS, (k+1) % NS; the new
 // row s goes to slot (k+2) % NS. NS = 2 overwrites n's slot; NS = 3 writes the free third
 // slot, so s and n never need the same registers and a group of G = 3 steps returns every
@@ -494,14 +512,51 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
 #pragma unroll
     for (int q = 0; q < NS; ++q) st[j][q].a = st[j][q].b = make_double2(0.0, 0.0);
   }
+  constexpr bool kRing = G == 3;
   Quad buf[P];
   const int64_t safe_off = r_first * ld;
+  // shared-memory row ring (kRing): this lane's 32 bytes of slot q at sring + q * 1024
+  extern __shared__ __align__(16) double tb_ring_smem[];
+  const uint32_t sring = (uint32_t)__cvta_generic_to_shared(tb_ring_smem) +
+                         (uint32_t)((threadIdx.x >> 5) * kTbRing * 1024 + lane * 32);
+  int rs = 0;  // ring slot of the current row
+  Quad snx;    // the current row, read from the ring one step ahead
+  int64_t roff = (r_first + kTbRing) * ld;
+  if constexpr (kRing) {
 #pragma unroll
-  for (int k = 0; k < P; ++k) {
-    const int64_t off = (r_first + k <= r_load_last) ? (r_first + k) * ld : safe_off;
-    buf[k].a = ldg2(spa + off);
-    buf[k].b = ldg2(spb + off);
+    for (int q = 0; q < kTbRing; ++q) {
+      const int64_t off = (r_first + q <= r_load_last) ? (r_first + q) * ld : safe_off;
+      tb_cp16(sring + q * 1024, spa + off);
+      tb_cp16(sring + q * 1024 + 16, spb + off);
+      tb_commit();
+    }
+    tb_wait_ring();
+    snx.a = tb_lds2(sring);
+    snx.b = tb_lds2(sring + 16);
+  } else {
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const int64_t off = (r_first + k <= r_load_last) ? (r_first + k) * ld : safe_off;
+      buf[k].a = ldg2(spa + off);
+      buf[k].b = ldg2(spb + off);
+    }
   }
+  // kRing: the current row; the slot it came from refills with row r + kTbRing, and
+  // row r + 1 is read into registers for the next step
+  auto ring_row = [&](int64_t r) -> Quad {
+    const Quad cur = snx;
+    const int64_t off = (r + kTbRing <= r_load_last) ? roff : safe_off;
+    roff += ld;
+    const uint32_t w = sring + rs * 1024;
+    tb_cp16(w, spa + off);
+    tb_cp16(w + 16, spb + off);
+    tb_commit();
+    rs = rs + 1 == kTbRing ? 0 : rs + 1;
+    tb_wait_ring();
+    snx.a = tb_lds2(sring + rs * 1024);
+    snx.b = tb_lds2(sring + rs * 1024 + 16);
+    return cur;
+  };
   int64_t loff = (r_first + P) * ld;
   double* out = dst + x + (r_first - T) * ld;
   double* out2 = dst2 ? dst2 + x + (r_first - T + delta2) * ld : nullptr;
@@ -527,11 +582,16 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
       Quad o[G];
 #pragma unroll
       for (int k = 0; k < G; ++k) {
-        const Quad s0 = buf[k % P];
-        const int64_t off = (r0 + k + P <= r_load_last) ? loff : safe_off;
-        buf[k % P].a = ldg2(spa + off);
-        buf[k % P].b = ldg2(spb + off);
-        loff += ld;
+        Quad s0;
+        if constexpr (kRing) {
+          s0 = ring_row(r0 + k);
+        } else {
+          s0 = buf[k % P];
+          const int64_t off = (r0 + k + P <= r_load_last) ? loff : safe_off;
+          buf[k % P].a = ldg2(spa + off);
+          buf[k % P].b = ldg2(spb + off);
+          loff += ld;
+        }
         o[k] = tb4_levels<T, NS, false, false>(st, k, s0, r0 + k, ring, ring_lo, ring_hi);
       }
 #pragma unroll
@@ -547,11 +607,16 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
     for (int k = 0; k < G; ++k) {
       const int64_t r = r0 + k;
       if (r > r_end) break;
-      const Quad s0 = buf[k % P];
-      const int64_t off = (r + P <= r_load_last) ? loff : safe_off;
-      buf[k % P].a = ldg2(spa + off);
-      buf[k % P].b = ldg2(spb + off);
-      loff += ld;
+      Quad s0;
+      if constexpr (kRing) {
+        s0 = ring_row(r);
+      } else {
+        s0 = buf[k % P];
+        const int64_t off = (r + P <= r_load_last) ? loff : safe_off;
+        buf[k % P].a = ldg2(spa + off);
+        buf[k % P].b = ldg2(spb + off);
+        loff += ld;
+      }
       const bool rows_chk = (r - T <= ring_lo) || (r - 1 >= ring_hi);
       Quad o;
       if (rows_chk) {
@@ -600,14 +665,20 @@ st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int
   const int64_t nchunks = (rows + rpc - 1) / rpc;
   ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d tb: too many row chunks");
   dim3 grid((unsigned)blocks_x, (unsigned)nchunks);
-  // G = steps per group: 2 (measured best at T=8; 4 needs more than 255 registers);
-  // 3 = three row slots per level (no register copies at the loop edge; T <= 6 fits)
+  // G = steps per group: 2 (default) = two row slots + register prefetch; 3 = three row
+  // slots per level (no register copies at the loop edge) with the input rows staged in
+  // a shared-memory cp.async ring: 7 % more work per clock, but it runs into the power
+  // cap (sw_power_cap, 1833 MHz) and sustains the same 1619 Gpts/s as G=2 at 1965 MHz
+  // (DESIGN.md §6.2); 4 spills at T=8
   static const int kG = env_int("ST_JACOBI_TB4_G", 2);
   auto* kern = kG == 3 ? jacobi2d_tb4_kernel<T, 1, 3>
                : kOcc == 1 ? (kG == 4 ? jacobi2d_tb4_kernel<T, 1, 4> : jacobi2d_tb4_kernel<T, 1, 2>)
                            : (kG == 4 ? jacobi2d_tb4_kernel<T, 2, 4> : jacobi2d_tb4_kernel<T, 2, 2>);
-  kern<<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo, ring_hi, nrows_buf,
-                                       rem.base, rem.delta);
+  const size_t smem = kG == 3 ? (size_t)kStreamWarps * kTbRing * 1024 : 0;
+  if (smem > 0)
+    ST_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, kStreamThreads, smem, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo, ring_hi, nrows_buf,
+                                          rem.base, rem.delta);
   ST_LAUNCHED();
   return ST_OK;
 }
