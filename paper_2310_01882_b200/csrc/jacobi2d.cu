@@ -474,10 +474,7 @@ __global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
   static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
   constexpr int NS = G % 3 == 0 ? 3 : 2;  // row slots per level (tb4_levels)
   static_assert(G % NS == 0, "row-slot renaming needs a group of whole slot cycles");
-#ifndef ST_TB4_PREFETCH3
-#define ST_TB4_PREFETCH3 3
-#endif
-  constexpr int P = G == 3 ? ST_TB4_PREFETCH3 : G;  // rows loaded ahead (register buffer depth)
+  constexpr int P = G == 3 ? 1 : G;  // rows loaded ahead in registers (G = 3: the shared-memory ring instead)
   static_assert(G % P == 0, "prefetch slots renamed within a group");
   constexpr int kCols = 128, kStride = kCols - 2 * T;
   const int lane = threadIdx.x & 31;
