@@ -257,16 +257,11 @@ bool jacobi2d_resident_fits(int64_t nx, int64_t ny) {
 
 st_status jacobi2d_resident(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t iters,
                             cudaStream_t s) {
-  static const int kRegRes = env_int("ST_JACOBI_REGRES", kRegResRows);  // rows per warp (0: shared-memory kernel)
-  if (kRegRes && nx <= 64) {
-    const int64_t rr = kRegRes == 8 ? 8 : kRegRes == 2 ? 2 : kRegRes == 3 ? 3 : 4;
-    const int64_t warps = (ny + 1 + rr - 1) / rr;  // rows 1 .. ny+1 (incl. the ring row)
+  // register-resident kernel for grids up to 64 columns (C1); shared-memory kernel otherwise
+  if (nx <= 64) {
+    const int64_t warps = (ny + 1 + kRegResRows - 1) / kRegResRows;  // rows 1 .. ny+1 (incl. the ring row)
     if (warps <= kRegResMaxWarps) {
-      auto* k = rr == 8   ? jacobi2d_regres_kernel<8>
-                : rr == 2 ? jacobi2d_regres_kernel<2>
-                : rr == 3 ? jacobi2d_regres_kernel<3>
-                          : jacobi2d_regres_kernel<4>;
-      k<<<1, (unsigned)(32 * warps), 0, s>>>(a, b, (int)nx, (int)ny, ld, iters);
+      jacobi2d_regres_kernel<kRegResRows><<<1, (unsigned)(32 * warps), 0, s>>>(a, b, (int)nx, (int)ny, ld, iters);
       ST_LAUNCHED();
       return ST_OK;
     }
@@ -285,46 +280,117 @@ namespace {
 
 // Temporal blocking in registers (T sweeps per pass over HBM).
 //
-// A warp owns a strip of 64 columns (lane = column pair) that overlaps its
-// neighbours by 2T columns: after T levels only the centre 64-2T columns are
-// exact, so strips advance by 64-2T. Rows stream through a T-level software
-// pipeline held entirely in registers: level j keeps its two most recent rows
-// (N, C); when level j-1 delivers a new row S, level j produces row C. W/E
-// neighbours at every level come from warp shuffles. Dirichlet rows/columns are
-// passed through unchanged at every level, so every level is exactly one Jacobi
-// sweep and the result is bitwise T single sweeps.
+// A warp owns a strip of 128 columns (lane = two 16-byte column pairs) that
+// overlaps its neighbours by 2T columns: after T levels only the centre
+// 128-2T columns are exact, so strips advance by 128-2T. Rows stream through a
+// T-level software pipeline held entirely in registers: level j keeps its two
+// most recent rows (N, C); when level j-1 delivers a new row S, level j
+// produces row C. W/E neighbours at every level come from warp shuffles.
+// Dirichlet rows/columns are passed through unchanged at every level, so every
+// level is exactly one Jacobi sweep and the result is bitwise T single sweeps.
 //
-// Instruction diet (the kernel is issue-bound once T >= 4): each level keeps two
-// row slots; N is slot k%2 and C slot (k+1)%2, and the new row S overwrites the
-// N slot once N has been consumed, so with steps unrolled in groups of
-// kTbGroup (even) the rotation is register renaming, not moves. The refill
-// load of every step is unconditional (its address is clamped to a valid row),
-// so no select ever waits on an in-flight load; the per-level Dirichlet-row and
-// Dirichlet-column handling is compiled into separate level bodies chosen per
-// step by a block-/warp-uniform branch, so steady-state steps carry no checks.
-// Load and store addresses advance by one pitch per step.
-constexpr int kTbGroup = 4;  // steps per unrolled group (even: the slot rotation period is 2)
+// Work decomposition: one warp = one (strip, row chunk) item, items numbered
+// chunk-major over a 1-D grid, so the chunk height is chosen for whole waves of
+// resident warps (not of 8-strip CTAs): for C2 147 strips x 8 chunks of 2048
+// rows = 1176 warps <= 148 SMs x 8, one wave, 16 warm-up rows per 2048.
+//
+// Power-of-two folding (the level multiplies): level j < T-1 keeps 4^(j+1)
+// times its state, i.e. it stores the raw sum ((N+S)+W)+E without the * 0.25,
+// and the last level multiplies by 2^-2T. Scaling by a power of two commutes
+// with round-to-nearest addition (no overflow; subnormal sums are exact), so
+// this is bitwise the Listing-1 arithmetic whenever every intermediate
+// quotient sum/4 is exact — guaranteed if each input of the pass is zero or
+// has a biased exponent in [1+2T, 2045-2T]. Each input row is
+// checked with integer ops as it enters the pipeline; a warp that meets an
+// unsafe value restarts its item with the exact multiplies (stores are
+// idempotent, and every row stored before the check fired used checked rows).
+// One fp64 multiply per T updates instead of one per update.
+//
+// Instruction diet: each level keeps two row slots; N is slot k%2 and C slot
+// (k+1)%2, and the new row S overwrites the N slot once N has been consumed,
+// so with steps unrolled in groups of kTbGroup = 2 the rotation is register
+// renaming, not moves. The refill load of every step is unconditional (its
+// address is clamped to a valid row), so no select ever waits on an in-flight
+// load; the per-level Dirichlet-row and Dirichlet-column handling is compiled
+// into separate level bodies chosen per group by a warp-uniform branch.
+constexpr int kTbGroup = 2;   // steps per unrolled group (= the row-slot period)
+constexpr int kTbCols = 128;  // columns per warp strip (32 lanes x 4)
 
-template <int T, bool kRows, bool kCols>
-__device__ __forceinline__ double2 tb_levels(double2 (&st)[T][2], const int k, double2 s, int64_t r,
-                                             bool ring0, bool ring1, int64_t ring_lo, int64_t ring_hi) {
+struct Quad {
+  double2 a, b;  // columns x, x+1 | x+2, x+3
+};
+
+__host__ __device__ constexpr double pow2i(int k) {
+  double r = 1.0;
+  for (int i = 0; i < (k < 0 ? -k : k); ++i) r = k < 0 ? r * 0.5 : r * 2.0;
+  return r;
+}
+
+// 64-bit warp shuffles as two explicit 32-bit shuffles (the generic double
+// overload let ptxas swap the halves through three XORs per shuffle).
+__device__ __forceinline__ double shfl_up1(double v) {
+  const int lo = __shfl_up_sync(0xffffffffu, __double2loint(v), 1);
+  const int hi = __shfl_up_sync(0xffffffffu, __double2hiint(v), 1);
+  return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ double shfl_down1(double v) {
+  const int lo = __shfl_down_sync(0xffffffffu, __double2loint(v), 1);
+  const int hi = __shfl_down_sync(0xffffffffu, __double2hiint(v), 1);
+  return __hiloint2double(hi, lo);
+}
+// Predicated stores (no branch, so the warp provably stays converged for the
+// shuffles that follow; a branch here cost a divergence check per step).
+__device__ __forceinline__ void stg2_if(bool pred, double* p, double2 v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q st.global.v2.f64 [%0], {%1, %2};\n}" ::"l"(p),
+               "d"(v.x), "d"(v.y), "r"((unsigned)pred)
+               : "memory");
+}
+__device__ __forceinline__ void stg1_if(bool pred, double* p, double v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}" ::"l"(p), "d"(v),
+               "r"((unsigned)pred)
+               : "memory");
+}
+
+template <int T, bool kScaled, bool kRows, bool kCols>
+__device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][2], const int k, Quad s, int64_t r, const bool (&ring)[4],
+                                           int64_t ring_lo, int64_t ring_hi) {
 #pragma unroll
   for (int j = 0; j < T; ++j) {
-    // level j: N = slot k%2, C = slot (k+1)%2; S (from level j-1) replaces N afterwards
-    const double2 n = st[j][k & 1];
-    const double2 c = st[j][(k + 1) & 1];
-    const double w = __shfl_up_sync(0xffffffffu, c.y, 1);
-    const double e = __shfl_down_sync(0xffffffffu, c.x, 1);
-    double2 o;
-    o.x = dmul(dadd(dadd(dadd(n.x, s.x), w), c.y), 0.25);
-    o.y = dmul(dadd(dadd(dadd(n.y, s.y), c.x), e), 0.25);
-    if (kCols) {  // Dirichlet columns pass through
-      if (ring0) o.x = c.x;
-      if (ring1) o.y = c.y;
+    const Quad n = st[j][k & 1];
+    const Quad c = st[j][(k + 1) & 1];
+    const double w = shfl_up1(c.b.y);
+    const double e = shfl_down1(c.a.x);
+    Quad o;
+    o.a.x = dadd(dadd(dadd(n.a.x, s.a.x), w), c.a.y);
+    o.a.y = dadd(dadd(dadd(n.a.y, s.a.y), c.a.x), c.b.x);
+    o.b.x = dadd(dadd(dadd(n.b.x, s.b.x), c.a.y), c.b.y);
+    o.b.y = dadd(dadd(dadd(n.b.y, s.b.y), c.b.x), e);
+    if (!kScaled || j == T - 1) {  // folded: only the last level scales (by 2^-2T)
+      const double m = kScaled ? pow2i(-2 * T) : 0.25;
+      o.a.x = dmul(o.a.x, m);
+      o.a.y = dmul(o.a.y, m);
+      o.b.x = dmul(o.b.x, m);
+      o.b.y = dmul(o.b.y, m);
+    }
+    // a Dirichlet cell keeps its value; folded, its level-j copy carries level j's scale
+    const double rs = j == T - 1 ? pow2i(2 - 2 * T) : 4.0;
+    if (kCols) {
+      if (ring[0]) o.a.x = kScaled ? dmul(c.a.x, rs) : c.a.x;
+      if (ring[1]) o.a.y = kScaled ? dmul(c.a.y, rs) : c.a.y;
+      if (ring[2]) o.b.x = kScaled ? dmul(c.b.x, rs) : c.b.x;
+      if (ring[3]) o.b.y = kScaled ? dmul(c.b.y, rs) : c.b.y;
     }
     if (kRows) {
       const int64_t row = r - j - 1;
-      if (row <= ring_lo || row >= ring_hi) o = c;  // Dirichlet rows never change
+      if (row <= ring_lo || row >= ring_hi) {
+        o = c;
+        if (kScaled) {
+          o.a.x = dmul(c.a.x, rs);
+          o.a.y = dmul(c.a.y, rs);
+          o.b.x = dmul(c.b.x, rs);
+          o.b.y = dmul(c.b.y, rs);
+        }
+      }
     }
     st[j][k & 1] = s;
     s = o;
@@ -332,376 +398,393 @@ __device__ __forceinline__ double2 tb_levels(double2 (&st)[T][2], const int k, d
   return s;
 }
 
-template <int T, int kMinBlocks>
-__global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
-    jacobi2d_tb_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
-                       int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk, int64_t nstrips, int64_t ring_lo,
-                       int64_t ring_hi, int64_t nrows_buf, double* __restrict__ dst2, int64_t delta2) {
-  static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
-  constexpr int kStride = kStripCols - 2 * T;
-  const int lane = threadIdx.x & 31;
-  const int64_t strip = (int64_t)blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
-  if (strip >= nstrips) return;
-  const int64_t yc0 = y_lo + (int64_t)blockIdx.y * rows_per_chunk;
-  if (yc0 > y_hi) return;
-  const int64_t yc1 = min(y_hi, yc0 + rows_per_chunk - 1);
-
-  const int64_t x = strip * kStride - T + 2 * lane;
-  const bool has_pair = x >= 0 && x < nxp2;
-  const bool st_lane = lane >= T / 2 && lane <= 31 - T / 2;
-  const bool st0 = st_lane && x >= 0 && x < nxp2;
-  const bool st1 = st_lane && x + 1 >= 0 && x + 1 < nxp2;
-  const bool ring0 = (x == 0) || (x == nxp2 - 1);
-  const bool ring1 = (x + 1 == nxp2 - 1);
-  const int64_t x_first = strip * kStride - T;
-  const bool col_ring = x_first <= 0 || x_first + kStripCols >= nxp2 - 1;  // warp-uniform
-  const double* sp = src + (has_pair ? x : 0);  // every lane loads from a valid column
-
-  // input rows the pipeline reads: [r_first, r_load_last]; steps run to r_end
-  const int64_t r_first = max(max(ring_lo, (int64_t)0), yc0 - T);
-  const int64_t r_load_last = min(min(ring_hi, nrows_buf - 1), yc1 + T);
-  const int64_t r_end = yc1 + T;
-
-  double2 st[T][2];
-#pragma unroll
-  for (int j = 0; j < T; ++j) st[j][0] = st[j][1] = make_double2(0.0, 0.0);
-  double2 buf[kTbGroup];  // input rows r0..r0+G-1; slot k is refilled with row r0+k+G after use
-  const double* safe = sp + r_first * ld;
-#pragma unroll
-  for (int k = 0; k < kTbGroup; ++k) buf[k] = ldg2(r_first + k <= r_load_last ? sp + (r_first + k) * ld : safe);
-  const double* lp = sp + (r_first + kTbGroup) * ld;  // next row to load
-  double* sp_out = dst + x + (r_first - T) * ld;      // row the next step stores
-  double* sp_out2 = dst2 ? dst2 + x + (r_first - T + delta2) * ld : nullptr;
-
-  for (int64_t r0 = r_first; r0 <= r_end; r0 += kTbGroup) {
-#pragma unroll
-    for (int k = 0; k < kTbGroup; ++k) {
-      const int64_t r = r0 + k;
-      if (r > r_end) break;
-      const double2 s0 = buf[k];
-      buf[k] = ldg2(r + kTbGroup <= r_load_last ? lp : safe);
-      lp += ld;
-      // does any level of this step touch a Dirichlet row (rows r-1 .. r-T)?
-      const bool rows_chk = (r - T <= ring_lo) || (r - 1 >= ring_hi);
-      double2 o;
-      if (rows_chk) {
-        o = col_ring ? tb_levels<T, true, true>(st, k, s0, r, ring0, ring1, ring_lo, ring_hi)
-                     : tb_levels<T, true, false>(st, k, s0, r, ring0, ring1, ring_lo, ring_hi);
-      } else {
-        o = col_ring ? tb_levels<T, false, true>(st, k, s0, r, ring0, ring1, ring_lo, ring_hi)
-                     : tb_levels<T, false, false>(st, k, s0, r, ring0, ring1, ring_lo, ring_hi);
-      }
-      // o = level T, row r-T
-      if (r - T >= yc0 && r - T <= yc1) {
-        if (st0 && st1) stg2(sp_out, o);
-        else if (st0) sp_out[0] = o.x;
-        else if (st1) sp_out[1] = o.y;
-        if (sp_out2) {  // fused halo swap
-          if (st0 && st1) stg2(sp_out2, o);
-          else if (st0) sp_out2[0] = o.x;
-          else if (st1) sp_out2[1] = o.y;
-        }
-      }
-      sp_out += ld;
-      if (sp_out2) sp_out2 += ld;
-    }
+// Range check of the folding (lazy: accumulated per lane, voted once per item).
+// The folded arithmetic is bitwise Listing 1 when every input value is zero or
+// has a biased exponent in [1+2T, 2045-2T]. Integer ops on the bit patterns:
+// t = the high word << 1 (sign dropped, exponent in bits 31..21) is tracked by
+// its maximum; k = t + min(lo, 1) - 1 by its minimum, so an exact zero maps to
+// 0xffffffff (exempt) and a subnormal with a zero high word to 0 (caught).
+struct TbRange {
+  unsigned mn = 0xffffffffu, mx = 0u;
+  __device__ __forceinline__ void add(const Quad& q) {
+    auto key = [](double x, unsigned& t, unsigned& k) {
+      t = (unsigned)__double2hiint(x) << 1;
+      k = t + min((unsigned)__double2loint(x), 1u) - 1u;
+    };
+    unsigned t0, t1, t2, t3, k0, k1, k2, k3;
+    key(q.a.x, t0, k0);
+    key(q.a.y, t1, k1);
+    key(q.b.x, t2, k2);
+    key(q.b.y, t3, k3);
+    mn = __vimin3_u32(mn, k0, k1);
+    mn = __vimin3_u32(mn, k2, k3);
+    mx = __vimax3_u32(mx, t0, t1);
+    mx = __vimax3_u32(mx, t2, t3);
   }
-}
-
-// ---- 4 columns per lane (two 16-byte pairs): 128-column strips, half the
-// shuffles per point and 2T/128 instead of 2T/64 redundant columns.
-struct Quad {
-  double2 a, b;  // columns x, x+1 | x+2, x+3
+  template <int T>
+  __device__ __forceinline__ bool unsafe() const {
+    constexpr unsigned kLo = (1u + 2u * T) << 21, kHi = (2046u - 2u * T) << 21;
+    return mn < kLo - 1u || mx >= kHi;
+  }
 };
 
-// G = 3 variant: input rows staged in a per-warp shared-memory ring of kTbRing
-// rows by cp.async (each lane copies and later reads only its own 32 bytes, so
-// no barrier is needed), read back one step ahead so the LDS latency is off the
-// chain; frees the register prefetch for the three-slot level state.
-constexpr int kTbRing = 8;
-__device__ __forceinline__ void tb_cp16(uint32_t smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
+// Per-warp constants of one (strip, row chunk) item.
+struct Tb4Item {
+  const double *spa, *spb;  // the lane's two column pairs (clamped to valid columns)
+  double *out, *out2;       // stores of the row r_first - T (out2: fused halo swap, or null)
+  int64_t ld, yc0, yc1, r_first, r_load_last, r_end, ring_lo, ring_hi;
+  bool col_ring;
+  bool ring[4], stm[4];  // Dirichlet column / stored column, per lane column
+};
+
+// ---- rotated-register steady state ------------------------------------------
+// Each level's update is done IN PLACE in the register of its oldest row N:
+// P_j = ((N_j + S_j) + W) + E overwrites N_j, and P_j is the next level's S.
+// One step later the roles shift: level j's C becomes its N, and the register
+// holding P_{j-1} becomes its C. So a physical register climbs one level every
+// two steps, and the assignment repeats every M = 2T + 2 steps (the +2: the
+// input row of the step and the next one, read from shared memory one step
+// ahead). A block of M unrolled steps therefore uses only compile-time register
+// indices — no register copies at all (the two-slot rotation of the general
+// path spends ~30 % of its instructions on moves). At the start of step k:
+//   level j: N = R[(k - 2j) mod M], C = R[(k + 1 - 2j) mod M]
+//   input row of step k: R[(k + 2) mod M]
+//   free: R[(k + 3) mod M] (it held step k-1's output, already stored).
+// Input rows stream through a per-warp shared-memory ring of kTbRing slots by
+// cp.async, kTbRing-1 rows ahead: each lane copies and later reads only its own
+// 32 bytes, so no barrier is needed, and the registers hold one row in flight
+// instead of enough rows to cover the HBM latency. Rows past the item's last
+// loaded row are zero-filled (src-size 0), so a block may overrun the item's
+// end; its surplus outputs are not stored.
+template <int T>
+struct TbRot {
+  static constexpr int M = 2 * T + 2;
+  static constexpr int RS = M / 2 >= 7 ? M / 2 : M;  // ring slots per warp; divides M, so slots are compile-time
+  __host__ __device__ static constexpr int at(int i) { return ((i % M) + M) % M; }
+};
+
+__device__ __forceinline__ void cp16_zfill(uint32_t smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem), "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
 }
-__device__ __forceinline__ void tb_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void tb_wait_ring() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(kTbRing - 1) : "memory");
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-__device__ __forceinline__ double2 tb_lds2(uint32_t smem) {
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ double2 lds2(uint32_t smem) {
   double2 v;
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem) : "memory");
   return v;
 }
 
-// State of level j: rows n, c of level j-1's output in slots k % NS, (k+1) % NS; the new
-// row s goes to slot (k+2) % NS. NS = 2 overwrites n's slot; NS = 3 writes the free third
-// slot, so s and n never need the same registers and a group of G = 3 steps returns every
-// value to its register with no copies at the loop edge.
-template <int T, int NS, bool kRows, bool kCols>
-__device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][NS], const int k, Quad s, int64_t r, const bool (&ring)[4],
-                                           int64_t ring_lo, int64_t ring_hi) {
-#pragma unroll
-  for (int j = 0; j < T; ++j) {
-    const Quad n = st[j][k % NS];
-    const Quad c = st[j][(k + 1) % NS];
-    const double w = __shfl_up_sync(0xffffffffu, c.b.y, 1);
-    const double e = __shfl_down_sync(0xffffffffu, c.a.x, 1);
-    Quad o;
-    o.a.x = dmul(dadd(dadd(dadd(n.a.x, s.a.x), w), c.a.y), 0.25);
-    o.a.y = dmul(dadd(dadd(dadd(n.a.y, s.a.y), c.a.x), c.b.x), 0.25);
-    o.b.x = dmul(dadd(dadd(dadd(n.b.x, s.b.x), c.a.y), c.b.y), 0.25);
-    o.b.y = dmul(dadd(dadd(dadd(n.b.y, s.b.y), c.b.x), e), 0.25);
-    if (kCols) {
-      if (ring[0]) o.a.x = c.a.x;
-      if (ring[1]) o.a.y = c.a.y;
-      if (ring[2]) o.b.x = c.b.x;
-      if (ring[3]) o.b.y = c.b.y;
-    }
-    if (kRows) {
-      const int64_t row = r - j - 1;
-      if (row <= ring_lo || row >= ring_hi) o = c;
-    }
-    st[j][(k + 2) % NS] = s;
-    s = o;
+// The warp's shared-memory row ring: slot q holds lane l's column pair a at
+// q*1024 + l*16 and b at q*1024 + 512 + l*16 (contiguous 16-byte lanes:
+// conflict-free). A run of blocks starting at row r0 keeps row r0 + m in slot
+// m mod RS, so every slot offset inside a block is a compile-time constant.
+struct TbRing {
+  uint32_t lane_base;  // slot 0, column pair a of this lane
+  const double* gp;    // this lane's column x in the next row to copy
+  int valid;           // rows left before the item's last loaded row (later rows are zero-filled)
+  __device__ __forceinline__ void copy(int slot, int64_t ld) {
+    const uint32_t s = lane_base + (uint32_t)slot * 1024u;
+    cp16_zfill(s, gp, valid > 0);
+    cp16_zfill(s + 512, gp + 2, valid > 0);
+    cp_commit();
+    gp += ld;
+    --valid;
   }
-  return s;
+  __device__ __forceinline__ Quad read(int slot) const {
+    const uint32_t s = lane_base + (uint32_t)slot * 1024u;
+    Quad q;
+    q.a = lds2(s);
+    q.b = lds2(s + 512);
+    return q;
+  }
+};
+
+// One block of M steps; the run's first row (in slot 0) is a multiple of M rows back.
+template <int T, bool kScaled>
+__device__ __forceinline__ void tb4_rot_block(Quad (&R)[TbRot<T>::M], TbRing& ring, double*& out, int& i,
+                                              const int i_lo, const unsigned i_span, const int64_t ld, const bool sa,
+                                              const bool sb, TbRange& rng) {
+  using Rot = TbRot<T>;
+  constexpr int M = Rot::M, RS = Rot::RS;
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    ring.copy((k + RS - 1) % RS, ld);    // row r + RS - 1
+    cp_wait<RS - 2>();                   // row r + 1 has landed
+    R[Rot::at(k + 3)] = ring.read((k + 1) % RS);  // row r + 1, read one step ahead
+    if (kScaled) rng.add(R[Rot::at(k + 2)]);
+#pragma unroll
+    for (int j = 0; j < T; ++j) {
+      Quad& n = R[Rot::at(k - 2 * j)];
+      const Quad& c = R[Rot::at(k + 1 - 2 * j)];
+      const Quad& s = R[Rot::at(j == 0 ? k + 2 : k - 2 * j + 2)];
+      const double w = shfl_up1(c.b.y);
+      const double e = shfl_down1(c.a.x);
+      n.a.x = dadd(dadd(dadd(n.a.x, s.a.x), w), c.a.y);
+      n.a.y = dadd(dadd(dadd(n.a.y, s.a.y), c.a.x), c.b.x);
+      n.b.x = dadd(dadd(dadd(n.b.x, s.b.x), c.a.y), c.b.y);
+      n.b.y = dadd(dadd(dadd(n.b.y, s.b.y), c.b.x), e);
+      if (!kScaled || j == T - 1) {
+        const double m = kScaled ? pow2i(-2 * T) : 0.25;
+        n.a.x = dmul(n.a.x, m);
+        n.a.y = dmul(n.a.y, m);
+        n.b.x = dmul(n.b.x, m);
+        n.b.y = dmul(n.b.y, m);
+      }
+    }
+    const Quad& o = R[Rot::at(k - 2 * (T - 1))];  // level T-1 output: row r - T
+    const bool in = (unsigned)(i - i_lo) <= i_span;
+    stg2_if(in && sa, out, o.a);
+    stg2_if(in && sb, out + 2, o.b);
+    out += ld;
+    ++i;
+  }
 }
 
-template <int T, int kMinBlocks, int G>
-__global__ void __launch_bounds__(kStreamThreads, kMinBlocks)
-    jacobi2d_tb4_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
-                        int64_t y_lo, int64_t y_hi, int64_t rows_per_chunk, int64_t nstrips, int64_t ring_lo,
-                        int64_t ring_hi, int64_t nrows_buf, double* __restrict__ dst2, int64_t delta2) {
-  static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
-  constexpr int NS = G % 3 == 0 ? 3 : 2;  // row slots per level (tb4_levels)
-  static_assert(G % NS == 0, "row-slot renaming needs a group of whole slot cycles");
-  constexpr int P = G == 3 ? 1 : G;  // rows loaded ahead in registers (G = 3: the shared-memory ring instead)
-  static_assert(G % P == 0, "prefetch slots renamed within a group");
-  constexpr int kCols = 128, kStride = kCols - 2 * T;
-  const int lane = threadIdx.x & 31;
-  const int64_t strip = (int64_t)blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
-  if (strip >= nstrips) return;
-  const int64_t yc0 = y_lo + (int64_t)blockIdx.y * rows_per_chunk;
-  if (yc0 > y_hi) return;
-  const int64_t yc1 = min(y_hi, yc0 + rows_per_chunk - 1);
-
-  const int64_t x = strip * kStride - T + 4 * lane;
-  const int64_t x_first = strip * kStride - T;
-  const int64_t lo_c = x_first + T, hi_c = x_first + kCols - T;  // exact columns [lo_c, hi_c)
-  const bool has_a = x >= 0 && x < nxp2, has_b = x + 2 >= 0 && x + 2 < nxp2;
-  const bool sta0 = x >= lo_c && x < hi_c && x >= 0 && x < nxp2;
-  const bool sta1 = x + 1 >= lo_c && x + 1 < hi_c && x + 1 >= 0 && x + 1 < nxp2;
-  const bool stb0 = x + 2 >= lo_c && x + 2 < hi_c && x + 2 >= 0 && x + 2 < nxp2;
-  const bool stb1 = x + 3 >= lo_c && x + 3 < hi_c && x + 3 >= 0 && x + 3 < nxp2;
-  bool ring[4];
+// Streams one item; returns false if kScaled and an input broke the folding's
+// range (the caller reruns the item exactly; stores are idempotent).
+template <int T, bool kScaled>
+__device__ __forceinline__ bool tb4_item(const Tb4Item& it, const double* __restrict__ src_x, const bool use_rot,
+                                        const uint32_t smem_lane) {
+  constexpr int G = kTbGroup;
+  using Rot = TbRot<T>;
+  constexpr int M = Rot::M, RS = Rot::RS;
+  const int64_t ld = it.ld;
+  TbRange rng;
+  Quad st[T][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) ring[i] = (x + i == 0) || (x + i == nxp2 - 1);
-  const bool col_ring = x_first <= 0 || x_first + kCols >= nxp2 - 1;
-  const double* spa = src + (has_a ? x : 0);
-  const double* spb = src + (has_b ? x + 2 : 0);
-
-  const int64_t r_first = max(max(ring_lo, (int64_t)0), yc0 - T);
-  const int64_t r_load_last = min(min(ring_hi, nrows_buf - 1), yc1 + T);
-  const int64_t r_end = yc1 + T;
-
-  Quad st[T][NS];
+  for (int j = 0; j < T; ++j) st[j][0].a = st[j][0].b = st[j][1].a = st[j][1].b = make_double2(0.0, 0.0);
+  Quad buf[G];  // input rows r0 .. r0+G-1; slot k is refilled with row r0+k+G once used
+  const int64_t safe_off = it.r_first * ld;
 #pragma unroll
-  for (int j = 0; j < T; ++j) {
-#pragma unroll
-    for (int q = 0; q < NS; ++q) st[j][q].a = st[j][q].b = make_double2(0.0, 0.0);
+  for (int k = 0; k < G; ++k) {
+    const int64_t off = (it.r_first + k <= it.r_load_last) ? (it.r_first + k) * ld : safe_off;
+    buf[k].a = ldg2(it.spa + off);
+    buf[k].b = ldg2(it.spb + off);
   }
-  constexpr bool kRing = G == 3;
-  Quad buf[P];
-  const int64_t safe_off = r_first * ld;
-  // shared-memory row ring (kRing): this lane's 32 bytes of slot q at sring + q * 1024
-  extern __shared__ __align__(16) double tb_ring_smem[];
-  const uint32_t sring = (uint32_t)__cvta_generic_to_shared(tb_ring_smem) +
-                         (uint32_t)((threadIdx.x >> 5) * kTbRing * 1024 + lane * 32);
-  int rs = 0;  // ring slot of the current row
-  Quad snx;    // the current row, read from the ring one step ahead
-  int64_t roff = (r_first + kTbRing) * ld;
-  if constexpr (kRing) {
-#pragma unroll
-    for (int q = 0; q < kTbRing; ++q) {
-      const int64_t off = (r_first + q <= r_load_last) ? (r_first + q) * ld : safe_off;
-      tb_cp16(sring + q * 1024, spa + off);
-      tb_cp16(sring + q * 1024 + 16, spb + off);
-      tb_commit();
-    }
-    tb_wait_ring();
-    snx.a = tb_lds2(sring);
-    snx.b = tb_lds2(sring + 16);
-  } else {
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const int64_t off = (r_first + k <= r_load_last) ? (r_first + k) * ld : safe_off;
-      buf[k].a = ldg2(spa + off);
-      buf[k].b = ldg2(spb + off);
-    }
-  }
-  // kRing: the current row; the slot it came from refills with row r + kTbRing, and
-  // row r + 1 is read into registers for the next step
-  auto ring_row = [&](int64_t r) -> Quad {
-    const Quad cur = snx;
-    const int64_t off = (r + kTbRing <= r_load_last) ? roff : safe_off;
-    roff += ld;
-    const uint32_t w = sring + rs * 1024;
-    tb_cp16(w, spa + off);
-    tb_cp16(w + 16, spb + off);
-    tb_commit();
-    rs = rs + 1 == kTbRing ? 0 : rs + 1;
-    tb_wait_ring();
-    snx.a = tb_lds2(sring + rs * 1024);
-    snx.b = tb_lds2(sring + rs * 1024 + 16);
-    return cur;
+  int64_t loff = (it.r_first + G) * ld;
+  double* out = it.out;
+  double* out2 = it.out2;
+  // per-lane stored columns: whole 16-byte pairs where possible (predicated, no branches)
+  const bool pa = it.stm[0] && it.stm[1], pb = it.stm[2] && it.stm[3];
+  const bool pa0 = it.stm[0] && !it.stm[1], pa1 = !it.stm[0] && it.stm[1];
+  const bool pb0 = it.stm[2] && !it.stm[3], pb1 = !it.stm[2] && it.stm[3];
+  auto store_row = [&](bool in, double* p, const Quad& o) {
+    stg2_if(in && pa, p, o.a);
+    stg1_if(in && pa0, p, o.a.x);
+    stg1_if(in && pa1, p + 1, o.a.y);
+    stg2_if(in && pb, p + 2, o.b);
+    stg1_if(in && pb0, p + 2, o.b.x);
+    stg1_if(in && pb1, p + 3, o.b.y);
   };
-  int64_t loff = (r_first + P) * ld;
-  double* out = dst + x + (r_first - T) * ld;
-  double* out2 = dst2 ? dst2 + x + (r_first - T + delta2) * ld : nullptr;
-
-  auto store_row = [&](double* p, const Quad& o) {
-    if (sta0 && sta1) stg2(p, o.a);
-    else if (sta0) p[0] = o.a.x;
-    else if (sta1) p[1] = o.a.y;
-    if (stb0 && stb1) stg2(p + 2, o.b);
-    else if (stb0) p[2] = o.b.x;
-    else if (stb1) p[3] = o.b.y;
-  };
-
-  for (int64_t r0 = r_first; r0 <= r_end; r0 += G) {
-    // Steady state: every step of the group stores, touches no ring row and no
-    // ring column. The G steps form ONE basic block (no per-step dispatch), so the
-    // scheduler can run step k+1's level j beside step k's level j+1 — G times the
-    // independent dependency chains of one step (the kernel is latency-bound at
-    // 8 warps/SM). A shared-memory cp.async row ring (prefetch 8-16 rows ahead
-    // instead of G) measured 16-25 % slower and was dropped.
-    if (!col_ring && r0 + G - 1 <= r_end && r0 - T >= yc0 && r0 + G - 1 - T <= yc1 && r0 - T > ring_lo &&
-        r0 + G - 2 < ring_hi) {
-      Quad o[G];
+  // the rotated path: no ring column, no Dirichlet row in reach of the block's levels, no
+  // fused second store (a block may run past r_end: later rows are zero-filled, outputs
+  // past yc1 are not stored)
+  auto rot_ok = [&](int64_t r0) { return use_rot && r0 - T > it.ring_lo && r0 + M - 2 < it.ring_hi; };
+  int64_t r0 = it.r_first;
+  while (r0 <= it.r_end) {
+    if (rot_ok(r0)) {
+      Quad R[M];
 #pragma unroll
-      for (int k = 0; k < G; ++k) {
-        Quad s0;
-        if constexpr (kRing) {
-          s0 = ring_row(r0 + k);
-        } else {
-          s0 = buf[k % P];
-          const int64_t off = (r0 + k + P <= r_load_last) ? loff : safe_off;
-          buf[k % P].a = ldg2(spa + off);
-          buf[k % P].b = ldg2(spb + off);
-          loff += ld;
-        }
-        o[k] = tb4_levels<T, NS, false, false>(st, k, s0, r0 + k, ring, ring_lo, ring_hi);
+      for (int j = 0; j < T; ++j) {
+        R[Rot::at(-2 * j)] = st[j][0];
+        R[Rot::at(1 - 2 * j)] = st[j][1];
+      }
+      R[2] = buf[0];  // row r0; rows r0 + 1 .. come through the ring
+      TbRing ring;
+      ring.lane_base = smem_lane;
+      ring.gp = src_x + (r0 + 1) * ld;
+      ring.valid = (int)min(it.r_load_last - r0, (int64_t)INT32_MAX);
+#pragma unroll
+      for (int q = 1; q < RS - 1; ++q) ring.copy(q, ld);
+      int i = (int)(r0 - it.r_first);
+      const int i_lo = (int)(it.yc0 + T - it.r_first);
+      const unsigned i_span = (unsigned)(it.yc1 - it.yc0);
+      const bool sa = it.stm[0] && it.stm[1], sb = it.stm[2] && it.stm[3];
+      do {
+        tb4_rot_block<T, kScaled>(R, ring, out, i, i_lo, i_span, ld, sa, sb, rng);
+        r0 += M;
+      } while (r0 <= it.r_end && rot_ok(r0));
+      cp_wait_all();
+      if (r0 > it.r_end) break;
+#pragma unroll
+      for (int j = 0; j < T; ++j) {
+        st[j][0] = R[Rot::at(-2 * j)];
+        st[j][1] = R[Rot::at(1 - 2 * j)];
       }
 #pragma unroll
       for (int k = 0; k < G; ++k) {
-        store_row(out + k * ld, o[k]);
-        if (out2) store_row(out2 + k * ld, o[k]);
+        const int64_t off = (r0 + k <= it.r_load_last) ? (r0 + k) * ld : safe_off;
+        buf[k].a = ldg2(it.spa + off);
+        buf[k].b = ldg2(it.spb + off);
       }
-      out += G * ld;
-      if (out2) out2 += G * ld;
+      loff = (r0 + G) * ld;
       continue;
+    }
+    if (kScaled) {
+#pragma unroll
+      for (int k = 0; k < G; ++k) rng.add(buf[k]);
     }
 #pragma unroll
     for (int k = 0; k < G; ++k) {
       const int64_t r = r0 + k;
-      if (r > r_end) break;
-      Quad s0;
-      if constexpr (kRing) {
-        s0 = ring_row(r);
-      } else {
-        s0 = buf[k % P];
-        const int64_t off = (r + P <= r_load_last) ? loff : safe_off;
-        buf[k % P].a = ldg2(spa + off);
-        buf[k % P].b = ldg2(spb + off);
-        loff += ld;
-      }
-      const bool rows_chk = (r - T <= ring_lo) || (r - 1 >= ring_hi);
+      if (r > it.r_end) break;
+      const Quad s0 = buf[k];
+      const int64_t off = (r + G <= it.r_load_last) ? loff : safe_off;
+      buf[k].a = ldg2(it.spa + off);
+      buf[k].b = ldg2(it.spb + off);
+      loff += ld;
+      const bool rows_chk = (r - T <= it.ring_lo) || (r - 1 >= it.ring_hi);
       Quad o;
       if (rows_chk) {
-        o = col_ring ? tb4_levels<T, NS, true, true>(st, k, s0, r, ring, ring_lo, ring_hi)
-                     : tb4_levels<T, NS, true, false>(st, k, s0, r, ring, ring_lo, ring_hi);
+        o = it.col_ring ? tb4_levels<T, kScaled, true, true>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi)
+                        : tb4_levels<T, kScaled, true, false>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi);
       } else {
-        o = col_ring ? tb4_levels<T, NS, false, true>(st, k, s0, r, ring, ring_lo, ring_hi)
-                     : tb4_levels<T, NS, false, false>(st, k, s0, r, ring, ring_lo, ring_hi);
+        o = it.col_ring ? tb4_levels<T, kScaled, false, true>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi)
+                        : tb4_levels<T, kScaled, false, false>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi);
       }
-      if (r - T >= yc0 && r - T <= yc1) {
-        store_row(out, o);
-        if (out2) store_row(out2, o);  // fused halo swap: the same row into the neighbour's ghost row
-      }
+      const bool in = r - T >= it.yc0 && r - T <= it.yc1;
+      store_row(in, out, o);
+      store_row(in && out2, out2, o);  // fused halo swap: the same row into the neighbour's ghost row
       out += ld;
       if (out2) out2 += ld;
     }
+    r0 += G;
   }
+  if (kScaled) return !__any_sync(0xffffffffu, rng.unsafe<T>());
+  return true;
+}
+
+// Item numbering: items [0, n_int) are the interior strips (no ring column)
+// chunk-major, rows_int rows each; items [n_int, n_int + n_edge) the strips that
+// hold a ring column (the slower general path), rows_edge rows each.
+struct Tb4Grid {
+  int64_t s_lo, n_int_strips, rows_int, n_int;  // interior strips s_lo .. s_lo + n_int_strips - 1
+  int64_t n_edge_strips, rows_edge, n_edge;     // edge strips: 0 .. s_lo-1 and s_lo + n_int_strips ..
+};
+
+template <int T>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+    jacobi2d_tb4_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
+                        int64_t y_lo, int64_t y_hi, Tb4Grid g, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf,
+                        double* __restrict__ dst2, int64_t delta2, int fold) {
+  static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
+  constexpr int kStride = kTbCols - 2 * T;
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
+  int64_t strip, chunk, rpc;
+  if (item < g.n_int) {
+    strip = g.s_lo + item % g.n_int_strips;
+    chunk = item / g.n_int_strips;
+    rpc = g.rows_int;
+  } else if (item < g.n_int + g.n_edge) {
+    const int64_t e = item - g.n_int, es = e % g.n_edge_strips;
+    strip = es < g.s_lo ? es : es + g.n_int_strips;
+    chunk = e / g.n_edge_strips;
+    rpc = g.rows_edge;
+  } else {
+    return;  // warp-uniform
+  }
+  Tb4Item it;
+  it.ld = ld;
+  it.yc0 = y_lo + chunk * rpc;
+  it.yc1 = min(y_hi, it.yc0 + rpc - 1);
+  const int64_t x_first = strip * kStride - T;
+  const int64_t x = x_first + 4 * lane;
+  const int64_t lo_c = x_first + T, hi_c = x_first + kTbCols - T;  // exact columns [lo_c, hi_c)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    it.ring[i] = (x + i == 0) || (x + i == nxp2 - 1);
+    it.stm[i] = x + i >= lo_c && x + i < hi_c && x + i >= 0 && x + i < nxp2;
+  }
+  it.col_ring = x_first <= 0 || x_first + kTbCols >= nxp2 - 1;
+  const bool has_a = x >= 0 && x < nxp2, has_b = x + 2 >= 0 && x + 2 < nxp2;
+  it.spa = src + (has_a ? x : 0);
+  it.spb = src + (has_b ? x + 2 : 0);
+  it.ring_lo = ring_lo;
+  it.ring_hi = ring_hi;
+  it.r_first = max(max(ring_lo, (int64_t)0), it.yc0 - T);
+  it.r_load_last = min(min(ring_hi, nrows_buf - 1), it.yc1 + T);
+  it.r_end = it.yc1 + T;
+  it.out = dst + x + (it.r_first - T) * ld;
+  it.out2 = dst2 ? dst2 + x + (it.r_first - T + delta2) * ld : nullptr;
+  // the rotated path needs whole column pairs in every lane and no fused second store
+  const bool use_rot = !it.col_ring && !dst2;
+  extern __shared__ __align__(16) unsigned char tb_ring_smem[];
+  const uint32_t smem_lane = (uint32_t)__cvta_generic_to_shared(tb_ring_smem) +
+                             (uint32_t)((threadIdx.x >> 5) * TbRot<T>::RS * 1024 + lane * 16);
+  if (fold && (tb4_item<T, true>(it, src + x, use_rot, smem_lane) || fold == 2)) return;
+  tb4_item<T, false>(it, src + x, use_rot, smem_lane);
+}
+
+// Work decomposition: interior strips run the rotated path at ~R rows per item, the
+// (up to 3) strips holding a ring column the general path, which is slower
+// (kEdgeCost), so they get shorter chunks. Warps are resident in waves of
+// num_sms x 8; the chunk counts minimise waves x the longest item (in rotated-row
+// units, warm-up 2T rows included). ST_JACOBI_TB4_ROWS overrides the interior height.
+Tb4Grid tb4_grid(int64_t nxp2, int64_t rows, int T) {
+  const int64_t stride = kTbCols - 2 * T;
+  const int64_t nstrips = (nxp2 + stride - 1) / stride;
+  Tb4Grid g{};
+  // interior strips: x_first > 0 and x_first + 128 < nxp2 - 1
+  int64_t s_hi = -1;
+  for (int64_t s = 1; s < nstrips; ++s)
+    if (s * stride - T + kTbCols < nxp2 - 1) s_hi = s;
+  g.s_lo = 1;
+  g.n_int_strips = s_hi >= 1 ? s_hi : 0;
+  g.n_edge_strips = nstrips - g.n_int_strips;
+  static const int kRows = env_int("ST_JACOBI_TB4_ROWS", 0);
+  static const int kEdgeCostPct = env_int("ST_JACOBI_TB4_EDGE_COST", 280);
+  const int64_t slots = (int64_t)num_sms() * kStreamWarps;
+  auto edge_rows_for = [&](int64_t r_int, int64_t* n_chunks) {  // edge items no longer than interior ones
+    const int64_t budget = std::max<int64_t>(1, (r_int + 2 * T) * 100 / kEdgeCostPct - 2 * T);
+    const int64_t ne = (rows + budget - 1) / budget;
+    *n_chunks = ne;
+    return (rows + ne - 1) / ne;
+  };
+  int64_t best = INT64_MAX, best_r = rows;
+  const int64_t max_chunks = std::min<int64_t>(rows, 16 * slots / std::max<int64_t>(1, nstrips) + 1);
+  for (int64_t nch = 1; nch <= max_chunks; ++nch) {
+    const int64_t r = kRows > 0 ? std::min<int64_t>(kRows, rows) : (rows + nch - 1) / nch;
+    const int64_t ni = g.n_int_strips * ((rows + r - 1) / r);
+    int64_t ne_chunks = 0;
+    edge_rows_for(r, &ne_chunks);
+    const int64_t items = ni + g.n_edge_strips * ne_chunks;
+    const int64_t cost = ((items + slots - 1) / slots) * (r + 2 * T);
+    if (cost < best) {
+      best = cost;
+      best_r = r;
+    }
+    if (kRows > 0) break;
+  }
+  g.rows_int = best_r;
+  g.n_int = g.n_int_strips * ((rows + best_r - 1) / best_r);
+  int64_t ne_chunks = 0;
+  g.rows_edge = edge_rows_for(best_r, &ne_chunks);
+  g.n_edge = g.n_edge_strips * ne_chunks;
+  return g;
 }
 
 template <int T>
 st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
                      int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
   const int64_t nxp2 = nx + 2;
-  constexpr int kStride = 128 - 2 * T;
-  const int64_t nstrips = (nxp2 + kStride - 1) / kStride;
-  const int64_t rows = y_hi - y_lo + 1;
-  const int64_t blocks_x = (nstrips + kStreamWarps - 1) / kStreamWarps;
-  static const int kOcc = env_int("ST_JACOBI_TB4_OCC", 1);
-  // Row chunk: every chunk recomputes 2T warm-up rows, and with one CTA per SM
-  // a partly filled last wave idles SMs, so pick the chunk height R that
-  // minimises waves(R) x (R + 2T) (C2: R = 357 -> 6 waves of 874 CTAs, +2 %
-  // over the fixed 192-row chunks, measured). ST_JACOBI_TB4_ROWS overrides.
-  static const int kRows = env_int("ST_JACOBI_TB4_ROWS", 0);
-  int64_t rpc = kRows;
-  if (rpc <= 0) {
-    const int64_t slots = (int64_t)num_sms() * kOcc;
-    int64_t best = INT64_MAX;
-    rpc = rows;
-    for (int64_t r = 160; r <= 448; ++r) {
-      const int64_t ctas = blocks_x * ((rows + r - 1) / r);
-      const int64_t cost = ((ctas + slots - 1) / slots) * (std::min(r, rows) + 2 * T);
-      if (cost < best) { best = cost; rpc = r; }
-    }
-  }
-  rpc = std::max<int64_t>(1, std::min<int64_t>(rpc, rows));
-  const int64_t nchunks = (rows + rpc - 1) / rpc;
-  ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d tb: too many row chunks");
-  dim3 grid((unsigned)blocks_x, (unsigned)nchunks);
-  // G = steps per group: 2 (default) = two row slots + register prefetch; 3 = three row
-  // slots per level (no register copies at the loop edge) with the input rows staged in
-  // a shared-memory cp.async ring: 7 % more work per clock, but it runs into the power
-  // cap (sw_power_cap, 1833 MHz) and sustains the same 1619 Gpts/s as G=2 at 1965 MHz
-  // (DESIGN.md §6.2); 4 spills at T=8
-  static const int kG = env_int("ST_JACOBI_TB4_G", 2);
-  auto* kern = kG == 3 ? jacobi2d_tb4_kernel<T, 1, 3>
-               : kOcc == 1 ? (kG == 4 ? jacobi2d_tb4_kernel<T, 1, 4> : jacobi2d_tb4_kernel<T, 1, 2>)
-                           : (kG == 4 ? jacobi2d_tb4_kernel<T, 2, 4> : jacobi2d_tb4_kernel<T, 2, 2>);
-  const size_t smem = kG == 3 ? (size_t)kStreamWarps * kTbRing * 1024 : 0;
-  if (smem > 0)
-    ST_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<grid, kStreamThreads, smem, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo, ring_hi, nrows_buf,
-                                          rem.base, rem.delta);
-  ST_LAUNCHED();
-  return ST_OK;
-}
-
-template <int T>
-st_status launch_tb(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
-                    int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
-  const int64_t nxp2 = nx + 2;
-  constexpr int kStride = kStripCols - 2 * T;
-  const int64_t nstrips = (nxp2 + kStride - 1) / kStride;
-  const int64_t rows = y_hi - y_lo + 1;
-  static const int kRows = env_int("ST_JACOBI_TB_ROWS", 512);
-  const int64_t rpc = std::max<int64_t>(1, std::min<int64_t>(kRows, rows));
-  const int64_t nchunks = (rows + rpc - 1) / rpc;
-  ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d tb: too many row chunks");
-  dim3 grid((unsigned)((nstrips + kStreamWarps - 1) / kStreamWarps), (unsigned)nchunks);
-  static const int kOcc = env_int("ST_JACOBI_TB_OCC", 2);
-  if (kOcc == 3)
-    jacobi2d_tb_kernel<T, 3><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
-                                                             ring_hi, nrows_buf, rem.base, rem.delta);
-  else if (kOcc == 2)
-    jacobi2d_tb_kernel<T, 2><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
-                                                             ring_hi, nrows_buf, rem.base, rem.delta);
-  else
-    jacobi2d_tb_kernel<T, 1><<<grid, kStreamThreads, 0, s>>>(src, dst, nxp2, ld, y_lo, y_hi, rpc, nstrips, ring_lo,
-                                                             ring_hi, nrows_buf, rem.base, rem.delta);
+  const Tb4Grid g = tb4_grid(nxp2, y_hi - y_lo + 1, T);
+  const int64_t blocks = (g.n_int + g.n_edge + kStreamWarps - 1) / kStreamWarps;
+  ST_RETURN_IF(blocks > INT32_MAX, ST_ENOTSUP, "jacobi2d tb: grid too large");
+  // power-of-two folding of the level multiplies (ST_JACOBI_FOLD=1; bitwise, every input
+  // range-checked; 2 = folding WITHOUT the check, test-only: shows the tests' out-of-range
+  // grids would break an unchecked fold). Off by default: on B200 the check costs as many
+  // integer instructions as the folded multiplies save (ncu).
+  static const int kFold = env_int("ST_JACOBI_FOLD", 0);
+  const size_t smem = (size_t)kStreamWarps * TbRot<T>::RS * 1024;
+  ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi2d_tb4_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  jacobi2d_tb4_kernel<T><<<(unsigned)blocks, kStreamThreads, smem, s>>>(src, dst, nxp2, ld, y_lo, y_hi, g, ring_lo,
+                                                                     ring_hi, nrows_buf, rem.base, rem.delta, kFold);
   ST_LAUNCHED();
   return ST_OK;
 }
@@ -714,63 +797,22 @@ st_status jacobi2d_preload() {
   cudaFuncAttributes fa;
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_stream_kernel<4>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_resident_kernel));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<3>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<8>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<2, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<2, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<2, 3>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<4, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<4, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<4, 3>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<6, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<6, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<6, 3>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb_kernel<8, 3>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 1, 3>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, 2, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 1, 3>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, 2, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 1, 3>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, 2, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 1, 3>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, 2, 4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<kRegResRows>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8>));
   return ST_OK;
 }
 
 st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
                            int t, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
   if (y_hi < y_lo) return ST_OK;
-  static const int kColsPerLane = env_int("ST_JACOBI_TB_COLS", 4);
-  if (kColsPerLane == 4) {
-    switch (t) {
-      case 2: return launch_tb4<2>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
-      case 4: return launch_tb4<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
-      case 6: return launch_tb4<6>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
-      case 8: return launch_tb4<8>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
-      default: break;
-    }
-  }
   switch (t) {
-    case 2: return launch_tb<2>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
-    case 4: return launch_tb<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
-    case 6: return launch_tb<6>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
-    case 8: return launch_tb<8>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
+    case 2: return launch_tb4<2>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
+    case 4: return launch_tb4<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
+    case 6: return launch_tb4<6>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
+    case 8: return launch_tb4<8>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
     default: set_error("jacobi2d: tblock=%d not supported (2, 4, 6, 8)", t); return ST_ENOTSUP;
   }
 }
