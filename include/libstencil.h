@@ -104,8 +104,29 @@ st_status st_comm_from_nccl(st_comm** out, void* nccl_comm, int32_t cuda_device)
  * typically a neighbour that never joined a halo swap. On timeout an NCCL
  * communicator is aborted (ncclCommAbort) so its kernels drain; a LOCAL/IPC
  * flag wait cannot be cancelled: the work completes if the late rank joins,
- * otherwise the caller must tear the process down. timeout_ms <= 0: no limit. */
+ * otherwise the caller must tear the process down. After a timeout the comm is
+ * marked broken (any transport): later calls on it fail with ST_ENCCL instead of
+ * queueing behind the stuck wait. timeout_ms <= 0: no limit. */
 st_status st_comm_wait(st_comm* comm, void* cuda_stream, int32_t timeout_ms);
+
+/* Phase profiler (SURVEY.md §5 "overlap evidence"; PAPER.md:268 halo swap
+ * overlapped with interior compute). With profiling enabled, every st_* call on
+ * `comm` records CUDA timing events around its phases:
+ *   ST_PHASE_BOUNDARY    boundary rows/planes (their fused neighbour stores included)
+ *   ST_PHASE_INTERIOR    rows/planes computed while the swap is in flight (and
+ *                        whole-slab sweeps that overlap nothing)
+ *   ST_PHASE_JOIN_WAIT   time the caller's stream is blocked waiting for the
+ *                        neighbours' ghosts (0 when the swap is fully hidden)
+ *   ST_PHASE_SWAP        the swap on the comm stream (copy-engine / NCCL transports)
+ *   ST_PHASE_READY_WAIT  fused transport: waiting until the neighbours' ghost rows
+ *                        may be overwritten
+ * st_comm_profile_read waits for the recorded events, writes per-phase totals in
+ * milliseconds and interval counts, and clears them. Profiling adds event records
+ * to the streams; leave it off for timed runs. enable = 0 stops recording. */
+enum { ST_PHASE_BOUNDARY = 0, ST_PHASE_INTERIOR = 1, ST_PHASE_JOIN_WAIT = 2, ST_PHASE_SWAP = 3,
+       ST_PHASE_READY_WAIT = 4, ST_PHASES = 5 };
+st_status st_comm_profile(st_comm* comm, int32_t enable);
+st_status st_comm_profile_read(st_comm* comm, double ms[ST_PHASES], int64_t counts[ST_PHASES]);
 
 /* Single-process group of `nranks` ranks (LOCAL transport): comms[r] is rank r,
  * on CUDA device devices[r] (devices may repeat; distinct devices get peer
@@ -113,7 +134,10 @@ st_status st_comm_wait(st_comm* comm, void* cuda_stream, int32_t timeout_ms);
  * neighbour's ghost slabs with the copy engines, ordered by device-side flags
  * (stream memory operations), so no SM and no host synchronisation is used and
  * the ranks' st_* calls may be issued sequentially from one host thread.
- * Every rank must st_comm_bind the buffers it will swap. */
+ * Every rank must st_comm_bind the buffers it will swap. Ranks that share a device
+ * order each other with stream waits, which deadlock if two of their streams share a
+ * hardware queue: with k > 1 ranks on one device CUDA_DEVICE_MAX_CONNECTIONS must be
+ * >= 2k+1 (set before CUDA initialises), else ST_ENOTSUP. */
 st_status st_comm_init_local(st_comm** comms, int32_t nranks, const int32_t* devices);
 
 /* One rank of a multi-process group using the IPC transport: the LOCAL
@@ -131,7 +155,9 @@ st_status st_comm_export(st_comm* comm, double* const* buffers, int32_t nbuffers
                          uint8_t* blob, int64_t cap, int64_t* used);
 
 /* Maps the blob exported by rank `peer` if it is a neighbour (rank -/+ 1);
- * other ranks' blobs are ignored. IPC comms only. */
+ * other ranks' blobs are ignored. IPC comms only. Re-importing a peer replaces its
+ * mappings; the library synchronises the device before unmapping the old ones, so
+ * work still queued against them completes first. */
 st_status st_comm_import(st_comm* comm, int32_t peer, const uint8_t* blob, int64_t bytes);
 
 /* Pencils (2-D (y, z) process grid, "decompose the 3D space into two

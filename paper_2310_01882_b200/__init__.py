@@ -52,6 +52,7 @@ class Op(ctypes.Structure):
 
 
 OP_SWEEP, OP_EXCHANGE, OP_JOIN, OP_SWAP = 1, 2, 3, 4
+PHASES = ("boundary", "interior", "join_wait", "swap", "ready_wait")  # ST_PHASE_* order
 
 _vp, _i64, _i32, _dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
 
@@ -64,6 +65,8 @@ _SIGS = {
     "st_comm_destroy": (ctypes.c_int, [_vp]),
     "st_comm_from_nccl": (ctypes.c_int, [ctypes.POINTER(_vp), _vp, _i32]),
     "st_comm_wait": (ctypes.c_int, [_vp, _vp, _i32]),
+    "st_comm_profile": (ctypes.c_int, [_vp, _i32]),
+    "st_comm_profile_read": (ctypes.c_int, [_vp, ctypes.POINTER(_dbl), ctypes.POINTER(_i64)]),
     "st_stencil2d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp,
                                         ctypes.POINTER(_i32)]),
     "st_stencil2d_expr_halo": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_i32)]),
@@ -204,6 +207,16 @@ class Comm:
         """Failure detection: wait for the queued work (raises StencilError with code
         ST_ETIMEDOUT if it is still pending after timeout_ms, ST_ENCCL on an async NCCL error)."""
         _check(lib().st_comm_wait(self.handle, _stream_ptr(stream), int(timeout_ms)), "st_comm_wait")
+
+    def profile(self, enable: bool = True) -> None:
+        """Phase profiler on/off (include/libstencil.h st_comm_profile)."""
+        _check(lib().st_comm_profile(self.handle, int(bool(enable))), "st_comm_profile")
+
+    def profile_read(self) -> dict:
+        """{phase: (milliseconds, intervals)} since the last read (waits for the events)."""
+        ms, cnt = (_dbl * len(PHASES))(), (_i64 * len(PHASES))()
+        _check(lib().st_comm_profile_read(self.handle, ms, cnt), "st_comm_profile_read")
+        return {p: (ms[i], cnt[i]) for i, p in enumerate(PHASES)}
 
     @classmethod
     def local_group(cls, nranks: int, devices=None) -> list["Comm"]:

@@ -116,25 +116,38 @@ st_status run_schedule_generic(const std::vector<st_op>& ops, st_comm* comm, dou
     if (fuse && o.kind == ST_OP_SWEEP && i + 2 < ops.size() && ops[i + 1].kind == ST_OP_SWEEP &&
         ops[i + 2].kind == ST_OP_EXCHANGE && ops[i + 2].flag == 1 && ops[i + 2].buf == 1 - o.buf) {
       Remote lo, hi;
+      cudaEvent_t p0 = prof_mark(comm, s);
       ST_TRY(fused_halo_begin(comm, buf[1 - o.buf], n, s, &lo, &hi));
+      cudaEvent_t p1 = prof_mark(comm, s);
+      prof_add(comm, ST_PHASE_READY_WAIT, p0, p1);
       ST_TRY(sweep(buf[o.buf], buf[1 - o.buf], o, lo));               // first owned slabs -> rank-1
       ST_TRY(sweep(buf[o.buf], buf[1 - o.buf], ops[i + 1], hi));      // last owned slabs  -> rank+1
+      prof_add(comm, ST_PHASE_BOUNDARY, p1, prof_mark(comm, s));
       ST_TRY(fused_halo_signal(comm, s));
       pending_fused = true;
       i += 2;  // the exchange op is replaced by the fused stores + flags
       continue;
     }
     switch (o.kind) {
-      case ST_OP_SWEEP:
+      case ST_OP_SWEEP: {
+        // a sweep right before an asynchronous exchange computes boundary slabs; others the interior
+        const bool boundary = i + 1 < ops.size() && (ops[i + 1].kind == ST_OP_EXCHANGE ||
+                                                     (ops[i + 1].kind == ST_OP_SWEEP && i + 2 < ops.size() &&
+                                                      ops[i + 2].kind == ST_OP_EXCHANGE && ops[i + 2].flag == 1));
+        cudaEvent_t p0 = prof_mark(comm, s);
         ST_TRY(sweep(buf[o.buf], buf[1 - o.buf], o, Remote()));
+        prof_add(comm, boundary ? ST_PHASE_BOUNDARY : ST_PHASE_INTERIOR, p0, prof_mark(comm, s));
         break;
+      }
       case ST_OP_EXCHANGE:
         ST_TRY(halo_exchange_async(comm, &buf[o.buf], 1, n, pitch, o.sweeps, s, o.flag == 0));
         break;
       case ST_OP_JOIN:
         if (comm && comm->nranks > 1) {
+          cudaEvent_t p0 = prof_mark(comm, s);
           if (pending_fused) ST_TRY(fused_halo_join(comm, s));
           else ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
+          prof_add(comm, ST_PHASE_JOIN_WAIT, p0, prof_mark(comm, s));
         }
         pending_fused = false;
         break;
@@ -414,6 +427,8 @@ st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
     ST_TRY(halo_exchange_async(comm, &a, 1, nz, plane, halo, s, true));
     ST_TRY(jacobi3d_copy_faces(a, b, nx, ny, ldx, 0, halo - 1, s));
     ST_TRY(jacobi3d_copy_faces(a, b, nx, ny, ldx, halo + nz, nz + 2 * halo - 1, s));
+    // that swap already refreshed a's ghost planes: the schedule's leading swap of a is redundant
+    if (!ops.empty() && ops[0].kind == ST_OP_EXCHANGE && ops[0].buf == 0 && ops[0].flag == 0) ops.erase(ops.begin());
   }
   // two sweeps per pass (temporal blocking T = 2) where the ghosts allow it: the single domain
   // and slabs with halo >= 2 (schedule.cu choose_tblock3d); the schedule keeps the parity so
@@ -512,10 +527,16 @@ st_status st_pw_advect3d(double* u, double* v, double* w, double* su, double* sv
   double* fields[3] = {u, v, w};
   const int64_t plane = (ny + 2) * ldx;
   ST_TRY(halo_exchange_async(comm, fields, 3, nz, plane, 1, s, false));
+  cudaEvent_t p0 = prof_mark(comm, s);
   ST_TRY(pw_advect3d_planes(args, 2, nz - 1, s));
+  cudaEvent_t p1 = prof_mark(comm, s);
+  prof_add(comm, ST_PHASE_INTERIOR, p0, p1);
   ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
+  cudaEvent_t p2 = prof_mark(comm, s);
+  prof_add(comm, ST_PHASE_JOIN_WAIT, p1, p2);
   ST_TRY(pw_advect3d_planes(args, 1, 1, s));
   if (nz >= 2) ST_TRY(pw_advect3d_planes(args, nz, nz, s));
+  prof_add(comm, ST_PHASE_BOUNDARY, p2, prof_mark(comm, s));
   return ST_OK;
 }
 

@@ -10,8 +10,10 @@
 #include <cuda.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <set>
 #include <thread>
 
 #include "comm.h"
@@ -53,6 +55,28 @@ st_status halo_plan(int32_t rank, int32_t nranks, int64_t n_slow_local, int64_t 
   *nsend = ns;
   *nrecv = nr;
   return ST_OK;
+}
+
+// ------------------------------------------------------------ profiler ---
+cudaEvent_t prof_mark(st_comm* c, cudaStream_t s) {
+  if (!c || !c->prof) return nullptr;
+  cudaEvent_t e = nullptr;
+  if (!c->prof_pool.empty()) {
+    e = c->prof_pool.back();
+    c->prof_pool.pop_back();
+  } else if (cudaEventCreate(&e) != cudaSuccess) {
+    return nullptr;
+  }
+  if (cudaEventRecord(e, s) != cudaSuccess) {
+    c->prof_pool.push_back(e);
+    return nullptr;
+  }
+  return e;
+}
+
+void prof_add(st_comm* c, int phase, cudaEvent_t a, cudaEvent_t b) {
+  if (!c || !a || !b || phase < 0 || phase >= ST_PHASES) return;
+  c->prof_ev[phase].emplace_back(a, b);
 }
 
 // ------------------------------------------------ stream memory operations ---
@@ -150,6 +174,7 @@ st_status local_exchange(st_comm* c, double* const* fields, int32_t nfields, int
   cudaStream_t cs = c->comm_stream;
   ST_CHECK_CUDA(cudaEventRecord(c->ev_ready, main));
   ST_CHECK_CUDA(cudaStreamWaitEvent(cs, c->ev_ready, 0));
+  cudaEvent_t p0 = prof_mark(c, cs);
   // my ghost slabs may now be overwritten: tell both neighbours (I am rank-1's high, rank+1's low neighbour)
   for (int side = 0; side < 2; ++side) {
     st_peer pc;
@@ -175,6 +200,7 @@ st_status local_exchange(st_comm* c, double* const* fields, int32_t nfields, int
   }
   if (c->rank > 0) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromLo, k));
   if (c->rank < c->nranks - 1) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromHi, k));
+  prof_add(c, ST_PHASE_SWAP, p0, prof_mark(c, cs));
   ST_CHECK_CUDA(cudaEventRecord(c->ev_done, cs));
   if (join) ST_CHECK_CUDA(cudaStreamWaitEvent(main, c->ev_done, 0));
   return ST_OK;
@@ -184,6 +210,7 @@ st_status local_exchange(st_comm* c, double* const* fields, int32_t nfields, int
 st_status pencil_exchange_async(st_comm* c, double* const* fields, int32_t nfields, int64_t nx, int64_t nyl,
                                 int64_t nzl, int64_t ldx, cudaStream_t main, bool join) {
   ST_RETURN_IF(c->kind == st_comm::NCCL, ST_ENOTSUP, "pencil decomposition needs the IPC or LOCAL transport");
+  ST_RETURN_IF(c->broken, ST_ENCCL, "st_comm is unusable after an earlier error or timeout");
   ST_RETURN_IF(c->grid_py < 1 || c->nranks % c->grid_py != 0, ST_EINVAL, "pencils: st_comm_set_grid first");
   ST_RETURN_IF(c->bound.empty(), ST_EINVAL, "pencils: st_comm_bind/st_comm_export the swapped buffers first");
   ST_RETURN_IF(nyl != c->n_mid || nzl != c->bound_n_slow, ST_EINVAL, "pencils: block %lldx%lld, bound %lldx%lld",
@@ -203,6 +230,7 @@ st_status pencil_exchange_async(st_comm* c, double* const* fields, int32_t nfiel
   const int64_t my_plane = (nyl + 2) * ldx;
   ST_CHECK_CUDA(cudaEventRecord(c->ev_ready, main));
   ST_CHECK_CUDA(cudaStreamWaitEvent(cs, c->ev_ready, 0));
+  cudaEvent_t p0 = prof_mark(c, cs);
   // my ghosts may now be overwritten: tell the y and z neighbours
   for (int side = 0; side < 2; ++side) {
     if (!((side == 0 && iy == 0) || (side == 1 && iy == py - 1))) {
@@ -252,6 +280,7 @@ st_status pencil_exchange_async(st_comm* c, double* const* fields, int32_t nfiel
   }
   if (iz > 0) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromLo, k));
   if (iz < pz - 1) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromHi, k));
+  prof_add(c, ST_PHASE_SWAP, p0, prof_mark(c, cs));
   ST_CHECK_CUDA(cudaEventRecord(c->ev_done, cs));
   if (join) ST_CHECK_CUDA(cudaStreamWaitEvent(main, c->ev_done, 0));
   return ST_OK;
@@ -317,11 +346,12 @@ st_status halo_exchange_async(st_comm* comm, double* const* fields, int32_t nfie
   int32_t ns = 0, nr = 0;
   ST_TRY(halo_plan(comm->rank, comm->nranks, n_slow_local, slab_pitch, width, sends, &ns, recvs, &nr));
   if (comm->nranks == 1) return ST_OK;
+  ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier error or timeout");
   if (comm->kind != st_comm::NCCL)
     return local_exchange(comm, fields, nfields, n_slow_local, slab_pitch, width, main, join);
-  ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier NCCL error");
   ST_CHECK_CUDA(cudaEventRecord(comm->ev_ready, main));
   ST_CHECK_CUDA(cudaStreamWaitEvent(comm->comm_stream, comm->ev_ready, 0));
+  cudaEvent_t p0 = prof_mark(comm, comm->comm_stream);
   ST_CHECK_NCCL(comm, ncclGroupStart());
   for (int f = 0; f < nfields; ++f) {
     for (int i = 0; i < ns; ++i)
@@ -332,6 +362,7 @@ st_status halo_exchange_async(st_comm* comm, double* const* fields, int32_t nfie
                                    recvs[i].peer, comm->nccl, comm->comm_stream));
   }
   ST_CHECK_NCCL(comm, ncclGroupEnd());
+  prof_add(comm, ST_PHASE_SWAP, p0, prof_mark(comm, comm->comm_stream));
   ST_CHECK_CUDA(cudaEventRecord(comm->ev_done, comm->comm_stream));
   if (join) ST_CHECK_CUDA(cudaStreamWaitEvent(main, comm->ev_done, 0));
   return ST_OK;
@@ -443,8 +474,8 @@ st_status st_comm_wait(st_comm* c, void* cuda_stream, int32_t timeout_ms) {
       if (c->nccl && !c->borrowed) {
         ncclCommAbort(c->nccl);
         c->nccl = nullptr;
-        c->broken = true;
       }
+      c->broken = true;  // later calls fail fast instead of queueing behind a wait that may never end
       set_error("st_comm_wait: rank %d: work still pending after %d ms (a neighbour did not join the swap?)",
                 c->rank, timeout_ms);
       return ST_ETIMEDOUT;
@@ -461,6 +492,21 @@ st_status st_comm_init_local(st_comm** comms, int32_t nranks, const int32_t* dev
   ST_CHECK_CUDA(cudaGetDeviceCount(&ndev));
   for (int r = 0; r < nranks; ++r)
     ST_RETURN_IF(devices[r] < 0 || devices[r] >= ndev, ST_EINVAL, "st_comm_init_local: device %d", devices[r]);
+  // Ranks sharing a device order each other with stream waits (cuStreamWaitValue32). If two
+  // of their streams share a hardware queue, a waiting stream blocks the one that would
+  // release it, so every stream of the group on a device needs its own connection:
+  // 2 per rank (main + comm) plus the legacy default stream.
+  {
+    const char* cv = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    const int conns = (cv && *cv) ? std::atoi(cv) : 8;
+    for (int r = 0; r < nranks; ++r) {
+      int same = 0;
+      for (int q = 0; q < nranks; ++q) same += devices[q] == devices[r];
+      ST_RETURN_IF(same > 1 && conns < 2 * same + 1, ST_ENOTSUP,
+                   "st_comm_init_local: %d ranks share device %d; set CUDA_DEVICE_MAX_CONNECTIONS >= %d before "
+                   "CUDA initialises (now %d)", same, devices[r], 2 * same + 1, conns);
+    }
+  }
   int prev = 0;
   cudaGetDevice(&prev);
   // peer access between the distinct devices of the group (copies and flag writes go device to device)
@@ -611,6 +657,12 @@ st_status st_comm_import(st_comm* c, int32_t peer, const uint8_t* blob, int64_t 
     pp = &c->ipc_peers.back().second;
   }
   st_peer& p = *pp;
+  if (!p.opened.empty()) {
+    // kernels (fused stores) or copies queued earlier may still write through the old
+    // mappings: drain the device before unmapping them
+    ST_CHECK_CUDA(cudaSetDevice(c->device));
+    ST_CHECK_CUDA(cudaDeviceSynchronize());
+  }
   for (void* q : p.opened) cudaIpcCloseMemHandle(q);
   p = st_peer();
   const BlobEntry* e = reinterpret_cast<const BlobEntry*>(blob + sizeof(h));
@@ -677,12 +729,18 @@ st_status st_comm_destroy(st_comm* c) {
   clear_error();
   if (!c) return ST_OK;
   cudaSetDevice(c->device);
+  // the caller's streams may still run fused stores through IPC mappings or copies into peers
+  if (!c->ipc_peers.empty()) cudaDeviceSynchronize();
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   st_status s = ST_OK;
   if (c->nccl && !c->borrowed && ncclCommDestroy(c->nccl) != ncclSuccess) s = ST_ENCCL;
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  std::set<cudaEvent_t> evs(c->prof_pool.begin(), c->prof_pool.end());
+  for (int p = 0; p < ST_PHASES; ++p)
+    for (auto& ab : c->prof_ev[p]) evs.insert(ab.first), evs.insert(ab.second);
+  for (cudaEvent_t e : evs) cudaEventDestroy(e);
   for (auto& kv : c->ipc_peers)
     for (void* p : kv.second.opened) cudaIpcCloseMemHandle(p);
   if (c->flags) cudaFree(c->flags);
@@ -693,6 +751,42 @@ st_status st_comm_destroy(st_comm* c) {
   }
   delete c;
   return s;
+}
+
+st_status st_comm_profile(st_comm* c, int32_t enable) {
+  clear_error();
+  ST_RETURN_IF(!c, ST_EINVAL, "st_comm_profile: null comm");
+  c->prof = enable != 0;
+  return ST_OK;
+}
+
+st_status st_comm_profile_read(st_comm* c, double ms[ST_PHASES], int64_t counts[ST_PHASES]) {
+  clear_error();
+  ST_RETURN_IF(!c || !ms || !counts, ST_EINVAL, "st_comm_profile_read: null argument");
+  ST_CHECK_CUDA(cudaSetDevice(c->device));
+  st_status st = ST_OK;
+  std::set<cudaEvent_t> used;  // an event may close one interval and open the next
+  for (int p = 0; p < ST_PHASES; ++p) {
+    double tot = 0.0;
+    for (auto& ab : c->prof_ev[p]) {
+      float t = 0.f;
+      if (cudaEventSynchronize(ab.second) == cudaSuccess && cudaEventElapsedTime(&t, ab.first, ab.second) == cudaSuccess)
+        tot += t;
+      else
+        st = ST_ECUDA;
+      used.insert(ab.first);
+      used.insert(ab.second);
+    }
+    ms[p] = tot;
+    counts[p] = (int64_t)c->prof_ev[p].size();
+    c->prof_ev[p].clear();
+  }
+  c->prof_pool.insert(c->prof_pool.end(), used.begin(), used.end());
+  if (st != ST_OK) {
+    cudaGetLastError();
+    set_error("st_comm_profile_read: an event could not be timed");
+  }
+  return st;
 }
 
 st_status st_comm_query(const st_comm* c, int32_t* rank, int32_t* nranks, int32_t* dev) {

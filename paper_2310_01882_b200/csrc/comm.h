@@ -60,6 +60,11 @@ struct st_comm {
   // rank = iz * grid_py + iy; n_mid = this rank's owned rows. grid_py == 0: slabs.
   int32_t grid_py = 0;
   int64_t n_mid = 0;
+  // phase profiler (st_comm_profile): CUDA-event pairs per phase, summed and reset by
+  // st_comm_profile_read; events come from a pool owned by the comm
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[ST_PHASES];
 };
 
 struct st_local_group {
@@ -95,6 +100,11 @@ st_status fused_halo_join(st_comm* comm, cudaStream_t main);
 // then whole planes with the z neighbours (corner ghosts included).
 st_status pencil_exchange_async(st_comm* comm, double* const* fields, int32_t nfields, int64_t nx, int64_t nyl,
                                 int64_t nzl, int64_t ldx, cudaStream_t main, bool join);
+
+// Phase profiler: prof_mark records a timing event on `s` (nullptr when profiling is
+// off); prof_add files the interval [a, b] under `phase`.
+cudaEvent_t prof_mark(st_comm* comm, cudaStream_t s);
+void prof_add(st_comm* comm, int phase, cudaEvent_t a, cudaEvent_t b);
 
 st_status halo_plan(int32_t rank, int32_t nranks, int64_t n_slow_local, int64_t slab_pitch,
                     int32_t width, st_xfer sends[2], int32_t* nsend, st_xfer recvs[2],

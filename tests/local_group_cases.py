@@ -5,6 +5,7 @@ CUDA_DEVICE_MAX_CONNECTIONS is set before CUDA initialises (each rank uses its
 own main + comm stream; the ranks' calls are issued one after another and
 ordered on the device)."""
 import pathlib
+import os
 import sys
 
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
@@ -243,19 +244,40 @@ def late_rank_case():
         comms[0].wait(streams[0], timeout_ms=300)
     except st.StencilError as e:
         timed_out = e.code == st.ST_ETIMEDOUT
+    # the timed-out comm is broken: a new swap fails fast instead of queueing behind the wait
+    refused = False
+    try:
+        st.st_halo_exchange(comms[0], [bufs[0]], n, nx + 2, w)
+    except st.StencilError as e:
+        refused = e.code == st.ST_ENCCL
     with torch.cuda.stream(streams[1]):
         st.halo_exchange(comms[1], [bufs[1]], w)  # SURVEY §8(b) convention (shape-derived slabs)
     comms[0].wait(streams[0], timeout_ms=10000)
     comms[1].wait(streams[1], timeout_ms=10000)
     torch.cuda.synchronize()
-    ok = timed_out and bool((bufs[0][n + w:] == 2.0).all()) and bool((bufs[1][:w] == 1.0).all())
+    ok = timed_out and refused and bool((bufs[0][n + w:] == 2.0).all()) and bool((bufs[1][:w] == 1.0).all())
     for c in comms:
         c.close()
     return ok
 
 
+def connections_case():
+    """Ranks sharing a device need CUDA_DEVICE_MAX_CONNECTIONS >= 2k+1 (run with it unset:
+    the default 8 admits 3 ranks per device, not 4)."""
+    assert "CUDA_DEVICE_MAX_CONNECTIONS" not in os.environ
+    three = st.Comm.local_group(3)
+    for c in three:
+        c.close()
+    try:
+        st.Comm.local_group(4)
+    except st.StencilError as e:
+        return e.code == st.ST_ENOTSUP and "CUDA_DEVICE_MAX_CONNECTIONS" in str(e)
+    return False
+
+
 CASES = {
     "late_rank": late_rank_case,
+    "connections": connections_case,
     "pen_j3_2x1": lambda: pencils_j3_case(2, 1, 70, 40, 33, 6),
     "pen_j3_1x2": lambda: pencils_j3_case(1, 2, 70, 40, 33, 6),
     "pen_j3_2x2": lambda: pencils_j3_case(2, 2, 66, 37, 31, 7),

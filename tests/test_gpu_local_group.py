@@ -33,3 +33,12 @@ def test_late_rank_is_detected_not_hung(cuda_lib):
     r = subprocess.run([sys.executable, str(HERE / "local_group_cases.py"), "late_rank"], env=env, capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0 and "CASES OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+def test_shared_device_needs_enough_connections(cuda_lib):
+    # k LOCAL ranks on one device deadlock if their 2k streams share hardware
+    # queues; st_comm_init_local refuses k=4 under the default 8 connections
+    env = {k: v for k, v in os.environ.items() if k != "CUDA_DEVICE_MAX_CONNECTIONS"}
+    r = subprocess.run([sys.executable, str(HERE / "local_group_cases.py"), "connections"], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "CASES OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]

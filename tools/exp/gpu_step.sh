@@ -1,10 +1,6 @@
 # scratch GPU step (edited per experiment); run under gpurun from the repo root
-OUT=gpurun_out/${TAG:-r2e}; mkdir -p $OUT
+OUT=gpurun_out/${TAG:-r2g}; mkdir -p $OUT
 make -j8 all > $OUT/build.log 2>&1 || { tail -20 $OUT/build.log; exit 1; }
-q() { python -c "import json,sys;d=json.load(open('$1'));print(d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'], d['clocks']['reasons'])" 2>&1 | tail -1; }
-tune() {
-for cfg in "$@"; do
-  env $(echo $cfg | tr ',' ' ') timeout 300 python bench.py --steps 3 --warmup 3 --sweeps 400 --no-e2e --no-cpu --no-pw --no-j3 --no-gs --no-generic > $OUT/t_$cfg$SUF.json 2>$OUT/t_$cfg$SUF.err
-  echo "$cfg$SUF: $(q $OUT/t_$cfg$SUF.json)"
-done; }
-tune ST_JACOBI_TB4_EDGE_COST=220 ST_JACOBI_TB4_EDGE_COST=260 ST_JACOBI_TB4_EDGE_COST=300 ST_JACOBI_TB4_EDGE_COST=360 ST_JACOBI_TB4_EDGE_COST=260,ST_JACOBI_TB4_ROWS=357
+PYTHONFAULTHANDLER=1 CUDA_DEVICE_MAX_CONNECTIONS=32 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 \
+  bench.py --gpus 2 --same-gpu --steps 1 --warmup 3 --sweeps 16 --pw-apps 2 --scale-steps 1 --j3-sweeps 6 --no-e2e --no-cpu > $OUT/n2.out 2> $OUT/n2.err
+echo "rc=$?"; tail -c 1500 $OUT/n2.out; grep -v "^\s*$" $OUT/n2.err | grep -A25 "Fatal\|Error\|error" | head -60
