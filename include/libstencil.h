@@ -339,12 +339,20 @@ st_status st_stencil3d_expr_run(double* a, double* b, int64_t nx, int64_t ny, in
  * fields are (nz + 2R) x (ny + 2R) x ldx, x fastest, R = max |offset|; only
  * interior points of the outputs are written. Inputs may alias each other,
  * outputs may not overlap anything. One application per call (not iterated).
- * The Piacsek-Williams advection is pw_fused_expressions() of the binding. */
+ * The Piacsek-Williams advection as such a region: st_pw_fused_expression. */
 st_status st_stencil3d_fused_run(const double* const* inputs, int32_t nin, double* const* outputs, int32_t nout,
                                  const char* const* exprs, const double* const* plane_coefs, int32_t ncoef,
                                  int64_t nx, int64_t ny, int64_t nz, int64_t ldx, void* cuda_stream);
 st_status st_stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, const char* expr,
                                 int64_t iters, void* cuda_stream, int32_t* result_in_b);
+
+/* The Piacsek-Williams advection (association trees of DESIGN.md
+ * reading R6) as the expression `which` (0 = su, 1 = sv, 2 = sw) of a fused region
+ * over f0 = u, f1 = v, f2 = w and per-plane coefficients k0 = tzc1, k1 = tzc2,
+ * k2 = tzd1, k3 = tzd2, with tcx and tcy written as 17-significant-digit literals
+ * (they round-trip binary64). Writes the NUL-terminated text into out[0..cap) and
+ * its size incl. the NUL into *used (cap = 0: size only). Host-only. */
+st_status st_pw_fused_expression(double tcx, double tcy, int32_t which, char* out, int64_t cap, int64_t* used);
 
 /* Listing 1 taken literally (R22; NEXT #4): `iters`
  * IN-PLACE lexicographic Gauss-Seidel sweeps of `a` ((ny+2) rows x ld, ring =

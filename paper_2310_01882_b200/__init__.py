@@ -70,6 +70,7 @@ _SIGS = {
     "st_stencil2d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp,
                                         ctypes.POINTER(_i32)]),
     "st_stencil2d_expr_halo": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_i32)]),
+    "st_pw_fused_expression": (ctypes.c_int, [_dbl, _dbl, _i32, ctypes.c_char_p, _i64, ctypes.POINTER(_i64)]),
     "st_stencil_expr_info": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "st_stencil3d_fused_run": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, ctypes.POINTER(_vp), _i32,
                                               ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_vp), _i32, _i64, _i64,
@@ -549,21 +550,20 @@ def st_stencil3d_fused_run(inputs, outputs, exprs, plane_coefs=(), nx: int | Non
                                         ldx, _stream_ptr(stream)), "st_stencil3d_fused_run")
 
 
+def st_pw_fused_expression(tcx: float, tcy: float, which: int) -> str:
+    """The PW advection's su/sv/sw (which = 0/1/2) as a fused-region expression (C library text)."""
+    n = _i64()
+    _check(lib().st_pw_fused_expression(float(tcx), float(tcy), which, None, 0, ctypes.byref(n)),
+           "st_pw_fused_expression")
+    buf = ctypes.create_string_buffer(n.value)
+    _check(lib().st_pw_fused_expression(float(tcx), float(tcy), which, buf, n.value, ctypes.byref(n)),
+           "st_pw_fused_expression")
+    return buf.value.decode()
+
+
 def pw_fused_expressions(tcx: float, tcy: float) -> list[str]:
-    """The Piacsek-Williams advection (reading R6's association trees) as the three
-    expressions of one fused region over f0 = u, f1 = v, f2 = w with per-plane coefficients
-    k0 = tzc1, k1 = tzc2, k2 = tzd1, k3 = tzd2 (tcx, tcy inlined at full binary64 precision)."""
-    X, Y = repr(float(tcx)), repr(float(tcy))
-    su = (f"(({X} * (f0(0,0,-1)*(f0(0,0,0)+f0(0,0,-1)) - f0(0,0,1)*(f0(0,0,0)+f0(0,0,1))))"
-          f" + ({Y} * (f0(0,-1,0)*(f1(0,-1,0)+f1(0,-1,1)) - f0(0,1,0)*(f1(0,0,0)+f1(0,0,1)))))"
-          " + ((k0*f0(-1,0,0))*(f2(-1,0,0)+f2(-1,0,1)) - (k1*f0(1,0,0))*(f2(0,0,0)+f2(0,0,1)))")
-    sv = (f"(({X} * (f1(0,0,-1)*(f0(0,0,-1)+f0(0,1,-1)) - f1(0,0,1)*(f0(0,0,0)+f0(0,1,0))))"
-          f" + ({Y} * (f1(0,-1,0)*(f1(0,0,0)+f1(0,-1,0)) - f1(0,1,0)*(f1(0,0,0)+f1(0,1,0)))))"
-          " + ((k0*f1(-1,0,0))*(f2(-1,0,0)+f2(-1,1,0)) - (k1*f1(1,0,0))*(f2(0,0,0)+f2(0,1,0)))")
-    sw = (f"(({X} * (f2(0,0,-1)*(f0(0,0,-1)+f0(1,0,-1)) - f2(0,0,1)*(f0(0,0,0)+f0(1,0,0))))"
-          f" + ({Y} * (f2(0,-1,0)*(f1(0,-1,0)+f1(1,-1,0)) - f2(0,1,0)*(f1(0,0,0)+f1(1,0,0)))))"
-          " + ((k2*f2(-1,0,0))*(f2(0,0,0)+f2(-1,0,0)) - (k3*f2(1,0,0))*(f2(0,0,0)+f2(1,0,0)))")
-    return [su, sv, sw]
+    """[su, sv, sw] expressions of the PW fused region (st_pw_fused_expression)."""
+    return [st_pw_fused_expression(tcx, tcy, w) for w in range(3)]
 
 
 def st_selftest_div6(x) -> int:

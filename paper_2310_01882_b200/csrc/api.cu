@@ -67,21 +67,6 @@ st_status make_tmap_3d_f64(CUtensorMap* map, const double* base, const uint64_t 
   return ST_OK;
 }
 
-st_status make_tmap_2d_f64(CUtensorMap* map, const double* base, const uint64_t dims[2],
-                           uint64_t pitch_bytes, const uint32_t box[2]) {
-  PFN_encodeTiled enc;
-  ST_TRY(get_encode_tiled(&enc));
-  const cuuint64_t gdim[2] = {dims[0], dims[1]};
-  const cuuint64_t gstride[1] = {pitch_bytes};
-  const cuuint32_t bx[2] = {box[0], box[1]};
-  const cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride,
-                   bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  ST_RETURN_IF(r != CUDA_SUCCESS, ST_ECUDA, "cuTensorMapEncodeTiled(2d) failed: %d", (int)r);
-  return ST_OK;
-}
-
 // ------------------------------------------------------- Jacobi driver ---
 namespace {
 

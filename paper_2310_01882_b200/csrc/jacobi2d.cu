@@ -504,11 +504,38 @@ struct TbRing {
   }
 };
 
+// Neighbour exchange through shared memory instead of warp shuffles: a 64-bit
+// shuffle is two 32-bit SHFLs whose halves ptxas then moves into an aligned
+// register pair (~4 extra instructions per level at 255 registers); an LDS.64
+// lands in a pair directly. Level j's C at step k+1 is P_{j-1} of step k (the
+// input row for j = 0), so each lane publishes those rows' edge columns (a.x,
+// b.y) one step ahead into X[(k+1)&1][j], and at step k reads its neighbours'
+// from X[k&1][j]; a __syncwarp per step orders the two. Per warp:
+// X[parity 2][level T][a.x | b.y][34] doubles, entry l+1 = lane l, so lane l
+// reads W at entry l (lane l-1's b.y) and E at entry l+2 (lane l+1's a.x); the
+// pad entries only feed the garbage columns of the strip edges.
+__device__ __forceinline__ void sts1(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ double lds1(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+template <int T>
+struct TbX {
+  static constexpr int kBytes = 2 * T * 2 * 34 * 8;  // per warp
+  // byte offset of entry idx of (parity, level, which) from the warp's base
+  __host__ __device__ static constexpr uint32_t off(int par, int j, int which, int idx) {
+    return (uint32_t)((((par * T + j) * 2 + which) * 34 + idx) * 8);
+  }
+};
+
 // One block of M steps; the run's first row (in slot 0) is a multiple of M rows back.
 template <int T, bool kScaled>
-__device__ __forceinline__ void tb4_rot_block(Quad (&R)[TbRot<T>::M], TbRing& ring, double*& out, int& i,
-                                              const int i_lo, const unsigned i_span, const int64_t ld, const bool sa,
-                                              const bool sb, TbRange& rng) {
+__device__ __forceinline__ void tb4_rot_block(Quad (&R)[TbRot<T>::M], TbRing& ring, const uint32_t xl, double*& out,
+                                              int& i, const int i_lo, const unsigned i_span, const int64_t ld,
+                                              const bool sa, const bool sb, TbRange& rng) {
   using Rot = TbRot<T>;
   constexpr int M = Rot::M, RS = Rot::RS;
 #pragma unroll
@@ -517,13 +544,20 @@ __device__ __forceinline__ void tb4_rot_block(Quad (&R)[TbRot<T>::M], TbRing& ri
     cp_wait<RS - 2>();                   // row r + 1 has landed
     R[Rot::at(k + 3)] = ring.read((k + 1) % RS);  // row r + 1, read one step ahead
     if (kScaled) rng.add(R[Rot::at(k + 2)]);
+    using X = TbX<T>;
+    const int par = k & 1, npar = (k + 1) & 1;
+    {  // level 0's C of step k+1 is this step's input row
+      const Quad& s0 = R[Rot::at(k + 2)];
+      sts1(xl + X::off(npar, 0, 0, 1), s0.a.x);
+      sts1(xl + X::off(npar, 0, 1, 1), s0.b.y);
+    }
 #pragma unroll
     for (int j = 0; j < T; ++j) {
       Quad& n = R[Rot::at(k - 2 * j)];
       const Quad& c = R[Rot::at(k + 1 - 2 * j)];
       const Quad& s = R[Rot::at(j == 0 ? k + 2 : k - 2 * j + 2)];
-      const double w = shfl_up1(c.b.y);
-      const double e = shfl_down1(c.a.x);
+      const double w = lds1(xl + X::off(par, j, 1, 0));  // lane-1's b.y
+      const double e = lds1(xl + X::off(par, j, 0, 2));  // lane+1's a.x
       n.a.x = dadd(dadd(dadd(n.a.x, s.a.x), w), c.a.y);
       n.a.y = dadd(dadd(dadd(n.a.y, s.a.y), c.a.x), c.b.x);
       n.b.x = dadd(dadd(dadd(n.b.x, s.b.x), c.a.y), c.b.y);
@@ -535,7 +569,12 @@ __device__ __forceinline__ void tb4_rot_block(Quad (&R)[TbRot<T>::M], TbRing& ri
         n.b.x = dmul(n.b.x, m);
         n.b.y = dmul(n.b.y, m);
       }
+      if (j + 1 < T) {  // P_j is level j+1's C at step k+1
+        sts1(xl + X::off(npar, j + 1, 0, 1), n.a.x);
+        sts1(xl + X::off(npar, j + 1, 1, 1), n.b.y);
+      }
     }
+    __syncwarp();
     const Quad& o = R[Rot::at(k - 2 * (T - 1))];  // level T-1 output: row r - T
     const bool in = (unsigned)(i - i_lo) <= i_span;
     stg2_if(in && sa, out, o.a);
@@ -549,7 +588,7 @@ __device__ __forceinline__ void tb4_rot_block(Quad (&R)[TbRot<T>::M], TbRing& ri
 // range (the caller reruns the item exactly; stores are idempotent).
 template <int T, bool kScaled>
 __device__ __forceinline__ bool tb4_item(const Tb4Item& it, const double* __restrict__ src_x, const bool use_rot,
-                                        const uint32_t smem_lane) {
+                                        const uint32_t smem_lane, const uint32_t xl) {
   constexpr int G = kTbGroup;
   using Rot = TbRot<T>;
   constexpr int M = Rot::M, RS = Rot::RS;
@@ -595,6 +634,12 @@ __device__ __forceinline__ bool tb4_item(const Tb4Item& it, const double* __rest
         R[Rot::at(1 - 2 * j)] = st[j][1];
       }
       R[2] = buf[0];  // row r0; rows r0 + 1 .. come through the ring
+#pragma unroll
+      for (int j = 0; j < T; ++j) {  // the neighbour exchange of step 0: every level's C
+        sts1(xl + TbX<T>::off(0, j, 0, 1), st[j][1].a.x);
+        sts1(xl + TbX<T>::off(0, j, 1, 1), st[j][1].b.y);
+      }
+      __syncwarp();
       TbRing ring;
       ring.lane_base = smem_lane;
       ring.gp = src_x + (r0 + 1) * ld;
@@ -606,7 +651,7 @@ __device__ __forceinline__ bool tb4_item(const Tb4Item& it, const double* __rest
       const unsigned i_span = (unsigned)(it.yc1 - it.yc0);
       const bool sa = it.stm[0] && it.stm[1], sb = it.stm[2] && it.stm[3];
       do {
-        tb4_rot_block<T, kScaled>(R, ring, out, i, i_lo, i_span, ld, sa, sb, rng);
+        tb4_rot_block<T, kScaled>(R, ring, xl, out, i, i_lo, i_span, ld, sa, sb, rng);
         r0 += M;
       } while (r0 <= it.r_end && rot_ok(r0));
       cp_wait_all();
@@ -715,10 +760,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   // the rotated path needs whole column pairs in every lane and no fused second store
   const bool use_rot = !it.col_ring && !dst2;
   extern __shared__ __align__(16) unsigned char tb_ring_smem[];
-  const uint32_t smem_lane = (uint32_t)__cvta_generic_to_shared(tb_ring_smem) +
-                             (uint32_t)((threadIdx.x >> 5) * TbRot<T>::RS * 1024 + lane * 16);
-  if (fold && (tb4_item<T, true>(it, src + x, use_rot, smem_lane) || fold == 2)) return;
-  tb4_item<T, false>(it, src + x, use_rot, smem_lane);
+  const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(tb_ring_smem);
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t smem_lane = smem0 + warp * TbRot<T>::RS * 1024 + lane * 16;
+  const uint32_t xl = smem0 + kStreamWarps * TbRot<T>::RS * 1024 + warp * TbX<T>::kBytes + lane * 8;
+  if (fold && (tb4_item<T, true>(it, src + x, use_rot, smem_lane, xl) || fold == 2)) return;
+  tb4_item<T, false>(it, src + x, use_rot, smem_lane, xl);
 }
 
 // Work decomposition: interior strips run the rotated path at ~R rows per item, the
@@ -781,7 +828,7 @@ st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int
   // grids would break an unchecked fold). Off by default: on B200 the check costs as many
   // integer instructions as the folded multiplies save (ncu).
   static const int kFold = env_int("ST_JACOBI_FOLD", 0);
-  const size_t smem = (size_t)kStreamWarps * TbRot<T>::RS * 1024;
+  const size_t smem = (size_t)kStreamWarps * (TbRot<T>::RS * 1024 + TbX<T>::kBytes);
   ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi2d_tb4_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   jacobi2d_tb4_kernel<T><<<(unsigned)blocks, kStreamThreads, smem, s>>>(src, dst, nxp2, ld, y_lo, y_hi, g, ring_lo,
                                                                      ring_hi, nrows_buf, rem.base, rem.delta, kFold);

@@ -521,4 +521,49 @@ st_status stencil3d_fused_run(const double* const* in, int32_t nin, double* cons
   return launch_fused_translated(bodies, in, nin, out, coefs, ncoef, nx, ny, nz, ldx, R, s);
 }
 
+// The Piacsek-Williams advection (association trees of reading R6)
+// written as the three expressions of one fused region over f0 = u, f1 = v,
+// f2 = w with per-plane coefficients k0 = tzc1, k1 = tzc2, k2 = tzd1, k3 = tzd2;
+// tcx, tcy are printed with 17 significant digits (round-trips binary64).
+st_status pw_fused_expression(double tcx, double tcy, int which, std::string* out) {
+  char X[40], Y[40];
+  snprintf(X, sizeof X, "%.17g", tcx);
+  snprintf(Y, sizeof Y, "%.17g", tcy);
+  const std::string x = std::string("(") + X + ")", y = std::string("(") + Y + ")";
+  switch (which) {
+    case 0:
+      *out = "((" + x + " * (f0(0,0,-1)*(f0(0,0,0)+f0(0,0,-1)) - f0(0,0,1)*(f0(0,0,0)+f0(0,0,1))))" + " + (" + y +
+             " * (f0(0,-1,0)*(f1(0,-1,0)+f1(0,-1,1)) - f0(0,1,0)*(f1(0,0,0)+f1(0,0,1)))))" +
+             " + ((k0*f0(-1,0,0))*(f2(-1,0,0)+f2(-1,0,1)) - (k1*f0(1,0,0))*(f2(0,0,0)+f2(0,0,1)))";
+      return ST_OK;
+    case 1:
+      *out = "((" + x + " * (f1(0,0,-1)*(f0(0,0,-1)+f0(0,1,-1)) - f1(0,0,1)*(f0(0,0,0)+f0(0,1,0))))" + " + (" + y +
+             " * (f1(0,-1,0)*(f1(0,0,0)+f1(0,-1,0)) - f1(0,1,0)*(f1(0,0,0)+f1(0,1,0)))))" +
+             " + ((k0*f1(-1,0,0))*(f2(-1,0,0)+f2(-1,1,0)) - (k1*f1(1,0,0))*(f2(0,0,0)+f2(0,1,0)))";
+      return ST_OK;
+    case 2:
+      *out = "((" + x + " * (f2(0,0,-1)*(f0(0,0,-1)+f0(1,0,-1)) - f2(0,0,1)*(f0(0,0,0)+f0(1,0,0))))" + " + (" + y +
+             " * (f2(0,-1,0)*(f1(0,-1,0)+f1(1,-1,0)) - f2(0,1,0)*(f1(0,0,0)+f1(1,0,0)))))" +
+             " + ((k2*f2(-1,0,0))*(f2(0,0,0)+f2(-1,0,0)) - (k3*f2(1,0,0))*(f2(0,0,0)+f2(1,0,0)))";
+      return ST_OK;
+    default:
+      set_error("pw_fused_expression: which = %d (0 su, 1 sv, 2 sw)", which);
+      return ST_EINVAL;
+  }
+}
+
 }  // namespace st
+
+extern "C" st_status st_pw_fused_expression(double tcx, double tcy, int32_t which, char* out, int64_t cap,
+                                            int64_t* used) {
+  st::clear_error();
+  ST_RETURN_IF(!used || (cap > 0 && !out), ST_EINVAL, "st_pw_fused_expression: null output");
+  std::string e;
+  ST_TRY(st::pw_fused_expression(tcx, tcy, which, &e));
+  *used = (int64_t)e.size() + 1;
+  if (cap == 0) return ST_OK;
+  ST_RETURN_IF(cap < *used, ST_EINVAL, "st_pw_fused_expression: buffer of %lld bytes < %lld", (long long)cap,
+               (long long)*used);
+  memcpy(out, e.c_str(), e.size() + 1);
+  return ST_OK;
+}

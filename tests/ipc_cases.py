@@ -157,6 +157,93 @@ def pencils(rank, world, dev, which):
     return all(oks)
 
 
+def c4_bands(rank, world, dev, iters=24, h=8, ny_rank=4096):
+    """Pre-flight of the N = 8 launch shapes: C4's full width (32768
+    interior columns), slabs of 4096 rows as at N = 8, H = 8 ghost rows, T = 8
+    across ranks, fused neighbour stores. Bands around every slab boundary and the
+    ring rows are compared bitwise with the oracle run on windows widened by the
+    influence radius (`iters` rows)."""
+    nx = 32768
+    ny = ny_rank * world
+    ld = nx + 2
+    start, n = st.st_block_split(ny, world, rank)
+    lo, hi = max(0, start + 1 - h), min(ny + 1, start + n + h)  # global padded rows present in the slab
+    loc = np.zeros((n + 2 * h, ld))
+    loc[lo - (start + 1 - h): hi - (start + 1 - h) + 1] = si.jacobi2d_grid(nx, ny, ld=ld, row0=lo, rows=hi - lo + 1)
+    a = torch.from_numpy(loc).to(dev)
+    del loc
+    if rank > 0:
+        a[:h] = float("nan")
+    if rank < world - 1:
+        a[h + n:] = float("nan")
+    b = torch.full_like(a, float("nan"))
+    comm = st.Comm.ipc_from_process_group(dev.index)
+    comm.bind_ipc([a, b], n)
+    r = st.st_jacobi2d_run(a, b, iters, tblock=0, halo=h, comm=comm)
+    torch.cuda.synchronize()
+    band = 40
+    mine = {}
+    for g0 in (start + 1, start + n - band + 1):  # first / last `band` owned rows (global padded index)
+        l0 = g0 - (start + 1) + h
+        mine[g0] = r[l0:l0 + band].cpu().numpy()
+    parts = [None] * world
+    dist.all_gather_object(parts, mine)
+    comm.close()
+    if rank != 0:
+        return True
+    ok = True
+    for part in parts:
+        for g0, got in part.items():
+            w0, w1 = max(0, g0 - iters), min(ny + 1, g0 + band - 1 + iters)
+            win = si.jacobi2d_grid(nx, ny, ld=ld, row0=w0, rows=w1 - w0 + 1)
+            want = oracle.jacobi2d(win, iters, nx=nx)[g0 - w0: g0 - w0 + band]
+            bad = np.argwhere(got.view(np.uint64) != want.view(np.uint64))
+            if bad.size:
+                print(f"rows {g0}..{g0 + band - 1}: {len(bad)} mismatches, first {bad[:3].tolist()}", flush=True)
+                ok = False
+    return ok
+
+
+def c5_planes(rank, world, dev):
+    """Pre-flight of C5's slab shapes: PW 1024 x 1024 x 512 in z-slabs (128 planes at
+    P = 4), ghost planes swapped by the transport; the first/last owned planes of
+    every slab (the ones that read swapped ghosts) and one interior plane are
+    compared bitwise with the oracle on their 3-plane input windows."""
+    nx = ny = 1024
+    nz = 512
+    z0, n = st.st_block_split(nz, world, rank)
+    dl = si.pw_inputs(nx, ny, nz, plane0=z0, planes=n + 2)
+    g = {k: (torch.from_numpy(v).to(dev) if isinstance(v, np.ndarray) else v) for k, v in dl.items()}
+    del dl
+    for k in "uvw":
+        if rank > 0:
+            g[k][0] = float("nan")
+        if rank < world - 1:
+            g[k][-1] = float("nan")
+    outs = [torch.zeros_like(g["u"]) for _ in range(3)]
+    comm = st.Comm.ipc_from_process_group(dev.index)
+    comm.bind_ipc([g["u"], g["v"], g["w"]], n)
+    st.st_pw_advect3d(g["u"], g["v"], g["w"], *outs, g["tcx"], g["tcy"], g["tzc1"], g["tzc2"], g["tzd1"], g["tzd2"],
+                      comm=comm)
+    torch.cuda.synchronize()
+    mine = {z0 + l: [o[l].cpu().numpy() for o in outs] for l in (1, n // 2, n)}  # local plane l = global z0 + l
+    parts = [None] * world
+    dist.all_gather_object(parts, mine)
+    comm.close()
+    if rank != 0:
+        return True
+    ok = True
+    for part in parts:
+        for z, got in part.items():
+            win = si.pw_inputs(nx, ny, nz, plane0=z - 1, planes=3)
+            want = oracle.pw_advect3d(win["u"], win["v"], win["w"], win, nx=nx)
+            for name, gg, ww in zip(("su", "sv", "sw"), got, want):
+                if not np.array_equal(gg[1:ny + 1, 1:nx + 1], ww[1, 1:ny + 1, 1:nx + 1]):
+                    print(f"plane {z} {name} mismatch", flush=True)
+                    ok = False
+    return ok
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     ngpu = torch.cuda.device_count()
@@ -174,7 +261,9 @@ def main():
                                      int(os.environ["J3_TB"]), *[int(v) for v in os.environ["J3_DIMS"].split(",")]),
           "j3_h3_t2": lambda: jacobi3d(rank, world, dev, 3, 8, 2),
           "pen_j3": lambda: pencils(rank, world, dev, "j3"),
-          "pen_pw": lambda: pencils(rank, world, dev, "pw")}[case]()
+          "pen_pw": lambda: pencils(rank, world, dev, "pw"),
+          "c4_bands": lambda: c4_bands(rank, world, dev),
+          "c5_planes": lambda: c5_planes(rank, world, dev)}[case]()
     if rank == 0:
         print("IPC CASE", case, "OK" if ok else "FAILED", flush=True)
     dist.destroy_process_group()

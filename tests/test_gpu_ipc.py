@@ -24,8 +24,7 @@ CASES = [(w, c, f) for w in (2, 3) for c in ("j2_h1", "j2_h4_t4", "pw", "j3_h1",
 CASES += [(w, c, "1") for w in (2, 3, 4) for c in ("pen_j3", "pen_pw")]  # pencils: y-z process grids
 
 
-@pytest.mark.parametrize("world,case,fused", CASES)
-def test_ipc_multiprocess_equals_oracle(cuda_lib, world, case, fused):
+def _run(world, case, fused, timeout=240):
     port = _port()
     procs = []
     for r in range(world):
@@ -36,7 +35,7 @@ def test_ipc_multiprocess_equals_oracle(cuda_lib, world, case, fused):
     outs = []
     for p in procs:
         try:
-            o, e = p.communicate(timeout=240)
+            o, e = p.communicate(timeout=timeout)
         except subprocess.TimeoutExpired:
             for q in procs:
                 q.kill()
@@ -44,3 +43,16 @@ def test_ipc_multiprocess_equals_oracle(cuda_lib, world, case, fused):
         outs.append((p.returncode, o, e))
     assert all(rc == 0 for rc, _, _ in outs), [(rc, o[-500:], e[-1500:]) for rc, o, e in outs]
     assert "OK" in outs[0][1]
+
+
+@pytest.mark.parametrize("world,case,fused", CASES)
+def test_ipc_multiprocess_equals_oracle(cuda_lib, world, case, fused):
+    _run(world, case, fused)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case", ["c4_bands", "c5_planes"])
+def test_ipc_preflight_full_width_shapes(cuda_lib, case):
+    # the launch shapes of the 8-GPU scaling run (C4 width, 4096-row slabs, H = T = 8;
+    # C5 slabs) with 4 processes on one GPU: bitwise on the bands/planes at every slab edge
+    _run(4, case, "1", timeout=900)
