@@ -12,7 +12,7 @@ sweeps; `c5`: configs[4] PW 1024x1024x512), configs[2] PW 512^3
 configs[0]).
 
 N > 1 (torchrun, one rank per GPU): strong scaling of configs[3] (C4, row
-slabs, 8 ghost rows, T = 8 across ranks) and configs[4] (C5, z-slabs). Halo
+slabs, 10 ghost rows, T = 10 across ranks) and configs[4] (C5, z-slabs). Halo
 transport: fused neighbour stores + device flags over CUDA-IPC mappings
 (NVLink peer memory), or NCCL send/recv (--transport nccl, and the loud
 fallback if the IPC probe fails). Rank 0 also times the same C4/C5 step on
@@ -876,7 +876,7 @@ def main():
     ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
     ap.add_argument("--sweeps", type=int, default=1000, help="Jacobi sweeps per step (configs[1], [3]: 1000)")
     ap.add_argument("--tblock", type=int, default=0)
-    ap.add_argument("--halo", type=int, default=8, help="ghost rows per side across ranks (N>1)")
+    ap.add_argument("--halo", type=int, default=10, help="ghost rows per side across ranks (N>1; = the auto T)")
     ap.add_argument("--transport", choices=["ipc", "nccl"], default="ipc",
                     help="N>1 halo transport: ipc = fused neighbour stores over CUDA-IPC (default), nccl")
     ap.add_argument("--same-gpu", action="store_true", help="all ranks on cuda:0 (functional check only)")

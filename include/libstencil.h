@@ -279,9 +279,10 @@ st_status st_jacobi3d_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_t
  *             row. Requires ny_local >= halo. The exact step sequence is
  *             st_jacobi2d_schedule's.
  *   iters     >= 0; 0 is a no-op.
- *   tblock    0 = auto; 1 = one sweep per pass over HBM; T >= 2 = temporal
- *             blocking (T sweeps per pass). Any choice gives bitwise the same
- *             result.
+ *   tblock    0 = auto (10 on grids >= 128^2, capped by the ghost depth across
+ *             ranks); 1 = one sweep per pass over HBM; T in {2, 4, 6, 8, 10} =
+ *             temporal blocking (T sweeps per pass); other T: ST_ENOTSUP. Any
+ *             choice gives bitwise the same result.
  *   *result_in_b (may be NULL) set to 1 if the result is in b (iters odd),
  *             else 0. The other buffer's interior is unspecified afterwards.
  */

@@ -838,7 +838,7 @@ st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int
 
 }  // namespace
 
-bool jacobi2d_tb_supported(int t) { return t == 2 || t == 4 || t == 6 || t == 8; }
+bool jacobi2d_tb_supported(int t) { return t == 2 || t == 4 || t == 6 || t == 8 || t == 10; }
 
 st_status jacobi2d_preload() {
   cudaFuncAttributes fa;
@@ -849,6 +849,7 @@ st_status jacobi2d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<10>));
   return ST_OK;
 }
 
@@ -860,7 +861,8 @@ st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t l
     case 4: return launch_tb4<4>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
     case 6: return launch_tb4<6>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
     case 8: return launch_tb4<8>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
-    default: set_error("jacobi2d: tblock=%d not supported (2, 4, 6, 8)", t); return ST_ENOTSUP;
+    case 10: return launch_tb4<10>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
+    default: set_error("jacobi2d: tblock=%d not supported (2, 4, 6, 8, 10)", t); return ST_ENOTSUP;
   }
 }
 

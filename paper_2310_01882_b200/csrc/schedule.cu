@@ -17,7 +17,7 @@
 namespace st {
 
 namespace {
-constexpr int kAutoTblock = 8;  // tblock=0 (tuned on B200)
+constexpr int kAutoTblock = 10;  // tblock=0 (tuned on B200 under the board power cap)
 constexpr int64_t kAutoMinExtent = 128;  // ... on grids at least this large in x and y
 
 void push(std::vector<st_op>& v, int32_t kind, int32_t buf, int32_t sweeps, int32_t flag, int64_t lo = 0,
@@ -61,7 +61,7 @@ st_status build_jacobi_schedule(int32_t rank, int32_t nranks, int64_t nx, int64_
   ST_RETURN_IF(dims == 3 && tblock > 2, ST_ENOTSUP, "jacobi3d: tblock=%d not supported (0, 1, 2)", tblock);
   const int T = dims == 3 ? choose_tblock3d(nranks, h, tblock) : choose_tblock(nranks, nx, n, h, tblock);
   ST_RETURN_IF(dims == 2 && T > 1 && !jacobi2d_tb_supported(T), ST_ENOTSUP,
-               "jacobi2d: tblock=%d not supported (1, 2, 4, 6, 8)", T);
+               "jacobi2d: tblock=%d not supported (1, 2, 4, 6, 8, 10)", T);
   ST_RETURN_IF(nranks > 1 && T > h, ST_EINVAL, "jacobi%dd: tblock=%d needs halo >= %d", dims, T, T);
 
   // passes: T-sweep (temporally blocked) passes, a remainder, and the parity

@@ -44,7 +44,7 @@ SHAPES = [  # (nx, ny, ld, iters): odd/even nx, nx not a multiple of the 64-col 
 
 
 @pytest.mark.parametrize("nx,ny,ld,iters", SHAPES)
-@pytest.mark.parametrize("tblock", [0, 1, 2, 4, 6, 8])
+@pytest.mark.parametrize("tblock", [0, 1, 2, 4, 6, 8, 10])
 def test_ragged_shapes(cuda_lib, nx, ny, ld, iters, tblock):
     a = si.jacobi2d_grid(nx, ny, ld=ld)
     want = oracle.jacobi2d(a, iters, nx=nx)
@@ -55,7 +55,7 @@ def test_ragged_shapes(cuda_lib, nx, ny, ld, iters, tblock):
     assert np.all(np.isnan(pad)) if in_b else np.array_equal(pad, a[:, nx + 2:])
 
 
-@pytest.mark.parametrize("tblock", [2, 4, 6, 8])
+@pytest.mark.parametrize("tblock", [2, 4, 6, 8, 10])
 @pytest.mark.parametrize("iters", [1, 2, 3, 5, 8, 13, 17, 33])
 def test_temporal_blocking_equals_single_sweeps(cuda_lib, tblock, iters):
     # T sweeps per HBM pass is bitwise T single sweeps, for every remainder/parity
@@ -107,7 +107,7 @@ def c2_case():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("tblock", [1, 0, 4, 8])
+@pytest.mark.parametrize("tblock", [1, 0, 4, 8, 10])
 def test_C2_full_size_10_sweeps(cuda_lib, c2_case, tblock):
     # configs[1] grid (16384^2 interior), 10 sweeps, every element vs the oracle,
     # in the launch configurations bench.py times (tblock=0 = auto)

@@ -1,6 +1,11 @@
 # scratch GPU step (edited per experiment); run under gpurun from the repo root
-OUT=gpurun_out/${TAG:-r2g}; mkdir -p $OUT
+OUT=gpurun_out/${TAG:-r2l}; mkdir -p $OUT
 make -j8 all > $OUT/build.log 2>&1 || { tail -20 $OUT/build.log; exit 1; }
-PYTHONFAULTHANDLER=1 CUDA_DEVICE_MAX_CONNECTIONS=32 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 \
-  bench.py --gpus 2 --same-gpu --steps 1 --warmup 3 --sweeps 16 --pw-apps 2 --scale-steps 1 --j3-sweeps 6 --no-e2e --no-cpu > $OUT/n2.out 2> $OUT/n2.err
-echo "rc=$?"; tail -c 1500 $OUT/n2.out; grep -v "^\s*$" $OUT/n2.err | grep -A25 "Fatal\|Error\|error" | head -60
+timeout 900 python -m pytest tests/test_gpu_jacobi.py -x -q > $OUT/pytest.log 2>&1; echo "pytest rc=$?"; tail -2 $OUT/pytest.log
+q() { python -c "import json,sys;d=json.load(open('$1'));print(d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'], d['clocks']['reasons'], d['clocks'].get('power_w_median'))" 2>&1 | tail -1; }
+i=0
+for cfg in ST_JACOBI_TB4_EDGE_COST=280 ST_JACOBI_TB4_EDGE_COST=350 ST_JACOBI_TB4_EDGE_COST=450 ST_JACOBI_TB4_EDGE_COST=280; do
+  i=$((i+1))
+  env $(echo $cfg | tr ',' ' ') timeout 300 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu --no-pw --no-j3 --no-gs --no-generic --no-scaling > $OUT/t_$i.json 2>$OUT/t_$i.err
+  echo "$cfg: $(q $OUT/t_$i.json)"
+done

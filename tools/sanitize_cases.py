@@ -9,7 +9,9 @@ import torch
 import paper_2310_01882_b200 as st
 import stencil_inputs as si
 
-for nx, ny, iters, tb in ((64, 64, 5, 0), (130, 70, 3, 1), (130, 70, 5, 2), (130, 1100, 9, 4), (61, 37, 8, 8)):
+# (500, 400, 16, 8) etc.: interior strips with enough rows for the rotated-register blocks
+for nx, ny, iters, tb in ((64, 64, 5, 0), (130, 70, 3, 1), (130, 70, 5, 2), (130, 1100, 9, 4), (61, 37, 8, 8),
+                          (500, 400, 16, 8), (400, 300, 12, 6), (300, 200, 8, 4), (300, 200, 6, 2)):
     a = torch.from_numpy(si.jacobi2d_grid(nx, ny)).cuda()
     b = torch.empty_like(a)
     st.st_jacobi2d_run(a, b, iters, tblock=tb)
