@@ -668,7 +668,7 @@ def gs_leg(ctx):
     args, st, torch = ctx.args, ctx.st, ctx.torch
     ngs = C2_N
     ags = torch.from_numpy(si.jacobi2d_grid(ngs, ngs)).to(ctx.dev)
-    ws = torch.empty(int(st.lib().st_gauss_seidel2d_workspace_bytes(ngs)) // 8 + 1, dtype=torch.int64,
+    ws = torch.empty(int(st.lib().st_gauss_seidel2d_workspace_bytes(ngs, ngs)) // 8 + 1, dtype=torch.int64,
                      device=ctx.dev)
     st.st_gauss_seidel2d_run(ags, 1, workspace=ws)  # warm-up (module load)
     l0 = st.launch_count()

@@ -360,11 +360,15 @@ st_status st_pw_fused_expression(double tcx, double tcy, int32_t which, char* ou
  * Dirichlet): rows in increasing y, columns in increasing x, each point
  *     a[y][x] = (((a[y-1][x] + a[y+1][x]) + a[y][x-1]) + a[y][x+1]) * 0.25
  * with the values the sequential loop sees (N, W already updated). Bitwise the
- * sequential loop nest. `workspace` = st_gauss_seidel2d_workspace_bytes(ny)
- * bytes of caller-owned device memory (progress words of the wavefront).
- * ST_ENOTSUP if ceil(ny/32) warps cannot all be resident on the device; the
- * launch is cooperative (co-residency guaranteed by the driver, or ST_ECUDA). */
-int64_t st_gauss_seidel2d_workspace_bytes(int64_t ny);
+ * sequential loop nest. `workspace` = st_gauss_seidel2d_workspace_bytes(nx, ny)
+ * bytes of caller-owned device memory (progress words of the wavefront and, for
+ * the multi-sweep schedule, one edge row per strip: ~32 B x (nx+2) x ny/29).
+ * Grids at least 224 columns wide run K = 4 sweeps per pass over the grid
+ * (strips of 29 rows; ST_GS_MS_K = 1..4 overrides K, ST_GS_MS=0 disables it),
+ * narrower ones one sweep per pass (strips of 32 rows). ST_ENOTSUP if the
+ * strips cannot all be resident on the device; the launch is cooperative
+ * (co-residency guaranteed by the driver, or ST_ECUDA). */
+int64_t st_gauss_seidel2d_workspace_bytes(int64_t nx, int64_t ny);
 st_status st_gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters, void* workspace,
                                 int64_t workspace_bytes, void* cuda_stream);
 

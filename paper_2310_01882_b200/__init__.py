@@ -98,7 +98,7 @@ _SIGS = {
     "st_jacobi3d_run": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i64, _i32, _vp, _vp,
                                        ctypes.POINTER(_i32)]),
     "st_selftest_div6": (ctypes.c_int, [_vp, _i64, _vp, _vp]),
-    "st_gauss_seidel2d_workspace_bytes": (ctypes.c_int64, [_i64]),
+    "st_gauss_seidel2d_workspace_bytes": (ctypes.c_int64, [_i64, _i64]),
     "st_gauss_seidel2d_run": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp]),
     "st_comm_set_grid": (ctypes.c_int, [_vp, _i32, _i64]),
     "st_pencil_split": (ctypes.c_int, [_i64, _i64, _i32, _i32, _i32] + [ctypes.POINTER(_i64)] * 4),
@@ -444,7 +444,7 @@ def st_gauss_seidel2d_run(a, iters: int, nx: int | None = None, workspace=None, 
         raise ValueError("a: 2-D row-major tensor")
     ny, ld = a.shape[0] - 2, a.stride(0)
     nx = a.shape[1] - 2 if nx is None else nx
-    need = int(lib().st_gauss_seidel2d_workspace_bytes(ny))
+    need = int(lib().st_gauss_seidel2d_workspace_bytes(nx, ny))
     if workspace is None:
         workspace = torch.empty(max(1, need // 8), dtype=torch.int64, device=a.device)
     _check(lib().st_gauss_seidel2d_run(a.data_ptr(), nx, ny, ld, iters, workspace.data_ptr(),

@@ -342,23 +342,24 @@ st_status st_stencil3d_fused_run(const double* const* inputs, int32_t nin, doubl
                              static_cast<cudaStream_t>(cuda_stream));
 }
 
-int64_t st_gauss_seidel2d_workspace_bytes(int64_t ny) { return ny < 1 ? 0 : gauss_seidel2d_workspace_bytes(ny); }
+int64_t st_gauss_seidel2d_workspace_bytes(int64_t nx, int64_t ny) {
+  return nx < 1 || ny < 1 ? 0 : gauss_seidel2d_workspace_bytes(nx, ny);
+}
 
 st_status st_gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters, void* workspace,
                                 int64_t workspace_bytes, void* cuda_stream) {
   clear_error();
   ST_RETURN_IF(!a || !workspace, ST_EINVAL, "st_gauss_seidel2d_run: null pointer");
   ST_RETURN_IF(nx < 1 || ny < 1 || ld < nx + 2 || iters < 0, ST_EINVAL, "st_gauss_seidel2d_run: bad extents");
-  ST_RETURN_IF(workspace_bytes < gauss_seidel2d_workspace_bytes(ny), ST_EINVAL,
+  ST_RETURN_IF(workspace_bytes < gauss_seidel2d_workspace_bytes(nx, ny), ST_EINVAL,
                "st_gauss_seidel2d_run: workspace of %lld bytes < %lld", (long long)workspace_bytes,
-               (long long)gauss_seidel2d_workspace_bytes(ny));
+               (long long)gauss_seidel2d_workspace_bytes(nx, ny));
   ST_RETURN_IF(overlaps(a, (size_t)(ny + 2) * (size_t)ld * sizeof(double), workspace, (size_t)workspace_bytes),
                ST_EINVAL, "st_gauss_seidel2d_run: workspace overlaps the field");
   ST_TRY(check_device_ptr(a, "a"));
   ST_TRY(check_device_ptr(workspace, "workspace"));
   if (iters == 0) return ST_OK;
-  return gauss_seidel2d_run(a, nx, ny, ld, iters, static_cast<unsigned long long*>(workspace),
-                            static_cast<cudaStream_t>(cuda_stream));
+  return gauss_seidel2d_run(a, nx, ny, ld, iters, workspace, static_cast<cudaStream_t>(cuda_stream));
 }
 
 st_status st_selftest_div6(const double* x, int64_t n, unsigned long long* mismatches, void* cuda_stream) {

@@ -352,9 +352,11 @@ __global__ void __launch_bounds__(32)
 
 }  // namespace
 
-st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters,
-                             unsigned long long* progress, cudaStream_t s) {
+st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters, void* workspace,
+                             cudaStream_t s) {
   ST_RETURN_IF(nx > (1 << 30), ST_ENOTSUP, "gauss_seidel2d: nx = %lld > 2^30", (long long)nx);
+  if (gauss_seidel2d_ms_supported(nx, ny)) return gauss_seidel2d_ms_run(a, nx, ny, ld, iters, workspace, s);
+  unsigned long long* progress = static_cast<unsigned long long*>(workspace);
   const int64_t nstrips = (ny + 31) / 32;
   // the tiled kernel moves 16-byte row chunks: even pitch, 16-byte aligned base
   static const int kVariant = env_int("ST_GS_TILED", 1);
@@ -393,7 +395,10 @@ st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int6
   return ST_OK;
 }
 
-int64_t gauss_seidel2d_workspace_bytes(int64_t ny) { return 2 * ((ny + 31) / 32) * 8; }
+int64_t gauss_seidel2d_workspace_bytes(int64_t nx, int64_t ny) {
+  const int64_t single = 2 * ((ny + 31) / 32) * 8;
+  return gauss_seidel2d_ms_supported(nx, ny) ? std::max(single, gauss_seidel2d_ms_workspace_bytes(nx, ny)) : single;
+}
 
 st_status gauss_seidel2d_preload() {
   cudaFuncAttributes fa;
@@ -404,7 +409,7 @@ st_status gauss_seidel2d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_tiled_kernel<2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_tiled_kernel<4>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_tiled_kernel<8>));
-  return ST_OK;
+  return gauss_seidel2d_ms_preload();
 }
 
 }  // namespace st

@@ -78,12 +78,19 @@ st_status jacobi3d_copy_faces(const double* src, double* dst, int64_t nx, int64_
                               int64_t z_hi, cudaStream_t s);
 
 // ------------------------------------------------------------ Gauss-Seidel 2-D ---
-// `iters` in-place lexicographic sweeps (Listing 1 literally); `progress` =
-// gauss_seidel2d_workspace_bytes(ny) of device scratch.
-st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters,
-                             unsigned long long* progress, cudaStream_t s);
-int64_t gauss_seidel2d_workspace_bytes(int64_t ny);
+// `iters` in-place lexicographic sweeps (Listing 1 literally); `workspace` =
+// gauss_seidel2d_workspace_bytes(nx, ny) of device scratch.
+st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters, void* workspace,
+                             cudaStream_t s);
+int64_t gauss_seidel2d_workspace_bytes(int64_t nx, int64_t ny);
 st_status gauss_seidel2d_preload();
+// multi-sweep wavefront (gauss_seidel2d_ms.cu): K sweeps in flight per warp
+int gauss_seidel2d_ms_depth();
+bool gauss_seidel2d_ms_supported(int64_t nx, int64_t ny);
+int64_t gauss_seidel2d_ms_workspace_bytes(int64_t nx, int64_t ny);
+st_status gauss_seidel2d_ms_run(double* a, int64_t nx, int64_t ny, int64_t ld, int64_t iters, void* workspace,
+                                cudaStream_t s);
+st_status gauss_seidel2d_ms_preload();
 
 // ------------------------------------------------------------ PW 3-D ---
 struct PwArgs {
