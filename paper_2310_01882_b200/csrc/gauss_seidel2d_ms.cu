@@ -61,16 +61,18 @@ namespace st {
 namespace {
 
 constexpr int kMsStrips = 4;          // strips (compute warps) per CTA; warps 4..7 are the helpers
-constexpr int kMsSlots = 5;           // 32-column tiles in flight per strip
-constexpr int kMsNP = 32 * kMsSlots;  // ring positions per row
+constexpr int kMsTW = 16;             // tile width (columns) = steps per compute group
+constexpr int kMsSlots = 10;          // tiles in the ring per strip
+constexpr int kMsNP = kMsTW * kMsSlots;  // ring positions per row
 constexpr int kMsP = 2;               // shared-memory prefetch distance (steps)
 constexpr int kMsProgStride = 16;     // u64 per progress word (one 128-byte line each)
-constexpr int kMsMinTiles = 12;       // narrower grids take the single-sweep kernel (helper/compute coupling)
+constexpr int kMsMinTiles = 24;       // narrower grids take the single-sweep kernel (helper/compute coupling)
+constexpr int kMsL2Ahead = 8;         // tiles prefetched into L2 ahead of their load
 constexpr int kMsEdgePad = 8;         // edge entries per strip: columns 0 .. nx + 2K - 2 (< nx + 8)
 
 template <int KC>
 struct MsGeo {
-  static constexpr int kEntD = KC == 3 ? 4 : KC;  // doubles per edge entry (16-byte multiple for KC >= 2)
+  static constexpr int kEntD = KC == 1 ? 2 : KC == 3 ? 4 : KC;  // doubles per edge entry (a 16-byte multiple)
   static constexpr int EB = 8 * kEntD;
   static constexpr int MIR = kMsP + 2 * KC + 1;    // mirrored tail of a tile row (reads reach base+31+P+2KC-2)
   static constexpr int L = (kMsNP + MIR + 1) | 1;  // row length in doubles, odd: conflict-free column access
@@ -82,9 +84,11 @@ struct MsGeo {
   static constexpr int STAGE_OFF = ABOVE_OFF + ABOVE_B;
   static constexpr int STAGE_B = kMsNP * EB;
   static constexpr int BAR_OFF = STAGE_OFF + STAGE_B;
-  static constexpr int STRIP_B = (BAR_OFF + 3 * kMsSlots * 8 + 127) / 128 * 128;
+  static constexpr int STRIP_B = (BAR_OFF + (3 * kMsSlots + 1) * 8 + 127) / 128 * 128;
   static constexpr int CTA_B = kMsStrips * STRIP_B;
-  static constexpr int kLagT = KC <= 2 ? 1 : 2;    // a tile is finished kLagT groups after its own
+  // a tile is finished (results of its columns final, its edge entries staged)
+  // kLagT groups after its own: stores of step k reach back to column k - 28 - 2KC
+  static constexpr int kLagT = (27 + 2 * KC) / kMsTW + 1;
   static constexpr int SH = 2 * KC;                // S history ring (the sd lane's S_j = S_0 of step k - 2j)
   static constexpr int DR = 2 * KC - 2;            // ring offset of chain 0's reads (E, S) from the step
 };
@@ -145,6 +149,27 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return done != 0;
 }
+// Helper-warp waits must not take issue slots from the compute warp on the same
+// SMSP. __nanosleep measured ineffective here (a test + nanosleep(256) loop ran
+// every ~5 ns); mbarrier.try_wait with a suspend-time hint parks the warp in
+// hardware until the phase completes or the hint elapses.
+__device__ __forceinline__ bool mbar_try_hint(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_try_hint(bar, parity, ns)) {
+  }
+}
+// Sleeps up to ns: a try_wait on a barrier phase that never completes.
+__device__ __forceinline__ void park_ns(uint64_t* never, uint32_t ns) { (void)mbar_try_hint(never, 0, ns); }
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -219,14 +244,23 @@ __device__ __forceinline__ void ms_prefetch(MsState<KC>& S, const uint32_t gt, c
 
 // One group of 32 steps (k = k0 .. k0+31); gt/ga/gs = this lane's tile row, the
 // above ring and the staging ring at the group's base position.
-// gtp = the previous group's tile row base: chain KC-1's result of step d goes to
-// ring position base + d - 1 (d = 0: the previous group's base + 31).
+// One group of kMsTW steps (k = k0 .. k0+TW-1); gt/ga/gs = this lane's tile
+// row, the above ring and the staging ring at the group's base position. Chain
+// KC-1's result of step d goes to ring position base + d - 1; gst0 = the address
+// for d = 0 (the last position of the previous group's slot).
+#ifndef ST_GS_MS_UNROLL
+#define ST_GS_MS_UNROLL 16
+#endif
+constexpr int kMsHalf = ST_GS_MS_UNROLL;  // steps per unrolled body (a group runs TW / kMsHalf bodies):
+                                          // small bodies keep the compute loop in the instruction cache
+static_assert(kMsTW % kMsHalf == 0, "whole bodies per group");
 template <int KC, bool kChk>
-__device__ __forceinline__ void ms_group(MsState<KC>& S, const uint32_t gt, const uint32_t gtp, const uint32_t ga,
+__device__ __forceinline__ void ms_group(MsState<KC>& S, const uint32_t gt, const uint32_t gst0, const uint32_t ga,
                                          const uint32_t gs, const int k0, const MsLane& L) {
   using G = MsGeo<KC>;
+  static_assert(kMsHalf % kMsP == 0, "prefetch slots must line up across halves");
 #pragma unroll
-  for (int d = 0; d < 32; ++d) {
+  for (int d = 0; d < kMsHalf; ++d) {
     const int k = k0 + d;
     const int q = d % kMsP;
     const double e0 = S.pe[q], s0 = S.ps[q];
@@ -266,7 +300,7 @@ __device__ __forceinline__ void ms_group(MsState<KC>& S, const uint32_t gt, cons
       const int c = k + 2 - L.R;
       pstg = pstg && c >= 0 && c <= L.nx + 2 * KC - 2;
     }
-    sts1_if(pst, d == 0 ? gtp + 31u * 8u : gt + (uint32_t)(d - 1) * 8u, v[KC - 1]);
+    sts1_if(pst, d == 0 ? gst0 : gt + (uint32_t)(d - 1) * 8u, v[KC - 1]);
     // edge entry (v_0[c], v_1[c-2], ...) of column c = k + 2 - R (lane R-1 only)
     const uint32_t os = gs + (uint32_t)d * G::EB;
     if (KC == 1) {
@@ -276,10 +310,10 @@ __device__ __forceinline__ void ms_group(MsState<KC>& S, const uint32_t gt, cons
       for (int j = 0; j < KC; j += 2) sts2_if(pstg, os + 8 * j, v[j], j + 1 < KC ? v[j + 1] : 0.0);
     }
   }
-  if (32 % G::SH != 0) {  // re-align the S history ring to the next group's step numbering
+  if (kMsHalf % G::SH != 0) {  // re-align the S history ring to the next half's step numbering
     double t[G::SH];
 #pragma unroll
-    for (int i = 0; i < G::SH; ++i) t[i] = S.sh[(i + 32) % G::SH];
+    for (int i = 0; i < G::SH; ++i) t[i] = S.sh[(i + kMsHalf) % G::SH];
 #pragma unroll
     for (int i = 0; i < G::SH; ++i) S.sh[i] = t[i];
   }
@@ -318,7 +352,7 @@ __device__ __forceinline__ void ms_compute(const MsArgs& A, unsigned char* sm, c
     for (int j = 0; j < KC; ++j) S.pa[q][j] = 0.0;
   }
   const int ntiles = A.ntiles;
-  const int ngroups = (A.nx + 2 * KC + 29 + 31) / 32;  // steps 0 .. nx + 2KC + 28
+  const int ngroups = (A.nx + 2 * KC + 29 + kMsTW - 1) / kMsTW;  // steps 0 .. nx + 2KC + 28
   const int64_t Ttot = A.passes * ntiles;
   for (int64_t p = 0; p < A.passes; ++p) {
     const int64_t T0 = p * ntiles;
@@ -328,20 +362,26 @@ __device__ __forceinline__ void ms_compute(const MsArgs& A, unsigned char* sm, c
 #pragma unroll
     for (int j = 0; j < KC; ++j) S.res[j] = L.w0;
     {  // prologue: steps 0 .. P-1 from the group-0 base
-      const uint32_t b = (uint32_t)(T0 % kMsSlots) * 32u;
+      const uint32_t b = (uint32_t)(T0 % kMsSlots) * kMsTW;
 #pragma unroll
       for (int i = 0; i < kMsP; ++i) ms_prefetch<KC, true>(S, tbase + b * 8u, abase + b * G::EB, i, i, L);
     }
     for (int g = 0; g < ngroups; ++g) {
       const int64_t Gi = T0 + g;
       if (Gi + 1 < Ttot) mbar_wait_parity(&loaded[(Gi + 1) % kMsSlots], (uint32_t)(((Gi + 1) / kMsSlots) & 1));
-      const uint32_t b = (uint32_t)(Gi % kMsSlots) * 32u;
-      const uint32_t bp = (uint32_t)((Gi + kMsSlots - 1) % kMsSlots) * 32u;
-      const uint32_t gt = tbase + b * 8u, gtp = tbase + bp * 8u, ga = abase + b * G::EB, gs = sbase + b * G::EB;
-      if (g <= 1 || 32 * g + 31 >= A.nx)
-        ms_group<KC, true>(S, gt, gtp, ga, gs, 32 * g, L);
-      else
-        ms_group<KC, false>(S, gt, gtp, ga, gs, 32 * g, L);
+      const uint32_t b = (uint32_t)(Gi % kMsSlots) * kMsTW;
+      const uint32_t bp = (uint32_t)((Gi + kMsSlots - 1) % kMsSlots) * kMsTW;
+      // unchecked when every lane and chain stays inside columns 1..nx for the whole group
+      const bool chk = kMsTW * g < 2 * KC + 29 || kMsTW * (g + 1) > A.nx;
+#pragma unroll 1
+      for (int h = 0; h < kMsTW; h += kMsHalf) {
+        const uint32_t gt = tbase + (b + h) * 8u, ga = abase + (b + h) * G::EB, gs = sbase + (b + h) * G::EB;
+        const uint32_t gst0 = h == 0 ? tbase + (bp + kMsTW - 1) * 8u : gt - 8u;
+        if (chk)
+          ms_group<KC, true>(S, gt, gst0, ga, gs, kMsTW * g + h, L);
+        else
+          ms_group<KC, false>(S, gt, gst0, ga, gs, kMsTW * g + h, L);
+      }
       const int td = g - G::kLagT;
       if (td >= 0 && td < ntiles) {
         __syncwarp();
@@ -370,11 +410,12 @@ __device__ __forceinline__ void ms_load_tile(const MsArgs& A, unsigned char* sm,
   const int m = (int)(t % A.ntiles);
   const int64_t y0 = 1 + (int64_t)I * A.R;
   const int rows = (int)min((int64_t)33, A.ny + 2 - y0);
-  if (wide) {  // lanes 0..15: column pair 2*lane of row rho; lanes 16..31: the same of row rho + 1
-    const int c = 32 * m + 2 * (lane & 15);
+  constexpr int kPairs = kMsTW / 2, kRowsW = 32 / kPairs;  // wide: lanes per row, rows per warp op
+  if (wide) {  // lane: column pair 2 * (lane % kPairs) of row lane / kPairs (+ kRowsW per op)
+    const int cc = 2 * (lane % kPairs), c = kMsTW * m + cc;
     if (c <= A.nx + 1) {
-      for (int rho = lane >> 4; rho < rows; rho += 2) {
-        const int pos = ms_mod(32 * t + c - 32 * m + rho + 2 * KC - 4);
+      for (int rho = lane / kPairs; rho < rows; rho += kRowsW) {
+        const int pos = ms_mod(kMsTW * t + cc + rho + 2 * KC - 4);
         const uint32_t dst = s0 + (uint32_t)rho * G::ROWB + (uint32_t)pos * 8u;
         const double* gp = A.a + (y0 + rho) * A.ld + c;
         cp16(dst, gp);  // at pos = NP-1 the second value lands on the mirror of position 0 ...
@@ -382,25 +423,23 @@ __device__ __forceinline__ void ms_load_tile(const MsArgs& A, unsigned char* sm,
         if (pos == kMsNP - 1) cp8(s0 + (uint32_t)rho * G::ROWB, gp + 1);  // ... and position 0 itself
       }
     }
-  } else {
-    const int c = 32 * m + lane;
+  } else {  // lane: column lane % TW of row lane / TW (+ 32 / TW per op)
+    const int cc = lane % kMsTW, c = kMsTW * m + cc;
     if (c <= A.nx + 1) {
-      int pos = ms_mod(32 * t + lane + 2 * KC - 4);
-      const double* gp = A.a + y0 * A.ld + c;
-      for (int rho = 0; rho < rows; ++rho) {
+      for (int rho = lane / kMsTW; rho < rows; rho += 32 / kMsTW) {
+        const int pos = ms_mod(kMsTW * t + cc + rho + 2 * KC - 4);
         const uint32_t dst = s0 + (uint32_t)rho * G::ROWB + (uint32_t)pos * 8u;
+        const double* gp = A.a + (y0 + rho) * A.ld + c;
         cp8(dst, gp);
         if (pos < G::MIR) cp8(dst + kMsNP * 8, gp);
-        gp += A.ld;
-        pos = pos + 1 == kMsNP ? 0 : pos + 1;
       }
     }
   }
   // above entries of column c (lane 0's chain j reads entry x_j + 2j <= nx + 2KC - 2): row 0
   // for the first strip, else the strip above's edge
-  const int c = 32 * m + lane;
-  if (c <= A.nx + 2 * KC - 2) {
-    const int pa = ms_mod(32 * t + lane);
+  const int c = kMsTW * m + lane;
+  if (lane < kMsTW && c <= A.nx + 2 * KC - 2) {
+    const int pa = ms_mod(kMsTW * t + lane);
     const uint32_t dst = s0 + G::ABOVE_OFF + (uint32_t)pa * G::EB;
     if (I == 0) {
 #pragma unroll
@@ -412,15 +451,10 @@ __device__ __forceinline__ void ms_load_tile(const MsArgs& A, unsigned char* sm,
       }
     } else {
       const char* src = A.edge + (int64_t)(I - 1) * A.edge_stride + (int64_t)c * G::EB;
-      if (KC == 1) {
-        cp8(dst, src);
-        if (pa < G::MIRA) cp8(dst + kMsNP * G::EB, src);
-      } else {
 #pragma unroll
-        for (int j = 0; j < G::EB; j += 16) {
-          cp16(dst + j, src + j);
-          if (pa < G::MIRA) cp16(dst + kMsNP * G::EB + j, src + j);
-        }
+      for (int j = 0; j < G::EB; j += 16) {  // 16-byte copies bypass L1: never a stale line
+        cp16(dst + j, src + j);
+        if (pa < G::MIRA) cp16(dst + kMsNP * G::EB + j, src + j);
       }
     }
   }
@@ -437,11 +471,12 @@ __device__ __forceinline__ void ms_writeback_tile(const MsArgs& A, unsigned char
   const int64_t y0 = 1 + (int64_t)I * A.R;
   const bool last = I == A.nstrips - 1;
   const int nreal = last ? (int)(A.ny - y0 + 1) : A.R;
+  constexpr int kPairs = kMsTW / 2, kRowsW = 32 / kPairs;
   if (wide) {  // pairs (c, c+1), c even: column 0 / nx+1 in a pair are written back unchanged (Dirichlet)
-    const int c = 32 * m + 2 * (lane & 15);
+    const int cc = 2 * (lane % kPairs), c = kMsTW * m + cc;
     if (c <= A.nx) {
-      for (int rho = lane >> 4; rho < nreal; rho += 2) {
-        const int pos = ms_mod(32 * t + c - 32 * m + rho + 2 * KC - 4);
+      for (int rho = lane / kPairs; rho < nreal; rho += kRowsW) {
+        const int pos = ms_mod(kMsTW * t + cc + rho + 2 * KC - 4);
         const uint32_t row = s0 + (uint32_t)rho * G::ROWB;
         double2 v;
         if (pos == kMsNP - 1) {  // the pair wraps: results live at the canonical positions NP-1 and 0
@@ -454,27 +489,20 @@ __device__ __forceinline__ void ms_writeback_tile(const MsArgs& A, unsigned char
       }
     }
   } else {
-    const int c = 32 * m + lane;
+    const int cc = lane % kMsTW, c = kMsTW * m + cc;
     if (c >= 1 && c <= A.nx) {
-      int pos = ms_mod(32 * t + lane + 2 * KC - 4);
-      double* gp = A.a + y0 * A.ld + c;
-      for (int rho = 0; rho < nreal; ++rho) {
-        *gp = lds1(s0 + (uint32_t)rho * G::ROWB + (uint32_t)pos * 8u);
-        gp += A.ld;
-        pos = pos + 1 == kMsNP ? 0 : pos + 1;
+      for (int rho = lane / kMsTW; rho < nreal; rho += 32 / kMsTW) {
+        const int pos = ms_mod(kMsTW * t + cc + rho + 2 * KC - 4);
+        A.a[(y0 + rho) * A.ld + c] = lds1(s0 + (uint32_t)rho * G::ROWB + (uint32_t)pos * 8u);
       }
     }
   }
-  const int c = 32 * m + lane;
-  if (!last && c >= 1 && c <= A.nx + 2 * KC - 2) {  // edge entries of column c for the strip below
-    const uint32_t src = s0 + G::STAGE_OFF + (uint32_t)ms_mod(32 * t + lane + A.R - 2) * G::EB;
+  const int c = kMsTW * m + lane;
+  if (!last && lane < kMsTW && c >= 1 && c <= A.nx + 2 * KC - 2) {  // edge entries of column c for the strip below
+    const uint32_t src = s0 + G::STAGE_OFF + (uint32_t)ms_mod(kMsTW * t + lane + A.R - 2) * G::EB;
     char* dst = A.edge + (int64_t)I * A.edge_stride + (int64_t)c * G::EB;
-    if (KC == 1) {
-      *reinterpret_cast<double*>(dst) = lds1(src);
-    } else {
 #pragma unroll
-      for (int j = 0; j < G::EB; j += 16) *reinterpret_cast<double2*>(dst + j) = lds2(src + j);
-    }
+    for (int j = 0; j < G::EB; j += 16) *reinterpret_cast<double2*>(dst + j) = lds2(src + j);
   }
 }
 
@@ -489,19 +517,39 @@ __device__ __forceinline__ void ms_loader(const MsArgs& A, unsigned char* sm, co
   const int64_t Ttot = A.passes * A.ntiles;
   const unsigned long long* up = I > 0 ? A.prog + (int64_t)(I - 1) * kMsProgStride : nullptr;
   const unsigned long long* dn = I + 1 < A.nstrips ? A.prog + (int64_t)(I + 1) * kMsProgStride : nullptr;
+  const int64_t y0 = 1 + (int64_t)I * A.R;
+  const int prow = (int)min((int64_t)33, A.ny + 2 - y0);  // rows of a tile
+  unsigned long long acq_up = 0, acq_dn = 0;
+  uint64_t* never = reinterpret_cast<uint64_t*>(sm + G::BAR_OFF) + 3 * kMsSlots;  // never arrived on
   for (int64_t t = 0; t < Ttot; ++t) {
-    if (t >= kMsSlots) mbar_wait_parity(&freed[t % kMsSlots], (uint32_t)((t / kMsSlots - 1) & 1));
+    // pull tile t + kMsL2Ahead into L2 now (the rows last written a pass ago are in HBM);
+    // if the strip below has not written its part back yet this only wastes bandwidth
+    if (t + kMsL2Ahead < Ttot) {  // one 128-byte line per row and tile
+      const int c = kMsTW * (int)((t + kMsL2Ahead) % A.ntiles);
+      if (lane < prow && c <= A.nx + 1)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.a + (y0 + lane) * A.ld + c) : "memory");
+      if (lane == 0 && prow == 33 && c <= A.nx + 1)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.a + (y0 + 32) * A.ld + c) : "memory");
+    }
     const unsigned long long need_up = (unsigned long long)(t + 1);
     const int64_t need_dn = t - A.ntiles + 1;
     const bool wu = up != nullptr, wd = dn != nullptr && need_dn > 0;
-    bool ok = (!wu || ld_relaxed(up) >= need_up) && (!wd || ld_relaxed(dn) >= (unsigned long long)need_dn);
-    while (!__all_sync(0xffffffffu, ok)) {
-      __nanosleep(32);
-      ok = (!wu || ld_relaxed(up) >= need_up) && (!wd || ld_relaxed(dn) >= (unsigned long long)need_dn);
+    // progress seen by the last acquire covers this tile: no new acquire (with 16-byte
+    // copies everything bypasses L1); 8-byte copies go through L1, so they acquire per
+    // tile (its L1 invalidation drops stale lines)
+    const bool have = wide && (!wu || acq_up >= need_up) && (!wd || acq_dn >= (unsigned long long)need_dn);
+    if (!have) {
+      bool ok = (!wu || ld_relaxed(up) >= need_up) && (!wd || ld_relaxed(dn) >= (unsigned long long)need_dn);
+      while (!__all_sync(0xffffffffu, ok)) {
+        park_ns(never, 256);
+        ok = (!wu || ld_relaxed(up) >= need_up) && (!wd || ld_relaxed(dn) >= (unsigned long long)need_dn);
+      }
+      // acquire (taken before the slot wait, so its latency overlaps it)
+      if (wu) acq_up = ld_acquire(up);
+      if (wd) acq_dn = ld_acquire(dn);
+      if (!wu && !wd) (void)ld_acquire(A.prog + (int64_t)I * kMsProgStride);
     }
-    // one acquire per tile: orders the copies after the flags and drops stale L1
-    // lines (the 8-byte copies go through L1)
-    (void)ld_acquire(wu ? up : wd ? dn : A.prog + (int64_t)I * kMsProgStride);
+    if (t >= kMsSlots) mbar_wait_sleep(&freed[t % kMsSlots], (uint32_t)((t / kMsSlots - 1) & 1), 1000);
     ms_load_tile<KC>(A, sm, I, lane, t, wide);
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -509,7 +557,7 @@ __device__ __forceinline__ void ms_loader(const MsArgs& A, unsigned char* sm, co
 
 // Storer warp: writes finished tiles back, frees their slots, and publishes
 // progress (one GPU-scope fence per kMsPub tiles and at the end).
-constexpr int kMsPub = 2;
+constexpr int kMsPub = 4;
 template <int KC>
 __device__ __forceinline__ void ms_storer(const MsArgs& A, unsigned char* sm, const int I, const int lane,
                                           const bool wide) {
@@ -519,7 +567,7 @@ __device__ __forceinline__ void ms_storer(const MsArgs& A, unsigned char* sm, co
   const int64_t Ttot = A.passes * A.ntiles;
   unsigned long long* mine = A.prog + (int64_t)I * kMsProgStride;
   for (int64_t t = 0; t < Ttot; ++t) {
-    mbar_wait_parity(&consumed[t % kMsSlots], (uint32_t)((t / kMsSlots) & 1));
+    mbar_wait_sleep(&consumed[t % kMsSlots], (uint32_t)((t / kMsSlots) & 1), 1000);
     ms_writeback_tile<KC>(A, sm, I, lane, t, wide);
     __syncwarp();  // every lane's shared reads of the tile are done (their values are in the stores)
     if (lane == 0) mbar_arrive(&freed[t % kMsSlots]);
@@ -538,7 +586,10 @@ __global__ void __launch_bounds__(96 * kMsStrips, 1) gauss_seidel2d_ms_kernel(co
   // the role is warp-uniform; broadcasting it lets the compiler see that, so the
   // shuffles of the compute loop stay plain SHFL (no collective emulation)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int s = warp % kMsStrips, role = warp / kMsStrips;  // 0 compute, 1 loader, 2 storer
+  // the SMSP arbiter favours the highest warp id among eligible warps, so the compute
+  // warps take the top ids (8..11) and win every cycle they are eligible against a
+  // helper polling on the same SMSP (warps 0..3 load, 4..7 store)
+  const int s = warp % kMsStrips, role = (2 - warp / kMsStrips + 3) % 3;  // 0 compute, 1 loader, 2 storer
   const int I = blockIdx.x * kMsStrips + s;
   unsigned char* sm = ms_smem + s * G::STRIP_B;
   if (role == 1 && lane == 0 && I < A.nstrips) {
@@ -548,11 +599,14 @@ __global__ void __launch_bounds__(96 * kMsStrips, 1) gauss_seidel2d_ms_kernel(co
       mbar_init(&bars[kMsSlots + q], 1);      // consumed: the compute warp's lane 0
       mbar_init(&bars[2 * kMsSlots + q], 1);  // freed: the storer's lane 0
     }
+    mbar_init(&bars[3 * kMsSlots], 1);  // never arrived on: the loader's sleep
     fence_mbar_init();
   }
   __syncthreads();
   if (I >= A.nstrips) return;
-  const bool wide = (KC % 2 == 0) && (A.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(A.a) & 15) == 0);
+  // 16-byte tile copies: even pitch, aligned base (with the rotation c + rho + 2KC - 4, an even
+  // column c lands on a 16-byte aligned ring address in every row, for every KC)
+  const bool wide = (A.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(A.a) & 15) == 0);
   if (role == 0)
     ms_compute<KC>(A, sm, I, lane);
   else if (role == 1)
@@ -590,7 +644,7 @@ int gauss_seidel2d_ms_depth() {
 
 bool gauss_seidel2d_ms_supported(int64_t nx, int64_t ny) {
   const int K = gauss_seidel2d_ms_depth();
-  const int64_t ntiles = (nx + 2 + 31) / 32;
+  const int64_t ntiles = (nx + 2 + kMsTW - 1) / kMsTW;
   return env_int("ST_GS_MS", 1) != 0 && ntiles >= kMsMinTiles && nx <= (1 << 28) &&
          (int64_t)ms_strips(ny, 33 - K) <= (int64_t)kMsStrips * num_sms();
 }
@@ -615,13 +669,14 @@ st_status gauss_seidel2d_ms_run(double* a, int64_t nx, int64_t ny, int64_t ld, i
   A.prog = static_cast<unsigned long long*>(workspace);
   A.edge = static_cast<char*>(workspace) + (int64_t)A.nstrips * kMsProgStride * 8;
   A.edge_stride = (nx + kMsEdgePad) * 32;
+
   const int64_t full = iters / K;
   const int rem = (int)(iters % K);
   for (int part = 0; part < 2; ++part) {
     const int kc = part == 0 ? K : rem;
     A.passes = part == 0 ? full : 1;
     if (kc == 0 || A.passes == 0) continue;
-    A.ntiles = (int)((std::max(nx + 2, nx + 2 * kc - 1) + 31) / 32);  // columns 0 .. nx+1 and edge entries
+    A.ntiles = (int)((std::max(nx + 2, nx + 2 * kc - 1) + kMsTW - 1) / kMsTW);  // columns 0..nx+1, edge entries
     ST_CHECK_CUDA(cudaMemsetAsync(A.prog, 0, (size_t)A.nstrips * kMsProgStride * 8, s));
     switch (kc) {
       case 1: ST_TRY(launch_ms<1>(A, s)); break;

@@ -14,11 +14,11 @@ import oracle  # noqa: E402
 import paper_2310_01882_b200 as st  # noqa: E402
 import stencil_inputs as si  # noqa: E402
 
-# (nx, ny, ld, iters): >= 351 columns (12 tiles of 32) takes the multi-sweep schedule;
+# (nx, ny, ld, iters): >= 382 columns (24 tiles of 16) takes the multi-sweep schedule;
 # one strip (ny <= 32), a 4-row last strip, partial CTAs, odd pitch, every remainder
 CASES = [
-    (352, 1, 354, 5), (380, 32, 382, 6), (380, 33, 382, 7), (360, 60, 362, 9),
-    (400, 257, 402, 7), (433, 130, 435, 9), (1000, 300, 1002, 13), (357, 1000, 360, 5),
+    (382, 1, 384, 5), (390, 32, 392, 6), (390, 33, 392, 7), (400, 60, 402, 9),
+    (410, 257, 412, 7), (433, 130, 435, 9), (1000, 300, 1002, 13), (395, 1000, 398, 5),
     (480, 95, 482, 1), (480, 95, 482, 2), (480, 95, 482, 3), (480, 95, 482, 4), (480, 95, 482, 8),
     (481, 95, 484, 11),
 ]
