@@ -25,7 +25,9 @@ for nx, ny, nz in ((33, 31, 9), (70, 40, 66)):
     b = torch.empty_like(a)
     st.st_jacobi3d_run(a, b, 3)  # T=1 sweeps (odd pass count)
     st.st_jacobi3d_run(a, b, 4)  # two T=2 passes (jacobi3d_t2_kernel)
-for nx, ny, ld, iters in ((200, 95, 202, 3), (65, 33, 67, 2), (1000, 130, 1002, 2)):  # GS: tiled (even ld), register (odd)
+# GS: single-sweep tiled (even ld) and register (odd ld) kernels; multi-sweep wavefront (nx >= 382:
+# K = 4 passes plus a remainder pass, wide and 8-byte copies)
+for nx, ny, ld, iters in ((200, 95, 202, 3), (65, 33, 67, 2), (1000, 130, 1002, 6), (400, 70, 403, 5)):
     a = torch.from_numpy(si.jacobi2d_grid(nx, ny, ld=ld)).cuda()
     st.st_gauss_seidel2d_run(a, iters, nx=nx)
 for nx, ny in ((64, 64), (37, 21)):  # register-resident C1 kernel
