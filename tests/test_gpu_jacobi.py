@@ -212,3 +212,14 @@ def test_fold_check_is_necessary(cuda_lib):
     res = dict(_subprocess_bitwise(FOLD_CASES, {"ST_JACOBI_FOLD": "2"}))
     assert not res["tiny"] and not res["huge"] and not res["mid_band"], res
     assert res["edge_lo_safe"] and res["zeros"], res
+
+
+@pytest.mark.parametrize("tblock", [2, 4, 6, 8, 10])
+@pytest.mark.parametrize("nx,ny,ld,iters", [(2301, 700, 2304, 21), (3100, 181, 3102, 13), (1150, 400, 1152, 11)])
+def test_wide_grids_equal_single_sweeps(cuda_lib, tblock, nx, ny, ld, iters):
+    # wide ragged grids: many interior strips on the rotated path, both ring-column strips
+    # on the general path, several row chunks
+    a = si.jacobi2d_grid(nx, ny, ld=ld)
+    want = oracle.jacobi2d(a, iters, nx=nx)
+    got = run_gpu(cuda_lib, a, iters, tblock, nx=nx)
+    assert_bitwise(got[:, : nx + 2], want[:, : nx + 2])
