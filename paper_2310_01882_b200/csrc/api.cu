@@ -448,15 +448,30 @@ st_status st_jacobi3d_run_pencils(double* a, double* b, int64_t nx, int64_t nyl,
   ST_TRY(jacobi3d_copy_faces(a, b, nx, nyl, ldx, 1, nzl, s));
   double* src = a;
   double* dst = b;
+  const int64_t nb = nzl + 2;
   for (int64_t it = 0; it < iters; ++it) {
-    ST_TRY(pencil_exchange_async(comm, &src, 1, nx, nyl, nzl, ldx, s, true));
-    ST_TRY(jacobi3d_sweep_planes(src, dst, nx, nyl, nzl + 2, ldx, 1, nzl, s));
+    // the y/z ghost swap runs on the comm stream while the block that reads no ghost
+    // (planes 2..nzl-1 x rows 2..nyl-1) is swept; then the shell: planes 1 and nzl,
+    // and rows 1 and nyl of the planes between
+    ST_TRY(pencil_exchange_async(comm, &src, 1, nx, nyl, nzl, ldx, s, false));
+    ST_TRY(jacobi3d_sweep_block(src, dst, nx, nyl, nb, ldx, 2, nzl - 1, 2, nyl - 1, s));
+    ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
+    ST_TRY(jacobi3d_sweep_block(src, dst, nx, nyl, nb, ldx, 1, 1, 1, nyl, s));
+    if (nzl > 1) ST_TRY(jacobi3d_sweep_block(src, dst, nx, nyl, nb, ldx, nzl, nzl, 1, nyl, s));
+    if (nzl > 2) {
+      ST_TRY(jacobi3d_sweep_block(src, dst, nx, nyl, nb, ldx, 2, nzl - 1, 1, 1, s));
+      if (nyl > 1) ST_TRY(jacobi3d_sweep_block(src, dst, nx, nyl, nb, ldx, 2, nzl - 1, nyl, nyl, s));
+    }
     double* t = src;
     src = dst;
     dst = t;
   }
   return ST_OK;
 }
+
+static st_status pw_validate(double* u, double* v, double* w, double* su, double* sv, double* sw, int64_t nx,
+                             int64_t ny, int64_t nz, int64_t ldx, const double* tzc1, const double* tzc2,
+                             const double* tzd1, const double* tzd2, bool distinct);
 
 st_status st_pw_advect3d_pencils(double* u, double* v, double* w, double* su, double* sv, double* sw, int64_t nx,
                                  int64_t nyl, int64_t nzl, int64_t ldx, double tcx, double tcy, const double* tzc1,
@@ -466,24 +481,41 @@ st_status st_pw_advect3d_pencils(double* u, double* v, double* w, double* su, do
   if (!comm || comm->nranks == 1)
     return st_pw_advect3d(u, v, w, su, sv, sw, nx, nyl, nzl, ldx, tcx, tcy, tzc1, tzc2, tzd1, tzd2, nullptr,
                           cuda_stream);
-  // validate as the single-block call, then swap ghosts (incl. corners) and advect
-  double* f[3] = {u, v, w};
-  const size_t bytes = (size_t)(nzl + 2) * (size_t)(nyl + 2) * (size_t)ldx * sizeof(double);
-  ST_RETURN_IF(!u || !v || !w || overlaps(u, bytes, v, bytes) || overlaps(u, bytes, w, bytes) ||
-                   overlaps(v, bytes, w, bytes),
-               ST_EINVAL, "st_pw_advect3d_pencils: u, v, w must be distinct");
+  ST_TRY(pw_validate(u, v, w, su, sv, sw, nx, nyl, nzl, ldx, tzc1, tzc2, tzd1, tzd2, true));
   ST_RETURN_IF(comm->broken, ST_ENCCL, "st_comm is unusable after an earlier error");
   cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
-  ST_TRY(pencil_exchange_async(comm, f, 3, nx, nyl, nzl, ldx, s, true));
-  return st_pw_advect3d(u, v, w, su, sv, sw, nx, nyl, nzl, ldx, tcx, tcy, tzc1, tzc2, tzd1, tzd2, nullptr,
-                        cuda_stream);
+  // y/z ghosts (incl. the corners the diagonal offsets read) in flight on the comm stream
+  // while the block that reads none (planes 2..nzl-1 x rows 2..nyl-1) is advected; then
+  // the shell
+  double* f[3] = {u, v, w};
+  ST_TRY(pencil_exchange_async(comm, f, 3, nx, nyl, nzl, ldx, s, false));
+  PwArgs args{u, v, w, su, sv, sw, nx, nyl, nzl, ldx, tcx, tcy, tzc1, tzc2, tzd1, tzd2};
+  auto window = [&](int64_t z0, int64_t z1, int64_t y0, int64_t y1) {
+    PwArgs a = args;
+    a.y_lo = y0;
+    a.y_hi = y1;
+    return pw_advect3d_planes(a, z0, z1, s);
+  };
+  cudaEvent_t p0 = prof_mark(comm, s);
+  ST_TRY(window(2, nzl - 1, 2, nyl - 1));
+  cudaEvent_t p1 = prof_mark(comm, s);
+  prof_add(comm, ST_PHASE_INTERIOR, p0, p1);
+  ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
+  cudaEvent_t p2 = prof_mark(comm, s);
+  prof_add(comm, ST_PHASE_JOIN_WAIT, p1, p2);
+  ST_TRY(window(1, 1, 1, nyl));
+  if (nzl > 1) ST_TRY(window(nzl, nzl, 1, nyl));
+  if (nzl > 2) {
+    ST_TRY(window(2, nzl - 1, 1, 1));
+    if (nyl > 1) ST_TRY(window(2, nzl - 1, nyl, nyl));
+  }
+  prof_add(comm, ST_PHASE_BOUNDARY, p2, prof_mark(comm, s));
+  return ST_OK;
 }
 
-st_status st_pw_advect3d(double* u, double* v, double* w, double* su, double* sv, double* sw,
-                         int64_t nx, int64_t ny, int64_t nz, int64_t ldx, double tcx, double tcy,
-                         const double* tzc1, const double* tzc2, const double* tzd1,
-                         const double* tzd2, st_comm* comm, void* cuda_stream) {
-  clear_error();
+static st_status pw_validate(double* u, double* v, double* w, double* su, double* sv, double* sw, int64_t nx,
+                             int64_t ny, int64_t nz, int64_t ldx, const double* tzc1, const double* tzc2,
+                             const double* tzd1, const double* tzd2, bool distinct) {
   const double* f[6] = {u, v, w, su, sv, sw};
   for (int i = 0; i < 6; ++i) {
     ST_RETURN_IF(!f[i], ST_EINVAL, "st_pw_advect3d: null field %d", i);
@@ -501,10 +533,19 @@ st_status st_pw_advect3d(double* u, double* v, double* w, double* su, double* sv
       if (i != o)
         ST_RETURN_IF(overlaps(f[o], bytes, f[i], bytes), ST_EINVAL,
                      "st_pw_advect3d: output %d overlaps field %d", o, i);
-  if (comm)
+  if (distinct)
     ST_RETURN_IF(overlaps(u, bytes, v, bytes) || overlaps(u, bytes, w, bytes) || overlaps(v, bytes, w, bytes),
                  ST_EINVAL, "st_pw_advect3d: u, v, w must be distinct with a comm");
   for (int i = 0; i < 6; ++i) ST_TRY(check_device_ptr(f[i], "st_pw_advect3d field"));
+  return ST_OK;
+}
+
+st_status st_pw_advect3d(double* u, double* v, double* w, double* su, double* sv, double* sw,
+                         int64_t nx, int64_t ny, int64_t nz, int64_t ldx, double tcx, double tcy,
+                         const double* tzc1, const double* tzc2, const double* tzd1,
+                         const double* tzd2, st_comm* comm, void* cuda_stream) {
+  clear_error();
+  ST_TRY(pw_validate(u, v, w, su, sv, sw, nx, ny, nz, ldx, tzc1, tzc2, tzd1, tzd2, comm != nullptr));
   cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
   PwArgs args{u, v, w, su, sv, sw, nx, ny, nz, ldx, tcx, tcy, tzc1, tzc2, tzd1, tzd2};
   if (!comm || comm->nranks == 1) return pw_advect3d_planes(args, 1, nz, s);

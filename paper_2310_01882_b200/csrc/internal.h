@@ -72,6 +72,10 @@ st_status jacobi2d_tb_rows(const double* src, double* dst, int64_t nx, int64_t l
 // planes in the buffer (TMA extent).
 st_status jacobi3d_sweep_planes(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
                                 int64_t ldx, int64_t z_lo, int64_t z_hi, cudaStream_t s, Remote rem = Remote());
+// The same over output rows [y_lo, y_hi] only (pencils: the interior block while the halo is in flight).
+st_status jacobi3d_sweep_block(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
+                               int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t y_lo, int64_t y_hi, cudaStream_t s,
+                               Remote rem = Remote());
 st_status ddiv6_selftest(const double* x, int64_t n, unsigned long long* mismatches, cudaStream_t s);
 // dst's side faces (x = 0, nx+1; y = 0, ny+1) of planes [z_lo, z_hi] <- src.
 st_status jacobi3d_copy_faces(const double* src, double* dst, int64_t nx, int64_t ny, int64_t ldx, int64_t z_lo,
@@ -99,6 +103,7 @@ struct PwArgs {
   int64_t nx, ny, nz, ldx;
   double tcx, tcy;
   const double *tzc1, *tzc2, *tzd1, *tzd2;
+  int64_t y_lo = 1, y_hi = -1;  // output rows [y_lo, y_hi] (-1: ny); pencils sweep windows
 };
 // Computes output planes [z_lo, z_hi] (local plane indices, 1-based interior).
 st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s);

@@ -38,8 +38,8 @@ struct J3Tile {
 template <int BX, int BY, int S, int R>
 __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
     jacobi3d_kernel(const __grid_constant__ CUtensorMap tm, double* __restrict__ dst, int64_t nx, int64_t ny,
-                    int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t planes_per_chunk, double* __restrict__ dst2,
-                    int64_t delta2) {
+                    int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t y_first, int64_t y_last,
+                    int64_t planes_per_chunk, double* __restrict__ dst2, int64_t delta2) {
   using T = J3Tile<BX, BY>;
   constexpr int kSX = T::SX, WX = BX / 32;
   static_assert(S >= 4 && BY % R == 0 && BX % 32 == 0, "ring depth / rows per thread / tile width");
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
   const int wx = (threadIdx.x >> 5) % WX;
   const int wy = (threadIdx.x >> 5) / WX;
   const int64_t x0 = 1 + (int64_t)blockIdx.x * BX;
-  const int64_t y0 = 1 + (int64_t)blockIdx.y * BY;
+  const int64_t y0 = y_first + (int64_t)blockIdx.y * BY;  // output rows [y_first, y_last] (a window for pencils)
   const int64_t za = z_lo + (int64_t)blockIdx.z * planes_per_chunk;
   const int64_t zb = min(z_hi, za + planes_per_chunk - 1);
   const int np = (int)(zb - za + 3);
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
   const int64_t x = x0 + wx * 32 + lane;
   bool ok[R];
 #pragma unroll
-  for (int i = 0; i < R; ++i) ok[i] = (yb + i <= ny) && (x <= nx);
+  for (int i = 0; i < R; ++i) ok[i] = (yb + i <= y_last) && (x <= nx);
   const int64_t plane_elems = (ny + 2) * ldx;
   double* out = dst + (za * (ny + 2) + yb) * ldx + x;
   double* out2 = dst2 ? dst2 + ((za + delta2) * (ny + 2) + yb) * ldx + x : nullptr;  // fused halo swap
@@ -155,7 +155,7 @@ __global__ void jacobi3d_copy_faces_kernel(const double* __restrict__ src, doubl
 
 template <int BX, int BY, int S, int R>
 st_status launch_j3(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf, int64_t ldx,
-                    int64_t z_lo, int64_t z_hi, cudaStream_t s, Remote rem) {
+                    int64_t z_lo, int64_t z_hi, int64_t y_lo, int64_t y_hi, cudaStream_t s, Remote rem) {
   using T = J3Tile<BX, BY>;
   CUtensorMap tm;
   const uint64_t dims[3] = {(uint64_t)(nx + 2), (uint64_t)(ny + 2), (uint64_t)nplanes_buf};
@@ -164,14 +164,14 @@ st_status launch_j3(const double* src, double* dst, int64_t nx, int64_t ny, int6
   const size_t smem = (size_t)S * T::kPlaneStride * sizeof(double) + S * sizeof(uint64_t);
   ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi3d_kernel<BX, BY, S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-  const int64_t ntx = (nx + BX - 1) / BX, nty = (ny + BY - 1) / BY, nz = z_hi - z_lo + 1;
+  const int64_t ntx = (nx + BX - 1) / BX, nty = (y_hi - y_lo + BY) / BY, nz = z_hi - z_lo + 1;
   static const int kPpc = env_int("ST_J3_PLANES", 64);
   const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(kPpc, nz));
   const int64_t nzc = (nz + ppc - 1) / ppc;
   ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "jacobi3d: grid too large");
   jacobi3d_kernel<BX, BY, S, R><<<dim3((unsigned)ntx, (unsigned)nty, (unsigned)nzc), (BX / 32) * (BY / R) * 32,
                                   smem, s>>>(
-      tm, dst, nx, ny, ldx, z_lo, z_hi, ppc, rem.base, rem.delta);
+      tm, dst, nx, ny, ldx, z_lo, z_hi, y_lo, y_hi, ppc, rem.base, rem.delta);
   ST_LAUNCHED();
   return ST_OK;
 }
@@ -389,25 +389,9 @@ st_status launch_j3t2(const double* src, double* dst, int64_t nx, int64_t ny, in
 
 st_status jacobi3d_preload() {
   cudaFuncAttributes fa;
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 16, 4, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 16, 6, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 16, 8, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 4, 8, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 8, 12, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 8, 6, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 8, 8, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<192, 8, 6, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<192, 8, 8, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<32, 16, 6, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<32, 32, 6, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<64, 16, 6, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<64, 16, 8, 1>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_copy_faces_kernel));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 6, 2, false>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 4, 2, false>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 5, 2, false>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 5, 2, false>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 16, 4, 4, false>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 5, 2, true>));
   return ST_OK;
 }
@@ -416,36 +400,19 @@ st_status jacobi3d_two_sweeps(const double* src, double* dst, int64_t nx, int64_
                               int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi,
                               cudaStream_t s, Remote rem) {
   if (z_hi < z_lo) return ST_OK;
-  static const int kV = env_int("ST_J3T2_VARIANT", 0);
-  switch (kV) {
-    case 1: return launch_j3t2<128, 16, 4, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);
-    case 2: return launch_j3t2<128, 16, 5, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);
-    case 3: return launch_j3t2<128, 8, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);
-    case 4: return launch_j3t2<128, 16, 4, 4>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);
-    default: return launch_j3t2<128, 8, 5, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);
-  }
+  return launch_j3t2<128, 8, 5, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);  // §6.5
+}
+
+st_status jacobi3d_sweep_block(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
+                               int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t y_lo, int64_t y_hi, cudaStream_t s,
+                               Remote rem) {
+  if (z_hi < z_lo || y_hi < y_lo) return ST_OK;
+  return launch_j3<128, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, y_lo, y_hi, s, rem);
 }
 
 st_status jacobi3d_sweep_planes(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
                                 int64_t ldx, int64_t z_lo, int64_t z_hi, cudaStream_t s, Remote rem) {
-  if (z_hi < z_lo) return ST_OK;
-  static const int kVariant = env_int("ST_J3_VARIANT", 0);
-  switch (kVariant) {
-    case 1: return launch_j3<32, 32, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 2: return launch_j3<64, 16, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 3: return launch_j3<128, 16, 4, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 4: return launch_j3<64, 16, 8, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 5: return launch_j3<128, 16, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 6: return launch_j3<192, 8, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 7: return launch_j3<128, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 8: return launch_j3<128, 4, 8, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 9: return launch_j3<32, 16, 6, 1>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 10: return launch_j3<128, 8, 12, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 11: return launch_j3<192, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 12: return launch_j3<128, 16, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    case 13: return launch_j3<128, 8, 6, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);
-    default: return launch_j3<128, 8, 8, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, s, rem);  // tuned
-  }
+  return jacobi3d_sweep_block(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, 1, ny, s, rem);
 }
 
 st_status ddiv6_selftest(const double* x, int64_t n, unsigned long long* mismatches, cudaStream_t s) {

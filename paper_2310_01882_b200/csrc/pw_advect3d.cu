@@ -107,8 +107,8 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
                        double* __restrict__ sv, double* __restrict__ sw, int64_t nx, int64_t ny,
                        int64_t ldx, double tcx, double tcy, const double* __restrict__ tzc1,
                        const double* __restrict__ tzc2, const double* __restrict__ tzd1,
-                       const double* __restrict__ tzd2, int64_t z_lo, int64_t z_hi,
-                       int64_t planes_per_chunk) {
+                       const double* __restrict__ tzd2, int64_t z_lo, int64_t z_hi, int64_t y_first,
+                       int64_t y_last, int64_t planes_per_chunk) {
   using T = PwTile<BX, BY>;
   constexpr int kSX = T::SX, WX = BX / 32;
   static_assert(S >= 4, "ring needs planes z-1, z, z+1 and at least one in flight");
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
   const int wx = (threadIdx.x >> 5) % WX;
   const int wy = (threadIdx.x >> 5) / WX;
   const int64_t x0 = 1 + (int64_t)blockIdx.x * BX;
-  const int64_t y0 = 1 + (int64_t)blockIdx.y * BY;
+  const int64_t y0 = y_first + (int64_t)blockIdx.y * BY;  // output rows [y_first, y_last] (pencils: windows)
   const int64_t za = z_lo + (int64_t)blockIdx.z * planes_per_chunk;
   const int64_t zb = min(z_hi, za + planes_per_chunk - 1);
   const int np = (int)(zb - za + 3);  // input planes za-1 .. zb+1
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
   const int64_t x = x0 + wx * 32 + lane;
   bool ok[R];
 #pragma unroll
-  for (int i = 0; i < R; ++i) ok[i] = (yb + i <= ny) && (x <= nx);
+  for (int i = 0; i < R; ++i) ok[i] = (yb + i <= y_last) && (x <= nx);
   const int64_t plane_elems = (ny + 2) * ldx;
   const int64_t g0 = (za * (ny + 2) + yb) * ldx + x;
   double* pu = su + g0;
@@ -277,7 +277,9 @@ st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s)
   ST_CHECK_CUDA(cudaFuncSetAttribute(pw_advect3d_kernel<BX, BY, S, R>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t ntx = (a.nx + BX - 1) / BX;
-  const int64_t nty = (a.ny + BY - 1) / BY;
+  const int64_t y_lo = a.y_lo, y_hi = a.y_hi < 0 ? a.ny : a.y_hi;
+  if (y_hi < y_lo) return ST_OK;
+  const int64_t nty = (y_hi - y_lo + BY) / BY;
   const int64_t nz = z_hi - z_lo + 1;
   static const int kPpc = env_int("ST_PW_PLANES", 128);
   const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(std::min(kPpc, kMaxPlanesPerChunk), nz));
@@ -286,7 +288,7 @@ st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s)
   dim3 grid((unsigned)ntx, (unsigned)nty, (unsigned)nzc);
   pw_advect3d_kernel<BX, BY, S, R><<<grid, (BX / 32) * (BY / R) * 32, smem, s>>>(tm[0], tm[1], tm[2], a.su, a.sv, a.sw, a.nx,
                                                         a.ny, a.ldx, a.tcx, a.tcy, a.tzc1, a.tzc2,
-                                                        a.tzd1, a.tzd2, z_lo, z_hi, ppc);
+                                                        a.tzd1, a.tzd2, z_lo, z_hi, y_lo, y_hi, ppc);
   ST_LAUNCHED();
   return ST_OK;
 }
@@ -295,47 +297,13 @@ st_status launch_pw(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s)
 
 st_status pw_advect3d_preload() {
   cudaFuncAttributes fa;
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 4, 5, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 4, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 5, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 5, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 6, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<192, 8, 4, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<32, 16, 5, 1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<32, 32, 5, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<64, 16, 5, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<64, 16, 6, 2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<64, 8, 6, 1>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 5, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<64, 16, 5, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 4, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 6, 4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, pw_advect3d_kernel<128, 8, 5, 8>));
   return ST_OK;
 }
 
 st_status pw_advect3d_planes(const PwArgs& a, int64_t z_lo, int64_t z_hi, cudaStream_t s) {
   if (z_hi < z_lo) return ST_OK;
-  static const int kVariant = env_int("ST_PW_VARIANT", 0);
-  switch (kVariant) {
-    case 1: return launch_pw<32, 16, 5, 1>(a, z_lo, z_hi, s);
-    case 2: return launch_pw<64, 16, 5, 2>(a, z_lo, z_hi, s);
-    case 3: return launch_pw<128, 8, 4, 2>(a, z_lo, z_hi, s);
-    case 4: return launch_pw<128, 8, 5, 2>(a, z_lo, z_hi, s);
-    case 5: return launch_pw<128, 4, 5, 1>(a, z_lo, z_hi, s);
-    case 6: return launch_pw<64, 8, 6, 1>(a, z_lo, z_hi, s);
-    case 7: return launch_pw<128, 8, 6, 2>(a, z_lo, z_hi, s);
-    case 8: return launch_pw<64, 16, 6, 2>(a, z_lo, z_hi, s);
-    case 9: return launch_pw<192, 8, 4, 2>(a, z_lo, z_hi, s);
-    case 10: return launch_pw<32, 32, 5, 2>(a, z_lo, z_hi, s);
-    case 11: return launch_pw<128, 8, 5, 1>(a, z_lo, z_hi, s);
-    case 12: return launch_pw<128, 8, 5, 4>(a, z_lo, z_hi, s);
-    case 13: return launch_pw<64, 16, 5, 4>(a, z_lo, z_hi, s);
-    case 14: return launch_pw<128, 8, 4, 4>(a, z_lo, z_hi, s);
-    case 15: return launch_pw<128, 8, 6, 4>(a, z_lo, z_hi, s);
-    case 16: return launch_pw<128, 8, 5, 8>(a, z_lo, z_hi, s);
-    default: return launch_pw<128, 8, 5, 4>(a, z_lo, z_hi, s);  // tuned on B200
-  }
+  return launch_pw<128, 8, 5, 4>(a, z_lo, z_hi, s);  // tuned on B200
 }
 
 }  // namespace st

@@ -134,7 +134,96 @@ def jacobi3d(P, n=512, sweeps=100, h=2):
     return n ** 3 * sweeps / (ms / 1e3) / 1e9, ms
 
 
+def pencils_j3(py, pz, n=512, sweeps=50):
+    """3-D Jacobi on a py x pz (y, z) pencil grid of LOCAL ranks (T = 1 sweeps; swap overlapped with the
+    interior block). py = pz = 1: the single domain at tblock = 1 (same sweep kernel, no decomposition)."""
+    if n not in _G3:
+        _G3[n] = torch.from_numpy(si.jacobi3d_grid(n, n, n)).cuda()
+    g = _G3[n]
+    P = py * pz
+    comms = st.Comm.local_group(P) if P > 1 else [None]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    bufs = []
+    for r in range(P):
+        y0, nyl, z0, nzl = st.st_pencil_split(n, n, py, pz, r) if P > 1 else (0, n, 0, n)
+        a = g[z0:z0 + nzl + 2, y0:y0 + nyl + 2].contiguous()
+        b = torch.empty_like(a)
+        if comms[r] is not None:
+            comms[r].set_grid(py, nyl)
+            comms[r].bind([a, b], nzl)
+        bufs.append((a, b))
+    torch.cuda.synchronize()
+
+    def run():
+        for r in range(P):
+            a, b = bufs[r]
+            with torch.cuda.stream(streams[r]):
+                if comms[r] is None:
+                    st.st_jacobi3d_run(a, b, sweeps, tblock=1)
+                else:
+                    st.st_jacobi3d_run_pencils(a, b, sweeps, comm=comms[r], nx=n)
+
+    ms = timed(run, streams, 2)
+    for c in comms:
+        if c is not None:
+            c.close()
+    return n ** 3 * sweeps / (ms / 1e3) / 1e9, ms
+
+
+def pencils_pw(py, pz, n=512, apps=20):
+    d = si.pw_inputs(n, n, n)
+    P = py * pz
+    comms = st.Comm.local_group(P) if P > 1 else [None]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    parts = []
+    for r in range(P):
+        y0, nyl, z0, nzl = st.st_pencil_split(n, n, py, pz, r) if P > 1 else (0, n, 0, n)
+        g = {k: torch.from_numpy(np.ascontiguousarray(d[k][z0:z0 + nzl + 2, y0:y0 + nyl + 2])).cuda() for k in "uvw"}
+        for k in ("tzc1", "tzc2", "tzd1", "tzd2"):
+            g[k] = torch.from_numpy(np.ascontiguousarray(d[k][z0:z0 + nzl + 2])).cuda()
+        outs = [torch.empty_like(g["u"]) for _ in range(3)]
+        if comms[r] is not None:
+            comms[r].set_grid(py, nyl)
+            comms[r].bind([g["u"], g["v"], g["w"]], nzl)
+        parts.append((g, outs))
+    del d
+    torch.cuda.synchronize()
+
+    def run():
+        for r in range(P):
+            g, outs = parts[r]
+            with torch.cuda.stream(streams[r]):
+                if comms[r] is None:
+                    st.st_pw_advect3d(g["u"], g["v"], g["w"], *outs, 0.25 / 3, 0.05, g["tzc1"], g["tzc2"],
+                                      g["tzd1"], g["tzd2"])
+                else:
+                    st.st_pw_advect3d_pencils(g["u"], g["v"], g["w"], *outs, 0.25 / 3, 0.05, g["tzc1"],
+                                              g["tzc2"], g["tzd1"], g["tzd2"], comm=comms[r])
+
+    ms = timed(run, streams, apps)
+    for c in comms:
+        if c is not None:
+            c.close()
+    return n ** 3 / (ms / 1e3) / 1e9, ms
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["pencils"]:  # the (y, z) pencil decomposition (NEXT #2) on one GPU
+        out = {"what": "LOCAL pencil grids (py x pz) on one B200: throughput at fixed total work vs the single "
+                       "domain with the same sweep kernel (T = 1)", "jacobi3d_512^3_50sw": {}, "pw_512^3": {}}
+        for py, pz in ((1, 1), (2, 1), (1, 2), (2, 2), (4, 2)):
+            v, ms = pencils_j3(py, pz)
+            out["jacobi3d_512^3_50sw"][f"{py}x{pz}"] = {"gpts": round(v, 1), "ms": round(ms, 2)}
+            print(f"pencils j3 {py}x{pz}: {v:.1f} Gpts/s", file=sys.stderr, flush=True)
+            v, ms = pencils_pw(py, pz)
+            out["pw_512^3"][f"{py}x{pz}"] = {"gpts": round(v, 2), "ms_per_app": round(ms, 4)}
+            print(f"pencils pw {py}x{pz}: {v:.2f} Gpts/s", file=sys.stderr, flush=True)
+        for k in ("jacobi3d_512^3_50sw", "pw_512^3"):
+            base = out[k]["1x1"]["gpts"]
+            for g in out[k]:
+                out[k][g]["vs_1x1"] = round(out[k][g]["gpts"] / base, 3)
+        print(json.dumps(out))
+        sys.exit(0)
     only3d = sys.argv[1:] == ["3d"]  # just the 3-D Jacobi legs
     out = {"what": "LOCAL rank group on one B200: throughput at fixed total work vs P=1", "jacobi2d_16384^2_200sw": {},
            "pw_512^3": {}, "jacobi3d_512^3_100sw_h2": {}, "jacobi3d_512^3_100sw_h1": {}}
