@@ -364,11 +364,7 @@ st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int6
   ST_CHECK_CUDA(cudaMemsetAsync(progress, 0, (size_t)(2 * nstrips) * sizeof(unsigned long long), s));
   int per_sm = 0;
   if (tiled) {
-    static const int kPubT = env_int("ST_GS_PUBT", 4);
-    auto* tk = kPubT == 1   ? gauss_seidel2d_tiled_kernel<1>
-               : kPubT == 2 ? gauss_seidel2d_tiled_kernel<2>
-               : kPubT == 8 ? gauss_seidel2d_tiled_kernel<8>
-                            : gauss_seidel2d_tiled_kernel<4>;
+    auto* tk = gauss_seidel2d_tiled_kernel<4>;  // a fence per 4 written-back tiles
     ST_CHECK_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTiledSmem));
     ST_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tk, 32, kTiledSmem));
     // every strip's warp must be resident at once (the strips spin on each other)
@@ -382,8 +378,7 @@ st_status gauss_seidel2d_run(double* a, int64_t nx, int64_t ny, int64_t ld, int6
     ST_LAUNCHED();
     return ST_OK;
   }
-  static const int kPub = env_int("ST_GS_PUB", 1);  // groups of kPf columns per progress publication
-  auto* kern = kPub == 1 ? gauss_seidel2d_kernel<1> : kPub == 4 ? gauss_seidel2d_kernel<4> : gauss_seidel2d_kernel<2>;
+  auto* kern = gauss_seidel2d_kernel<1>;  // a publication per group of kPf columns
   ST_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kGsWarps, 0));
   const int64_t blocks = (nstrips + kGsWarps - 1) / kGsWarps;
   ST_RETURN_IF(blocks > (int64_t)per_sm * num_sms(), ST_ENOTSUP,
@@ -403,12 +398,7 @@ int64_t gauss_seidel2d_workspace_bytes(int64_t nx, int64_t ny) {
 st_status gauss_seidel2d_preload() {
   cudaFuncAttributes fa;
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_kernel<1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_kernel<2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_kernel<4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_tiled_kernel<1>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_tiled_kernel<2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_tiled_kernel<4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, gauss_seidel2d_tiled_kernel<8>));
   return gauss_seidel2d_ms_preload();
 }
 

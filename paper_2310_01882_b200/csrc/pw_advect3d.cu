@@ -5,20 +5,22 @@
 // cell), formula and association trees = DESIGN.md reading R6 (MONC
 // pwadvection form); every binary op rounds once.
 //
-// Design (HBM-bound: 48 algorithmic bytes per point, 63 fp64 flops):
-//  * A CTA owns a 32(x) x BY(y) column of the interior and streams a chunk of z
-//    planes. Each input plane of u, v, w (with a 1-cell x/y apron) is brought
-//    into a shared-memory ring of S plane slots by three TMA tile loads
-//    (cp.async.bulk.tensor.3d, issued by one thread, completed on an
-//    mbarrier), so S-3 planes are in flight while the CTA computes.
-//  * Tiles are aligned to the interior (x0 = 1 + 32*bx): the TMA box then starts
+// Design (HBM-bound: 48 algorithmic bytes per point, 63 fp64 flops; DESIGN.md §6.4):
+//  * A CTA owns a BX(x) x BY(y) = 128 x 8 tile of the interior and streams a
+//    chunk of up to 128 z planes. Each input plane of u, v, w (with a 1-cell
+//    x/y apron) is brought into a shared-memory ring of S = 5 plane slots by
+//    three TMA tile loads (cp.async.bulk.tensor.3d, issued by one thread,
+//    completed on an mbarrier), so S-3 planes are in flight while the CTA computes.
+//  * Tiles are aligned to the interior (x0 = 1 + BX*bx): the TMA box then starts
 //    at the even coordinate x0-1, which TMA requires (the innermost start
-//    coordinate must be a multiple of 16 bytes; odd fp64 coordinates fault),
-//    and nx = 512 splits into 16 full tiles with no ragged tile.
-//  * A thread owns one point per plane; its own column of u, v, w at planes
-//    z-1, z rides in registers, all other neighbours are 8-byte shared loads
-//    (a warp's 32 consecutive doubles = 2 wavefronts). Outputs are coalesced
-//    8-byte stores straight to HBM; halo cells of su, sv, sw are never written.
+//    coordinate must be a multiple of 16 bytes; odd fp64 coordinates fault).
+//  * A thread owns R = 4 consecutive rows of one column; its own column of u, v,
+//    w at planes z-1, z rides in registers and neighbours shared by its R points
+//    come from registers, the rest are 8-byte shared loads (11 + 10/R per point).
+//    Outputs are coalesced 8-byte stores straight to HBM; halo cells of su, sv,
+//    sw are never written.
+//  * An output row window [y_first, y_last] lets the pencil decomposition
+//    advect the ghost-free block while the halo is in flight.
 #include <algorithm>
 
 #include "common.cuh"
