@@ -183,6 +183,9 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 struct MsArgs {
   double* a;
@@ -557,7 +560,10 @@ __device__ __forceinline__ void ms_loader(const MsArgs& A, unsigned char* sm, co
 
 // Storer warp: writes finished tiles back, frees their slots, and publishes
 // progress (one GPU-scope fence per kMsPub tiles and at the end).
-constexpr int kMsPub = 4;
+#ifndef ST_GS_MS_PUB
+#define ST_GS_MS_PUB 4
+#endif
+constexpr int kMsPub = ST_GS_MS_PUB;  // tiles per progress publication
 template <int KC>
 __device__ __forceinline__ void ms_storer(const MsArgs& A, unsigned char* sm, const int I, const int lane,
                                           const bool wide) {
@@ -572,9 +578,11 @@ __device__ __forceinline__ void ms_storer(const MsArgs& A, unsigned char* sm, co
     __syncwarp();  // every lane's shared reads of the tile are done (their values are in the stores)
     if (lane == 0) mbar_arrive(&freed[t % kMsSlots]);
     if ((t + 1) % kMsPub == 0 || t + 1 == Ttot) {
-      __threadfence();
+      // publish: the warp's write-back and edge stores, then the progress word. A
+      // release store by lane 0 after the warp barrier (which orders the other lanes'
+      // stores before it) instead of a full __threadfence on every lane.
       __syncwarp();
-      if (lane == 0) st_relaxed(mine, (unsigned long long)(t + 1));
+      if (lane == 0) st_release(mine, (unsigned long long)(t + 1));
     }
   }
 }
