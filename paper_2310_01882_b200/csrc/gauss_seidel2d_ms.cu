@@ -67,7 +67,6 @@ constexpr int kMsNP = kMsTW * kMsSlots;  // ring positions per row
 constexpr int kMsP = 2;               // shared-memory prefetch distance (steps)
 constexpr int kMsProgStride = 16;     // u64 per progress word (one 128-byte line each)
 constexpr int kMsMinTiles = 24;       // narrower grids take the single-sweep kernel (helper/compute coupling)
-constexpr int kMsL2Ahead = 8;         // tiles prefetched into L2 ahead of their load
 constexpr int kMsEdgePad = 8;         // edge entries per strip: columns 0 .. nx + 2K - 2 (< nx + 8)
 
 template <int KC>
@@ -521,36 +520,37 @@ __device__ __forceinline__ void ms_loader(const MsArgs& A, unsigned char* sm, co
   const unsigned long long* up = I > 0 ? A.prog + (int64_t)(I - 1) * kMsProgStride : nullptr;
   const unsigned long long* dn = I + 1 < A.nstrips ? A.prog + (int64_t)(I + 1) * kMsProgStride : nullptr;
   const int64_t y0 = 1 + (int64_t)I * A.R;
-  const int prow = (int)min((int64_t)33, A.ny + 2 - y0);  // rows of a tile
   unsigned long long acq_up = 0, acq_dn = 0;
   uint64_t* never = reinterpret_cast<uint64_t*>(sm + G::BAR_OFF) + 3 * kMsSlots;  // never arrived on
   for (int64_t t = 0; t < Ttot; ++t) {
-    // pull tile t + kMsL2Ahead into L2 now (the rows last written a pass ago are in HBM);
-    // if the strip below has not written its part back yet this only wastes bandwidth
-    if (t + kMsL2Ahead < Ttot) {  // one 128-byte line per row and tile
-      const int c = kMsTW * (int)((t + kMsL2Ahead) % A.ntiles);
-      if (lane < prow && c <= A.nx + 1)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.a + (y0 + lane) * A.ld + c) : "memory");
-      if (lane == 0 && prow == 33 && c <= A.nx + 1)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.a + (y0 + 32) * A.ld + c) : "memory");
-    }
     const unsigned long long need_up = (unsigned long long)(t + 1);
     const int64_t need_dn = t - A.ntiles + 1;
     const bool wu = up != nullptr, wd = dn != nullptr && need_dn > 0;
-    // progress seen by the last acquire covers this tile: no new acquire (with 16-byte
-    // copies everything bypasses L1); 8-byte copies go through L1, so they acquire per
-    // tile (its L1 invalidation drops stale lines)
+    // Wait for the neighbours' progress words. With 16-byte copies (cp.async.cg) every
+    // read of another strip's data goes to L2, the coherence point, and is issued only
+    // after the poll has returned a value published by a release store that followed
+    // the data: a relaxed poll suffices, and no acquire is taken — an ld.acquire.gpu is
+    // LDG.STRONG + CCTL.IVALL, and the L1 invalidation stalls the SM's L1TEX pipeline,
+    // shared memory included (measured: it and L2 prefetch hints cost the compute warps
+    // ~8 %). 8-byte copies (odd pitch) go through L1: they acquire per tile.
     const bool have = wide && (!wu || acq_up >= need_up) && (!wd || acq_dn >= (unsigned long long)need_dn);
     if (!have) {
-      bool ok = (!wu || ld_relaxed(up) >= need_up) && (!wd || ld_relaxed(dn) >= (unsigned long long)need_dn);
+      unsigned long long vu = wu ? ld_relaxed(up) : 0, vd = wd ? ld_relaxed(dn) : 0;
+      bool ok = (!wu || vu >= need_up) && (!wd || vd >= (unsigned long long)need_dn);
       while (!__all_sync(0xffffffffu, ok)) {
         park_ns(never, 256);
-        ok = (!wu || ld_relaxed(up) >= need_up) && (!wd || ld_relaxed(dn) >= (unsigned long long)need_dn);
+        vu = wu ? ld_relaxed(up) : 0;
+        vd = wd ? ld_relaxed(dn) : 0;
+        ok = (!wu || vu >= need_up) && (!wd || vd >= (unsigned long long)need_dn);
       }
-      // acquire (taken before the slot wait, so its latency overlaps it)
-      if (wu) acq_up = ld_acquire(up);
-      if (wd) acq_dn = ld_acquire(dn);
-      if (!wu && !wd) (void)ld_acquire(A.prog + (int64_t)I * kMsProgStride);
+      if (wide) {
+        acq_up = vu;
+        acq_dn = vd;
+      } else {
+        if (wu) (void)ld_acquire(up);
+        if (wd) (void)ld_acquire(dn);
+        if (!wu && !wd) (void)ld_acquire(A.prog + (int64_t)I * kMsProgStride);
+      }
     }
     if (t >= kMsSlots) mbar_wait_sleep(&freed[t % kMsSlots], (uint32_t)((t / kMsSlots - 1) & 1), 1000);
     ms_load_tile<KC>(A, sm, I, lane, t, wide);
