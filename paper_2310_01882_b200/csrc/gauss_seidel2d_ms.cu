@@ -67,6 +67,17 @@ constexpr int kMsNP = kMsTW * kMsSlots;  // ring positions per row
 constexpr int kMsP = 2;               // shared-memory prefetch distance (steps)
 constexpr int kMsProgStride = 16;     // u64 per progress word (one 128-byte line each)
 constexpr int kMsMinTiles = 24;       // narrower grids take the single-sweep kernel (helper/compute coupling)
+// helper wait loops sleep between tests (ns): a spinning helper takes issue slots and
+// shared-memory / L1TEX bandwidth from the compute warp on its SMSP
+#ifndef ST_GS_MS_SSLEEP
+#define ST_GS_MS_SSLEEP 2000  // storer: a tile is finished every ~2 us
+#endif
+#ifndef ST_GS_MS_LSLEEP
+#define ST_GS_MS_LSLEEP 500   // loader, slot wait (it runs several tiles ahead)
+#endif
+#ifndef ST_GS_MS_PSLEEP
+#define ST_GS_MS_PSLEEP 200   // loader, neighbour progress polls
+#endif  // tiles per progress publication
 constexpr int kMsEdgePad = 8;         // edge entries per strip: columns 0 .. nx + 2K - 2 (< nx + 8)
 
 template <int KC>
@@ -83,7 +94,7 @@ struct MsGeo {
   static constexpr int STAGE_OFF = ABOVE_OFF + ABOVE_B;
   static constexpr int STAGE_B = kMsNP * EB;
   static constexpr int BAR_OFF = STAGE_OFF + STAGE_B;
-  static constexpr int STRIP_B = (BAR_OFF + (3 * kMsSlots + 1) * 8 + 127) / 128 * 128;
+  static constexpr int STRIP_B = (BAR_OFF + 3 * kMsSlots * 8 + 127) / 128 * 128;
   static constexpr int CTA_B = kMsStrips * STRIP_B;
   // a tile is finished (results of its columns final, its edge entries staged)
   // kLagT groups after its own: stores of step k reach back to column k - 28 - 2KC
@@ -148,27 +159,10 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return done != 0;
 }
-// Helper-warp waits must not take issue slots from the compute warp on the same
-// SMSP. __nanosleep measured ineffective here (a test + nanosleep(256) loop ran
-// every ~5 ns); mbarrier.try_wait with a suspend-time hint parks the warp in
-// hardware until the phase completes or the hint elapses.
-__device__ __forceinline__ bool mbar_try_hint(uint64_t* bar, uint32_t parity, uint32_t ns) {
-  uint32_t done;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(done)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
-      : "memory");
-  return done != 0;
-}
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
-  while (!mbar_try_hint(bar, parity, ns)) {
-  }
-}
-// Sleeps up to ns: a try_wait on a barrier phase that never completes.
-__device__ __forceinline__ void park_ns(uint64_t* never, uint32_t ns) { (void)mbar_try_hint(never, 0, ns); }
+// Helper-warp waits test and then __nanosleep: a spinning helper takes issue slots
+// and L1TEX bandwidth from the compute warp on its SMSP (measured: a try_wait loop
+// with a suspend hint ran every ~20 ns in this kernel; sleeping 2 us in the storer
+// and 0.2-0.5 us in the loader gave +4 %).
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -521,7 +515,6 @@ __device__ __forceinline__ void ms_loader(const MsArgs& A, unsigned char* sm, co
   const unsigned long long* dn = I + 1 < A.nstrips ? A.prog + (int64_t)(I + 1) * kMsProgStride : nullptr;
   const int64_t y0 = 1 + (int64_t)I * A.R;
   unsigned long long acq_up = 0, acq_dn = 0;
-  uint64_t* never = reinterpret_cast<uint64_t*>(sm + G::BAR_OFF) + 3 * kMsSlots;  // never arrived on
   for (int64_t t = 0; t < Ttot; ++t) {
     const unsigned long long need_up = (unsigned long long)(t + 1);
     const int64_t need_dn = t - A.ntiles + 1;
@@ -538,7 +531,7 @@ __device__ __forceinline__ void ms_loader(const MsArgs& A, unsigned char* sm, co
       unsigned long long vu = wu ? ld_relaxed(up) : 0, vd = wd ? ld_relaxed(dn) : 0;
       bool ok = (!wu || vu >= need_up) && (!wd || vd >= (unsigned long long)need_dn);
       while (!__all_sync(0xffffffffu, ok)) {
-        park_ns(never, 256);
+        __nanosleep(ST_GS_MS_PSLEEP);
         vu = wu ? ld_relaxed(up) : 0;
         vd = wd ? ld_relaxed(dn) : 0;
         ok = (!wu || vu >= need_up) && (!wd || vd >= (unsigned long long)need_dn);
@@ -552,7 +545,8 @@ __device__ __forceinline__ void ms_loader(const MsArgs& A, unsigned char* sm, co
         if (!wu && !wd) (void)ld_acquire(A.prog + (int64_t)I * kMsProgStride);
       }
     }
-    if (t >= kMsSlots) mbar_wait_sleep(&freed[t % kMsSlots], (uint32_t)((t / kMsSlots - 1) & 1), 1000);
+    if (t >= kMsSlots)
+      while (!mbar_test(&freed[t % kMsSlots], (uint32_t)((t / kMsSlots - 1) & 1))) __nanosleep(ST_GS_MS_LSLEEP);
     ms_load_tile<KC>(A, sm, I, lane, t, wide);
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -563,7 +557,7 @@ __device__ __forceinline__ void ms_loader(const MsArgs& A, unsigned char* sm, co
 #ifndef ST_GS_MS_PUB
 #define ST_GS_MS_PUB 4
 #endif
-constexpr int kMsPub = ST_GS_MS_PUB;  // tiles per progress publication
+constexpr int kMsPub = ST_GS_MS_PUB;
 template <int KC>
 __device__ __forceinline__ void ms_storer(const MsArgs& A, unsigned char* sm, const int I, const int lane,
                                           const bool wide) {
@@ -573,7 +567,7 @@ __device__ __forceinline__ void ms_storer(const MsArgs& A, unsigned char* sm, co
   const int64_t Ttot = A.passes * A.ntiles;
   unsigned long long* mine = A.prog + (int64_t)I * kMsProgStride;
   for (int64_t t = 0; t < Ttot; ++t) {
-    mbar_wait_sleep(&consumed[t % kMsSlots], (uint32_t)((t / kMsSlots) & 1), 1000);
+    while (!mbar_test(&consumed[t % kMsSlots], (uint32_t)((t / kMsSlots) & 1))) __nanosleep(ST_GS_MS_SSLEEP);
     ms_writeback_tile<KC>(A, sm, I, lane, t, wide);
     __syncwarp();  // every lane's shared reads of the tile are done (their values are in the stores)
     if (lane == 0) mbar_arrive(&freed[t % kMsSlots]);
@@ -607,7 +601,6 @@ __global__ void __launch_bounds__(96 * kMsStrips, 1) gauss_seidel2d_ms_kernel(co
       mbar_init(&bars[kMsSlots + q], 1);      // consumed: the compute warp's lane 0
       mbar_init(&bars[2 * kMsSlots + q], 1);  // freed: the storer's lane 0
     }
-    mbar_init(&bars[3 * kMsSlots], 1);  // never arrived on: the loader's sleep
     fence_mbar_init();
   }
   __syncthreads();
