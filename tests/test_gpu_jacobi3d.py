@@ -113,3 +113,25 @@ def test_fast_div6_is_correctly_rounded(cuda_lib):
             edge += [(e << 52) | m, (1 << 63) | (e << 52) | m]
     ev = torch.from_numpy(np.array(edge, dtype=np.uint64).view(np.float64)).cuda()
     assert cuda_lib.st_selftest_div6(ev) == 0
+
+
+@pytest.mark.parametrize("tblock", [1, 2])
+@pytest.mark.parametrize("shape", [(150, 37, 23), (129, 17, 40)])
+def test_quotients_outside_the_fast_division_range(cuda_lib, tblock, shape):
+    # sums that leave ddiv6's fast range (zero, subnormal/tiny, huge, non-finite) take the
+    # exact division: per quotient (T = 1) or by the deferred per-plane check of the
+    # two-sweep kernel, which recomputes a plane when any quotient of the CTA was out of range
+    import torch
+    nx, ny, nz = shape
+    g = si.jacobi3d_grid(nx, ny, nz).copy()
+    g[3:6, 2:9, 10:40] = 0.0                       # zero sums
+    g[8:11, 5:15, 60:100] *= 2.0 ** -1040          # subnormal neighbourhoods
+    g[12:14, 20:30, 5:30] *= 2.0 ** 1021           # near overflow (sums overflow to inf)
+    g[15, 3, 7] = float("inf")
+    g[16, 4, 8] = -0.0
+    want = oracle.jacobi3d(g, 4)
+    a = torch.from_numpy(g).cuda()
+    r = cuda_lib.st_jacobi3d_run(a, torch.full_like(a, float("nan")), 4, tblock=tblock)
+    torch.cuda.synchronize()
+    got = r.cpu().numpy()
+    assert np.array_equal(got, want, equal_nan=True)
