@@ -64,7 +64,10 @@ constexpr int kMsStrips = 4;          // strips (compute warps) per CTA; warps 4
 constexpr int kMsTW = 16;             // tile width (columns) = steps per compute group
 constexpr int kMsSlots = 10;          // tiles in the ring per strip
 constexpr int kMsNP = kMsTW * kMsSlots;  // ring positions per row
-constexpr int kMsP = 2;               // shared-memory prefetch distance (steps)
+#ifndef ST_GS_MS_P
+#define ST_GS_MS_P 2
+#endif
+constexpr int kMsP = ST_GS_MS_P;      // shared-memory prefetch distance (steps)
 constexpr int kMsProgStride = 16;     // u64 per progress word (one 128-byte line each)
 constexpr int kMsMinTiles = 24;       // narrower grids take the single-sweep kernel (helper/compute coupling)
 // helper wait loops sleep between tests (ns): a spinning helper takes issue slots and
