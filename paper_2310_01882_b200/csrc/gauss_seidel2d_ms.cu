@@ -41,12 +41,14 @@
 // computes in one step — into a global edge buffer. The ghost rows read the
 // strip below's rows as of the previous pass, which that strip writes back.
 //
-// Warp roles. A CTA holds 4 strips: warps 0..3 compute, warps 4..7 are their
-// helpers (so SMSP w % 4 runs one compute warp and one helper). A helper
-// streams 32-column tiles of its strip's 33 rows into a 5-tile shared-memory
-// ring (cp.async, completion on an mbarrier), writes finished tiles back, copies
-// edge entries out, and publishes progress (fence + flag): the compute warp
-// never waits on global memory or a fence. Tile rows are stored rotated (column
+// Warp roles. A CTA holds 4 strips, each served by three warps: compute (warp
+// ids 8..11), loader (4..7) and storer (0..3), so SMSP w % 4 runs one of each.
+// The loader streams 16-column tiles of the strip's 33 rows and the above
+// entries into a 10-tile shared-memory ring (16-byte cp.async, completion on an
+// mbarrier) once the neighbours' progress words allow; the storer writes
+// finished tiles back, copies edge entries out and publishes progress (release
+// store): the compute warp never waits on global memory or a fence. Helpers
+// sleep between tests of their waits. Tile rows are stored rotated (column
 // c of row rho at ring position c + rho + 2KC - 4) so every shared-memory access
 // of the compute warp is lane-independent: one base register per group plus an
 // immediate offset (a mirrored tail absorbs the ring wrap inside a group).
@@ -60,7 +62,7 @@ namespace st {
 
 namespace {
 
-constexpr int kMsStrips = 4;          // strips (compute warps) per CTA; warps 4..7 are the helpers
+constexpr int kMsStrips = 4;          // strips per CTA (compute warps 8..11, loaders 4..7, storers 0..3)
 constexpr int kMsTW = 16;             // tile width (columns) = steps per compute group
 constexpr int kMsSlots = 10;          // tiles in the ring per strip
 constexpr int kMsNP = kMsTW * kMsSlots;  // ring positions per row
@@ -80,14 +82,14 @@ constexpr int kMsMinTiles = 24;       // narrower grids take the single-sweep ke
 #endif
 #ifndef ST_GS_MS_PSLEEP
 #define ST_GS_MS_PSLEEP 200   // loader, neighbour progress polls
-#endif  // tiles per progress publication
+#endif
 constexpr int kMsEdgePad = 8;         // edge entries per strip: columns 0 .. nx + 2K - 2 (< nx + 8)
 
 template <int KC>
 struct MsGeo {
   static constexpr int kEntD = KC == 1 ? 2 : KC == 3 ? 4 : KC;  // doubles per edge entry (a 16-byte multiple)
   static constexpr int EB = 8 * kEntD;
-  static constexpr int MIR = kMsP + 2 * KC + 1;    // mirrored tail of a tile row (reads reach base+31+P+2KC-2)
+  static constexpr int MIR = kMsP + 2 * KC + 1;    // mirrored tail of a tile row (reads reach base+TW-1+P+2KC-2)
   static constexpr int L = (kMsNP + MIR + 1) | 1;  // row length in doubles, odd: conflict-free column access
   static constexpr int ROWB = 8 * L;
   static constexpr int TILE_B = 33 * ROWB;
@@ -176,9 +178,6 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -191,7 +190,7 @@ struct MsArgs {
   int R;           // rows owned by every strip but the last (= 33 - K of the run)
   int nstrips, ntiles;
   unsigned long long* prog;  // prog[I * kMsProgStride] = tiles of strip I written back and edge-published
-  char* edge;                // edge[I] = (nx + 2) entries of EB bytes
+  char* edge;                // edge[I] = nx + kMsEdgePad entries of EB bytes
   int64_t edge_stride;       // bytes per strip
 };
 
