@@ -555,7 +555,7 @@ __device__ __forceinline__ void ms_loader(const MsArgs& A, unsigned char* sm, co
 }
 
 // Storer warp: writes finished tiles back, frees their slots, and publishes
-// progress (one GPU-scope fence per kMsPub tiles and at the end).
+// progress (a release store of its progress word every kMsPub tiles and at the end).
 #ifndef ST_GS_MS_PUB
 #define ST_GS_MS_PUB 4
 #endif
