@@ -404,13 +404,23 @@ st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
                           int32_t halo, int64_t iters, int32_t tblock, st_comm* comm,
                           void* cuda_stream, int32_t* result_in_b);
 
-/* The 3-D 7-point Jacobi on a pencil block: a, b hold (nz_local+2) planes x
- * (ny_local+2) rows x ldx (one ghost layer in y and z; on the grid's edges the
- * ghost layer is the global Dirichlet face). Before every sweep the y ghost rows
- * and then the z ghost planes are swapped with the 4 grid neighbours (comm set
- * up with st_comm_set_grid; IPC or LOCAL transport). comm NULL: single block. */
+/* The 3-D 7-point Jacobi on a pencil block (the paper's "decompose the 3D
+ * space into two dimensions"): a, b hold (nz_local+2*halo)
+ * planes x (ny_local+2*halo) rows x ldx (halo ghost layers in y and z; on the
+ * grid's edges the ghost layer next to the block holds the global Dirichlet
+ * face). Before every pass the halo y ghost rows and then the halo z ghost
+ * planes are swapped with the 4 grid neighbours (comm set up with
+ * st_comm_set_grid; IPC or LOCAL transport; NCCL -> ST_ENOTSUP), overlapped
+ * with the part of the block that reads no ghost.
+ *   halo     1 or 2 (<= ny_local, nz_local); 1 without a comm.
+ *   tblock   1 = one sweep per pass; 2 = two sweeps per pass (needs halo 2:
+ *            the first sweep also runs on the first ghost layer); 0 = auto
+ *            (2 if halo >= 2). Bitwise the same result either way.
+ *   comm NULL: single block (st_jacobi3d_run).
+ *   *result_in_b (may be NULL) = iters & 1. */
 st_status st_jacobi3d_run_pencils(double* a, double* b, int64_t nx, int64_t ny_local, int64_t nz_local, int64_t ldx,
-                                  int64_t iters, st_comm* comm, void* cuda_stream, int32_t* result_in_b);
+                                  int32_t halo, int64_t iters, int32_t tblock, st_comm* comm, void* cuda_stream,
+                                  int32_t* result_in_b);
 
 /* Diagnostic: counts into *mismatches (device, uint64, caller-zeroed) the x[i]
  * (device, n doubles) for which the kernels' fast correctly rounded x/6 differs

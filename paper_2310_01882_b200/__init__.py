@@ -102,7 +102,7 @@ _SIGS = {
     "st_gauss_seidel2d_run": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp]),
     "st_comm_set_grid": (ctypes.c_int, [_vp, _i32, _i64]),
     "st_pencil_split": (ctypes.c_int, [_i64, _i64, _i32, _i32, _i32] + [ctypes.POINTER(_i64)] * 4),
-    "st_jacobi3d_run_pencils": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp,
+    "st_jacobi3d_run_pencils": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i64, _i32, _vp, _vp,
                                                ctypes.POINTER(_i32)]),
     "st_pw_advect3d_pencils": (ctypes.c_int, [_vp] * 6 + [_i64] * 4 + [_dbl, _dbl] + [_vp] * 4 + [_vp, _vp]),
     "st_pw_advect3d": (ctypes.c_int, [_vp] * 6 + [_i64] * 4 + [_dbl, _dbl] + [_vp] * 4 + [_vp, _vp]),
@@ -373,17 +373,19 @@ def st_jacobi3d_run(a, b, iters: int, tblock: int = 0, halo: int = 1, comm: Comm
     return b if rib.value else a
 
 
-def st_jacobi3d_run_pencils(a, b, iters: int, comm: Comm | None = None, nx: int | None = None, stream=None):
-    """3-D Jacobi on a pencil block (nz_local+2, ny_local+2, ldx); see include/libstencil.h."""
+def st_jacobi3d_run_pencils(a, b, iters: int, comm: Comm | None = None, nx: int | None = None, halo: int = 1,
+                            tblock: int = 0, stream=None):
+    """3-D Jacobi on a pencil block (nz_local+2*halo, ny_local+2*halo, ldx); see include/libstencil.h."""
     _f64_cuda(a, "a")
     _f64_cuda(b, "b")
     if a.dim() != 3 or a.shape != b.shape or not a.is_contiguous() or not b.is_contiguous():
         raise ValueError("a, b: contiguous 3-D tensors of equal shape")
-    nzl, nyl, ldx = a.shape[0] - 2, a.shape[1] - 2, a.shape[2]
+    nzl, nyl, ldx = a.shape[0] - 2 * halo, a.shape[1] - 2 * halo, a.shape[2]
     nx = ldx - 2 if nx is None else nx
     rib = _i32()
-    _check(lib().st_jacobi3d_run_pencils(a.data_ptr(), b.data_ptr(), nx, nyl, nzl, ldx, iters, _comm_ptr(comm),
-                                         _stream_ptr(stream), ctypes.byref(rib)), "st_jacobi3d_run_pencils")
+    _check(lib().st_jacobi3d_run_pencils(a.data_ptr(), b.data_ptr(), nx, nyl, nzl, ldx, halo, iters, tblock,
+                                         _comm_ptr(comm), _stream_ptr(stream), ctypes.byref(rib)),
+           "st_jacobi3d_run_pencils")
     return b if rib.value else a
 
 

@@ -423,15 +423,27 @@ st_status st_jacobi3d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t 
 }
 
 st_status st_jacobi3d_run_pencils(double* a, double* b, int64_t nx, int64_t nyl, int64_t nzl, int64_t ldx,
-                                  int64_t iters, st_comm* comm, void* cuda_stream, int32_t* result_in_b) {
+                                  int32_t halo, int64_t iters, int32_t tblock, st_comm* comm, void* cuda_stream,
+                                  int32_t* result_in_b) {
   clear_error();
-  if (!comm || comm->nranks == 1) return st_jacobi3d_run(a, b, nx, nyl, nzl, ldx, 1, iters, 1, nullptr, cuda_stream,
-                                                         result_in_b);
+  if (!comm || comm->nranks == 1) {
+    ST_RETURN_IF(halo != 1, ST_EINVAL, "st_jacobi3d_run_pencils: halo must be 1 without a comm");
+    return st_jacobi3d_run(a, b, nx, nyl, nzl, ldx, 1, iters, tblock, nullptr, cuda_stream, result_in_b);
+  }
   ST_RETURN_IF(!a || !b || nx < 1 || nyl < 1 || nzl < 1 || iters < 0, ST_EINVAL,
                "st_jacobi3d_run_pencils: bad arguments");
+  ST_RETURN_IF(halo < 1 || halo > 2 || nyl < halo || nzl < halo, ST_EINVAL,
+               "st_jacobi3d_run_pencils: halo %d (1 or 2, <= the block's %lld rows and %lld planes)", halo,
+               (long long)nyl, (long long)nzl);
+  ST_RETURN_IF(tblock < 0 || tblock > 2, ST_ENOTSUP, "st_jacobi3d_run_pencils: tblock=%d not supported (0, 1, 2)",
+               tblock);
+  ST_RETURN_IF(tblock == 2 && halo < 2, ST_EINVAL, "st_jacobi3d_run_pencils: tblock=2 needs halo >= 2");
   ST_RETURN_IF(ldx < nx + 2 || (ldx & 1) || !aligned16(a) || !aligned16(b), ST_EINVAL,
                "st_jacobi3d_run_pencils: ldx even >= nx+2, 16-byte aligned fields");
-  const size_t bytes = (size_t)(nzl + 2) * (size_t)(nyl + 2) * (size_t)ldx * sizeof(double);
+  const int64_t H = halo, nyb = nyl + 2 * H, nb = nzl + 2 * H;
+  ST_RETURN_IF(nx + 2 > (int64_t)INT32_MAX || nyb > (int64_t)INT32_MAX || nb > (int64_t)INT32_MAX, ST_EINVAL,
+               "st_jacobi3d_run_pencils: extents exceed TMA coordinate range");
+  const size_t bytes = (size_t)nb * (size_t)nyb * (size_t)ldx * sizeof(double);
   ST_RETURN_IF(overlaps(a, bytes, b, bytes), ST_EINVAL, "st_jacobi3d_run_pencils: a and b overlap");
   ST_TRY(check_device_ptr(a, "a"));
   ST_TRY(check_device_ptr(b, "b"));
@@ -439,29 +451,63 @@ st_status st_jacobi3d_run_pencils(double* a, double* b, int64_t nx, int64_t nyl,
   if (result_in_b) *result_in_b = (int32_t)(iters & 1);
   if (iters == 0) return ST_OK;
   cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
-  // ghost / Dirichlet shell a -> b: planes 0 and nzl+1, side faces (x and y) of the owned planes
+  // passes: the single-domain schedule's (two sweeps per pass where tblock allows; parity
+  // kept so the result lands in b iff iters is odd)
+  const int32_t T = tblock == 0 ? (halo >= 2 ? 2 : 1) : tblock;
+  std::vector<st_op> ops;
+  ST_TRY(build_jacobi_schedule(0, 1, nx, nzl, 1, iters, T, ops, 3));
+  // ghost / Dirichlet shell a -> b (the global boundary faces of an edge block live in its
+  // ghost layer; interior ghosts are refreshed before every pass)
   const size_t pitch = (size_t)ldx * sizeof(double), width = (size_t)(nx + 2) * sizeof(double);
-  const int64_t plane = (nyl + 2) * ldx;
-  ST_CHECK_CUDA(cudaMemcpy2DAsync(b, pitch, a, pitch, width, (size_t)(nyl + 2), cudaMemcpyDeviceToDevice, s));
-  ST_CHECK_CUDA(cudaMemcpy2DAsync(b + (nzl + 1) * plane, pitch, a + (nzl + 1) * plane, pitch, width,
-                                  (size_t)(nyl + 2), cudaMemcpyDeviceToDevice, s));
-  ST_TRY(jacobi3d_copy_faces(a, b, nx, nyl, ldx, 1, nzl, s));
+  const int64_t plane = nyb * ldx;
+  if (H == 1) {
+    ST_CHECK_CUDA(cudaMemcpy2DAsync(b, pitch, a, pitch, width, (size_t)nyb, cudaMemcpyDeviceToDevice, s));
+    ST_CHECK_CUDA(cudaMemcpy2DAsync(b + (nzl + 1) * plane, pitch, a + (nzl + 1) * plane, pitch, width, (size_t)nyb,
+                                    cudaMemcpyDeviceToDevice, s));
+    ST_TRY(jacobi3d_copy_faces(a, b, nx, nyl, ldx, 1, nzl, s));
+  } else {
+    ST_CHECK_CUDA(cudaMemcpy2DAsync(b, pitch, a, pitch, width, (size_t)(nb * nyb), cudaMemcpyDeviceToDevice, s));
+  }
+  // Dirichlet rows / planes of the first sweep of a two-sweep pass: the global boundary (in
+  // the ghost layer next to the block) on the grid's edges; none elsewhere (ghosts are swept)
+  const int32_t py = comm->grid_py, iy = comm->rank % py, iz = comm->rank / py, pz = comm->nranks / py;
+  const int64_t yr_lo = iy == 0 ? H - 1 : -1, yr_hi = iy == py - 1 ? H + nyl : nyb;
+  const int64_t zr_lo = iz == 0 ? H - 1 : -1, zr_hi = iz == pz - 1 ? H + nzl : nb;
+  const int64_t ny_k = nyb - 2;  // the kernels address ny_k + 2 rows per plane
+  // one pass over the output block [z0, z1] x [y0, y1] (buffer coordinates)
+  auto pass = [&](const double* src, double* dst, int sweeps, int64_t z0, int64_t z1, int64_t y0,
+                  int64_t y1) -> st_status {
+    if (z1 < z0 || y1 < y0) return ST_OK;
+    if (sweeps == 2)
+      return jacobi3d_two_sweeps_block(src, dst, nx, ny_k, nb, ldx, z0, z1, zr_lo, zr_hi, y0, y1, yr_lo, yr_hi, s);
+    return jacobi3d_sweep_block(src, dst, nx, ny_k, nb, ldx, z0, z1, y0, y1, s);
+  };
   double* src = a;
   double* dst = b;
-  const int64_t nb = nzl + 2;
-  for (int64_t it = 0; it < iters; ++it) {
+  for (const st_op& o : ops) {
+    if (o.kind != ST_OP_SWEEP) continue;
+    const int64_t d = o.sweeps;  // the ghost depth one pass reads
     // the y/z ghost swap runs on the comm stream while the block that reads no ghost
-    // (planes 2..nzl-1 x rows 2..nyl-1) is swept; then the shell: planes 1 and nzl,
-    // and rows 1 and nyl of the planes between
-    ST_TRY(pencil_exchange_async(comm, &src, 1, nx, nyl, nzl, ldx, s, false));
-    ST_TRY(jacobi3d_sweep_block(src, dst, nx, nyl, nb, ldx, 2, nzl - 1, 2, nyl - 1, s));
+    // (d layers in from every side) is swept; then the shell
+    ST_TRY(pencil_exchange_async(comm, &src, 1, nx, nyl, nzl, ldx, halo, s, false));
+    const int64_t zi0 = H + d, zi1 = H + nzl - 1 - d, yi0 = H + d, yi1 = H + nyl - 1 - d;
+    cudaEvent_t p0 = prof_mark(comm, s);
+    const bool split = zi1 >= zi0 && yi1 >= yi0;
+    if (split) ST_TRY(pass(src, dst, (int)d, zi0, zi1, yi0, yi1));
+    cudaEvent_t p1 = prof_mark(comm, s);
+    prof_add(comm, ST_PHASE_INTERIOR, p0, p1);
     ST_CHECK_CUDA(cudaStreamWaitEvent(s, comm->ev_done, 0));
-    ST_TRY(jacobi3d_sweep_block(src, dst, nx, nyl, nb, ldx, 1, 1, 1, nyl, s));
-    if (nzl > 1) ST_TRY(jacobi3d_sweep_block(src, dst, nx, nyl, nb, ldx, nzl, nzl, 1, nyl, s));
-    if (nzl > 2) {
-      ST_TRY(jacobi3d_sweep_block(src, dst, nx, nyl, nb, ldx, 2, nzl - 1, 1, 1, s));
-      if (nyl > 1) ST_TRY(jacobi3d_sweep_block(src, dst, nx, nyl, nb, ldx, 2, nzl - 1, nyl, nyl, s));
+    cudaEvent_t p2 = prof_mark(comm, s);
+    prof_add(comm, ST_PHASE_JOIN_WAIT, p1, p2);
+    if (split) {
+      ST_TRY(pass(src, dst, (int)d, H, zi0 - 1, H, H + nyl - 1));              // low z band
+      ST_TRY(pass(src, dst, (int)d, zi1 + 1, H + nzl - 1, H, H + nyl - 1));    // high z band
+      ST_TRY(pass(src, dst, (int)d, zi0, zi1, H, yi0 - 1));                    // low y band
+      ST_TRY(pass(src, dst, (int)d, zi0, zi1, yi1 + 1, H + nyl - 1));          // high y band
+    } else {
+      ST_TRY(pass(src, dst, (int)d, H, H + nzl - 1, H, H + nyl - 1));
     }
+    prof_add(comm, ST_PHASE_BOUNDARY, p2, prof_mark(comm, s));
     double* t = src;
     src = dst;
     dst = t;
@@ -488,7 +534,7 @@ st_status st_pw_advect3d_pencils(double* u, double* v, double* w, double* su, do
   // while the block that reads none (planes 2..nzl-1 x rows 2..nyl-1) is advected; then
   // the shell
   double* f[3] = {u, v, w};
-  ST_TRY(pencil_exchange_async(comm, f, 3, nx, nyl, nzl, ldx, s, false));
+  ST_TRY(pencil_exchange_async(comm, f, 3, nx, nyl, nzl, ldx, 1, s, false));
   PwArgs args{u, v, w, su, sv, sw, nx, nyl, nzl, ldx, tcx, tcy, tzc1, tzc2, tzd1, tzd2};
   auto window = [&](int64_t z0, int64_t z1, int64_t y0, int64_t y1) {
     PwArgs a = args;

@@ -208,7 +208,7 @@ st_status local_exchange(st_comm* c, double* const* fields, int32_t nfields, int
 }  // namespace
 
 st_status pencil_exchange_async(st_comm* c, double* const* fields, int32_t nfields, int64_t nx, int64_t nyl,
-                                int64_t nzl, int64_t ldx, cudaStream_t main, bool join) {
+                                int64_t nzl, int64_t ldx, int32_t h, cudaStream_t main, bool join) {
   ST_RETURN_IF(c->kind == st_comm::NCCL, ST_ENOTSUP, "pencil decomposition needs the IPC or LOCAL transport");
   ST_RETURN_IF(c->broken, ST_ENCCL, "st_comm is unusable after an earlier error or timeout");
   ST_RETURN_IF(c->grid_py < 1 || c->nranks % c->grid_py != 0, ST_EINVAL, "pencils: st_comm_set_grid first");
@@ -216,6 +216,8 @@ st_status pencil_exchange_async(st_comm* c, double* const* fields, int32_t nfiel
   ST_RETURN_IF(nyl != c->n_mid || nzl != c->bound_n_slow, ST_EINVAL, "pencils: block %lldx%lld, bound %lldx%lld",
                (long long)nyl, (long long)nzl, (long long)c->n_mid, (long long)c->bound_n_slow);
   ST_RETURN_IF(nfields > 8, ST_EINVAL, "pencils: at most 8 fields per swap");
+  ST_RETURN_IF(h < 1 || h > nyl || h > nzl, ST_EINVAL, "pencils: ghost depth %d vs a %lldx%lld block", h,
+               (long long)nyl, (long long)nzl);
   int idx[8];
   for (int f = 0; f < nfields; ++f) {
     idx[f] = -1;
@@ -226,8 +228,9 @@ st_status pencil_exchange_async(st_comm* c, double* const* fields, int32_t nfiel
   const int32_t py = c->grid_py, iy = c->rank % py, iz = c->rank / py, pz = c->nranks / py;
   const uint32_t k = ++c->seq;
   cudaStream_t cs = c->comm_stream;
-  const size_t row_bytes = (size_t)(nx + 2) * sizeof(double);
-  const int64_t my_plane = (nyl + 2) * ldx;
+  // h rows of a plane: one span from the first row's column 0 to the last row's column nx+1
+  const size_t rows_bytes = (size_t)((h - 1) * ldx + nx + 2) * sizeof(double);
+  const int64_t my_plane = (nyl + 2 * (int64_t)h) * ldx;
   ST_CHECK_CUDA(cudaEventRecord(c->ev_ready, main));
   ST_CHECK_CUDA(cudaStreamWaitEvent(cs, c->ev_ready, 0));
   cudaEvent_t p0 = prof_mark(c, cs);
@@ -244,38 +247,38 @@ st_status pencil_exchange_async(st_comm* c, double* const* fields, int32_t nfiel
       ST_TRY(stream_write(cs, pc.flags + (side == 0 ? kFlagReadyFromHi : kFlagReadyFromLo), k));
     }
   }
-  // phase y: one boundary row per plane into the y neighbours' ghost rows. The
+  // phase y: h boundary rows per plane into the y neighbours' ghost rows. The
   // planes that are z ghosts (filled whole by phase z, possibly concurrently)
   // are skipped; the z-halo planes of the grid's z edges are global boundary
   // planes and are included (the diagonal PW offsets read their corners).
   // y neighbours share this rank's z range, so they skip the same planes.
-  const int64_t zlo = iz > 0 ? 1 : 0, zhi = iz < pz - 1 ? nzl : nzl + 1;
+  const int64_t zlo = iz > 0 ? h : 0, zhi = iz < pz - 1 ? h + nzl - 1 : nzl + 2 * (int64_t)h - 1;
   for (int side = 0; side < 2; ++side) {
     if ((side == 0 && iy == 0) || (side == 1 && iy == py - 1)) continue;
     st_peer pc;
     ST_TRY(peer_of(c, side == 0 ? c->rank - 1 : c->rank + 1, &pc));
     ST_TRY(stream_wait_geq(cs, c->flags + (side == 0 ? kFlagReadyFromYLo : kFlagReadyFromYHi), k));
-    const int64_t peer_plane = (pc.n_mid + 2) * ldx;
-    const int64_t src_row = side == 0 ? 1 : nyl, dst_row = side == 0 ? pc.n_mid + 1 : 0;
+    const int64_t peer_plane = (pc.n_mid + 2 * (int64_t)h) * ldx;
+    const int64_t src_row = side == 0 ? h : nyl, dst_row = side == 0 ? pc.n_mid + h : 0;
     for (int f = 0; f < nfields; ++f)
       ST_CHECK_CUDA(cudaMemcpy2DAsync(pc.bound[(size_t)idx[f]] + zlo * peer_plane + dst_row * ldx,
                                       (size_t)peer_plane * sizeof(double), fields[f] + zlo * my_plane + src_row * ldx,
-                                      (size_t)my_plane * sizeof(double), row_bytes, (size_t)(zhi - zlo + 1),
+                                      (size_t)my_plane * sizeof(double), rows_bytes, (size_t)(zhi - zlo + 1),
                                       cudaMemcpyDefault, cs));
     ST_TRY(stream_write(cs, pc.flags + (side == 0 ? kFlagDoneFromYHi : kFlagDoneFromYLo), k));
   }
   if (iy > 0) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromYLo, k));
   if (iy < py - 1) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromYHi, k));
-  // phase z: whole boundary planes (rows 0..nyl+1, i.e. with the fresh y ghosts)
+  // phase z: h whole boundary planes (all rows, i.e. with the fresh y ghosts)
   for (int side = 0; side < 2; ++side) {
     if ((side == 0 && iz == 0) || (side == 1 && iz == pz - 1)) continue;
     st_peer pc;
     ST_TRY(peer_of(c, side == 0 ? c->rank - py : c->rank + py, &pc));
     ST_TRY(stream_wait_geq(cs, c->flags + (side == 0 ? kFlagReadyFromLo : kFlagReadyFromHi), k));
-    const int64_t src_plane = side == 0 ? 1 : nzl, dst_plane = side == 0 ? pc.n_slow + 1 : 0;
+    const int64_t src_plane = side == 0 ? h : nzl, dst_plane = side == 0 ? pc.n_slow + h : 0;
     for (int f = 0; f < nfields; ++f)
       ST_CHECK_CUDA(cudaMemcpyAsync(pc.bound[(size_t)idx[f]] + dst_plane * my_plane, fields[f] + src_plane * my_plane,
-                                    (size_t)my_plane * sizeof(double), cudaMemcpyDefault, cs));
+                                    (size_t)h * (size_t)my_plane * sizeof(double), cudaMemcpyDefault, cs));
     ST_TRY(stream_write(cs, pc.flags + (side == 0 ? kFlagDoneFromHi : kFlagDoneFromLo), k));
   }
   if (iz > 0) ST_TRY(stream_wait_geq(cs, c->flags + kFlagDoneFromLo, k));

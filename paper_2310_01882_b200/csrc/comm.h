@@ -96,10 +96,11 @@ st_status fused_halo_begin(st_comm* comm, double* dst, int64_t n, cudaStream_t m
 st_status fused_halo_signal(st_comm* comm, cudaStream_t main);
 st_status fused_halo_join(st_comm* comm, cudaStream_t main);
 
-// Pencil halo swap (LOCAL/IPC): y rows of every plane with the y neighbours,
-// then whole planes with the z neighbours (corner ghosts included).
+// Pencil halo swap (LOCAL/IPC), ghost depth h (block of (nzl+2h) planes x (nyl+2h)
+// rows): h boundary rows of every plane with the y neighbours, then h whole planes
+// with the z neighbours (corner ghosts included).
 st_status pencil_exchange_async(st_comm* comm, double* const* fields, int32_t nfields, int64_t nx, int64_t nyl,
-                                int64_t nzl, int64_t ldx, cudaStream_t main, bool join);
+                                int64_t nzl, int64_t ldx, int32_t h, cudaStream_t main, bool join);
 
 // Phase profiler: prof_mark records a timing event on `s` (nullptr when profiling is
 // off); prof_add files the interval [a, b] under `phase`.

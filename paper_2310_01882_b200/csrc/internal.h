@@ -126,6 +126,13 @@ st_status jacobi3d_preload();
 st_status jacobi3d_two_sweeps(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
                               int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi,
                               cudaStream_t s, Remote rem = Remote());
+// the same for the output rows [y_lo, y_hi] only (a pencil block: the buffer has ny+2 rows per
+// plane; rows <= yring_lo / >= yring_hi are Dirichlet, the others of the first sweep's region
+// are swept — ghost rows included)
+st_status jacobi3d_two_sweeps_block(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
+                                    int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi,
+                                    int64_t y_lo, int64_t y_hi, int64_t yring_lo, int64_t yring_hi, cudaStream_t s,
+                                    Remote rem = Remote());
 st_status stencil2d_preload();
 st_status pw_advect3d_preload();
 inline st_status preload_kernels() {

@@ -205,13 +205,20 @@ struct J3T2Tile {
   static constexpr int kL0 = LX * LY;
 };
 
-template <int BX, int BY, int S, int R, bool kRem>
+template <int BX, int BY, int S, int R, bool kRem, bool kWin>
 __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
     jacobi3d_t2_kernel(const __grid_constant__ CUtensorMap tm, double* __restrict__ dst, int64_t nx, int64_t ny,
                        int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi,
-                       int64_t planes_per_chunk, double* __restrict__ dst2, int64_t delta2) {
+                       int64_t planes_per_chunk, double* __restrict__ dst2, int64_t delta2, int64_t y_lo,
+                       int64_t y_hi, int64_t yring_lo, int64_t yring_hi) {
   using T = J3T2Tile<BX, BY>;
   constexpr int NT = (BX / 32) * (BY / R) * 32, WX = BX / 32;
+  if (!kWin) {  // the whole y range, Dirichlet rows 0 and ny+1 (a separate instantiation keeps its registers)
+    y_lo = 1;
+    y_hi = ny;
+    yring_lo = 0;
+    yring_hi = ny + 1;
+  }
   constexpr int kHalo = 2 * T::LX + 2 * BY;  // first-sweep points outside the BX x BY tile
   static_assert(S >= 4 && BY % R == 0 && BX % 32 == 0 && kHalo <= NT, "ring depth / tile shape");
   extern __shared__ __align__(1024) double ring[];  // [S input planes][4 first-sweep planes][S mbarriers]
@@ -222,7 +229,7 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
   const int wx = (threadIdx.x >> 5) % WX;
   const int wy = (threadIdx.x >> 5) / WX;
   const int64_t x0 = 1 + (int64_t)blockIdx.x * BX;
-  const int64_t y0 = 1 + (int64_t)blockIdx.y * BY;
+  const int64_t y0 = y_lo + (int64_t)blockIdx.y * BY;
   const int64_t za = z_lo + (int64_t)blockIdx.z * planes_per_chunk;
   const int64_t zb = min(z_hi, za + planes_per_chunk - 1);
   const int np = (int)(zb - za + 5);  // input planes za-2 .. zb+2
@@ -250,8 +257,8 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
   bool ok[R], oring[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    ok[i] = (yb + i <= ny) && (x <= nx);
-    oring[i] = (x == nx + 1) || (yb + i == ny + 1);
+    ok[i] = (yb + i <= y_hi) && (x <= nx);
+    oring[i] = (x == nx + 1) || (kWin ? (yb + i <= yring_lo) || (yb + i >= yring_hi) : yb + i == ny + 1);
   }
   // Halo point (threads < kHalo): rows 0 and LY-1 of the region, then columns 0 and LX-1
   const bool has_h = threadIdx.x < kHalo;
@@ -267,7 +274,8 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
   const int hly = hq / T::LX, hlx = hq - hly * T::LX;
   const int hc = (hly + 1) * T::SX + hlx + 2;
   const int64_t hgx = x0 - 1 + hlx, hgy = y0 - 1 + hly;
-  const bool hring = hgx == 0 || hgx == nx + 1 || hgy == 0 || hgy == ny + 1;
+  const bool hring = hgx == 0 || hgx == nx + 1 ||
+                     (kWin ? hgy <= yring_lo || hgy >= yring_hi : hgy == 0 || hgy == ny + 1);
 
   const int64_t plane_elems = (ny + 2) * ldx;
   double* out = dst + (za * (ny + 2) + yb) * ldx + x;
@@ -365,7 +373,8 @@ __global__ void __launch_bounds__((BX / 32) * (BY / R) * 32)
 
 template <int BX, int BY, int S, int R>
 st_status launch_j3t2(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf, int64_t ldx,
-                      int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi, cudaStream_t s, Remote rem) {
+                      int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi, int64_t y_lo, int64_t y_hi,
+                      int64_t yring_lo, int64_t yring_hi, cudaStream_t s, Remote rem) {
   using T = J3T2Tile<BX, BY>;
   CUtensorMap tm;
   const uint64_t dims[3] = {(uint64_t)(nx + 2), (uint64_t)(ny + 2), (uint64_t)nplanes_buf};
@@ -373,15 +382,18 @@ st_status launch_j3t2(const double* src, double* dst, int64_t nx, int64_t ny, in
   ST_TRY(make_tmap_3d_f64(&tm, src, dims, (uint64_t)ldx * 8, (uint64_t)ldx * 8 * (uint64_t)(ny + 2), box));
   const size_t smem = (size_t)S * T::kPlaneStride * sizeof(double) + 4 * T::kL0 * sizeof(double) +
                       S * sizeof(uint64_t);
-  auto kern = rem.base ? jacobi3d_t2_kernel<BX, BY, S, R, true> : jacobi3d_t2_kernel<BX, BY, S, R, false>;
+  const bool win = y_lo != 1 || y_hi != ny || yring_lo != 0 || yring_hi != ny + 1;
+  ST_RETURN_IF(win && rem.base, ST_ENOTSUP, "jacobi3d: row windows with the fused swap");
+  auto kern = rem.base ? jacobi3d_t2_kernel<BX, BY, S, R, true, false>
+                       : (win ? jacobi3d_t2_kernel<BX, BY, S, R, false, true> : jacobi3d_t2_kernel<BX, BY, S, R, false, false>);
   ST_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t ntx = (nx + BX - 1) / BX, nty = (ny + BY - 1) / BY, nz = z_hi - z_lo + 1;
+  const int64_t ntx = (nx + BX - 1) / BX, nty = (y_hi - y_lo + BY) / BY, nz = z_hi - z_lo + 1;
   static const int kPpc = env_int("ST_J3T2_PLANES", 96);
   const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(kPpc, nz));
   const int64_t nzc = (nz + ppc - 1) / ppc;
   ST_RETURN_IF(nty > 65535 || nzc > 65535, ST_ENOTSUP, "jacobi3d: grid too large");
   kern<<<dim3((unsigned)ntx, (unsigned)nty, (unsigned)nzc), (BX / 32) * (BY / R) * 32, smem, s>>>(tm, dst, nx, ny, ldx, z_lo, z_hi, ring_lo, ring_hi, ppc,
-                                                rem.base, rem.delta);
+                                                rem.base, rem.delta, y_lo, y_hi, yring_lo, yring_hi);
   ST_LAUNCHED();
   return ST_OK;
 }
@@ -391,16 +403,26 @@ st_status jacobi3d_preload() {
   cudaFuncAttributes fa;
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_kernel<128, 8, 8, 2>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_copy_faces_kernel));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 5, 2, false>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 5, 2, true>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 5, 2, false, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 5, 2, true, false>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi3d_t2_kernel<128, 8, 5, 2, false, true>));
   return ST_OK;
 }
 
 st_status jacobi3d_two_sweeps(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
                               int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi,
                               cudaStream_t s, Remote rem) {
-  if (z_hi < z_lo) return ST_OK;
-  return launch_j3t2<128, 8, 5, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, s, rem);  // §6.5
+  return jacobi3d_two_sweeps_block(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, 1, ny, 0, ny + 1,
+                                   s, rem);
+}
+
+st_status jacobi3d_two_sweeps_block(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,
+                                    int64_t ldx, int64_t z_lo, int64_t z_hi, int64_t ring_lo, int64_t ring_hi,
+                                    int64_t y_lo, int64_t y_hi, int64_t yring_lo, int64_t yring_hi, cudaStream_t s,
+                                    Remote rem) {
+  if (z_hi < z_lo || y_hi < y_lo) return ST_OK;
+  return launch_j3t2<128, 8, 5, 2>(src, dst, nx, ny, nplanes_buf, ldx, z_lo, z_hi, ring_lo, ring_hi, y_lo, y_hi,
+                                   yring_lo, yring_hi, s, rem);  // §6.5
 }
 
 st_status jacobi3d_sweep_block(const double* src, double* dst, int64_t nx, int64_t ny, int64_t nplanes_buf,

@@ -128,14 +128,27 @@ def pencils(rank, world, dev, which):
             t[-1] = float("nan")
         return t
 
-    if which == "j3":
+    if which in ("j3", "j3t2"):
+        h = 2 if which == "j3t2" else 1
         g = si.jacobi3d_grid(nx, ny, nz)
-        a = block(g)
+        if h == 1:
+            a = block(g)
+        else:  # two ghost layers (beyond the global grid: NaN), two sweeps per pass
+            gp = np.pad(g, ((1, 1), (1, 1), (0, 0)), constant_values=np.nan)
+            a = torch.from_numpy(np.ascontiguousarray(gp[z0:z0 + nzl + 4, y0:y0 + nyl + 4])).to(dev)
+            if iy > 0:
+                a[:, :2] = float("nan")
+            if iy < py - 1:
+                a[:, -2:] = float("nan")
+            if iz > 0:
+                a[:2] = float("nan")
+            if iz < pz - 1:
+                a[-2:] = float("nan")
         b = torch.full_like(a, float("nan"))
         comm.bind_ipc([a, b], nzl)
-        r = st.st_jacobi3d_run_pencils(a, b, 7, comm=comm, nx=nx)
+        r = st.st_jacobi3d_run_pencils(a, b, 7, comm=comm, nx=nx, halo=h, tblock=h)
         torch.cuda.synchronize()
-        got = [r.cpu().numpy()[1:nzl + 1, 1:nyl + 1, :nx + 2]]
+        got = [r.cpu().numpy()[h:nzl + h, h:nyl + h, :nx + 2]]
         want_full = [oracle.jacobi3d(g, 7, nx=nx)]
         sl = (slice(z0 + 1, z0 + 1 + nzl), slice(y0 + 1, y0 + 1 + nyl), slice(0, nx + 2))
     else:
@@ -262,6 +275,7 @@ def main():
           "j3_h3_t2": lambda: jacobi3d(rank, world, dev, 3, 8, 2),
           "pen_j3": lambda: pencils(rank, world, dev, "j3"),
           "pen_pw": lambda: pencils(rank, world, dev, "pw"),
+          "pen_j3t2": lambda: pencils(rank, world, dev, "j3t2"),
           "c4_bands": lambda: c4_bands(rank, world, dev),
           "c5_planes": lambda: c5_planes(rank, world, dev)}[case]()
     if rank == 0:

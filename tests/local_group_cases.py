@@ -139,24 +139,34 @@ def pencil_block(g, ny, nz, py, pz, r):
     return np.ascontiguousarray(g[z0:z0 + nzl + 2, y0:y0 + nyl + 2]), y0, nyl, z0, nzl
 
 
-def pencils_j3_case(py, pz, nx, ny, nz, iters):
+def pencil_block_h(g, ny, nz, py, pz, r, h):
+    """Rank r's block with h ghost layers in y and z (layers beyond the global grid: NaN)."""
+    y0, nyl, z0, nzl = st.st_pencil_split(ny, nz, py, pz, r)
+    p = h - 1
+    gp = np.pad(g, ((p, p), (p, p), (0, 0)), constant_values=np.nan) if p else g
+    # global row y0 + 1 (the first owned) sits at buffer row h, i.e. gp row y0 + 1 + p
+    return np.ascontiguousarray(gp[z0:z0 + nzl + 2 * h, y0:y0 + nyl + 2 * h]), y0, nyl, z0, nzl
+
+
+def pencils_j3_case(py, pz, nx, ny, nz, iters, halo=1, tblock=0):
     P = py * pz
+    h = halo
     g = si.jacobi3d_grid(nx, ny, nz)
     comms = st.Comm.local_group(P)
     streams = [torch.cuda.Stream() for _ in range(P)]
     ranks = []
     for r in range(P):
-        loc, y0, nyl, z0, nzl = pencil_block(g, ny, nz, py, pz, r)
+        loc, y0, nyl, z0, nzl = pencil_block_h(g, ny, nz, py, pz, r, h)
         a = torch.from_numpy(loc).cuda()
         iy, iz = r % py, r // py
         if iy > 0:
-            a[:, 0] = float("nan")
+            a[:, :h] = float("nan")
         if iy < py - 1:
-            a[:, -1] = float("nan")
+            a[:, -h:] = float("nan")
         if iz > 0:
-            a[0] = float("nan")
+            a[:h] = float("nan")
         if iz < pz - 1:
-            a[-1] = float("nan")
+            a[-h:] = float("nan")
         b = torch.full_like(a, float("nan"))
         comms[r].set_grid(py, nyl)
         comms[r].bind([a, b], nzl)
@@ -166,13 +176,13 @@ def pencils_j3_case(py, pz, nx, ny, nz, iters):
     for r in range(P):
         a, b = ranks[r][:2]
         with torch.cuda.stream(streams[r]):
-            outs.append(st.st_jacobi3d_run_pencils(a, b, iters, comm=comms[r], nx=nx))
+            outs.append(st.st_jacobi3d_run_pencils(a, b, iters, comm=comms[r], nx=nx, halo=h, tblock=tblock))
     torch.cuda.synchronize()
     want = oracle.jacobi3d(g, iters, nx=nx)
     ok = True
     for r in range(P):
         _, _, y0, nyl, z0, nzl = ranks[r]
-        got = outs[r].cpu().numpy()[1:nzl + 1, 1:nyl + 1, :nx + 2]
+        got = outs[r].cpu().numpy()[h:nzl + h, h:nyl + h, :nx + 2]
         ok &= bool(np.array_equal(got, want[z0 + 1:z0 + 1 + nzl, y0 + 1:y0 + 1 + nyl, :nx + 2]))
     for c in comms:
         c.close()
@@ -282,6 +292,14 @@ CASES = {
     "pen_j3_1x2": lambda: pencils_j3_case(1, 2, 70, 40, 33, 6),
     "pen_j3_2x2": lambda: pencils_j3_case(2, 2, 66, 37, 31, 7),
     "pen_j3_3x2": lambda: pencils_j3_case(3, 2, 40, 50, 21, 5),
+    # two sweeps per pass on pencils (ghost depth 2): odd/even sweep counts, blocks thin
+    # enough that the ghost-free interior is empty, ragged tiles in y
+    "pen_j3t2_2x1": lambda: pencils_j3_case(2, 1, 70, 40, 33, 6, halo=2, tblock=2),
+    "pen_j3t2_1x2": lambda: pencils_j3_case(1, 2, 70, 40, 33, 7, halo=2, tblock=2),
+    "pen_j3t2_2x2": lambda: pencils_j3_case(2, 2, 130, 37, 31, 9, halo=2),
+    "pen_j3t2_3x2": lambda: pencils_j3_case(3, 2, 40, 50, 21, 4, halo=2, tblock=2),
+    "pen_j3t2_2x3_thin": lambda: pencils_j3_case(2, 3, 33, 7, 9, 5, halo=2, tblock=2),
+    "pen_j3h2_t1_2x2": lambda: pencils_j3_case(2, 2, 66, 37, 31, 5, halo=2, tblock=1),
     "pen_pw_2x2": lambda: pencils_pw_case(2, 2, 70, 30, 22),
     "pen_pw_3x2": lambda: pencils_pw_case(3, 2, 40, 33, 17),
     "pen_pw_1x3": lambda: pencils_pw_case(1, 3, 40, 20, 25),

@@ -21,7 +21,7 @@ def _port():
 
 CASES = [(w, c, f) for w in (2, 3) for c in ("j2_h1", "j2_h4_t4", "pw", "j3_h1", "j3_h2_t1", "j3_h2_t2", "j3_h3_t2")
          for f in ("1", "0")]
-CASES += [(w, c, "1") for w in (2, 3, 4) for c in ("pen_j3", "pen_pw")]  # pencils: y-z process grids
+CASES += [(w, c, "1") for w in (2, 3, 4) for c in ("pen_j3", "pen_j3t2", "pen_pw")]  # pencils: y-z process grids
 
 
 def _run(world, case, fused, timeout=240):

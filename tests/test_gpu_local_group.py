@@ -16,7 +16,8 @@ HERE = pathlib.Path(__file__).resolve().parent
 @pytest.mark.parametrize("case", ["j2_h1", "j2_p3_h1", "j2_h4_t4", "j2_p4_h6_t6", "j2_p3_h3_t1", "j3_h1", "j3_p3_h2",
                                   "j3_p3_h2_t1", "j3_p2_h2_t2", "j3_p4_h3_t2", "j3_p2_h4_t2",
                                   "pw_p2", "pw_p4", "pen_j3_2x1", "pen_j3_1x2", "pen_j3_2x2", "pen_j3_3x2",
-                                  "pen_pw_2x2", "pen_pw_3x2", "pen_pw_1x3"])
+                                  "pen_j3t2_2x1", "pen_j3t2_1x2", "pen_j3t2_2x2", "pen_j3t2_3x2", "pen_j3t2_2x3_thin",
+                                  "pen_j3h2_t1_2x2", "pen_pw_2x2", "pen_pw_3x2", "pen_pw_1x3"])
 @pytest.mark.parametrize("fused", ["1", "0"])
 def test_local_group_equals_oracle(cuda_lib, case, fused):
     # fused=1: boundary sweeps store straight into the neighbours' ghost rows (NEXT #3);

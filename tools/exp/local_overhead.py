@@ -134,19 +134,22 @@ def jacobi3d(P, n=512, sweeps=100, h=2):
     return n ** 3 * sweeps / (ms / 1e3) / 1e9, ms
 
 
-def pencils_j3(py, pz, n=512, sweeps=50):
-    """3-D Jacobi on a py x pz (y, z) pencil grid of LOCAL ranks (T = 1 sweeps; swap overlapped with the
-    interior block). py = pz = 1: the single domain at tblock = 1 (same sweep kernel, no decomposition)."""
+def pencils_j3(py, pz, n=512, sweeps=50, tblock=1):
+    """3-D Jacobi on a py x pz (y, z) pencil grid of LOCAL ranks (swap overlapped with the interior block;
+    tblock 2: two sweeps per pass on ghost depth 2). py = pz = 1: the single domain at the same tblock
+    (same sweep kernel, no decomposition)."""
     if n not in _G3:
         _G3[n] = torch.from_numpy(si.jacobi3d_grid(n, n, n)).cuda()
     g = _G3[n]
     P = py * pz
+    h = 2 if tblock == 2 and P > 1 else 1
+    gp = torch.nn.functional.pad(g, (0, 0, h - 1, h - 1, h - 1, h - 1)) if h > 1 else g
     comms = st.Comm.local_group(P) if P > 1 else [None]
     streams = [torch.cuda.Stream() for _ in range(P)]
     bufs = []
     for r in range(P):
         y0, nyl, z0, nzl = st.st_pencil_split(n, n, py, pz, r) if P > 1 else (0, n, 0, n)
-        a = g[z0:z0 + nzl + 2, y0:y0 + nyl + 2].contiguous()
+        a = gp[z0:z0 + nzl + 2 * h, y0:y0 + nyl + 2 * h].contiguous()
         b = torch.empty_like(a)
         if comms[r] is not None:
             comms[r].set_grid(py, nyl)
@@ -159,9 +162,9 @@ def pencils_j3(py, pz, n=512, sweeps=50):
             a, b = bufs[r]
             with torch.cuda.stream(streams[r]):
                 if comms[r] is None:
-                    st.st_jacobi3d_run(a, b, sweeps, tblock=1)
+                    st.st_jacobi3d_run(a, b, sweeps, tblock=tblock)
                 else:
-                    st.st_jacobi3d_run_pencils(a, b, sweeps, comm=comms[r], nx=n)
+                    st.st_jacobi3d_run_pencils(a, b, sweeps, comm=comms[r], nx=n, halo=h, tblock=tblock)
 
     ms = timed(run, streams, 2)
     for c in comms:
@@ -210,15 +213,19 @@ def pencils_pw(py, pz, n=512, apps=20):
 if __name__ == "__main__":
     if sys.argv[1:] == ["pencils"]:  # the (y, z) pencil decomposition (NEXT #2) on one GPU
         out = {"what": "LOCAL pencil grids (py x pz) on one B200: throughput at fixed total work vs the single "
-                       "domain with the same sweep kernel (T = 1)", "jacobi3d_512^3_50sw": {}, "pw_512^3": {}}
+                       "domain with the same sweep kernel (T = 1; t2: two sweeps per pass, ghost depth 2)",
+               "jacobi3d_512^3_50sw": {}, "jacobi3d_t2_512^3_50sw": {}, "pw_512^3": {}}
         for py, pz in ((1, 1), (2, 1), (1, 2), (2, 2), (4, 2)):
             v, ms = pencils_j3(py, pz)
             out["jacobi3d_512^3_50sw"][f"{py}x{pz}"] = {"gpts": round(v, 1), "ms": round(ms, 2)}
             print(f"pencils j3 {py}x{pz}: {v:.1f} Gpts/s", file=sys.stderr, flush=True)
+            v, ms = pencils_j3(py, pz, tblock=2)
+            out["jacobi3d_t2_512^3_50sw"][f"{py}x{pz}"] = {"gpts": round(v, 1), "ms": round(ms, 2)}
+            print(f"pencils j3 t2 {py}x{pz}: {v:.1f} Gpts/s", file=sys.stderr, flush=True)
             v, ms = pencils_pw(py, pz)
             out["pw_512^3"][f"{py}x{pz}"] = {"gpts": round(v, 2), "ms_per_app": round(ms, 4)}
             print(f"pencils pw {py}x{pz}: {v:.2f} Gpts/s", file=sys.stderr, flush=True)
-        for k in ("jacobi3d_512^3_50sw", "pw_512^3"):
+        for k in ("jacobi3d_512^3_50sw", "jacobi3d_t2_512^3_50sw", "pw_512^3"):
             base = out[k]["1x1"]["gpts"]
             for g in out[k]:
                 out[k][g]["vs_1x1"] = round(out[k][g]["gpts"] / base, 3)
