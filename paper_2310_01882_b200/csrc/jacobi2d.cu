@@ -551,13 +551,19 @@ __device__ __forceinline__ void tb4_rot_block(Quad (&R)[TbRot<T>::M], TbRing& ri
       sts1(xl + X::off(npar, 0, 0, 1), s0.a.x);
       sts1(xl + X::off(npar, 0, 1, 1), s0.b.y);
     }
+    // exchange loads one level ahead of their use (X[par] was written by the previous step)
+    double wn = lds1(xl + X::off(par, 0, 1, 0)), en = lds1(xl + X::off(par, 0, 0, 2));
 #pragma unroll
     for (int j = 0; j < T; ++j) {
       Quad& n = R[Rot::at(k - 2 * j)];
       const Quad& c = R[Rot::at(k + 1 - 2 * j)];
       const Quad& s = R[Rot::at(j == 0 ? k + 2 : k - 2 * j + 2)];
-      const double w = lds1(xl + X::off(par, j, 1, 0));  // lane-1's b.y
-      const double e = lds1(xl + X::off(par, j, 0, 2));  // lane+1's a.x
+      const double w = wn;  // lane-1's b.y
+      const double e = en;  // lane+1's a.x
+      if (j + 1 < T) {
+        wn = lds1(xl + X::off(par, j + 1, 1, 0));
+        en = lds1(xl + X::off(par, j + 1, 0, 2));
+      }
       n.a.x = dadd(dadd(dadd(n.a.x, s.a.x), w), c.a.y);
       n.a.y = dadd(dadd(dadd(n.a.y, s.a.y), c.a.x), c.b.x);
       n.b.x = dadd(dadd(dadd(n.b.x, s.b.x), c.a.y), c.b.y);
@@ -712,15 +718,15 @@ struct Tb4Grid {
   int64_t n_edge_strips, rows_edge, n_edge;     // edge strips: 0 .. s_lo-1 and s_lo + n_int_strips ..
 };
 
-template <int T>
-__global__ void __launch_bounds__(kStreamThreads, 1)
+template <int T, int W, int kMinBlocks>
+__global__ void __launch_bounds__(32 * W, kMinBlocks)
     jacobi2d_tb4_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
                         int64_t y_lo, int64_t y_hi, Tb4Grid g, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf,
                         double* __restrict__ dst2, int64_t delta2, int fold) {
   static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
   constexpr int kStride = kTbCols - 2 * T;
   const int lane = threadIdx.x & 31;
-  const int64_t item = (int64_t)blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
+  const int64_t item = (int64_t)blockIdx.x * W + (threadIdx.x >> 5);
   int64_t strip, chunk, rpc;
   if (item < g.n_int) {
     strip = g.s_lo + item % g.n_int_strips;
@@ -763,7 +769,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(tb_ring_smem);
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t smem_lane = smem0 + warp * TbRot<T>::RS * 1024 + lane * 16;
-  const uint32_t xl = smem0 + kStreamWarps * TbRot<T>::RS * 1024 + warp * TbX<T>::kBytes + lane * 8;
+  const uint32_t xl = smem0 + W * TbRot<T>::RS * 1024 + warp * TbX<T>::kBytes + lane * 8;
   if (fold && (tb4_item<T, true>(it, src + x, use_rot, smem_lane, xl) || fold == 2)) return;
   tb4_item<T, false>(it, src + x, use_rot, smem_lane, xl);
 }
@@ -773,7 +779,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 // (kEdgeCost), so they get shorter chunks. Warps are resident in waves of
 // num_sms x 8; the chunk counts minimise waves x the longest item (in rotated-row
 // units, warm-up 2T rows included). ST_JACOBI_TB4_ROWS overrides the interior height.
-Tb4Grid tb4_grid(int64_t nxp2, int64_t rows, int T) {
+Tb4Grid tb4_grid(int64_t nxp2, int64_t rows, int T, int64_t warps_per_sm) {
   const int64_t stride = kTbCols - 2 * T;
   const int64_t nstrips = (nxp2 + stride - 1) / stride;
   Tb4Grid g{};
@@ -786,7 +792,7 @@ Tb4Grid tb4_grid(int64_t nxp2, int64_t rows, int T) {
   g.n_edge_strips = nstrips - g.n_int_strips;
   static const int kRows = env_int("ST_JACOBI_TB4_ROWS", 0);
   static const int kEdgeCostPct = env_int("ST_JACOBI_TB4_EDGE_COST", 280);
-  const int64_t slots = (int64_t)num_sms() * kStreamWarps;
+  const int64_t slots = (int64_t)num_sms() * warps_per_sm;
   auto edge_rows_for = [&](int64_t r_int, int64_t* n_chunks) {  // edge items no longer than interior ones
     const int64_t budget = std::max<int64_t>(1, (r_int + 2 * T) * 100 / kEdgeCostPct - 2 * T);
     const int64_t ne = (rows + budget - 1) / budget;
@@ -816,24 +822,35 @@ Tb4Grid tb4_grid(int64_t nxp2, int64_t rows, int T) {
   return g;
 }
 
+// Resident warps per SM of an instantiation: W warps per CTA x kMinBlocks CTAs
+// (the register budget is 65536 / (32 W kMinBlocks)). Only 8 x 1 is built: 4 x 3
+// (T = 6, 168 registers) and 4 x 4 (T = 4, 128 registers) measured slower — the
+// extra warps queue on the shared-memory pipe (row ring + exchange).
+template <int T, int W, int kMinBlocks>
+st_status launch_tb4_occ(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
+                         int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem, int fold) {
+  const int64_t nxp2 = nx + 2;
+  const Tb4Grid g = tb4_grid(nxp2, y_hi - y_lo + 1, T, W * kMinBlocks);
+  const int64_t blocks = (g.n_int + g.n_edge + W - 1) / W;
+  ST_RETURN_IF(blocks > INT32_MAX, ST_ENOTSUP, "jacobi2d tb: grid too large");
+  const size_t smem = (size_t)W * (TbRot<T>::RS * 1024 + TbX<T>::kBytes);
+  auto kern = jacobi2d_tb4_kernel<T, W, kMinBlocks>;
+  ST_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)blocks, 32 * W, smem, s>>>(src, dst, nxp2, ld, y_lo, y_hi, g, ring_lo, ring_hi, nrows_buf,
+                                              rem.base, rem.delta, fold);
+  ST_LAUNCHED();
+  return ST_OK;
+}
+
 template <int T>
 st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
                      int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
-  const int64_t nxp2 = nx + 2;
-  const Tb4Grid g = tb4_grid(nxp2, y_hi - y_lo + 1, T);
-  const int64_t blocks = (g.n_int + g.n_edge + kStreamWarps - 1) / kStreamWarps;
-  ST_RETURN_IF(blocks > INT32_MAX, ST_ENOTSUP, "jacobi2d tb: grid too large");
   // power-of-two folding of the level multiplies (ST_JACOBI_FOLD=1; bitwise, every input
   // range-checked; 2 = folding WITHOUT the check, test-only: shows the tests' out-of-range
   // grids would break an unchecked fold). Off by default: on B200 the check costs as many
   // integer instructions as the folded multiplies save (ncu).
   static const int kFold = env_int("ST_JACOBI_FOLD", 0);
-  const size_t smem = (size_t)kStreamWarps * (TbRot<T>::RS * 1024 + TbX<T>::kBytes);
-  ST_CHECK_CUDA(cudaFuncSetAttribute(jacobi2d_tb4_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  jacobi2d_tb4_kernel<T><<<(unsigned)blocks, kStreamThreads, smem, s>>>(src, dst, nxp2, ld, y_lo, y_hi, g, ring_lo,
-                                                                     ring_hi, nrows_buf, rem.base, rem.delta, kFold);
-  ST_LAUNCHED();
-  return ST_OK;
+  return launch_tb4_occ<T, kStreamWarps, 1>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem, kFold);
 }
 
 }  // namespace
@@ -845,11 +862,11 @@ st_status jacobi2d_preload() {
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_stream_kernel<4>));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_resident_kernel));
   ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_regres_kernel<kRegResRows>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8>));
-  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<10>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<2, kStreamWarps, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<4, kStreamWarps, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<6, kStreamWarps, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<8, kStreamWarps, 1>));
+  ST_CHECK_CUDA(cudaFuncGetAttributes(&fa, jacobi2d_tb4_kernel<10, kStreamWarps, 1>));
   return ST_OK;
 }
 
