@@ -294,18 +294,6 @@ namespace {
 // resident warps (not of 8-strip CTAs): for C2 147 strips x 8 chunks of 2048
 // rows = 1176 warps <= 148 SMs x 8, one wave, 16 warm-up rows per 2048.
 //
-// Power-of-two folding (the level multiplies): level j < T-1 keeps 4^(j+1)
-// times its state, i.e. it stores the raw sum ((N+S)+W)+E without the * 0.25,
-// and the last level multiplies by 2^-2T. Scaling by a power of two commutes
-// with round-to-nearest addition (no overflow; subnormal sums are exact), so
-// this is bitwise the Listing-1 arithmetic whenever every intermediate
-// quotient sum/4 is exact — guaranteed if each input of the pass is zero or
-// has a biased exponent in [1+2T, 2045-2T]. Each input row is
-// checked with integer ops as it enters the pipeline; a warp that meets an
-// unsafe value restarts its item with the exact multiplies (stores are
-// idempotent, and every row stored before the check fired used checked rows).
-// One fp64 multiply per T updates instead of one per update.
-//
 // Instruction diet: each level keeps two row slots; N is slot k%2 and C slot
 // (k+1)%2, and the new row S overwrites the N slot once N has been consumed,
 // so with steps unrolled in groups of kTbGroup = 2 the rotation is register
@@ -319,12 +307,6 @@ constexpr int kTbCols = 128;  // columns per warp strip (32 lanes x 4)
 struct Quad {
   double2 a, b;  // columns x, x+1 | x+2, x+3
 };
-
-__host__ __device__ constexpr double pow2i(int k) {
-  double r = 1.0;
-  for (int i = 0; i < (k < 0 ? -k : k); ++i) r = k < 0 ? r * 0.5 : r * 2.0;
-  return r;
-}
 
 // 64-bit warp shuffles as two explicit 32-bit shuffles (the generic double
 // overload let ptxas swap the halves through three XORs per shuffle).
@@ -351,7 +333,7 @@ __device__ __forceinline__ void stg1_if(bool pred, double* p, double v) {
                : "memory");
 }
 
-template <int T, bool kScaled, bool kRows, bool kCols>
+template <int T, bool kRows, bool kCols>
 __device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][2], const int k, Quad s, int64_t r, const bool (&ring)[4],
                                            int64_t ring_lo, int64_t ring_hi) {
 #pragma unroll
@@ -365,68 +347,25 @@ __device__ __forceinline__ Quad tb4_levels(Quad (&st)[T][2], const int k, Quad s
     o.a.y = dadd(dadd(dadd(n.a.y, s.a.y), c.a.x), c.b.x);
     o.b.x = dadd(dadd(dadd(n.b.x, s.b.x), c.a.y), c.b.y);
     o.b.y = dadd(dadd(dadd(n.b.y, s.b.y), c.b.x), e);
-    if (!kScaled || j == T - 1) {  // folded: only the last level scales (by 2^-2T)
-      const double m = kScaled ? pow2i(-2 * T) : 0.25;
-      o.a.x = dmul(o.a.x, m);
-      o.a.y = dmul(o.a.y, m);
-      o.b.x = dmul(o.b.x, m);
-      o.b.y = dmul(o.b.y, m);
-    }
-    // a Dirichlet cell keeps its value; folded, its level-j copy carries level j's scale
-    const double rs = j == T - 1 ? pow2i(2 - 2 * T) : 4.0;
-    if (kCols) {
-      if (ring[0]) o.a.x = kScaled ? dmul(c.a.x, rs) : c.a.x;
-      if (ring[1]) o.a.y = kScaled ? dmul(c.a.y, rs) : c.a.y;
-      if (ring[2]) o.b.x = kScaled ? dmul(c.b.x, rs) : c.b.x;
-      if (ring[3]) o.b.y = kScaled ? dmul(c.b.y, rs) : c.b.y;
+    o.a.x = dmul(o.a.x, 0.25);
+    o.a.y = dmul(o.a.y, 0.25);
+    o.b.x = dmul(o.b.x, 0.25);
+    o.b.y = dmul(o.b.y, 0.25);
+    if (kCols) {  // a Dirichlet cell keeps its value
+      if (ring[0]) o.a.x = c.a.x;
+      if (ring[1]) o.a.y = c.a.y;
+      if (ring[2]) o.b.x = c.b.x;
+      if (ring[3]) o.b.y = c.b.y;
     }
     if (kRows) {
       const int64_t row = r - j - 1;
-      if (row <= ring_lo || row >= ring_hi) {
-        o = c;
-        if (kScaled) {
-          o.a.x = dmul(c.a.x, rs);
-          o.a.y = dmul(c.a.y, rs);
-          o.b.x = dmul(c.b.x, rs);
-          o.b.y = dmul(c.b.y, rs);
-        }
-      }
+      if (row <= ring_lo || row >= ring_hi) o = c;
     }
     st[j][k & 1] = s;
     s = o;
   }
   return s;
 }
-
-// Range check of the folding (lazy: accumulated per lane, voted once per item).
-// The folded arithmetic is bitwise Listing 1 when every input value is zero or
-// has a biased exponent in [1+2T, 2045-2T]. Integer ops on the bit patterns:
-// t = the high word << 1 (sign dropped, exponent in bits 31..21) is tracked by
-// its maximum; k = t + min(lo, 1) - 1 by its minimum, so an exact zero maps to
-// 0xffffffff (exempt) and a subnormal with a zero high word to 0 (caught).
-struct TbRange {
-  unsigned mn = 0xffffffffu, mx = 0u;
-  __device__ __forceinline__ void add(const Quad& q) {
-    auto key = [](double x, unsigned& t, unsigned& k) {
-      t = (unsigned)__double2hiint(x) << 1;
-      k = t + min((unsigned)__double2loint(x), 1u) - 1u;
-    };
-    unsigned t0, t1, t2, t3, k0, k1, k2, k3;
-    key(q.a.x, t0, k0);
-    key(q.a.y, t1, k1);
-    key(q.b.x, t2, k2);
-    key(q.b.y, t3, k3);
-    mn = __vimin3_u32(mn, k0, k1);
-    mn = __vimin3_u32(mn, k2, k3);
-    mx = __vimax3_u32(mx, t0, t1);
-    mx = __vimax3_u32(mx, t2, t3);
-  }
-  template <int T>
-  __device__ __forceinline__ bool unsafe() const {
-    constexpr unsigned kLo = (1u + 2u * T) << 21, kHi = (2046u - 2u * T) << 21;
-    return mn < kLo - 1u || mx >= kHi;
-  }
-};
 
 // Per-warp constants of one (strip, row chunk) item.
 struct Tb4Item {
@@ -532,10 +471,10 @@ struct TbX {
 };
 
 // One block of M steps; the run's first row (in slot 0) is a multiple of M rows back.
-template <int T, bool kScaled>
+template <int T>
 __device__ __forceinline__ void tb4_rot_block(Quad (&R)[TbRot<T>::M], TbRing& ring, const uint32_t xl, double*& out,
                                               int& i, const int i_lo, const unsigned i_span, const int64_t ld,
-                                              const bool sa, const bool sb, TbRange& rng) {
+                                              const bool sa, const bool sb) {
   using Rot = TbRot<T>;
   constexpr int M = Rot::M, RS = Rot::RS;
 #pragma unroll
@@ -543,7 +482,6 @@ __device__ __forceinline__ void tb4_rot_block(Quad (&R)[TbRot<T>::M], TbRing& ri
     ring.copy((k + RS - 1) % RS, ld);    // row r + RS - 1
     cp_wait<RS - 2>();                   // row r + 1 has landed
     R[Rot::at(k + 3)] = ring.read((k + 1) % RS);  // row r + 1, read one step ahead
-    if (kScaled) rng.add(R[Rot::at(k + 2)]);
     using X = TbX<T>;
     const int par = k & 1, npar = (k + 1) & 1;
     {  // level 0's C of step k+1 is this step's input row
@@ -568,13 +506,10 @@ __device__ __forceinline__ void tb4_rot_block(Quad (&R)[TbRot<T>::M], TbRing& ri
       n.a.y = dadd(dadd(dadd(n.a.y, s.a.y), c.a.x), c.b.x);
       n.b.x = dadd(dadd(dadd(n.b.x, s.b.x), c.a.y), c.b.y);
       n.b.y = dadd(dadd(dadd(n.b.y, s.b.y), c.b.x), e);
-      if (!kScaled || j == T - 1) {
-        const double m = kScaled ? pow2i(-2 * T) : 0.25;
-        n.a.x = dmul(n.a.x, m);
-        n.a.y = dmul(n.a.y, m);
-        n.b.x = dmul(n.b.x, m);
-        n.b.y = dmul(n.b.y, m);
-      }
+      n.a.x = dmul(n.a.x, 0.25);
+      n.a.y = dmul(n.a.y, 0.25);
+      n.b.x = dmul(n.b.x, 0.25);
+      n.b.y = dmul(n.b.y, 0.25);
       if (j + 1 < T) {  // P_j is level j+1's C at step k+1
         sts1(xl + X::off(npar, j + 1, 0, 1), n.a.x);
         sts1(xl + X::off(npar, j + 1, 1, 1), n.b.y);
@@ -590,16 +525,14 @@ __device__ __forceinline__ void tb4_rot_block(Quad (&R)[TbRot<T>::M], TbRing& ri
   }
 }
 
-// Streams one item; returns false if kScaled and an input broke the folding's
-// range (the caller reruns the item exactly; stores are idempotent).
-template <int T, bool kScaled>
-__device__ __forceinline__ bool tb4_item(const Tb4Item& it, const double* __restrict__ src_x, const bool use_rot,
+// Streams one item.
+template <int T>
+__device__ __forceinline__ void tb4_item(const Tb4Item& it, const double* __restrict__ src_x, const bool use_rot,
                                         const uint32_t smem_lane, const uint32_t xl) {
   constexpr int G = kTbGroup;
   using Rot = TbRot<T>;
   constexpr int M = Rot::M, RS = Rot::RS;
   const int64_t ld = it.ld;
-  TbRange rng;
   Quad st[T][2];
 #pragma unroll
   for (int j = 0; j < T; ++j) st[j][0].a = st[j][0].b = st[j][1].a = st[j][1].b = make_double2(0.0, 0.0);
@@ -657,7 +590,7 @@ __device__ __forceinline__ bool tb4_item(const Tb4Item& it, const double* __rest
       const unsigned i_span = (unsigned)(it.yc1 - it.yc0);
       const bool sa = it.stm[0] && it.stm[1], sb = it.stm[2] && it.stm[3];
       do {
-        tb4_rot_block<T, kScaled>(R, ring, xl, out, i, i_lo, i_span, ld, sa, sb, rng);
+        tb4_rot_block<T>(R, ring, xl, out, i, i_lo, i_span, ld, sa, sb);
         r0 += M;
       } while (r0 <= it.r_end && rot_ok(r0));
       cp_wait_all();
@@ -676,10 +609,6 @@ __device__ __forceinline__ bool tb4_item(const Tb4Item& it, const double* __rest
       loff = (r0 + G) * ld;
       continue;
     }
-    if (kScaled) {
-#pragma unroll
-      for (int k = 0; k < G; ++k) rng.add(buf[k]);
-    }
 #pragma unroll
     for (int k = 0; k < G; ++k) {
       const int64_t r = r0 + k;
@@ -692,11 +621,11 @@ __device__ __forceinline__ bool tb4_item(const Tb4Item& it, const double* __rest
       const bool rows_chk = (r - T <= it.ring_lo) || (r - 1 >= it.ring_hi);
       Quad o;
       if (rows_chk) {
-        o = it.col_ring ? tb4_levels<T, kScaled, true, true>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi)
-                        : tb4_levels<T, kScaled, true, false>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi);
+        o = it.col_ring ? tb4_levels<T, true, true>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi)
+                        : tb4_levels<T, true, false>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi);
       } else {
-        o = it.col_ring ? tb4_levels<T, kScaled, false, true>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi)
-                        : tb4_levels<T, kScaled, false, false>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi);
+        o = it.col_ring ? tb4_levels<T, false, true>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi)
+                        : tb4_levels<T, false, false>(st, k, s0, r, it.ring, it.ring_lo, it.ring_hi);
       }
       const bool in = r - T >= it.yc0 && r - T <= it.yc1;
       store_row(in, out, o);
@@ -706,8 +635,6 @@ __device__ __forceinline__ bool tb4_item(const Tb4Item& it, const double* __rest
     }
     r0 += G;
   }
-  if (kScaled) return !__any_sync(0xffffffffu, rng.unsafe<T>());
-  return true;
 }
 
 // Item numbering: items [0, n_int) are the interior strips (no ring column)
@@ -722,7 +649,7 @@ template <int T, int W, int kMinBlocks>
 __global__ void __launch_bounds__(32 * W, kMinBlocks)
     jacobi2d_tb4_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nxp2, int64_t ld,
                         int64_t y_lo, int64_t y_hi, Tb4Grid g, int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf,
-                        double* __restrict__ dst2, int64_t delta2, int fold) {
+                        double* __restrict__ dst2, int64_t delta2) {
   static_assert(T >= 2 && T % 2 == 0 && T <= 16, "even T");
   constexpr int kStride = kTbCols - 2 * T;
   const int lane = threadIdx.x & 31;
@@ -770,8 +697,7 @@ __global__ void __launch_bounds__(32 * W, kMinBlocks)
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t smem_lane = smem0 + warp * TbRot<T>::RS * 1024 + lane * 16;
   const uint32_t xl = smem0 + W * TbRot<T>::RS * 1024 + warp * TbX<T>::kBytes + lane * 8;
-  if (fold && (tb4_item<T, true>(it, src + x, use_rot, smem_lane, xl) || fold == 2)) return;
-  tb4_item<T, false>(it, src + x, use_rot, smem_lane, xl);
+  tb4_item<T>(it, src + x, use_rot, smem_lane, xl);
 }
 
 // Work decomposition: interior strips run the rotated path at ~R rows per item, the
@@ -828,7 +754,7 @@ Tb4Grid tb4_grid(int64_t nxp2, int64_t rows, int T, int64_t warps_per_sm) {
 // extra warps queue on the shared-memory pipe (row ring + exchange).
 template <int T, int W, int kMinBlocks>
 st_status launch_tb4_occ(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
-                         int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem, int fold) {
+                         int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
   const int64_t nxp2 = nx + 2;
   const Tb4Grid g = tb4_grid(nxp2, y_hi - y_lo + 1, T, W * kMinBlocks);
   const int64_t blocks = (g.n_int + g.n_edge + W - 1) / W;
@@ -837,7 +763,7 @@ st_status launch_tb4_occ(const double* src, double* dst, int64_t nx, int64_t ld,
   auto kern = jacobi2d_tb4_kernel<T, W, kMinBlocks>;
   ST_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)blocks, 32 * W, smem, s>>>(src, dst, nxp2, ld, y_lo, y_hi, g, ring_lo, ring_hi, nrows_buf,
-                                              rem.base, rem.delta, fold);
+                                              rem.base, rem.delta);
   ST_LAUNCHED();
   return ST_OK;
 }
@@ -845,12 +771,7 @@ st_status launch_tb4_occ(const double* src, double* dst, int64_t nx, int64_t ld,
 template <int T>
 st_status launch_tb4(const double* src, double* dst, int64_t nx, int64_t ld, int64_t y_lo, int64_t y_hi,
                      int64_t ring_lo, int64_t ring_hi, int64_t nrows_buf, cudaStream_t s, Remote rem) {
-  // power-of-two folding of the level multiplies (ST_JACOBI_FOLD=1; bitwise, every input
-  // range-checked; 2 = folding WITHOUT the check, test-only: shows the tests' out-of-range
-  // grids would break an unchecked fold). Off by default: on B200 the check costs as many
-  // integer instructions as the folded multiplies save (ncu).
-  static const int kFold = env_int("ST_JACOBI_FOLD", 0);
-  return launch_tb4_occ<T, kStreamWarps, 1>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem, kFold);
+  return launch_tb4_occ<T, kStreamWarps, 1>(src, dst, nx, ld, y_lo, y_hi, ring_lo, ring_hi, nrows_buf, s, rem);
 }
 
 }  // namespace

@@ -148,70 +148,37 @@ def test_launches_counted(cuda_lib):
     assert cuda_lib.launch_count() - n0 == 7
 
 
-def _subprocess_bitwise(cases_code, env_extra):
-    """Runs cases in a fresh process with environment knobs (read once per process by the library)."""
-    import os
-    import pathlib
-    import subprocess
-    import sys
-    code = r"""
-import sys, numpy as np, torch
-sys.path.insert(0, %r)
-import oracle, stencil_inputs as si, paper_2310_01882_b200 as st
-def run(a, it, tb, nx=None):
-    nx = a.shape[1] - 2 if nx is None else nx
-    ta = torch.from_numpy(a).cuda(); tb_ = torch.empty_like(ta)
-    return st.st_jacobi2d_run(ta, tb_, it, tblock=tb, nx=nx).cpu().numpy()
-res = []
-""" % str(pathlib.Path(__file__).resolve().parent.parent) + cases_code + "\nprint('RESULT', res)\n"
-    env = dict(os.environ, **env_extra)
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    line = [ln for ln in r.stdout.splitlines() if ln.startswith("RESULT")]
-    assert line, r.stdout + r.stderr[-3000:]
-    return eval(line[0][len("RESULT"):])
+# Extreme magnitudes through the temporally blocked kernels: tiny values whose
+# level sums round in the subnormal range, huge values, a tiny band deep inside a
+# chunk, zeros, and sign changes (cancellation to values near zero). Every level
+# multiplies by 0.25 exactly as Listing 1 does, so these stay bitwise.
+EXTREME_CASES = [
+    ("tiny", 2.0**-1060, 9, 8),
+    ("tiny_t2", 2.0**-1070, 5, 2),
+    ("huge", 2.0**1012, 16, 8),
+    ("mid_band", None, 17, 8),
+    ("edge_lo", 2.0**-1006, 16, 10),
+    ("zeros", 0.0, 24, 8),
+    ("signs", -1.0, 24, 10),
+]
 
 
-# Grids outside the folding's exactness range (DESIGN.md §6.2: every input zero or
-# with a biased exponent in [1+2T, 2045-2T]): tiny values whose level sums round
-# in the subnormal range, huge values, a single tiny row deep inside a chunk (the
-# warp restarts after it already stored rows), and the range edges for T = 8.
-FOLD_CASES = r"""
-rng = np.random.default_rng(7)
-base = si.jacobi2d_grid(300, 2600)
-cases = []
-cases.append(("tiny", base * 2.0**-1060, 9, 8))                 # subnormal sums: folding must not be used
-cases.append(("tiny_t2", base * 2.0**-1070, 5, 2))
-cases.append(("huge", base * 2.0**1012, 16, 8))                 # 4^8 x 2^1012 overflows
-mid = base.copy(); mid[1500:2000] *= 2.0**-1062; cases.append(("mid_band", mid, 17, 8))  # tiny band deep in the grid
-edge = base * 2.0**-1006; cases.append(("edge_lo_safe", edge, 16, 8))   # exponent -1006 (biased 17): folded
-edge2 = base * 2.0**-1007; cases.append(("edge_lo_unsafe", edge2, 16, 8))
-zero = base.copy(); zero[0, :] = 0.0; zero[:, 0] = 0.0; zero[5:9, 100:200] = 0.0; cases.append(("zeros", zero, 24, 8))
-neg = base - 1.0; cases.append(("signs", neg, 24, 8))           # cancellation -> values near zero, sign changes
-for name, a, it, tb in cases:
-    want = oracle.jacobi2d(a, it)
-    got = run(a, it, tb)
-    res.append((name, bool(np.array_equal(got.view(np.uint64), want.view(np.uint64)))))
-"""
-
-
-def test_fold_out_of_range_grids_bitwise(cuda_lib):
-    # ST_JACOBI_FOLD=1: folded levels with the per-row range check
-    res = _subprocess_bitwise(FOLD_CASES, {"ST_JACOBI_FOLD": "1"})
-    assert all(ok for _, ok in res), res
-
-
-def test_fold_exact_path_bitwise(cuda_lib):
-    # ST_JACOBI_FOLD=0 (the default): every level multiplies
-    res = _subprocess_bitwise(FOLD_CASES, {"ST_JACOBI_FOLD": "0"})
-    assert all(ok for _, ok in res), res
-
-
-def test_fold_check_is_necessary(cuda_lib):
-    # ST_JACOBI_FOLD=2 folds without the range check (test-only knob): the tiny and
-    # huge grids then differ from the oracle, so the range check is what keeps them exact
-    res = dict(_subprocess_bitwise(FOLD_CASES, {"ST_JACOBI_FOLD": "2"}))
-    assert not res["tiny"] and not res["huge"] and not res["mid_band"], res
-    assert res["edge_lo_safe"] and res["zeros"], res
+@pytest.mark.parametrize("name,scale,iters,tblock", EXTREME_CASES)
+def test_extreme_magnitudes_bitwise(cuda_lib, name, scale, iters, tblock):
+    a = si.jacobi2d_grid(300, 2600)
+    if name == "mid_band":
+        a[1500:2000] *= 2.0**-1062
+    elif name == "zeros":
+        a[0, :] = 0.0
+        a[:, 0] = 0.0
+        a[5:9, 100:200] = 0.0
+    elif name == "signs":
+        a = a - 1.0
+    else:
+        a = a * scale
+    want = oracle.jacobi2d(a, iters)
+    got = run_gpu(cuda_lib, a, iters, tblock)
+    assert_bitwise(got, want)
 
 
 @pytest.mark.parametrize("tblock", [2, 4, 6, 8, 10])
