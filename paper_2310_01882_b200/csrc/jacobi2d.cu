@@ -285,14 +285,16 @@ namespace {
 // 128-2T columns are exact, so strips advance by 128-2T. Rows stream through a
 // T-level software pipeline held entirely in registers: level j keeps its two
 // most recent rows (N, C); when level j-1 delivers a new row S, level j
-// produces row C. W/E neighbours at every level come from warp shuffles.
-// Dirichlet rows/columns are passed through unchanged at every level, so every
-// level is exactly one Jacobi sweep and the result is bitwise T single sweeps.
+// produces row C. W/E neighbours at every level come from the adjacent lanes:
+// warp shuffles in the general path below, a shared-memory exchange in the
+// rotated steady state. Dirichlet rows/columns are passed through unchanged at
+// every level, so every level is exactly one Jacobi sweep and the result is
+// bitwise T single sweeps.
 //
 // Work decomposition: one warp = one (strip, row chunk) item, items numbered
-// chunk-major over a 1-D grid, so the chunk height is chosen for whole waves of
-// resident warps (not of 8-strip CTAs): for C2 147 strips x 8 chunks of 2048
-// rows = 1176 warps <= 148 SMs x 8, one wave, 16 warm-up rows per 2048.
+// chunk-major over a 1-D grid; the chunk height is chosen per grid for whole
+// waves of resident warps against the 2T warm-up rows every chunk recomputes
+// (tb4_grid: C2 at T = 10 runs 150 interior strips x 46 chunks of 357 rows).
 //
 // Instruction diet: each level keeps two row slots; N is slot k%2 and C slot
 // (k+1)%2, and the new row S overwrites the N slot once N has been consumed,
