@@ -294,7 +294,8 @@ namespace {
 // Work decomposition: one warp = one (strip, row chunk) item, items numbered
 // chunk-major over a 1-D grid; the chunk height is chosen per grid for whole
 // waves of resident warps against the 2T warm-up rows every chunk recomputes
-// (tb4_grid: C2 at T = 10 runs 150 interior strips x 46 chunks of 357 rows).
+// (tb4_grid: C2 at T = 10 runs 150 interior strips x 15 chunks of 1093 rows plus
+// the 2 edge strips in shorter chunks: 2338 warps, two waves of 148 x 8).
 //
 // Instruction diet: each level keeps two row slots; N is slot k%2 and C slot
 // (k+1)%2, and the new row S overwrites the N slot once N has been consumed,
