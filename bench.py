@@ -754,6 +754,29 @@ def c1_leg(ctx):
         ev1.record(ctx.stream)
         ev1.synchronize()
         res[label] = round(ev0.elapsed_time(ev1) * 1e3 / reps, 2)
+    # the same 100 one-sweep launches captured once in a CUDA graph and replayed (the C-ABI
+    # call does no host synchronisation or allocation, so it is capturable as it stands)
+    try:
+        cap = torch.cuda.Stream()
+        cap.wait_stream(ctx.stream)
+        with torch.cuda.stream(cap):
+            st.st_jacobi2d_run(a1, b1, 100, tblock=1)  # warm the launch path outside capture
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            st.st_jacobi2d_run(a1, b1, 100, tblock=1)
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+        reps = 20
+        ev0.record(torch.cuda.current_stream())
+        for _ in range(reps):
+            graph.replay()
+        ev1.record(torch.cuda.current_stream())
+        ev1.synchronize()
+        res["cuda_graph_100_launches"] = round(ev0.elapsed_time(ev1) * 1e3 / reps, 2)
+    except Exception as exc:  # reported, never silently dropped
+        res["cuda_graph_100_launches"] = f"failed: {type(exc).__name__}: {exc}"[:200]
     res["value_resident_gpts"] = round(64 * 64 * 100 / (res["resident_single_cta"] * 1e-6) / 1e9, 3)
     return res
 

@@ -190,3 +190,28 @@ def test_wide_grids_equal_single_sweeps(cuda_lib, tblock, nx, ny, ld, iters):
     want = oracle.jacobi2d(a, iters, nx=nx)
     got = run_gpu(cuda_lib, a, iters, tblock, nx=nx)
     assert_bitwise(got[:, : nx + 2], want[:, : nx + 2])
+
+
+@pytest.mark.parametrize("tblock,iters", [(1, 7), (0, 23), (4, 10)])
+def test_cuda_graph_capture_bitwise(cuda_lib, tblock, iters):
+    # st_jacobi2d_run does no host synchronisation or allocation, so a whole multi-launch
+    # call can be captured in a CUDA graph once and replayed (the C1 bench leg times this)
+    import torch
+    st = cuda_lib
+    grid = si.jacobi2d_grid(1000, 500)
+    a0 = torch.from_numpy(grid).cuda()
+    a = a0.clone()
+    b = torch.empty_like(a)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        st.st_jacobi2d_run(a, b, iters, tblock=tblock)  # warm the launch path outside capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        r = st.st_jacobi2d_run(a, b, iters, tblock=tblock)
+    a.copy_(a0)
+    b.fill_(float("nan"))
+    graph.replay()
+    torch.cuda.synchronize()
+    assert_bitwise(r.cpu().numpy(), oracle.jacobi2d(grid, iters))
