@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B of kernel variants selected by environment settings: one T-blocked C2 launch under
 # ncu at locked base clocks (cycles per launch, no power-cap noise), then a short bench line.
-# usage: CFGS="ST_X=0 ST_X=1,ST_Y=2" bash tools/exp/gpu_ab.sh
+# usage: CFGS="ST_JACOBI_TB4_ROWS=0 ST_JACOBI_TB4_ROWS=512,ST_JACOBI_TB4_EDGE_COST=200" bash tools/exp/gpu_ab.sh
 OUT=gpurun_out/ab; mkdir -p $OUT
 make -j8 all > $OUT/build.log 2>&1 || { tail -20 $OUT/build.log; exit 1; }
 if [ -n "${TESTS:-}" ]; then timeout 900 python -m pytest $TESTS -x -q > $OUT/pytest.log 2>&1; echo "pytest rc=$?"; tail -2 $OUT/pytest.log; fi
