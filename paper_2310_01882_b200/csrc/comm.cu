@@ -85,6 +85,13 @@ using PFN_waitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned
 using PFN_writeValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 PFN_waitValue32 g_wait32 = nullptr;
 PFN_writeValue32 g_write32 = nullptr;
+// CU_STREAM_WAIT_VALUE_FLUSH where the device supports it: the flag a wait sees
+// was written by a peer after its data stores (the default write carries a
+// system-scope fence); the flush makes those remote data writes visible to the
+// work queued behind the wait on platforms that could otherwise hold them back.
+// (The B200s of this pool report no support: there the writer's fence, and NVLink
+// peer stores landing in the owner's L2 in order, are what order data and flag.)
+unsigned g_wait_flush = 0;
 
 st_status load_stream_memops() {
   static std::once_flag once;
@@ -99,6 +106,16 @@ st_status load_stream_memops() {
       g_wait32 = reinterpret_cast<PFN_waitValue32>(pw);
       g_write32 = reinterpret_cast<PFN_writeValue32>(pr);
       ok = true;
+      using PFN_attr = CUresult (*)(int*, CUdevice_attribute, CUdevice);
+      void* pa = nullptr;
+      cudaDriverEntryPointQueryResult q3;
+      int dev = 0, can = 0;
+      if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &pa, cudaEnableDefault, &q3) == cudaSuccess &&
+          q3 == cudaDriverEntryPointSuccess && pa && cudaGetDevice(&dev) == cudaSuccess &&
+          reinterpret_cast<PFN_attr>(pa)(&can, CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES, (CUdevice)dev) ==
+              CUDA_SUCCESS &&
+          can)
+        g_wait_flush = CU_STREAM_WAIT_VALUE_FLUSH;
     }
   });
   ST_RETURN_IF(!ok, ST_ECUDA, "stream memory operations (cuStreamWaitValue32) unavailable");
@@ -113,7 +130,7 @@ st_status stream_write(cudaStream_t s, uint32_t* addr, uint32_t v) {
 
 st_status stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t v) {
   CUresult r = g_wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
-                        CU_STREAM_WAIT_VALUE_GEQ);
+                        CU_STREAM_WAIT_VALUE_GEQ | g_wait_flush);
   ST_RETURN_IF(r != CUDA_SUCCESS, ST_ECUDA, "cuStreamWaitValue32 failed: %d", (int)r);
   return ST_OK;
 }
