@@ -133,3 +133,34 @@ def test_gauss_seidel_16384_full_grid_2_sweeps_and_fixed_point(cuda_lib):
     cuda_lib.st_gauss_seidel2d_run(g, 100)
     assert torch.equal(g, lin)
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("tblock", [0, 1])
+def test_C2_recipe_1024_full_1000_sweeps_every_point(cuda_lib, tblock):
+    # "full 1000 sweeps on a 1024^2 grid" — every point bitwise
+    # against the C oracle, at auto temporal blocking (T = 10: 100 passes) and at T = 1
+    import torch
+    n, iters = 1024, 1000
+    grid = si.jacobi2d_grid(n, n)
+    want = oracle.jacobi2d(grid, iters)
+    a = torch.from_numpy(grid).cuda()
+    b = torch.empty_like(a)
+    r = cuda_lib.st_jacobi2d_run(a, b, iters, tblock=tblock)
+    torch.cuda.synchronize()
+    got = r.cpu().numpy()
+    bad = np.argwhere(got.view(np.uint64) != want.view(np.uint64))
+    assert bad.size == 0, f"{len(bad)} mismatches, first at {bad[:5].tolist()}"
+
+
+def test_jacobi3d_128_cubed_100_sweeps_every_point(cuda_lib):
+    # the 3-D counterpart: 50 two-sweep passes (jacobi3d_t2_kernel) end to end, every point
+    import torch
+    n, iters = 128, 100
+    grid = si.jacobi3d_grid(n, n, n)
+    want = oracle.jacobi3d(grid, iters)
+    a = torch.from_numpy(grid).cuda()
+    b = torch.empty_like(a)
+    r = cuda_lib.st_jacobi3d_run(a, b, iters)
+    torch.cuda.synchronize()
+    got = r.cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
