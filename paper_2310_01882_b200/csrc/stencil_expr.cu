@@ -188,6 +188,40 @@ st_expr_kernel(const double* __restrict__ src, double* __restrict__ dst, long lo
 }
 )";
 
+// 2-D, streamed down y (even pitch, 16-byte aligned buffers): a thread owns one
+// 16-byte column pair (x, x+1) of a chunk of rows, every distinct pair offset m
+// (column x + 2m) the expression reads becomes a register queue of double2 over
+// its dy range, and the two outputs are stored as one 16-byte store — the
+// structure of the hand-written Listing-1 sweep, derived from the expression's
+// offsets (Listing 1: 3 pair loads per 2 points instead of 4 loads per point).
+// Pairs outside [0, ld-2] are clamped: they only feed outputs outside the
+// interior, which are not stored. Same tags as the fused template below.
+const char* kKernelTemplate2dStream = R"(
+extern "C" __global__ void __launch_bounds__(128)
+st_expr_kernel(const double* __restrict__ src, double* __restrict__ dst, long long nx, long long ny,
+               long long ld, long long R, long long yc) {
+  const long long xa = (R & ~1LL) + 2 * ((long long)blockIdx.x * 128 + threadIdx.x);
+  if (xa >= R + nx) return;
+  const bool w0 = xa >= R, w1 = xa + 1 < R + nx;
+  const long long y0 = R + (long long)blockIdx.y * yc;
+  const long long y1 = (y0 + yc < R + ny) ? y0 + yc : R + ny;
+#define PCOL(m) ((xa + 2 * (m) < 0) ? 0 : (xa + 2 * (m) > ld - 2) ? ld - 2 : xa + 2 * (m))
+#define PLD(m, row) __ldg(reinterpret_cast<const double2*>(src + (row) * ld + PCOL(m)))
+@DECL@
+@PRO@
+#pragma unroll 1
+  for (long long y = y0; y < y1; ++y) {
+@LOAD@
+    const double o0 = (@BODY@);
+@SHIFT@
+    double* d = dst + y * ld + xa;
+    if (w0 && w1) *reinterpret_cast<double2*>(d) = make_double2(o0, o1);
+    else if (w1) d[1] = o1;
+    else if (w0) d[0] = o0;
+  }
+}
+)";
+
 // Fused region: several outputs from several fields in one pass.
 // Code generation streams z: a thread owns one (x, y) column of a chunk of
 // planes, and every distinct (field, dy, dx) column the region reads becomes a
@@ -296,10 +330,15 @@ st_status compiled_kernel(const std::string& cexpr, int dims, int dev, CUfunctio
   const Nvrtc& f = nvrtc();
   ST_RETURN_IF(!f.ok, ST_ENOTSUP, "NVRTC (libnvrtc.so.12) is not available");
   std::string src;
-  if (dims == 4) {  // fused region: cexpr = DECL \x1f PRO \x1f LOAD \x1f COEF \x1f BODY \x1f SHIFT
-    src = kKernelTemplateFused;
+  if (dims == 4 || dims == 5) {  // cexpr = DECL \x1f PRO \x1f LOAD \x1f COEF \x1f BODY \x1f SHIFT
+    src = dims == 4 ? kKernelTemplateFused : kKernelTemplate2dStream;
     size_t start = 0;
     for (const char* tag : {"@DECL@", "@PRO@", "@LOAD@", "@COEF@", "@BODY@", "@SHIFT@"}) {
+      if (src.find(tag) == std::string::npos) {  // (the 2-D template has no @COEF@)
+        const size_t cut = cexpr.find('\x1f', start);
+        start = cut == std::string::npos ? cexpr.size() : cut + 1;
+        continue;
+      }
       const size_t cut = cexpr.find('\x1f', start);
       const std::string part = cexpr.substr(start, cut == std::string::npos ? std::string::npos : cut - start);
       src.replace(src.find(tag), std::strlen(tag), part);
@@ -348,24 +387,96 @@ st_status stencil_expr_translate(const char* expr, std::string* cexpr, int64_t* 
   return ST_OK;
 }
 
+namespace {
+// The y-streaming kernel's pieces for a translated 2-D expression (tokens A(dy,dx)):
+// one register queue per distinct dx over the dy range it is read at.
+std::string gen_2d_stream(const std::string& cexpr) {
+  auto enc = [](long v) { return (v < 0 ? "m" : "p") + std::to_string(std::labs(v)); };
+  auto fdiv2 = [](long v) { return v >= 0 ? v / 2 : -((-v + 1) / 2); };  // floor(v / 2)
+  auto scan = [&](auto&& on_access) {
+    std::string outs;
+    size_t i = 0;
+    while (i < cexpr.size()) {
+      if (cexpr[i] == 'A' && i + 1 < cexpr.size() && cexpr[i + 1] == '(') {
+        size_t j = i + 2;
+        long v[2];
+        for (int q = 0; q < 2; ++q) {
+          char* end = nullptr;
+          v[q] = std::strtol(cexpr.c_str() + j, &end, 10);
+          j = (size_t)(end - cexpr.c_str()) + 1;  // skip ',' or ')'
+        }
+        outs += on_access(v[0], v[1]);
+        i = j;
+      } else {
+        outs += cexpr[i++];
+      }
+    }
+    return outs;
+  };
+  std::map<long, std::pair<long, long>> pairs;  // pair offset m -> dy range (both outputs)
+  for (int out = 0; out < 2; ++out)
+    scan([&](long dy, long dx) {
+      const long m = fdiv2(dx + out);
+      auto it = pairs.find(m);
+      if (it == pairs.end()) pairs[m] = {dy, dy};
+      else it->second = {std::min(it->second.first, dy), std::max(it->second.second, dy)};
+      return std::string();
+    });
+  std::string decl, pro, load, shift;
+  for (const auto& kv : pairs) {
+    const long m = kv.first, lo = kv.second.first, hi = kv.second.second, n = hi - lo + 1;
+    const std::string q = "q_" + enc(m);
+    decl += "  double2 " + q + "[" + std::to_string(n) + "];\n";
+    for (long k = 0; k + 1 < n; ++k)
+      pro += "  " + q + "[" + std::to_string(k) + "] = PLD(" + std::to_string(m) + "LL, y0 + (" +
+             std::to_string(lo + k) + "LL));\n";
+    load += "    " + q + "[" + std::to_string(n - 1) + "] = PLD(" + std::to_string(m) + "LL, y + (" +
+            std::to_string(hi) + "LL));\n";
+    for (long k = 0; k + 1 < n; ++k)
+      shift += "    " + q + "[" + std::to_string(k) + "] = " + q + "[" + std::to_string(k + 1) + "];\n";
+  }
+  std::string body[2];
+  for (int out = 0; out < 2; ++out)
+    body[out] = scan([&](long dy, long dx) {
+      const long m = fdiv2(dx + out), h = dx + out - 2 * m;
+      return "q_" + enc(m) + "[" + std::to_string(dy - pairs[m].first) + "]." + (h ? "y" : "x");
+    });
+  // the second output is computed before the shift, right after the first
+  load += "";
+  const std::string o1 = "    const double o1 = (" + body[1] + ");\n";
+  const char sep = '\x1f';
+  return decl + sep + pro + sep + load + sep + std::string() + sep + body[0] + sep + o1 + shift;
+}
+}  // namespace
+
 st_status stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t R,
                              const std::string& cexpr, int64_t iters, cudaStream_t s) {
   int dev = 0;
   ST_CHECK_CUDA(cudaGetDevice(&dev));
   CUfunction k;
-  ST_TRY(compiled_kernel(cexpr, 2, dev, &k));
+  // column pairs need 16-byte rows; a body with a division stays on the per-point kernel,
+  // whose four rows per thread keep four independent quotients in flight (the pair kernel's
+  // two cost 9 % on the halo-2 division test expression, and gain 9 % on Listing 1)
+  const bool pairs = ld % 2 == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(b) & 15) == 0 && cexpr.find('/') == std::string::npos;
+  if (pairs) ST_TRY(compiled_kernel(gen_2d_stream(cexpr), 5, dev, &k));
+  else ST_TRY(compiled_kernel(cexpr, 2, dev, &k));
   Driver d;
   ST_TRY(driver(&d));
   ST_CHECK_CUDA(cudaMemcpyAsync(b, a, (size_t)(ny + 2 * R) * (size_t)ld * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  const int64_t gy = (ny + 15) / 16;
+  // pair kernel: 128 threads of column pairs, yc rows each; per-point kernel: 32 x 4 threads, 16 rows
+  static const int64_t yc = env_int("ST_EXPR_YC", 64);  // rows per thread (y-streaming chunk)
+  const int64_t gy = pairs ? (ny + yc - 1) / yc : (ny + 15) / 16;
   ST_RETURN_IF(gy > 65535, ST_ENOTSUP, "stencil2d_expr: ny = %lld too large for the grid", (long long)ny);
-  const unsigned gx = (unsigned)((nx + 31) / 32);
+  const int64_t npairs = (nx + (R & 1) + 1) / 2;  // column pairs from the even column R & ~1 to R + nx - 1
+  const unsigned gx = (unsigned)(pairs ? (npairs + 127) / 128 : (nx + 31) / 32);
+  const unsigned bx = pairs ? 128 : 32, by = pairs ? 1 : 4;
   const double* src = a;
   double* dst = b;
-  long long nxl = nx, nyl = ny, ldl = ld, Rl = R;
+  long long nxl = nx, nyl = ny, ldl = ld, Rl = R, ycl = yc;
   for (int64_t it = 0; it < iters; ++it) {
-    void* args[] = {&src, &dst, &nxl, &nyl, &ldl, &Rl};
-    ST_RETURN_IF(d.launch(k, gx, (unsigned)gy, 1, 32, 4, 1, 0, reinterpret_cast<CUstream>(s), args, nullptr) !=
+    void* args[] = {&src, &dst, &nxl, &nyl, &ldl, &Rl, &ycl};  // (the per-point kernel ignores yc)
+    ST_RETURN_IF(d.launch(k, gx, (unsigned)gy, 1, bx, by, 1, 0, reinterpret_cast<CUstream>(s), args, nullptr) !=
                      CUDA_SUCCESS,
                  ST_ECUDA, "cuLaunchKernel(st_expr_kernel) failed");
     launch_counter().fetch_add(1, std::memory_order_relaxed);

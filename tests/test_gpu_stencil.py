@@ -90,6 +90,25 @@ def test_expression_stencil_bitwise(cuda_lib, e, ny, nx, iters):
     assert np.array_equal(r.cpu().numpy(), ox.stencil2d_expr(a_np, e, iters))
 
 
+@pytest.mark.parametrize("e", EXPRS)
+@pytest.mark.parametrize("ny,nx,iters", [(1, 1, 2), (3, 2, 3), (37, 45, 3), (130, 257, 2), (70, 300, 3)])
+def test_expression_stencil_even_pitch_bitwise(cuda_lib, e, ny, nx, iters):
+    # 16-byte rows (even pitch, aligned base): the column-pair y-streaming kernel for bodies
+    # without a division; odd and even halos and widths exercise its edge clamps and the
+    # single-column stores of the pairs that straddle the Dirichlet ring
+    import torch
+    from oracle import expr as ox
+    R = ox.halo(e)
+    ld = nx + 2 * R + ((nx + 2 * R) & 1) + 2  # even, with pitch padding
+    full = rng.uniform(0.5, 1.5, size=(ny + 2 * R, ld))
+    a = torch.from_numpy(full).cuda()
+    b = torch.full_like(a, float("nan"))
+    r = cuda_lib.st_stencil2d_expr_run(a, b, e, iters, nx=nx)
+    torch.cuda.synchronize()
+    want = ox.stencil2d_expr(np.ascontiguousarray(full[:, : nx + 2 * R]), e, iters)
+    assert np.array_equal(r.cpu().numpy()[:, : nx + 2 * R], want)
+
+
 def test_listing1_expression_equals_jacobi_kernels(cuda_lib):
     # the NVRTC-compiled Listing 1 and the hand-written Jacobi kernels agree bitwise
     import torch
