@@ -42,6 +42,19 @@ def test_stencil_bitwise(cuda_lib, name, ny, nx, pad, iters):
     assert np.array_equal(got[:, :nx + 2 * R], want[:, :nx + 2 * R])
 
 
+@pytest.mark.parametrize("name", list(STENCILS))
+@pytest.mark.parametrize("ny,nx,iters", [(1, 1, 3), (3, 2, 2), (40, 65, 5), (97, 130, 4), (57, 301, 3)])
+def test_stencil_even_pitch_bitwise(cuda_lib, name, ny, nx, iters):
+    # 16-byte rows: the column-pair kernel (even and odd dx terms, pairs straddling the ring)
+    offs, coefs = STENCILS[name]
+    R = oracle.stencil_halo(offs)
+    ld = nx + 2 * R + ((nx + 2 * R) & 1)  # even, no spare column when nx + 2R is even
+    a = rng.standard_normal((ny + 2 * R, ld))
+    want = oracle.stencil2d(a, offs, coefs, iters, nx=nx)
+    got = run(cuda_lib, a, offs, coefs, iters, nx=nx)
+    assert np.array_equal(got[:, :nx + 2 * R], want[:, :nx + 2 * R])
+
+
 def test_random_stencils_bitwise(cuda_lib):
     for _ in range(10):
         n = int(rng.integers(1, 33))
