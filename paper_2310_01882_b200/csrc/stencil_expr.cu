@@ -254,6 +254,36 @@ st_expr_kernel(const __grid_constant__ Ptrs P, long long nx, long long ny, long 
 }
 )";
 
+// The same with column pairs (even pitch, 16-byte aligned fields): a thread owns
+// the pair (x, x+1) of its row, queues hold double2 per (field, dy, pair offset m),
+// and every output is one 16-byte store (see the 2-D pair template).
+const char* kKernelTemplateFusedPair = R"(
+struct Ptrs { const double* in[8]; double* out[8]; const double* k[8]; };
+extern "C" __global__ void __launch_bounds__(128)
+st_expr_kernel(const __grid_constant__ Ptrs P, long long nx, long long ny, long long nz, long long ldx,
+               long long R, long long zc) {
+  const long long x = (R & ~1LL) + 2 * ((long long)blockIdx.x * 32 + threadIdx.x);
+  const long long y = R + (long long)blockIdx.y * 4 + threadIdx.y;
+  if (x >= R + nx || y >= R + ny) return;
+  const bool w0 = x >= R, w1 = x + 1 < R + nx;
+#define PCOL(m) ((x + 2 * (m) < 0) ? 0LL : (x + 2 * (m) > ldx - 2) ? ldx - 2 : x + 2 * (m))
+  const long long plane = (ny + 2 * R) * ldx;
+  const long long col = y * ldx + x;
+  const long long z0 = R + (long long)blockIdx.z * zc;
+  const long long z1 = (z0 + zc < R + nz) ? z0 + zc : R + nz;
+@DECL@
+@PRO@
+#pragma unroll 1
+  for (long long z = z0; z < z1; ++z) {
+@LOAD@
+@COEF@
+    const long long o = z * plane + col;
+@BODY@
+@SHIFT@
+  }
+}
+)";
+
 // ------------------------------------------------------------------- NVRTC ---
 struct Nvrtc {
   decltype(&nvrtcCreateProgram) create = nullptr;
@@ -330,8 +360,8 @@ st_status compiled_kernel(const std::string& cexpr, int dims, int dev, CUfunctio
   const Nvrtc& f = nvrtc();
   ST_RETURN_IF(!f.ok, ST_ENOTSUP, "NVRTC (libnvrtc.so.12) is not available");
   std::string src;
-  if (dims == 4 || dims == 5) {  // cexpr = DECL \x1f PRO \x1f LOAD \x1f COEF \x1f BODY \x1f SHIFT
-    src = dims == 4 ? kKernelTemplateFused : kKernelTemplate2dStream;
+  if (dims >= 4) {  // cexpr = DECL \x1f PRO \x1f LOAD \x1f COEF \x1f BODY \x1f SHIFT
+    src = dims == 4 ? kKernelTemplateFused : dims == 5 ? kKernelTemplate2dStream : kKernelTemplateFusedPair;
     size_t start = 0;
     for (const char* tag : {"@DECL@", "@PRO@", "@LOAD@", "@COEF@", "@BODY@", "@SHIFT@"}) {
       if (src.find(tag) == std::string::npos) {  // (the 2-D template has no @COEF@)
@@ -530,37 +560,77 @@ st_status launch_fused_translated(const std::vector<std::string>& bodies, const 
       else it->second = {std::min(it->second.first, dz), std::max(it->second.second, dz)};
       return std::string();
     });
+  // column pairs: 16-byte rows and fields (even pitch, aligned pointers), division-free bodies
+  // (measured: benchmark 1's "/ 6" body 259 vs 292 Gpts/s with pairs, the PW region 74 vs 59)
+  bool pairs = ldx % 2 == 0;
+  for (const auto& b : bodies) pairs = pairs && b.find('/') == std::string::npos;
+  for (int i = 0; i < nin; ++i) pairs = pairs && (reinterpret_cast<uintptr_t>(in[i]) & 15) == 0;
+  for (size_t j = 0; j < bodies.size(); ++j) pairs = pairs && (reinterpret_cast<uintptr_t>(out[j]) & 15) == 0;
+  auto fdiv2 = [](long v) { return v >= 0 ? v / 2 : -((-v + 1) / 2); };  // floor(v / 2)
+  if (pairs) {  // queues per (field, dy, pair offset m) over the dz range both outputs read
+    cols.clear();
+    for (const auto& b : bodies)
+      for (int side = 0; side < 2; ++side)
+        scan(b, [&](int f, long dz, long dy, long dx) {
+          auto key = std::make_tuple(f, dy, fdiv2(dx + side));
+          auto it = cols.find(key);
+          if (it == cols.end()) cols[key] = {dz, dz};
+          else it->second = {std::min(it->second.first, dz), std::max(it->second.second, dz)};
+          return std::string();
+        });
+  }
   std::string decl, pro, load, coef, body, shift;
   for (const auto& kv : cols) {
     const int f = std::get<0>(kv.first);
     const long dy = std::get<1>(kv.first), dx = std::get<2>(kv.first);
     const long lo = kv.second.first, hi = kv.second.second, n = hi - lo + 1;
     const std::string q = "q" + std::to_string(f) + "_" + enc(dy) + "_" + enc(dx);
-    const std::string addr = "P.in[" + std::to_string(f) + "] + col + (" + std::to_string(dy) + "LL) * ldx + (" +
-                             std::to_string(dx) + "LL)";
-    decl += "  double " + q + "[" + std::to_string(n) + "];\n";
+    // (pairs: dx is the pair offset m, the address the clamped pair start)
+    const std::string addr =
+        pairs ? "reinterpret_cast<const double2*>(P.in[" + std::to_string(f) + "] + (y + (" + std::to_string(dy) +
+                    "LL)) * ldx + PCOL(" + std::to_string(dx) + "LL)"
+              : "P.in[" + std::to_string(f) + "] + col + (" + std::to_string(dy) + "LL) * ldx + (" +
+                    std::to_string(dx) + "LL)";
+    const std::string cl = pairs ? ")" : "";  // closes the reinterpret_cast
+    decl += std::string(pairs ? "  double2 " : "  double ") + q + "[" + std::to_string(n) + "];\n";
     for (long k = 0; k + 1 < n; ++k)
       pro += "  " + q + "[" + std::to_string(k) + "] = __ldg(" + addr + " + (z0 + (" + std::to_string(lo + k) +
-             "LL)) * plane);\n";
+             "LL)) * plane" + cl + ");\n";
     load += "    " + q + "[" + std::to_string(n - 1) + "] = __ldg(" + addr + " + (z + (" + std::to_string(hi) +
-            "LL)) * plane);\n";
+            "LL)) * plane" + cl + ");\n";
     for (long k = 0; k + 1 < n; ++k)
       shift += "    " + q + "[" + std::to_string(k) + "] = " + q + "[" + std::to_string(k + 1) + "];\n";
   }
   for (int j = 0; j < ncoef; ++j)
     coef += "    const double K" + std::to_string(j) + " = __ldg(P.k[" + std::to_string(j) + "] + z);\n";
   for (size_t j = 0; j < bodies.size(); ++j) {
-    const std::string e = scan(bodies[j], [&](int f, long dz, long dy, long dx) {
-      const long lo = cols[std::make_tuple(f, dy, dx)].first;
-      return "q" + std::to_string(f) + "_" + enc(dy) + "_" + enc(dx) + "[" + std::to_string(dz - lo) + "]";
-    });
-    body += "    P.out[" + std::to_string(j) + "][o] = (" + e + ");\n";
+    if (!pairs) {
+      const std::string e = scan(bodies[j], [&](int f, long dz, long dy, long dx) {
+        const long lo = cols[std::make_tuple(f, dy, dx)].first;
+        return "q" + std::to_string(f) + "_" + enc(dy) + "_" + enc(dx) + "[" + std::to_string(dz - lo) + "]";
+      });
+      body += "    P.out[" + std::to_string(j) + "][o] = (" + e + ");\n";
+      continue;
+    }
+    std::string e[2];
+    for (int side = 0; side < 2; ++side)
+      e[side] = scan(bodies[j], [&](int f, long dz, long dy, long dx) {
+        const long m = fdiv2(dx + side), h = dx + side - 2 * m;
+        const long lo = cols[std::make_tuple(f, dy, m)].first;
+        return "q" + std::to_string(f) + "_" + enc(dy) + "_" + enc(m) + "[" + std::to_string(dz - lo) + "]." +
+               (h ? "y" : "x");
+      });
+    const std::string J = std::to_string(j);
+    body += "    { const double v0 = (" + e[0] + "); const double v1 = (" + e[1] + "); double* d = P.out[" + J +
+            "] + o;\n      if (w0 && w1) *reinterpret_cast<double2*>(d) = make_double2(v0, v1); "
+            "else if (w1) d[1] = v1; else if (w0) d[0] = v0; }\n";
   }
   int dev = 0;
   ST_CHECK_CUDA(cudaGetDevice(&dev));
   CUfunction k;
   const char sep = '\x1f';
-  ST_TRY(compiled_kernel(decl + sep + pro + sep + load + sep + coef + sep + body + sep + shift, 4, dev, &k));
+  ST_TRY(compiled_kernel(decl + sep + pro + sep + load + sep + coef + sep + body + sep + shift, pairs ? 6 : 4, dev,
+                         &k));
   Driver d;
   ST_TRY(driver(&d));
   struct Ptrs {
@@ -576,7 +646,8 @@ st_status launch_fused_translated(const std::vector<std::string>& bodies, const 
   ST_RETURN_IF(gy > 65535 || gz > 65535, ST_ENOTSUP, "fused region: grid too large");
   long long nxl = nx, nyl = ny, nzl = nz, ldl = ldx, Rl = R, zcl = zc;
   void* args[] = {&P, &nxl, &nyl, &nzl, &ldl, &Rl, &zcl};
-  ST_RETURN_IF(d.launch(k, (unsigned)((nx + 31) / 32), (unsigned)gy, (unsigned)gz, 32, 4, 1, 0,
+  const int64_t xthreads = pairs ? (nx + (R & 1) + 1) / 2 : nx;  // pairs start at the even column R & ~1
+  ST_RETURN_IF(d.launch(k, (unsigned)((xthreads + 31) / 32), (unsigned)gy, (unsigned)gz, 32, 4, 1, 0,
                         reinterpret_cast<CUstream>(s), args, nullptr) != CUDA_SUCCESS,
                ST_ECUDA, "cuLaunchKernel(fused region) failed");
   launch_counter().fetch_add(1, std::memory_order_relaxed);

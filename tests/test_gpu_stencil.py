@@ -154,6 +154,24 @@ def test_expression_stencil_3d_bitwise(cuda_lib, e, nz, ny, nx, iters):
     assert np.array_equal(r.cpu().numpy(), ox.stencil3d_expr(a_np, e, iters))
 
 
+@pytest.mark.parametrize("e", ["a(1,0,-1)*a(0,2,0) - 3*a(-1,-1,1) + 0.5",
+                               "(a(-1,0,0) + a(1,0,0) + a(0,-1,0) + a(0,1,0)) * 0.25 - a(0,0,-3)*a(0,0,2)"])
+@pytest.mark.parametrize("nz,ny,nx,iters", [(3, 4, 1, 2), (5, 6, 9, 2), (17, 9, 70, 3)])
+def test_expression_stencil_3d_even_pitch_bitwise(cuda_lib, e, nz, ny, nx, iters):
+    # 16-byte rows and a division-free body: the column-pair register-queue kernel
+    # (odd and even halos and widths: pairs straddling the ring, clamped pair loads)
+    import torch
+    from oracle import expr as ox
+    R = ox.halo3(e)
+    ldx = nx + 2 * R + ((nx + 2 * R) & 1)
+    full = rng.uniform(0.5, 1.5, size=(nz + 2 * R, ny + 2 * R, ldx))
+    a = torch.from_numpy(full).cuda()
+    r = cuda_lib.st_stencil3d_expr_run(a, torch.full_like(a, float("nan")), e, iters, nx=nx)
+    torch.cuda.synchronize()
+    want = ox.stencil3d_expr(np.ascontiguousarray(full[:, :, : nx + 2 * R]), e, iters)
+    assert np.array_equal(r.cpu().numpy()[:, :, : nx + 2 * R], want)
+
+
 def test_benchmark1_expression_equals_jacobi3d_kernel(cuda_lib):
     # NVRTC-compiled benchmark 1 and the hand-written TMA jacobi3d kernel agree bitwise
     import torch
