@@ -239,7 +239,7 @@ st_status jacobi2d_sweep_rows(const double* src, double* dst, int64_t nx, int64_
   const int64_t nxp2 = nx + 2;
   const int64_t nstrips = (nxp2 + kStripCols - 1) / kStripCols;
   const int64_t rows = y_hi - y_lo + 1;
-  static const int kRows = env_int("ST_JACOBI_ROWS", 128);
+  static const int kRows = env_int("ST_JACOBI_ROWS", 32);  // 32-row chunks: 402 vs 393 Gpts/s at 128 (C2, round 2)
   const int64_t rpc = std::max<int64_t>(1, std::min<int64_t>(kRows, rows));
   const int64_t nchunks = (rows + rpc - 1) / rpc;
   ST_RETURN_IF(nchunks > 65535, ST_ENOTSUP, "jacobi2d: %lld row chunks exceed grid.y", (long long)nchunks);

@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -201,12 +202,18 @@ extern "C" __global__ void __launch_bounds__(128)
 st_expr_kernel(const double* __restrict__ src, double* __restrict__ dst, long long nx, long long ny,
                long long ld, long long R, long long yc) {
   const long long xa = (R & ~1LL) + 2 * ((long long)blockIdx.x * 128 + threadIdx.x);
-  if (xa >= R + nx) return;
-  const bool w0 = xa >= R, w1 = xa + 1 < R + nx;
+  const unsigned lane = threadIdx.x & 31;
+  // (no early exit: every lane takes part in the neighbour shuffles; lanes past the row
+  // load clamped pairs and store nothing)
+  const bool w0 = xa >= R && xa < R + nx, w1 = xa + 1 < R + nx;
   const long long y0 = R + (long long)blockIdx.y * yc;
   const long long y1 = (y0 + yc < R + ny) ? y0 + yc : R + ny;
 #define PCOL(m) ((xa + 2 * (m) < 0) ? 0 : (xa + 2 * (m) > ld - 2) ? ld - 2 : xa + 2 * (m))
 #define PLD(m, row) __ldg(reinterpret_cast<const double2*>(src + (row) * ld + PCOL(m)))
+#define SHF(v, d) __hiloint2double(__shfl_down_sync(0xffffffffu, __double2hiint(v), d), \
+                                   __shfl_down_sync(0xffffffffu, __double2loint(v), d))
+#define SHB(v, d) __hiloint2double(__shfl_up_sync(0xffffffffu, __double2hiint(v), d), \
+                                   __shfl_up_sync(0xffffffffu, __double2loint(v), d))
 @DECL@
 @PRO@
 #pragma unroll 1
@@ -443,13 +450,28 @@ std::string gen_2d_stream(const std::string& cexpr) {
     }
     return outs;
   };
-  std::map<long, std::pair<long, long>> pairs;  // pair offset m -> dy range (both outputs)
+  // pair offset m -> dy range; the m = 0 queue first (its rows feed the neighbour shuffles)
+  std::map<long, std::pair<long, long>> pairs;
+  auto widen = [&](long m, long dy) {
+    auto it = pairs.find(m);
+    if (it == pairs.end()) pairs[m] = {dy, dy};
+    else it->second = {std::min(it->second.first, dy), std::max(it->second.second, dy)};
+  };
+  for (int out = 0; out < 2; ++out)
+    scan([&](long dy, long dx) {
+      if (fdiv2(dx + out) == 0) widen(0, dy);
+      return std::string();
+    });
+  // accesses to the pairs of the neighbouring lanes (m = +-1) at rows the m = 0 queue holds
+  // come from that queue by a warp shuffle (lanes 31 / 0 load theirs); the rest get queues
+  auto shuffled = [&](long m, long dy) {
+    auto z = pairs.find(0);
+    return (m == 1 || m == -1) && z != pairs.end() && dy >= z->second.first && dy <= z->second.second;
+  };
   for (int out = 0; out < 2; ++out)
     scan([&](long dy, long dx) {
       const long m = fdiv2(dx + out);
-      auto it = pairs.find(m);
-      if (it == pairs.end()) pairs[m] = {dy, dy};
-      else it->second = {std::min(it->second.first, dy), std::max(it->second.second, dy)};
+      if (m != 0 && !shuffled(m, dy)) widen(m, dy);
       return std::string();
     });
   std::string decl, pro, load, shift;
@@ -465,14 +487,26 @@ std::string gen_2d_stream(const std::string& cexpr) {
     for (long k = 0; k + 1 < n; ++k)
       shift += "    " + q + "[" + std::to_string(k) + "] = " + q + "[" + std::to_string(k + 1) + "];\n";
   }
+  std::set<std::tuple<long, long, long>> shufs;  // (m, dy, half) read through a shuffle
   std::string body[2];
   for (int out = 0; out < 2; ++out)
     body[out] = scan([&](long dy, long dx) {
       const long m = fdiv2(dx + out), h = dx + out - 2 * m;
+      if (m != 0 && shuffled(m, dy)) {
+        shufs.insert(std::make_tuple(m, dy, h));
+        return "s_" + enc(m) + "_" + enc(dy) + "_" + std::to_string(h);
+      }
       return "q_" + enc(m) + "[" + std::to_string(dy - pairs[m].first) + "]." + (h ? "y" : "x");
     });
-  // the second output is computed before the shift, right after the first
-  load += "";
+  for (const auto& t : shufs) {
+    const long m = std::get<0>(t), dy = std::get<1>(t), h = std::get<2>(t);
+    const std::string v = "q_p0[" + std::to_string(dy - pairs[0].first) + "]." + (h ? "y" : "x");
+    const std::string name = "s_" + enc(m) + "_" + enc(dy) + "_" + std::to_string(h);
+    const char* edge = m > 0 ? "31u" : "0u";
+    load += "    double " + name + " = " + (m > 0 ? "SHF(" : "SHB(") + v + ", 1);\n";
+    load += "    if (lane == " + std::string(edge) + ") " + name + " = src[(y + (" + std::to_string(dy) +
+            "LL)) * ld + PCOL(" + std::to_string(m) + "LL) + " + std::to_string(h) + "];\n";
+  }
   const std::string o1 = "    const double o1 = (" + body[1] + ");\n";
   const char sep = '\x1f';
   return decl + sep + pro + sep + load + sep + std::string() + sep + body[0] + sep + o1 + shift;
@@ -495,7 +529,7 @@ st_status stencil2d_expr_run(double* a, double* b, int64_t nx, int64_t ny, int64
   ST_TRY(driver(&d));
   ST_CHECK_CUDA(cudaMemcpyAsync(b, a, (size_t)(ny + 2 * R) * (size_t)ld * sizeof(double), cudaMemcpyDeviceToDevice, s));
   // pair kernel: 128 threads of column pairs, yc rows each; per-point kernel: 32 x 4 threads, 16 rows
-  static const int64_t yc = env_int("ST_EXPR_YC", 64);  // rows per thread (y-streaming chunk)
+  static const int64_t yc = env_int("ST_EXPR_YC", 4);  // rows per thread (y-streaming chunk; 4: 401 vs 355 Gpts/s at 64)
   const int64_t gy = pairs ? (ny + yc - 1) / yc : (ny + 15) / 16;
   ST_RETURN_IF(gy > 65535, ST_ENOTSUP, "stencil2d_expr: ny = %lld too large for the grid", (long long)ny);
   const int64_t npairs = (nx + (R & 1) + 1) / 2;  // column pairs from the even column R & ~1 to R + nx - 1
