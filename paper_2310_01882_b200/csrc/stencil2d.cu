@@ -16,6 +16,9 @@
 // reads of a point are L1 hits except the tile's halo, and each warp row access
 // is a coalesced 256-byte segment.
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
 
 #include "common.cuh"
 #include "internal.h"
@@ -92,6 +95,33 @@ st_status stencil2d_preload() {
 
 st_status stencil2d_run(double* a, double* b, int64_t nx, int64_t ny, int64_t ld, int64_t R, const int32_t* off,
                         const double* coeffs, int32_t n, int64_t iters, cudaStream_t s) {
+  // 16-byte rows: specialise the stencil for its offsets — the terms written as the
+  // expression "(c0)*a(dy0,dx0) + (c1)*a(dy1,dx1) + ..." (left to right, one rounding per
+  // product and per sum: the same arithmetic as the kernel below; %.17g literals round-trip
+  // exactly) go through the NVRTC column-pair generator (§6.8 of DESIGN.md), whose register
+  // queues and neighbour shuffles the runtime-term kernel cannot have. Without NVRTC, or with
+  // a non-finite coefficient, the runtime-term kernel below runs.
+  static const int kJit = env_int("ST_STENCIL_JIT", 1);
+  const bool aligned16 = ld % 2 == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(b) & 15) == 0;
+  if (kJit && aligned16) {
+    std::string e;
+    bool finite = true;
+    for (int i = 0; i < n; ++i) {
+      char buf[96];
+      finite = finite && std::isfinite(coeffs[i]);
+      std::snprintf(buf, sizeof buf, "%s(%.17g)*a(%d,%d)", i ? " + " : "", coeffs[i], off[2 * i], off[2 * i + 1]);
+      e += buf;
+    }
+    std::string cexpr;
+    int64_t re = -1;
+    int dims = 0;
+    if (finite && stencil_expr_translate(e.c_str(), &cexpr, &re, &dims) == ST_OK && re == R && dims == 2) {
+      const st_status r = stencil2d_expr_run(a, b, nx, ny, ld, R, cexpr, iters, s);
+      if (r != ST_ENOTSUP) return r;  // ST_ENOTSUP: no NVRTC here — the runtime-term kernel instead
+      clear_error();
+    }
+  }
   Terms t{};
   t.n = n;
   for (int i = 0; i < n; ++i) {
